@@ -1,0 +1,428 @@
+"""Benchmark: Mrays/s and FPS of 1080p VOctree HH rendering (BASELINE.json configs[1]).
+
+Workload (config 2): depth-9 spherical-shell VOctree
+(3,557,912 leaves, n_max = 2 -> 104 f32 per leaf, 1.48 GB payload), T = 30
+frames, 1920x1080 camera look_at((1.6,1.3,0.9) -> (0.5,0.5,0.5)), uncached
+render (the fused ray-gen + traversal + HH shading + compositing +
+finalize kernel).  One step = one full 1080p frame; steps sweep frames
+0..29.  Synthetic data generated in-process (deterministic seeds).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: every rank holds a full tree replica and
+renders its interleaved 64x64 tiles of the same frame, then one NCCL
+all-gather per frame assembles the image (strong scaling: fixed work per
+step).  The reference arm (--impl reference) times the reference's own CPU
+renderer (voxvid from baseline/_ref, numba, all host threads) or, if that
+is not installed, the C oracle port (OpenMP, all host threads).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mrays/s and FPS at 1080p (VOctree HH render) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "Mrays/s"
+WIDTH, HEIGHT, FRAMES = 1920, 1080, 30
+C_COEF, K_HH = 31, 14
+L2_BYTES = 126 * 2**20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- helpers
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the render kernel from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "render_camera_ncu.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def make_tree(config: int):
+    from paper_2202_06088_b200 import synthetic
+
+    t0 = time.time()
+    if config == 3:
+        tree = synthetic.motion_tree(depth=9, n_max=2, frames=60, seed=0)
+    else:
+        tree = synthetic.shell_tree(depth=9, n_max=2, frames=FRAMES, seed=0)
+    log(f"[bench] tree: {tree.n_leaves} leaves, {tree.n_internal} internal, "
+        f"{tree.leaf_data.nbytes / 1e9:.3f} GB payload, built in {time.time() - t0:.1f}s")
+    return tree
+
+
+def algorithmic_bytes(tree, cam, frames, device):
+    """Reference-defined bytes per frame:
+    sum_rays 32 P + 4C V + 4(C+3K) S + 20, with P/V/S the internal-node pops,
+    visited leaves and shaded leaves of the reference traversal (early stop
+    1e-4), counted by the instrumented kernel on host-generated rays (bit-
+    exact with the reference's counts)."""
+    import torch
+
+    import paper_2202_06088_b200 as vv
+
+    o, d = cam.rays()
+    ot = torch.from_numpy(o).to(device)
+    dt = torch.from_numpy(d).to(device)
+    out = {}
+    c = tree.coeff_count
+    k = tree.basis_count
+    for f in frames:
+        _, _, _, st = vv.render_rays(tree, ot, dt, f, stats=True)
+        P = st["node_pops"].to(torch.int64).sum().item()
+        V = st["sample_count"].to(torch.int64).sum().item()
+        S = st["shaded"].to(torch.int64).sum().item()
+        n = o.shape[0]
+        out[f] = dict(P=P, V=V, S=S, bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * n)
+    return out
+
+
+# --------------------------------------------------------------------------- CPU baselines
+def cpu_reference_render(tree, cam, frames):
+    """Time the reference's own render() (voxvid numba) if installed in baseline/_ref."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "voxvid").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", str(ref_dir / ".numba_cache"))
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count()))
+    sys.path.insert(0, str(ref_dir))
+    import numba
+    from voxvid import render as rr
+    from voxvid.octree import VOctree as RV
+    from voxvid.temporal import TemporalBases as RTB
+
+    rtree = RV(tree.depth, tree.node_child, tree.leaf_coords, tree.leaf_data, RTB(tree.bases.a, tree.bases.b),
+               tree.n_max, tree.bbox_lo, tree.side)
+    rcam = rr.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
+    small = rr.Camera(64, 36, cam.fx / 30, cam.fy / 30, 32.0, 18.0, cam.c2w)
+    t0 = time.time()
+    rr.render(rtree, small, frames[0])  # JIT warm-up
+    log(f"[bench] reference JIT warm-up {time.time() - t0:.1f}s, numba threads {numba.get_num_threads()}")
+    times = []
+    for f in frames:
+        t0 = time.perf_counter()
+        rr.render(rtree, rcam, f)
+        times.append(time.perf_counter() - t0)
+    return dict(times=times, cores=int(numba.get_num_threads()), kind="reference",
+                impl="voxvid.render.render (numba, baseline/_ref), uncached")
+
+
+def cpu_port_render(tree, cam, frames):
+    """Time the C oracle port (OpenMP, all host threads): ray gen + render_kernel + finalize."""
+    from oracle import oracle
+
+    nt = oracle.num_procs()
+    times = []
+    for f in frames:
+        t0 = time.perf_counter()
+        o, d = cam.rays()
+        out = oracle.render_rays(tree, o, d, f, nthreads=nt)
+        oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+        times.append(time.perf_counter() - t0)
+    return dict(times=times, cores=nt, kind="port", impl="oracle/vv_oracle.c (OpenMP), uncached")
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    cam_mod = __import__("paper_2202_06088_b200.synthetic", fromlist=["bench_camera"])
+    tree = make_tree(args.config)
+    cam = cam_mod.bench_camera(WIDTH, HEIGHT)
+    frames = [i % FRAMES for i in range(args.warmup, args.warmup + args.steps)]
+    res = cpu_reference_render(tree, cam, frames) if not args.port else None
+    if res is None:
+        res = cpu_port_render(tree, cam, frames)
+    n_rays = WIDTH * HEIGHT
+    ms = 1e3 * sum(res["times"]) / len(res["times"])
+    value = n_rays * len(res["times"]) / sum(res["times"]) / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "fps": round(1e3 / ms, 4),
+        "config": {"workload": "cfg2: depth-9 shell VOctree, n_max 2, T 30, 1920x1080, uncached render, frame sweep",
+                   "frames": frames, "rays_per_step": n_rays},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
+                         "sample": f"{len(frames)} full 1080p frames {frames}", "impl": res["impl"]},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_06088_b200 as vv
+    from paper_2202_06088_b200 import synthetic
+    from paper_2202_06088_b200.device import replica, stream_ptr
+    from paper_2202_06088_b200.distributed import TileRenderer
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tree = make_tree(args.config)
+    cam = synthetic.bench_camera(WIDTH, HEIGHT)
+    n_rays = WIDTH * HEIGHT
+    t0 = time.time()
+    rep = replica(tree, dev)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: upload {time.time() - t0:.2f}s, {rep.device_bytes / 1e9:.3f} GB on device")
+
+    frames_total = FRAMES if args.config != 3 else 60
+    step_frames = [(args.warmup + i) % frames_total for i in range(args.steps)]
+    warm_frames = [i % frames_total for i in range(args.warmup)]
+
+    rgb = torch.empty((HEIGHT, WIDTH, 3), dtype=torch.float32, device=dev)
+    alpha = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
+    depth = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    tiles = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev) if world > 1 else None
+
+    def step(f):
+        if tiles is None:
+            vv.render_into(tree, cam, f, rgb, alpha, depth)
+        else:
+            tiles.render_slab(tree, cam, f)
+            tiles.gather()
+            if rank == 0:
+                tiles.unpack(rgb, alpha, depth)
+
+    for f in warm_frames:
+        step(f)
+    torch.cuda.synchronize()
+
+    # device-timed region: K steps, L2 flushed between steps (outside the events)
+    stream = torch.cuda.current_stream(dev)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    wall0 = time.perf_counter()
+    for i, f in enumerate(step_frames):
+        flush.zero_()
+        starts[i].record(stream)
+        step(f)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+
+    # end-to-end through the public API: render() -> host numpy images
+    e2e = None
+    if world == 1:
+        for f in warm_frames[:2]:
+            vv.render(tree, cam, f)
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for f in step_frames:
+            layer = vv.render(tree, cam, f)
+        e2e_s = time.perf_counter() - te
+        assert layer.rgb.shape == (HEIGHT, WIDTH, 3)
+        e2e = {"value": round(n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 168 + 48, "d2h_bytes_per_step": 5 * 4 * n_rays,
+               "api": "paper_2202_06088_b200.render(tree, cam, frame) -> numpy LayerImages (fp32)"}
+    else:
+        # tiles -> all-gather -> rank 0 unpack -> D2H on rank 0
+        host = torch.empty(5 * n_rays, dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        dist.barrier()
+        te = time.perf_counter()
+        for f in step_frames:
+            step(f)
+            if rank == 0:
+                host[: 3 * n_rays].copy_(rgb.view(-1), non_blocking=True)
+                host[3 * n_rays: 4 * n_rays].copy_(alpha.view(-1), non_blocking=True)
+                host[4 * n_rays:].copy_(depth.view(-1), non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e2e_s = time.perf_counter() - te
+        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_s = float(et.item())
+        e2e = {"value": round(n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 168 + 48, "d2h_bytes_per_step": 5 * 4 * n_rays,
+               "api": "TileRenderer.render_slab + NCCL all_gather + unpack -> pinned host (rank 0)"}
+
+    if rank != 0:
+        return
+
+    # roofline of the dominant kernel (k_render_camera), reference-defined bytes
+    ab = algorithmic_bytes(tree, cam, sorted(set(step_frames)), dev)
+    bytes_per_step = [ab[f]["bytes"] for f in step_frames]
+    kernel_s = total_ms / 1e3
+    achieved = sum(bytes_per_step) / kernel_s / 1e9 if world == 1 else sum(bytes_per_step) / kernel_s / 1e9 / world
+    peak, peak_kind = measured_peak()
+    mean_ab = {k: float(np.mean([ab[f][k] for f in step_frames]) / n_rays) for k in ("P", "V", "S")}
+
+    # CPU baseline: oracle port on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sample_frames = [step_frames[0]]
+        res = cpu_port_render(tree, cam, sample_frames)
+        cpu = {"value": round(n_rays * len(res["times"]) / sum(res["times"]) / 1e6, 4), "unit": UNIT,
+               "cores": res["cores"], "kind": res["kind"],
+               "sample": f"{len(sample_frames)} full 1080p frame(s) {sample_frames}, host ray gen + render + finalize"}
+
+    ms = total_ms / len(step_frames)
+    value = n_rays * len(step_frames) / (total_ms / 1e3) / 1e6
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "fps": round(1e3 / ms, 2),
+        "config": {
+            "workload": "cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached "
+                        "render (ray gen + traversal + HH shading + compositing + finalize), frame sweep",
+            "rays_per_step": n_rays, "frames": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
+            "l2": "inputs larger than L2 (1.54 GB tree) and L2 flushed between steps (252 MiB memset outside "
+                  "the per-step CUDA events)",
+            "parallelism": f"tile{world}" if world > 1 else "single",
+            "per_ray": mean_ab, "wall_ms_timed_region": round(wall * 1e3, 3),
+            "dtype_note": "f64 traversal/sigma/compositing, fp32 HH colour",
+        },
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                     "peak_kind": peak_kind, "kernel": "k_render_camera",
+                     "bytes_per_frame": float(np.mean(bytes_per_step))},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": len(step_frames) * (1 if world == 1 else 2),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--port", action="store_true", help="reference arm: force the C oracle port")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

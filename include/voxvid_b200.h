@@ -1,0 +1,212 @@
+/*
+ * voxvid_b200.h -- C ABI of the B200-native VOctree renderer.
+ *
+ * This is the drop-in boundary for the reference package `voxvid`'s render
+ * path.  The reference has no plugin registry: its boundary is the numba
+ * kernel call inside render.render_rays (pkg/src/voxvid/render.py:204-214)
+ * and its companion kernels.  Each entry point below names the reference
+ * interface it replaces.  All compute entry points run hand-written sm_100a
+ * CUDA kernels; there is no CPU fallback.  Every function returns 0 on
+ * success or a negative VV_E* code; vv_last_error() returns the message of
+ * the last failure on the calling thread.
+ *
+ * Pointers marked "device" are CUDA device pointers on the tree's device.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ * asynchronous with respect to the host unless stated otherwise.
+ */
+#ifndef VOXVID_B200_H
+#define VOXVID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VV_ABI_VERSION 1
+
+enum {
+    VV_OK = 0,
+    VV_E_INVALID = -1,  /* bad argument (the reference raises ValueError) */
+    VV_E_CUDA = -2,     /* CUDA runtime failure */
+    VV_E_NOMEM = -3,    /* device allocation failed */
+    VV_E_UNSUPPORTED = -4,
+    VV_E_FORMAT = -5,   /* .voct parse errors, see vv_voct_* */
+    VV_E_MAGIC = -6,
+    VV_E_VERSION = -7,
+    VV_E_TRUNCATED = -8,
+    VV_E_CHECKSUM = -9
+};
+
+typedef struct vv_tree vv_tree;    /* device replica of one VOctree */
+typedef struct vv_slice vv_slice;  /* per-frame slice cache (FrameSlice) */
+
+/* Host description of a VOctree: the arrays of voxvid.octree.VOctree
+ * (octree.py:84-108).  Pointers are HOST pointers for vv_tree_upload. */
+typedef struct {
+    int32_t depth;            /* leaf depth d >= 1 */
+    int32_t n_max;            /* HH truncation; K = sum_{n<=n_max} (n+1)^2 */
+    int32_t frames;           /* T */
+    int32_t coeff_count;      /* C */
+    int64_t n_internal;       /* rows of node_child */
+    int64_t n_leaves;         /* rows of leaf_data */
+    double bbox_lo[3];
+    double side;
+    const int32_t *node_child;  /* (n_internal, 8), BFS order, -1 = empty */
+    const float *leaf_data;     /* (n_leaves, 2C+3K) [w_sigma | w_gamma | w_hh] */
+    const float *basis_a;       /* (T, C) */
+    const float *basis_b;       /* (T, C) */
+    const float *edit_rgb;      /* (n_leaves, 4) or NULL (no edits) */
+    const int32_t *edit_t;      /* (n_leaves, 2) or NULL */
+} vv_tree_desc;
+
+/* RenderOptions (render.py:148-153) plus the ray-parameter clip that
+ * render_rays passes to render_kernel (tmin = 0, tmax = 1e30, render.py:212). */
+typedef struct {
+    double early_stop;   /* terminate once transmittance < early_stop */
+    double far_plane;    /* depth where alpha < alpha_floor */
+    double alpha_floor;
+    double edit_weight;
+    double tmin;
+    double tmax;
+} vv_render_opts;
+
+/* Pinhole camera (render.py:42-125): intrinsics in pixels, row-major c2w. */
+typedef struct {
+    int32_t width;
+    int32_t height;
+    double fx, fy, cx, cy;
+    double c2w[16];
+} vv_camera;
+
+/* One placed instance for vv_render_scene (compose.py:160-199, 418-440).
+ * mode 0 (rigid): rays are generated from the pulled-back camera pose
+ *   `pose` = inv(affine) @ c2w (compose.py:427-431).
+ * mode 1 (general affine): rays are generated from the scene camera and
+ *   pulled back per ray through `inv` = inv(affine) (compose.py:432-440). */
+typedef struct {
+    const vv_tree *tree;
+    int32_t frame;   /* local frame = timemap(global frame), host-resolved */
+    int32_t mode;
+    double pose[16]; /* mode 0 */
+    double inv[16];  /* mode 1 */
+} vv_instance;
+
+int vv_abi_version(void);
+const char *vv_last_error(void);
+int vv_device_count(int *count);
+
+/* Basis tables of kernels.basis_tables (kernels.py:56-76); host only, for
+ * parity checks of the constants.  sizes = {K, S, n_pairs}. */
+int vv_basis_tables(int n_max, int64_t *pair_n, int64_t *pair_l, double *pair_norm,
+                    int64_t *k2pair, int64_t *k2sh, double *sh_pref, int32_t *sizes);
+
+/* ---- tree replica --------------------------------------------------------
+ * Replaces: the implicit host arrays handed to render_kernel by
+ * render.render_rays (render.py:204-214) -- uploaded once per device.
+ * vv_tree_upload copies host arrays; vv_tree_bind takes a desc whose array
+ * pointers are DEVICE pointers (e.g. torch tensors) and copies on device.
+ * The replica owns its device memory either way.  Synchronous. */
+int vv_tree_upload(const vv_tree_desc *host, int device, vv_tree **out);
+int vv_tree_bind(const vv_tree_desc *dev, int device, vv_tree **out);
+int vv_tree_free(vv_tree *tree);
+int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, int32_t *depth,
+                 int32_t *frames, int64_t *device_bytes);
+
+/* ---- per-frame slice cache -----------------------------------------------
+ * Replaces build_frame_cache (render.py:170-179) -> build_slice_kernel
+ * (kernels.py:397-407).  sigma is float64 per leaf (bit-exact with the
+ * uncached path); the sliced SH coefficients are stored as fp32.
+ * Error: frame outside [0, T) -> VV_E_INVALID ("frame F out of range"). */
+int vv_slice_build(const vv_tree *tree, int32_t frame, void *stream, vv_slice **out);
+int vv_slice_free(vv_slice *slice);
+/* Copies the cache to caller device buffers: sigma (n_leaves) f64,
+ * q (n_leaves, 3S) f32. */
+int vv_slice_export(const vv_slice *slice, double *sigma, float *q, void *stream);
+int vv_slice_frame(const vv_slice *slice, int32_t *frame);
+
+/* ---- ray rendering -------------------------------------------------------
+ * Replaces render_rays (render.py:182-215) -> render_kernel
+ * (kernels.py:410-652).  origins/dirs: device (n, 3) f64, dirs unit length.
+ * Outputs (device): premult (n, 3) f64, alpha (n) f64, tbar (n) f64.
+ * Optional (NULL to skip): sample_count (n) i32 = leaf segments consumed
+ * up to and including the early-stop one (shade_forward's `used`,
+ * kernels.py:700-738); node_pops (n) i32 = internal-node pops; shaded (n)
+ * i32 = leaves with sigma > 0.  cache may be NULL (uncached).
+ * Errors: frame out of range; cache built for another frame. */
+int vv_render_rays(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                   const vv_render_opts *opts, const double *origins, const double *dirs,
+                   int64_t n, double *premult, double *alpha, double *tbar,
+                   int32_t *sample_count, int32_t *node_pops, int32_t *shaded, void *stream);
+
+/* Visited-leaf CSR for the same rays: visit_start (n+1) i64 device prefix
+ * sum of sample_count; writes visit_leaf[visit_start[r] + i] = leaf row of
+ * the i-th consumed segment of ray r (reference row ids). */
+int vv_render_rays_visits(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                          const vv_render_opts *opts, const double *origins,
+                          const double *dirs, int64_t n, const int64_t *visit_start,
+                          int64_t *visit_leaf, void *stream);
+
+/* ---- camera rendering ----------------------------------------------------
+ * Replaces render (render.py:236-240) = Camera.rays + render_rays +
+ * finalize_layer (render.py:218-233), fused into one kernel.  Outputs
+ * (device, fp32, row-major pixels): rgb (H, W, 3) unpremultiplied, alpha
+ * (H, W), depth (H, W) (far_plane where alpha < alpha_floor).  Any output
+ * may be NULL. */
+int vv_render_camera(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                     const vv_render_opts *opts, const vv_camera *cam, float *rgb,
+                     float *alpha, float *depth, void *stream);
+
+/* Tile-sharded variant for multi-GPU: renders only the square tiles of
+ * size `tile` whose linear index i (row-major over the tile grid) has
+ * i % n_shards == shard, writing them packed in tile order into `packed`
+ * as (n_my_tiles, tile*tile, 5) fp32 [r, g, b, alpha, depth]. */
+int vv_render_camera_tiles(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                           const vv_render_opts *opts, const vv_camera *cam, int32_t tile,
+                           int32_t shard, int32_t n_shards, float *packed, void *stream);
+/* Scatter packed tiles of every shard (shard-major, as all-gathered) into
+ * full images rgb (H, W, 3), alpha (H, W), depth (H, W). */
+int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int32_t tile,
+                    int32_t n_shards, float *rgb, float *alpha, float *depth, void *stream);
+
+/* ---- multi-instance scene -------------------------------------------------
+ * Replaces render_scene (compose.py:443-475) without lights: per pixel,
+ * every instance is rendered through its pulled-back ray (render_instance,
+ * compose.py:418-440), finalized, blended by Algorithm 1 in instance order
+ * (blend_layers, compose.py:373-406), unpremultiplied (compose.py:457-460)
+ * and composited over `background` (composite_background,
+ * render.py:243-251).  Outputs (device fp32): image (H, W, 3); optional
+ * blended alpha (H, W) and depth (H, W). */
+int vv_render_scene(const vv_instance *instances, int32_t n_instances,
+                    const vv_render_opts *opts, const vv_camera *cam, const double *background,
+                    float *image, float *alpha, float *depth, void *stream);
+
+/* ---- traversal only --------------------------------------------------------
+ * Replace count_segments_kernel / collect_segments_kernel
+ * (kernels.py:313-367) and VOctree.ray_segments (octree.py:296-326).
+ * Rays in world space (dirs need not be unit; t stays the world parameter). */
+int vv_count_segments(const vv_tree *tree, const double *origins, const double *dirs,
+                      int64_t n, double tmin, double tmax, int64_t *count, void *stream);
+int vv_collect_segments(const vv_tree *tree, const double *origins, const double *dirs,
+                        int64_t n, double tmin, double tmax, const int64_t *ray_start,
+                        int64_t *seg_leaf, double *seg_t0, double *seg_t1, void *stream);
+
+/* ---- .voct codec (host) ----------------------------------------------------
+ * Replaces the node-table loops of VOctree.to_bytes / from_bytes
+ * (octree.py:383-394, 440-455).  parse: reads n_internal BFS records
+ * (u8 mask + one u32 per set bit) starting at buf, writes node_child
+ * (n_internal, 8) and the byte length consumed; VV_E_TRUNCATED if the
+ * records run past len.  encode: writes into buf (capacity cap) and returns
+ * the bytes written in *used (pass buf = NULL to size). */
+int vv_voct_parse_nodes(const uint8_t *buf, size_t len, int64_t n_internal,
+                        int32_t *node_child, size_t *consumed);
+int vv_voct_encode_nodes(const int32_t *node_child, int64_t n_internal, uint8_t *buf,
+                         size_t cap, size_t *used);
+/* CRC-32 (zlib polynomial) of buf, continuing from crc. */
+uint32_t vv_crc32(uint32_t crc, const uint8_t *buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXVID_B200_H */

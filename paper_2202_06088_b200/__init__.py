@@ -1,0 +1,42 @@
+"""voxvid_b200 -- B200-native VOctree renderer (NeuVV, arXiv 2202.06088).
+
+Drop-in for the render path of the reference package ``voxvid``: the same
+module-level names (VOctree.load, render, render_rays, build_frame_cache,
+Camera, RenderOptions, LayerImages, Scene, SceneInstance, render_scene, ...)
+backed by hand-written sm_100a CUDA kernels in libvoxvid_b200.so.
+"""
+
+from .compose import Light, Scene, SceneInstance, TimeMap, blend_layers, duplicate, render_instance, render_scene
+from .octree import (
+    BadMagicError,
+    ChecksumError,
+    RaySegment,
+    TruncatedStreamError,
+    UnsupportedVersionError,
+    VOctree,
+    VoctError,
+)
+from .render import (
+    Camera,
+    FrameSlice,
+    LayerImages,
+    RenderOptions,
+    build_frame_cache,
+    collect_segments,
+    composite_background,
+    count_segments,
+    finalize_layer,
+    render,
+    render_into,
+    render_ray_visits,
+    render_rays,
+)
+from .temporal import TemporalBases, make_bump_bases
+
+__all__ = [
+    "VOctree", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
+    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into",
+    "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
+    "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
+    "render_instance", "render_scene", "duplicate", "TemporalBases", "make_bump_bases",
+]

@@ -1,0 +1,636 @@
+// vv_device.cuh -- device-side building blocks of the B200 VOctree renderer.
+//
+// One CUDA thread owns one ray.  The ray walks the BFS node table with the
+// reference's parametric near-to-far descent (kernels.py:171-310, 600-647)
+// and shades leaf segments as they are reached (kernels.py:539-599), so the
+// early-termination test also ends the tree walk.
+//
+// Numerics:
+//   * ray normalisation, plane crossings, sigma decode, transmittance, alpha
+//     and tbar are float64 with explicit round-to-nearest intrinsics (no FMA
+//     contraction) in the reference's operation order -> visited leaves,
+//     segment t values, sample counts and alpha are bit-exact with
+//     voxvid.kernels.render_kernel (modulo 1-ulp exp() differences);
+//   * the hyper-angle decode, HH radial profiles, SH basis, HH->SH slice and
+//     colour sigmoid run in fp32 (tolerance 1e-4 in the contract).
+//
+// Differences in mechanism (not in results) from the reference:
+//   * the stack holds only (node id, level, cell coords) -- 8 bytes -- in
+//     shared memory; a popped cell's [t_in, t_out] is recomputed from its six
+//     boundary planes.  Every boundary plane of a cell is a mid plane of an
+//     ancestor (or a root face), so the recomputed crossings are the very
+//     values the reference carried on its stack (proof sketch in DESIGN.md);
+//   * the nearest child continues in registers instead of push+pop, and the
+//     <= 4 leaves of a last-level node are shaded straight from registers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vv {
+
+constexpr int kMaxC = 64;       // max temporal basis count C supported on device
+constexpr int kMaxNmax = 3;     // HH truncation supported on device
+constexpr int kMaxDepth = 20;   // leaf depth supported on device
+constexpr int kNarrowDepth = 9; // depth <= 9 packs a stack entry in 8 bytes
+
+template <int NMAX> struct Basis {
+    static constexpr int S = (NMAX + 1) * (NMAX + 1);            // SH count
+    static constexpr int K = (NMAX + 1) * (NMAX + 2) * (2 * NMAX + 3) / 6;  // HH count
+    static constexpr int NPAIRS = (NMAX + 1) * (NMAX + 2) / 2;
+    static constexpr int HH4 = (3 * K + 3) / 4;                  // float4 per w_hh
+    static constexpr int Q4 = (3 * S + 3) / 4;                   // float4 per sliced q
+};
+
+// Constants of kernels.basis_tables (A_nl, SH prefactors), fp32.
+struct Consts {
+    float pair_norm[16];
+    float sh_pref[16];
+};
+
+// Device view of one uploaded tree.
+struct TreeView {
+    const int32_t *child;    // (n_internal, 8)
+    const float4 *sig;       // (n_leaves, sig4): w_sigma padded
+    const float4 *rest;      // (n_leaves, rest4): [w_gamma pad | w_hh pad]
+    const float4 *edit_rgb;  // (n_leaves) or null
+    const int2 *edit_t;      // (n_leaves) or null
+    const float *basis_a;    // (T, C)
+    const float *basis_b;    // (T, C)
+    double lo0, lo1, lo2, side;
+    int depth, C, sig4, rest4, hh_off4, frames, nmax;
+};
+
+struct SliceView {
+    const double *sigma;  // (n_leaves)
+    const float4 *q;      // (n_leaves, q4)
+    int q4;
+};
+
+// ------------------------------------------------------------ fp64 helpers
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+// Python builtin max/min of two floats (first argument wins ties)
+__device__ __forceinline__ double pmax(double a, double b) { return (b > a) ? b : a; }
+__device__ __forceinline__ double pmin(double a, double b) { return (b < a) ? b : a; }
+// exact 2^-k for 0 <= k <= 1022
+__device__ __forceinline__ double pow2neg(int k) {
+    return __longlong_as_double((long long)(1023 - k) << 52);
+}
+
+// ------------------------------------------------------------ ray setup
+// kernels.py:482-532 (== _collect_segments 180-236)
+struct Ray {
+    double o0, o1, o2, i0, i1, i2;
+    double rt_in, rt_out;
+    int mirror;
+};
+
+__device__ __forceinline__ bool ray_setup(const TreeView &T, double ox, double oy, double oz,
+                                          double dx, double dy, double dz, double tmin,
+                                          double tmax, Ray &r) {
+    double o0 = xdiv(xsub(ox, T.lo0), T.side);
+    double o1 = xdiv(xsub(oy, T.lo1), T.side);
+    double o2 = xdiv(xsub(oz, T.lo2), T.side);
+    double d0 = xdiv(dx, T.side);
+    double d1 = xdiv(dy, T.side);
+    double d2 = xdiv(dz, T.side);
+    int mirror = 0;
+    if (d0 < 0.0) { o0 = xsub(1.0, o0); d0 = -d0; mirror |= 1; }
+    if (d1 < 0.0) { o1 = xsub(1.0, o1); d1 = -d1; mirror |= 2; }
+    if (d2 < 0.0) { o2 = xsub(1.0, o2); d2 = -d2; mirror |= 4; }
+    bool ok = true;
+    double i0, i1, i2;
+    if (d0 < 1e-300) { if (o0 < 0.0 || o0 >= 1.0) ok = false; i0 = 1e300; } else i0 = xdiv(1.0, d0);
+    if (d1 < 1e-300) { if (o1 < 0.0 || o1 >= 1.0) ok = false; i1 = 1e300; } else i1 = xdiv(1.0, d1);
+    if (d2 < 1e-300) { if (o2 < 0.0 || o2 >= 1.0) ok = false; i2 = 1e300; } else i2 = xdiv(1.0, d2);
+    r.o0 = o0; r.o1 = o1; r.o2 = o2;
+    r.i0 = i0; r.i1 = i1; r.i2 = i2;
+    r.mirror = mirror;
+    if (!ok) return false;
+    r.rt_in = pmax(pmax(xmul(xsub(0.0, o0), i0), xmul(xsub(0.0, o1), i1)),
+                   pmax(xmul(xsub(0.0, o2), i2), tmin));
+    r.rt_out = pmin(pmin(xmul(xsub(1.0, o0), i0), xmul(xsub(1.0, o1), i1)),
+                    pmin(xmul(xsub(1.0, o2), i2), tmax));
+    return r.rt_in < r.rt_out;
+}
+
+// ------------------------------------------------------------ stack entries
+// narrow: ptr + (level | cx<<4 | cy<<13 | cz<<22), depth <= 9
+struct EntryN {
+    uint32_t ptr, code;
+    __device__ __forceinline__ static EntryN make(uint32_t p, int L, uint32_t x, uint32_t y, uint32_t z) {
+        EntryN e;
+        e.ptr = p;
+        e.code = (uint32_t)L | (x << 4) | (y << 13) | (z << 22);
+        return e;
+    }
+    __device__ __forceinline__ void get(uint32_t &p, int &L, uint32_t &x, uint32_t &y, uint32_t &z) const {
+        p = ptr;
+        L = (int)(code & 15u);
+        x = (code >> 4) & 511u;
+        y = (code >> 13) & 511u;
+        z = (code >> 22) & 511u;
+    }
+};
+// wide: depth <= 20
+struct __align__(16) EntryW {
+    uint32_t ptr, x, y, zl;
+    __device__ __forceinline__ static EntryW make(uint32_t p, int L, uint32_t x_, uint32_t y_, uint32_t z_) {
+        EntryW e;
+        e.ptr = p;
+        e.x = x_;
+        e.y = y_;
+        e.zl = z_ | ((uint32_t)L << 24);
+        return e;
+    }
+    __device__ __forceinline__ void get(uint32_t &p, int &L, uint32_t &x_, uint32_t &y_, uint32_t &z_) const {
+        p = ptr;
+        x_ = x;
+        y_ = y;
+        z_ = zl & 0xFFFFFFu;
+        L = (int)(zl >> 24);
+    }
+};
+
+__host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 : 3 * (depth - 1) + 1; }
+
+// ------------------------------------------------------------ traversal
+// Visitor interface:
+//   bool leaf(uint32_t row, double tin, double tout)  -> true = stop the ray
+//   void pop()                                         -> one internal-node pop
+template <class Entry, class Visitor>
+__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth,
+                                         const Ray &r, Entry *stk, int sstride, Visitor &vis) {
+    uint32_t ptr = 0, cx = 0, cy = 0, cz = 0;
+    int L = 0;
+    double tin = r.rt_in, tout = r.rt_out;
+    int top = 0;
+    const double o0 = r.o0, o1 = r.o1, o2 = r.o2, i0 = r.i0, i1 = r.i1, i2 = r.i2;
+    const int mirror = r.mirror;
+    while (true) {
+        vis.pop();
+        // mid-plane crossings of the current node (kernels.py:603-606)
+        const double hm = pow2neg(L + 1);
+        const double txm = xmul(xsub(xmul((double)(2u * cx + 1u), hm), o0), i0);
+        const double tym = xmul(xsub(xmul((double)(2u * cy + 1u), hm), o1), i1);
+        const double tzm = xmul(xsub(xmul((double)(2u * cz + 1u), hm), o2), i2);
+        int b = 0;
+        if (txm < tin) b |= 1;
+        if (tym < tin) b |= 2;
+        if (tzm < tin) b |= 4;
+        // walk the <= 4 pierced children near to far (kernels.py:614-638)
+        // step s covers [st[s], st[s+1]) in child sb[s]; at most 4 steps
+        // (each step sets one more bit; the reference loops until
+        // t_out >= node t_out, which happens by the 4th step for tmax < 1e301)
+        int sb[4];
+        double st[5];
+        int ns = 0;
+        bool walking = true;
+        st[0] = tin;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            sb[s] = b;
+            st[s + 1] = tout;
+            if (walking) {
+                const double tx = (b & 1) ? 1e301 : txm;
+                const double ty = (b & 2) ? 1e301 : tym;
+                const double tz = (b & 4) ? 1e301 : tzm;
+                const double tt = pmin(pmin(tx, ty), pmin(tz, tout));
+                st[s + 1] = tt;
+                ns = s + 1;
+                if (tt >= tout) {
+                    walking = false;
+                } else if (tx <= ty && tx <= tz) {
+                    b |= 1;
+                } else if (ty <= tz) {
+                    b |= 2;
+                } else {
+                    b |= 4;
+                }
+            }
+        }
+        // child pointers: independent loads
+        const int32_t *row = child + (size_t)ptr * 8u;
+        int32_t cp[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) cp[s] = (s < ns) ? __ldg(row + (sb[s] ^ mirror)) : -1;
+        int keep = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+            if (cp[s] >= 0 && st[s + 1] > st[s]) keep |= 1 << s;
+
+        if (L + 1 == depth) {
+            // children are leaf payload rows: shade near to far
+            bool stop = false;
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) {
+                if (keep & (1 << s)) {
+                    const int32_t lp = s == 0 ? cp[0] : s == 1 ? cp[1] : s == 2 ? cp[2] : cp[3];
+                    const double a = s == 0 ? st[0] : s == 1 ? st[1] : s == 2 ? st[2] : st[3];
+                    const double c = s == 0 ? st[1] : s == 1 ? st[2] : s == 2 ? st[3] : st[4];
+                    if (vis.leaf((uint32_t)lp, a, c)) { stop = true; break; }
+                }
+            }
+            if (stop) return;
+        } else if (keep) {
+            const int f = __ffs(keep) - 1;
+            // push the farther kept children far -> near (kernels.py:639-647)
+#pragma unroll
+            for (int s = 3; s >= 1; --s) {
+                if ((keep & (1 << s)) && s > f) {
+                    const int bs = sb[s];
+                    stk[top * sstride] = Entry::make((uint32_t)cp[s], L + 1, 2u * cx + (bs & 1),
+                                                     2u * cy + ((bs >> 1) & 1), 2u * cz + ((bs >> 2) & 1));
+                    ++top;
+                }
+            }
+            // continue with the nearest kept child in registers
+            const int bf = f == 0 ? sb[0] : f == 1 ? sb[1] : f == 2 ? sb[2] : sb[3];
+            const double a = f == 0 ? st[0] : f == 1 ? st[1] : f == 2 ? st[2] : st[3];
+            const double c = f == 0 ? st[1] : f == 1 ? st[2] : f == 2 ? st[3] : st[4];
+            ptr = (uint32_t)(f == 0 ? cp[0] : f == 1 ? cp[1] : f == 2 ? cp[2] : cp[3]);
+            cx = 2u * cx + (bf & 1);
+            cy = 2u * cy + ((bf >> 1) & 1);
+            cz = 2u * cz + ((bf >> 2) & 1);
+            ++L;
+            tin = a;
+            tout = c;
+            continue;
+        }
+        // pop the next pending cell; recompute its interval from its faces
+        if (top == 0) return;
+        --top;
+        stk[top * sstride].get(ptr, L, cx, cy, cz);
+        const double h = pow2neg(L);
+        const double xl = xmul((double)cx, h), xh = xmul((double)(cx + 1u), h);
+        const double yl = xmul((double)cy, h), yh = xmul((double)(cy + 1u), h);
+        const double zl = xmul((double)cz, h), zh = xmul((double)(cz + 1u), h);
+        tin = pmax(pmax(r.rt_in, xmul(xsub(xl, o0), i0)),
+                   pmax(xmul(xsub(yl, o1), i1), xmul(xsub(zl, o2), i2)));
+        tout = pmin(pmin(r.rt_out, xmul(xsub(xh, o0), i0)),
+                    pmin(xmul(xsub(yh, o1), i1), xmul(xsub(zh, o2), i2)));
+    }
+}
+
+// ------------------------------------------------------------ fp32 basis
+__device__ __forceinline__ float sigmoidf_(float x) {
+    if (x >= 0.0f) return __frcp_rn(1.0f + __expf(-x));
+    const float e = __expf(x);
+    return __fdiv_rn(e, 1.0f + e);
+}
+
+// Real SH stack at a unit direction, kernels.py:127-164 (fp32)
+template <int NMAX>
+__device__ __forceinline__ void sh_basis(float dx, float dy, float dz, const Consts &K, float *out) {
+    const float rxy = sqrtf(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)));
+    float cphi = 1.0f, sphi = 0.0f;
+    if (rxy > 0.0f) {
+        cphi = __fdiv_rn(dx, rxy);
+        sphi = __fdiv_rn(dy, rxy);
+    }
+    const float z = dz;
+    float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
+#pragma unroll
+    for (int mu = 0; mu <= NMAX; ++mu) {
+        if (mu > 0) {
+            const float ncm = cm * cphi - sm * sphi;
+            const float nsm = sm * cphi + cm * sphi;
+            cm = ncm;
+            sm = nsm;
+            pmm = pmm * (2.0f * mu - 1.0f) * rxy;
+        }
+        float p_prev = 0.0f, p = pmm;
+#pragma unroll
+        for (int l = mu; l <= NMAX; ++l) {
+            if (l == mu) {
+                p = pmm;
+            } else if (l == mu + 1) {
+                p_prev = p;
+                p = z * (2.0f * mu + 1.0f) * pmm;
+            } else {
+                const float np_ = (z * (float)(2 * l - 1) * p - (float)(l + mu - 1) * p_prev) / (float)(l - mu);
+                p_prev = p;
+                p = np_;
+            }
+            const int base = l * l + l;
+            if (mu == 0) {
+                out[base] = K.sh_pref[base] * p;
+            } else {
+                out[base + mu] = K.sh_pref[base + mu] * p * cm;
+                out[base - mu] = K.sh_pref[base - mu] * p * sm;
+            }
+        }
+    }
+}
+
+// Radial profiles A_nl sin^l(g) C^{l+1}_{n-l}(cos g), kernels.py:106-124 (fp32).
+// s = sigmoid(gamma_pre), gamma = pi * s, so sin/cos come from sincospi(s).
+template <int NMAX>
+__device__ __forceinline__ void radial(float s, const Consts &K, float *R) {
+    float sg, cg;
+    sincospif(s, &sg, &cg);
+    int p = 0;
+#pragma unroll
+    for (int n = 0; n <= NMAX; ++n) {
+#pragma unroll
+        for (int l = 0; l <= n; ++l) {
+            const int d = n - l;
+            const float alpha = (float)(l + 1);
+            float c = 1.0f;
+            if (d >= 1) {
+                float c_prev = 1.0f;
+                c = 2.0f * alpha * cg;
+#pragma unroll
+                for (int dd = 2; dd <= d; ++dd) {
+                    const float nc = (2.0f * cg * (float)(dd + l) * c - (float)(dd + 2 * l) * c_prev) / (float)dd;
+                    c_prev = c;
+                    c = nc;
+                }
+            }
+            float sl = 1.0f;
+#pragma unroll
+            for (int i = 0; i < l; ++i) sl *= sg;
+            R[p] = K.pair_norm[p] * sl * c;
+            ++p;
+        }
+    }
+}
+
+// HH->SH slice for one SH column j = (l, m): q_j,ch = sum_{n=l..NMAX}
+// R(n,l) * w_hh[k(n,l,m), ch]  (kernels.py:384-394, reordered per column;
+// pinned fp32 ops so cached and uncached renders agree bitwise).
+template <int NMAX>
+__device__ __forceinline__ void slice_col(const float *R, const float *wh, int l, int m, float &q0,
+                                          float &q1, float &q2) {
+    q0 = 0.0f;
+    q1 = 0.0f;
+    q2 = 0.0f;
+#pragma unroll
+    for (int n = 0; n <= NMAX; ++n) {
+        if (n >= l) {
+            const int kbase = n * (n + 1) * (2 * n + 1) / 6;  // sum_{n'<n} (n'+1)^2
+            const int k = kbase + l * l + (m + l);
+            const float rp = R[n * (n + 1) / 2 + l];
+            q0 = __fmaf_rn(rp, wh[3 * k + 0], q0);
+            q1 = __fmaf_rn(rp, wh[3 * k + 1], q1);
+            q2 = __fmaf_rn(rp, wh[3 * k + 2], q2);
+        }
+    }
+}
+
+// Decoded fp32 hyper-angle sigmoid s = sigmoid(B[t] . w_gamma) (fp32 dot).
+__device__ __forceinline__ float gamma_s(const float4 *__restrict__ rest_row, const float *sB, int C) {
+    float gp = 0.0f;
+    const int C4 = (C + 3) >> 2;
+#pragma unroll 4
+    for (int i = 0; i < C4; ++i) {
+        const float4 v = __ldg(rest_row + i);
+        const int c = 4 * i;
+        gp = __fmaf_rn(sB[c], v.x, gp);
+        if (c + 1 < C) gp = __fmaf_rn(sB[c + 1], v.y, gp);
+        if (c + 2 < C) gp = __fmaf_rn(sB[c + 2], v.z, gp);
+        if (c + 3 < C) gp = __fmaf_rn(sB[c + 3], v.w, gp);
+    }
+    return sigmoidf_(gp);
+}
+
+// sigma_pre = sum_c A[t,c] * w_sigma[c], float64, sequential (kernels.py:374-381)
+__device__ __forceinline__ double sigma_pre(const float4 *__restrict__ sig_row, const float *sA, int C) {
+    double sp = 0.0;
+    const int C4 = (C + 3) >> 2;
+#pragma unroll 4
+    for (int i = 0; i < C4; ++i) {
+        const float4 v = __ldg(sig_row + i);
+        const int c = 4 * i;
+        sp = xadd(sp, xmul((double)sA[c], (double)v.x));
+        if (c + 1 < C) sp = xadd(sp, xmul((double)sA[c + 1], (double)v.y));
+        if (c + 2 < C) sp = xadd(sp, xmul((double)sA[c + 2], (double)v.z));
+        if (c + 3 < C) sp = xadd(sp, xmul((double)sA[c + 3], (double)v.w));
+    }
+    return sp;
+}
+
+template <int NMAX>
+__device__ __forceinline__ void load_hh(const float4 *__restrict__ rest_row, int hh_off4, float *wh) {
+    constexpr int H4 = Basis<NMAX>::HH4;
+#pragma unroll
+    for (int i = 0; i < H4; ++i) {
+        const float4 v = __ldg(rest_row + hh_off4 + i);
+        wh[4 * i + 0] = v.x;
+        wh[4 * i + 1] = v.y;
+        wh[4 * i + 2] = v.z;
+        wh[4 * i + 3] = v.w;
+    }
+}
+
+// Full per-leaf slice (build_slice_kernel, kernels.py:397-407): sigma (f64)
+// and q (fp32, channel-interleaved 3S).
+template <int NMAX>
+__device__ __forceinline__ void slice_leaf(const TreeView &T, uint32_t row, const float *sA,
+                                           const float *sB, const Consts &K, double &sigma,
+                                           float *q) {
+    const double sp = sigma_pre(T.sig + (size_t)row * T.sig4, sA, T.C);
+    sigma = sp > 0.0 ? sp : 0.0;  // max(0.0, sp)
+    const float4 *rr = T.rest + (size_t)row * T.rest4;
+    const float s = gamma_s(rr, sB, T.C);
+    float R[Basis<NMAX>::NPAIRS];
+    radial<NMAX>(s, K, R);
+    float wh[4 * Basis<NMAX>::HH4];
+    load_hh<NMAX>(rr, T.hh_off4, wh);
+#pragma unroll
+    for (int l = 0; l <= NMAX; ++l)
+#pragma unroll
+        for (int m = -l; m <= l; ++m) {
+            const int j = l * l + l + m;
+            slice_col<NMAX>(R, wh, l, m, q[3 * j + 0], q[3 * j + 1], q[3 * j + 2]);
+        }
+}
+
+// ------------------------------------------------------------ shading visitor
+struct FrameCtx {
+    const float *sA;   // A[t] row in shared memory
+    const float *sB;   // B[t] row in shared memory
+    int frame;
+    double early_stop;
+    double edit_weight;
+};
+
+template <int NMAX, bool CACHED, bool EDITS, bool VISITS>
+struct Shader {
+    const TreeView &T;
+    const SliceView &S;
+    const FrameCtx &F;
+    const Consts &K;
+    float dx, dy, dz;
+    double trans, acc0, acc1, acc2, aacc, tacc;
+    int used, pops, shaded;
+    bool y_ready;
+    float y[Basis<NMAX>::S];
+    int64_t *visit;  // VISITS: this ray's slice of the CSR
+
+    __device__ __forceinline__ Shader(const TreeView &T_, const SliceView &S_, const FrameCtx &F_,
+                                      const Consts &K_, float dx_, float dy_, float dz_)
+        : T(T_), S(S_), F(F_), K(K_), dx(dx_), dy(dy_), dz(dz_), trans(1.0), acc0(0.0), acc1(0.0),
+          acc2(0.0), aacc(0.0), tacc(0.0), used(0), pops(0), shaded(0), y_ready(false), visit(nullptr) {}
+
+    __device__ __forceinline__ void pop() { ++pops; }
+
+    __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout) {
+        if (VISITS) visit[used] = (int64_t)L;
+        ++used;
+        double sigma;
+        if (CACHED) {
+            sigma = __ldg(S.sigma + L);
+        } else {
+            const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, F.sA, T.C);
+            sigma = sp > 0.0 ? sp : 0.0;
+        }
+        bool edited = false;
+        float4 erg = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (EDITS && T.edit_t != nullptr) {
+            const int2 et = __ldg(T.edit_t + L);
+            if (et.x <= F.frame && F.frame <= et.y) {
+                edited = true;
+                erg = __ldg(T.edit_rgb + L);
+                const double sd = (double)erg.w;
+                if (sd >= 0.0) sigma = sd;
+            }
+        }
+        if (sigma == 0.0) return false;  // zero optical depth (kernels.py:556-559)
+        ++shaded;
+        if (!y_ready) {
+            sh_basis<NMAX>(dx, dy, dz, K, y);
+            y_ready = true;
+        }
+        // colour: c_ch = sigmoid(sum_j y_j q_j,ch)
+        float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+        if (CACHED) {
+            constexpr int Q4 = Basis<NMAX>::Q4;
+            const float4 *qr = S.q + (size_t)L * S.q4;
+            float q[4 * Q4];
+#pragma unroll
+            for (int i = 0; i < Q4; ++i) {
+                const float4 v = __ldg(qr + i);
+                q[4 * i + 0] = v.x;
+                q[4 * i + 1] = v.y;
+                q[4 * i + 2] = v.z;
+                q[4 * i + 3] = v.w;
+            }
+#pragma unroll
+            for (int j = 0; j < Basis<NMAX>::S; ++j) {
+                c0 = __fmaf_rn(y[j], q[3 * j + 0], c0);
+                c1 = __fmaf_rn(y[j], q[3 * j + 1], c1);
+                c2 = __fmaf_rn(y[j], q[3 * j + 2], c2);
+            }
+        } else {
+            const float4 *rr = T.rest + (size_t)L * T.rest4;
+            const float s = gamma_s(rr, F.sB, T.C);
+            float R[Basis<NMAX>::NPAIRS];
+            radial<NMAX>(s, K, R);
+            float wh[4 * Basis<NMAX>::HH4];
+            load_hh<NMAX>(rr, T.hh_off4, wh);
+#pragma unroll
+            for (int l = 0; l <= NMAX; ++l)
+#pragma unroll
+                for (int m = -l; m <= l; ++m) {
+                    const int j = l * l + l + m;
+                    float q0, q1, q2;
+                    slice_col<NMAX>(R, wh, l, m, q0, q1, q2);
+                    c0 = __fmaf_rn(y[j], q0, c0);
+                    c1 = __fmaf_rn(y[j], q1, c1);
+                    c2 = __fmaf_rn(y[j], q2, c2);
+                }
+        }
+        double col0 = (double)sigmoidf_(c0);
+        double col1 = (double)sigmoidf_(c1);
+        double col2 = (double)sigmoidf_(c2);
+        if (EDITS && edited) {  // kernels.py:584-587
+            const double ew = F.edit_weight, om = xsub(1.0, ew);
+            col0 = xadd(xmul(ew, (double)erg.x), xmul(om, col0));
+            col1 = xadd(xmul(ew, (double)erg.y), xmul(om, col1));
+            col2 = xadd(xmul(ew, (double)erg.z), xmul(om, col2));
+        }
+        // front-to-back compositing, float64 (kernels.py:588-598)
+        const double delta = xsub(tout, tin);
+        const double e = exp(xmul(-sigma, delta));
+        const double a = xsub(1.0, e);
+        const double w = xmul(trans, a);
+        acc0 = xadd(acc0, xmul(w, col0));
+        acc1 = xadd(acc1, xmul(w, col1));
+        acc2 = xadd(acc2, xmul(w, col2));
+        aacc = xadd(aacc, w);
+        tacc = xadd(tacc, xmul(xmul(w, 0.5), xadd(tin, tout)));
+        trans = xmul(trans, e);
+        return trans < F.early_stop;
+    }
+};
+
+// Traversal-only visitors (count / collect, kernels.py:313-367)
+struct CountVisitor {
+    int64_t count = 0;
+    __device__ __forceinline__ void pop() {}
+    __device__ __forceinline__ bool leaf(uint32_t, double, double) { ++count; return false; }
+};
+struct CollectVisitor {
+    int64_t *leaf_out;
+    double *t0_out, *t1_out;
+    int64_t count, cap;
+    __device__ __forceinline__ void pop() {}
+    __device__ __forceinline__ bool leaf(uint32_t L, double a, double b) {
+        if (count < cap) {
+            leaf_out[count] = (int64_t)L;
+            t0_out[count] = a;
+            t1_out[count] = b;
+        }
+        ++count;
+        return false;
+    }
+};
+
+// ------------------------------------------------------------ camera rays
+// Camera.rays (render.py:74-83): pixel centre, d_cam = (x, y, 1),
+// d_world = R d_cam, normalised.  fp64.  The BLAS product of the reference
+// is not reproducible bit for bit across CPUs; parity for bit-exact visit
+// lists is therefore checked with host-generated rays (render_rays).
+struct CamView {
+    int width, height;
+    double fx, fy, cx, cy;
+    double r00, r01, r02, r10, r11, r12, r20, r21, r22;
+    double ox, oy, oz;
+};
+
+__device__ __forceinline__ void camera_ray(const CamView &c, int ix, int iy, double &dx, double &dy,
+                                           double &dz) {
+    const double x = xdiv(xsub(xadd((double)ix, 0.5), c.cx), c.fx);
+    const double y = xdiv(xsub(xadd((double)iy, 0.5), c.cy), c.fy);
+    const double w0 = __fma_rn(1.0, c.r02, __fma_rn(y, c.r01, xmul(x, c.r00)));
+    const double w1 = __fma_rn(1.0, c.r12, __fma_rn(y, c.r11, xmul(x, c.r10)));
+    const double w2 = __fma_rn(1.0, c.r22, __fma_rn(y, c.r21, xmul(x, c.r20)));
+    const double nrm = sqrt(xadd(xadd(xmul(w0, w0), xmul(w1, w1)), xmul(w2, w2)));
+    dx = xdiv(w0, nrm);
+    dy = xdiv(w1, nrm);
+    dz = xdiv(w2, nrm);
+}
+
+// finalize_layer (render.py:218-233) for one ray, fp64 -> fp32 outputs
+__device__ __forceinline__ void finalize(double p0, double p1, double p2, double alpha, double tbar,
+                                         double depth_scale, bool scaled, double alpha_floor,
+                                         double far_plane, float &r, float &g, float &b, float &a,
+                                         float &d) {
+    const double safe = alpha > 1e-300 ? alpha : 1e-300;
+    if (alpha > 0.0) {
+        r = (float)xdiv(p0, safe);
+        g = (float)xdiv(p1, safe);
+        b = (float)xdiv(p2, safe);
+    } else {
+        r = g = b = 0.0f;
+    }
+    double t = xdiv(tbar, safe);
+    if (scaled) t = xmul(t, depth_scale);
+    d = (float)(alpha >= alpha_floor ? t : far_plane);
+    a = (float)alpha;
+}
+
+}  // namespace vv

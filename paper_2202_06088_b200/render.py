@@ -1,0 +1,457 @@
+"""Volume rendering of one VOctree at a camera and frame index -- B200 path.
+
+Drop-in for the reference's ``voxvid.render`` (pkg/src/voxvid/render.py):
+``Camera``, ``LayerImages``, ``RenderOptions``, ``FrameSlice``,
+``render``, ``render_rays``, ``finalize_layer``, ``composite_background``
+and ``build_frame_cache`` keep their names, arguments, defaults and error
+behaviour (ValueError for a frame outside [0, T) or a cache built for
+another frame).  Every render runs the hand-written sm_100a kernels of
+libvoxvid_b200.so; there is no CPU fallback.
+
+Return types: ``render`` returns float32 numpy images by default
+(``out="torch"`` keeps them as CUDA tensors); ``render_rays`` returns
+float64 arrays like the reference -- numpy for numpy inputs, CUDA tensors
+for CUDA tensor inputs.  ``render`` fuses Camera.rays, the render kernel
+and finalize_layer into one launch; camera rays are generated on the GPU
+in float64 (they agree with the host's BLAS-built rays to <= 1 ulp; use
+``render_rays`` with host rays when bit-exact visit lists are required).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .device import replica, require_cuda, stream_ptr, torch_device
+
+__all__ = [
+    "Camera",
+    "LayerImages",
+    "RenderOptions",
+    "FrameSlice",
+    "render",
+    "render_into",
+    "render_rays",
+    "render_ray_visits",
+    "finalize_layer",
+    "composite_background",
+    "build_frame_cache",
+    "count_segments",
+    "collect_segments",
+]
+
+
+@dataclass(frozen=True)
+class Camera:
+    """Pinhole camera (render.py:42-125): pixel centres, +z forward, +y down."""
+
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    c2w: np.ndarray
+
+    def __post_init__(self):
+        if self.fx <= 0 or self.fy <= 0:
+            raise ValueError("focal lengths must be positive")
+        c2w = np.asarray(self.c2w, dtype=np.float64).reshape(4, 4)
+        object.__setattr__(self, "c2w", c2w)
+        r = c2w[:3, :3]
+        err = float(np.abs(r @ r.T - np.eye(3)).max())
+        if err > 1e-9:
+            raise ValueError(f"camera rotation not orthonormal: max deviation {err:.3e}")
+        if not np.allclose(c2w[3], [0, 0, 0, 1], atol=1e-12):
+            raise ValueError("camera pose must be a rigid transform (last row 0 0 0 1)")
+
+    @property
+    def origin(self) -> np.ndarray:
+        return self.c2w[:3, 3]
+
+    def rays(self):
+        """All pixel rays on the host, row-major, unit directions (render.py:74-83)."""
+        ix, iy = np.meshgrid(np.arange(self.width), np.arange(self.height), indexing="xy")
+        x = (ix + 0.5 - self.cx) / self.fx
+        y = (iy + 0.5 - self.cy) / self.fy
+        d_cam = np.stack([x, y, np.ones_like(x)], axis=-1).reshape(-1, 3)
+        d_world = d_cam @ self.c2w[:3, :3].T
+        d_world /= np.linalg.norm(d_world, axis=1, keepdims=True)
+        origins = np.broadcast_to(self.origin, d_world.shape).copy()
+        return origins, np.ascontiguousarray(d_world)
+
+    def pixel_rays(self, ix, iy):
+        ix = np.asarray(ix, dtype=np.float64)
+        iy = np.asarray(iy, dtype=np.float64)
+        x = (ix + 0.5 - self.cx) / self.fx
+        y = (iy + 0.5 - self.cy) / self.fy
+        d_cam = np.stack([x, y, np.ones_like(x)], axis=-1)
+        d_world = d_cam @ self.c2w[:3, :3].T
+        d_world /= np.linalg.norm(d_world, axis=-1, keepdims=True)
+        origins = np.broadcast_to(self.origin, d_world.shape).copy()
+        return origins.reshape(-1, 3), np.ascontiguousarray(d_world.reshape(-1, 3))
+
+    @staticmethod
+    def look_at(eye, target, up=(0.0, 0.0, 1.0), width=128, height=128, focal=None, cx=None, cy=None) -> "Camera":
+        eye = np.asarray(eye, dtype=np.float64)
+        target = np.asarray(target, dtype=np.float64)
+        fwd = target - eye
+        fwd /= np.linalg.norm(fwd)
+        upv = np.asarray(up, dtype=np.float64)
+        right = np.cross(fwd, upv)
+        if np.linalg.norm(right) < 1e-12:
+            upv = np.array([0.0, 1.0, 0.0])
+            right = np.cross(fwd, upv)
+        right /= np.linalg.norm(right)
+        down = np.cross(fwd, right)
+        c2w = np.eye(4)
+        c2w[:3, 0] = right
+        c2w[:3, 1] = down
+        c2w[:3, 2] = fwd
+        c2w[:3, 3] = eye
+        focal = float(focal) if focal is not None else 1.2 * max(width, height)
+        return Camera(width=width, height=height, fx=focal, fy=focal,
+                      cx=width / 2.0 if cx is None else cx, cy=height / 2.0 if cy is None else cy, c2w=c2w)
+
+    def desc(self) -> _native.CameraDesc:
+        d = _native.CameraDesc()
+        d.width = int(self.width)
+        d.height = int(self.height)
+        d.fx, d.fy, d.cx, d.cy = float(self.fx), float(self.fy), float(self.cx), float(self.cy)
+        flat = np.ascontiguousarray(self.c2w, dtype=np.float64).reshape(16)
+        for i in range(16):
+            d.c2w[i] = float(flat[i])
+        return d
+
+
+@dataclass
+class LayerImages:
+    """One rendered layer: unpremultiplied rgb, alpha matte, expected depth (render.py:128-145)."""
+
+    rgb: object
+    alpha: object
+    depth: object
+
+    def __post_init__(self):
+        if tuple(self.rgb.shape[:2]) != tuple(self.alpha.shape) or tuple(self.alpha.shape) != tuple(self.depth.shape):
+            raise ValueError("layer channel shapes disagree")
+
+    @property
+    def shape(self):
+        return tuple(self.alpha.shape)
+
+    def copy(self) -> "LayerImages":
+        c = (lambda x: x.clone()) if hasattr(self.rgb, "clone") else (lambda x: x.copy())
+        return LayerImages(c(self.rgb), c(self.alpha), c(self.depth))
+
+
+@dataclass(frozen=True)
+class RenderOptions:
+    early_stop: float = 1e-4
+    far_plane: float = 1e9
+    alpha_floor: float = 1e-3
+    edit_weight: float = 1.0
+
+    def c_struct(self, tmin: float = 0.0, tmax: float = 1e30) -> _native.RenderOpts:
+        o = _native.RenderOpts()
+        o.early_stop = float(self.early_stop)
+        o.far_plane = float(self.far_plane)
+        o.alpha_floor = float(self.alpha_floor)
+        o.edit_weight = float(self.edit_weight)
+        o.tmin = float(tmin)
+        o.tmax = float(tmax)
+        return o
+
+
+class FrameSlice:
+    """Per-frame device cache: sigma (f64) and sliced SH coefficients (fp32) per leaf.
+
+    Built by build_frame_cache (render.py:170-179); renders with and
+    without it are bitwise equal.  ``sigma`` (n_leaves,) float64 and ``q``
+    (n_leaves, 3S) float32 are exported lazily as CUDA tensors.
+    """
+
+    def __init__(self, frame: int, handle, rep, device):
+        self.frame = int(frame)
+        self._handle = handle
+        self._rep = rep
+        self._device = device
+        self._sigma = None
+        self._q = None
+
+    def _export(self):
+        torch = require_cuda()
+        n = self._rep.n_leaves
+        self._sigma = torch.empty(n, dtype=torch.float64, device=self._device)
+        self._q = torch.empty((n, 3 * self._rep.s), dtype=torch.float32, device=self._device)
+        _native.check(_native.lib().vv_slice_export(self._handle, self._sigma.data_ptr(), self._q.data_ptr(),
+                                                    stream_ptr(self._device)))
+
+    @property
+    def sigma(self):
+        if self._sigma is None:
+            self._export()
+        return self._sigma
+
+    @property
+    def q(self):
+        if self._q is None:
+            self._export()
+        return self._q
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                _native.lib().vv_slice_free(h)
+            except Exception:
+                pass
+            self._handle = None
+
+
+def _frame_index(frame) -> int:
+    if isinstance(frame, (float, np.floating)) and not float(frame).is_integer():
+        return int(round(float(frame)))  # continuous t -> nearest frame
+    return int(frame)
+
+
+def _check_frame(tree, frame: int):
+    frames = tree.bases.frames if hasattr(tree, "bases") else tree.frames
+    if not (0 <= frame < frames):
+        raise ValueError(f"frame {frame} out of range [0, {frames})")
+
+
+def _check_cache(cache, frame, rep):
+    if cache is None:
+        return None
+    if not isinstance(cache, FrameSlice):
+        raise TypeError("cache must be a FrameSlice from build_frame_cache")
+    if cache.frame != frame:
+        raise ValueError(f"cache built for frame {cache.frame}, not {frame}")
+    if cache._rep is not rep:
+        raise ValueError("cache was built for a different tree or device")
+    return cache._handle
+
+
+def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
+    frame = _frame_index(frame)
+    _check_frame(tree, frame)
+    dev = torch_device(device)
+    rep = replica(tree, dev)
+    handle = ctypes.c_void_p()
+    _native.check(_native.lib().vv_slice_build(rep.handle, frame, stream_ptr(dev), ctypes.byref(handle)))
+    return FrameSlice(frame, handle, rep, dev)
+
+
+def _as_device_rays(x, dev):
+    torch = require_cuda()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=dev, dtype=torch.float64)
+        return t.reshape(-1, 3).contiguous(), True
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1, 3))
+    return torch.from_numpy(a).to(dev, non_blocking=False), False
+
+
+def render_rays(tree, origins, dirs, frame: int, opts: RenderOptions = RenderOptions(), cache=None, *,
+                device=None, stats: bool = False):
+    """Raw per-ray accumulators (premult, alpha, tbar), float64 (render.py:182-215).
+
+    With ``stats=True`` also returns a dict of per-ray int32 counters:
+    ``sample_count`` (leaf segments consumed up to and including the
+    early-stop one), ``node_pops`` and ``shaded``.
+    """
+    torch = require_cuda()
+    frame = _frame_index(frame)
+    _check_frame(tree, frame)
+    if cache is not None and getattr(cache, "frame", frame) != frame:
+        raise ValueError(f"cache built for frame {cache.frame}, not {frame}")
+    dev = torch_device(device if device is not None else (origins.device if isinstance(origins, torch.Tensor) else None))
+    rep = replica(tree, dev)
+    ch = _check_cache(cache, frame, rep)
+    o, on_dev = _as_device_rays(origins, dev)
+    d, _ = _as_device_rays(dirs, dev)
+    n = o.shape[0]
+    premult = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    alpha = torch.empty(n, dtype=torch.float64, device=dev)
+    tbar = torch.empty(n, dtype=torch.float64, device=dev)
+    counters = None
+    if stats:
+        counters = {k: torch.empty(n, dtype=torch.int32, device=dev) for k in ("sample_count", "node_pops", "shaded")}
+    oc = opts.c_struct()
+    _native.check(_native.lib().vv_render_rays(
+        rep.handle, frame, ch, ctypes.byref(oc), o.data_ptr(), d.data_ptr(), n,
+        premult.data_ptr(), alpha.data_ptr(), tbar.data_ptr(),
+        counters["sample_count"].data_ptr() if stats else None,
+        counters["node_pops"].data_ptr() if stats else None,
+        counters["shaded"].data_ptr() if stats else None,
+        stream_ptr(dev)))
+    if on_dev:
+        out = (premult, alpha, tbar)
+        return out + (counters,) if stats else out
+    out = (premult.cpu().numpy(), alpha.cpu().numpy(), tbar.cpu().numpy())
+    if stats:
+        return out + ({k: v.cpu().numpy() for k, v in counters.items()},)
+    return out
+
+
+def render_ray_visits(tree, origins, dirs, frame: int, opts: RenderOptions = RenderOptions(), cache=None, *,
+                      device=None):
+    """Visited-leaf lists (reference row ids) for each ray, as CSR.
+
+    Returns (sample_count (n,) int32, visit_start (n+1,) int64, visit_leaf
+    (sum,) int64) as numpy arrays; visit_leaf[visit_start[r]:visit_start[r+1]]
+    are the leaves ray r consumed, near to far, up to and including the
+    early-stop one (the reference's seg_leaf[start:start+used],
+    train.py:269-296).
+    """
+    torch = require_cuda()
+    frame = _frame_index(frame)
+    _check_frame(tree, frame)
+    dev = torch_device(device)
+    rep = replica(tree, dev)
+    ch = _check_cache(cache, frame, rep)
+    o, _ = _as_device_rays(origins, dev)
+    d, _ = _as_device_rays(dirs, dev)
+    n = o.shape[0]
+    _, _, _, st = render_rays(tree, o, d, frame, opts, cache, device=dev, stats=True)
+    used = st["sample_count"]
+    start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    if n:
+        start[1:] = torch.cumsum(used.to(torch.int64), 0)
+    total = int(start[-1].item()) if n else 0
+    leaf = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    oc = opts.c_struct()
+    if n:
+        _native.check(_native.lib().vv_render_rays_visits(
+            rep.handle, frame, ch, ctypes.byref(oc), o.data_ptr(), d.data_ptr(), n, start.data_ptr(),
+            leaf.data_ptr(), stream_ptr(dev)))
+    return used.cpu().numpy(), start.cpu().numpy(), leaf[:total].cpu().numpy()
+
+
+def finalize_layer(premult, alpha, tbar, shape, opts: RenderOptions, depth_scale=None) -> LayerImages:
+    """LayerImages from raw accumulators (render.py:218-233), float64 numpy."""
+    h, w = shape
+    premult = np.asarray(premult, dtype=np.float64)
+    alpha = np.asarray(alpha, dtype=np.float64)
+    tbar = np.asarray(tbar, dtype=np.float64)
+    alpha_img = alpha.reshape(h, w)
+    safe = np.maximum(alpha, 1e-300)[:, None]
+    rgb = np.where(alpha[:, None] > 0.0, premult / safe, 0.0).reshape(h, w, 3)
+    t = tbar / np.maximum(alpha, 1e-300)
+    if depth_scale is not None:
+        t = t * depth_scale
+    depth = np.where(alpha >= opts.alpha_floor, t, opts.far_plane).reshape(h, w)
+    return LayerImages(rgb=rgb, alpha=alpha_img, depth=depth)
+
+
+def render_into(tree, cam: Camera, frame: int, rgb, alpha, depth, opts: RenderOptions = RenderOptions(),
+                cache=None, *, stream=None):
+    """Render into caller-owned CUDA float32 tensors (rgb (H,W,3), alpha/depth (H,W); any may be None).
+
+    The allocation-free device path used by the benchmark; asynchronous on
+    the current (or given) stream.
+    """
+    frame = _frame_index(frame)
+    _check_frame(tree, frame)
+    ref = next(x for x in (rgb, alpha, depth) if x is not None)
+    dev = ref.device
+    rep = replica(tree, dev)
+    ch = _check_cache(cache, frame, rep)
+    oc = opts.c_struct()
+    cd = cam.desc()
+    s = int(stream.cuda_stream) if stream is not None else stream_ptr(dev)
+    _native.check(_native.lib().vv_render_camera(
+        rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd),
+        rgb.data_ptr() if rgb is not None else None,
+        alpha.data_ptr() if alpha is not None else None,
+        depth.data_ptr() if depth is not None else None, s))
+
+
+def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(), cache=None, *,
+           out: str = "numpy", device=None) -> LayerImages:
+    """Render one VOctree (render.py:236-240): rays + render + finalize in one kernel."""
+    torch = require_cuda()
+    frame = _frame_index(frame)
+    _check_frame(tree, frame)
+    if cache is not None and getattr(cache, "frame", frame) != frame:
+        raise ValueError(f"cache built for frame {cache.frame}, not {frame}")
+    dev = torch_device(device)
+    h, w = int(cam.height), int(cam.width)
+    buf = torch.empty(5 * h * w, dtype=torch.float32, device=dev)
+    rgb = buf[: 3 * h * w].view(h, w, 3)
+    alpha = buf[3 * h * w: 4 * h * w].view(h, w)
+    depth = buf[4 * h * w:].view(h, w)
+    render_into(tree, cam, frame, rgb, alpha, depth, opts, cache)
+    if out == "torch":
+        return LayerImages(rgb, alpha, depth)
+    host = torch.empty(5 * h * w, dtype=torch.float32, pin_memory=True)
+    host.copy_(buf, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    a = host.numpy()
+    return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
+                       a[4 * h * w:].reshape(h, w))
+
+
+def composite_background(layer: LayerImages, bg) -> np.ndarray:
+    """alpha * rgb + (1 - alpha) * bg (render.py:243-251)."""
+    rgb = layer.rgb
+    if hasattr(rgb, "cpu"):
+        rgb = rgb.cpu().numpy()
+    alpha = layer.alpha.cpu().numpy() if hasattr(layer.alpha, "cpu") else layer.alpha
+    bg = np.asarray(bg, dtype=np.float64)
+    if bg.ndim == 1:
+        bg = np.broadcast_to(bg, rgb.shape)
+    if bg.shape != rgb.shape:
+        raise ValueError(f"background shape {bg.shape} != layer shape {rgb.shape}")
+    a = np.asarray(alpha)[..., None]
+    return a * rgb + (1.0 - a) * bg
+
+
+def _seg_rays(tree, origins, dirs, dev):
+    o, _ = _as_device_rays(origins, dev)
+    d, _ = _as_device_rays(dirs, dev)
+    return o, d
+
+
+def count_segments(tree, origins, dirs, tmin: float = 0.0, tmax: float = 1e30, *, device=None) -> np.ndarray:
+    """Leaf segments per ray without early stop (count_segments_kernel, kernels.py:313-335)."""
+    torch = require_cuda()
+    dev = torch_device(device)
+    rep = replica(tree, dev)
+    o, d = _seg_rays(tree, origins, dirs, dev)
+    n = o.shape[0]
+    cnt = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    _native.check(_native.lib().vv_count_segments(rep.handle, o.data_ptr(), d.data_ptr(), n, float(tmin),
+                                                  float(tmax), cnt.data_ptr(), stream_ptr(dev)))
+    return cnt[:n].cpu().numpy()
+
+
+def collect_segments(tree, origins, dirs, tmin: float = 0.0, tmax: float = 1e30, *, device=None):
+    """CSR of all leaf segments per ray (collect_segments_kernel, kernels.py:338-367).
+
+    Returns (ray_start (n+1,), seg_leaf, seg_t0, seg_t1) numpy arrays.
+    """
+    torch = require_cuda()
+    dev = torch_device(device)
+    rep = replica(tree, dev)
+    o, d = _seg_rays(tree, origins, dirs, dev)
+    n = o.shape[0]
+    cnt = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    lib = _native.lib()
+    s = stream_ptr(dev)
+    _native.check(lib.vv_count_segments(rep.handle, o.data_ptr(), d.data_ptr(), n, float(tmin), float(tmax),
+                                        cnt.data_ptr(), s))
+    start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    if n:
+        start[1:] = torch.cumsum(cnt[:n], 0)
+    total = int(start[-1].item()) if n else 0
+    leaf = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    t0 = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    t1 = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    if n:
+        _native.check(lib.vv_collect_segments(rep.handle, o.data_ptr(), d.data_ptr(), n, float(tmin), float(tmax),
+                                              start.data_ptr(), leaf.data_ptr(), t0.data_ptr(), t1.data_ptr(), s))
+    return (start.cpu().numpy(), leaf[:total].cpu().numpy(), t0[:total].cpu().numpy(), t1[:total].cpu().numpy())

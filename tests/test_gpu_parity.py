@@ -1,0 +1,271 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.
+
+Contract (BASELINE.json north_star): visited-leaf indices and per-ray sample
+counts bit-exact; RGB/alpha/depth within 1e-4 absolute.  Segment lists
+(leaf, t_in, t_out) are bit-exact as well.  alpha/tbar are float64 with the
+reference's operation order; they are compared at 1e-12 (CUDA exp() may
+differ from glibc by 1 ulp).
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import camera_from, load, tree_from
+from oracle import oracle
+import paper_2202_06088_b200 as vv
+from paper_2202_06088_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _exact(a, b, what=""):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    assert np.array_equal(a, b), f"{what}: {np.count_nonzero(a != b)} mismatches"
+
+
+def _check_rays(tree, o, d, frame, g, prefix="", early_stop=1e-4):
+    opts = vv.RenderOptions(early_stop=early_stop)
+    p, a, t, st = vv.render_rays(tree, o, d, frame, opts, stats=True)
+    assert np.abs(a - g[prefix + "alpha"]).max() <= 1e-12
+    assert np.abs(t - g[prefix + "tbar"]).max() <= 1e-9
+    assert np.abs(p - g[prefix + "premult"]).max() <= TOL
+    if prefix + "used" in g:
+        _exact(st["sample_count"], g[prefix + "used"], "sample counts")
+        used, start, leaf = vv.render_ray_visits(tree, o, d, frame, opts)
+        _exact(used, g[prefix + "used"], "visit counts")
+        _exact(start, g[prefix + "visit_start"], "visit starts")
+        _exact(leaf, g[prefix + "visit_leaf"], "visited leaves")
+    return p, a, t, st
+
+
+@pytest.mark.parametrize("tag,es", [("nostop", 0.0), ("stop", 1e-4)])
+def test_scalar_case(cuda, tag, es):
+    g = load("scalar_d2")
+    _check_rays(tree_from(g), g["origins"], g["dirs"], int(g["frame"]), g, f"{tag}_", es)
+
+
+@pytest.mark.parametrize("tag,es", [("nostop", 0.0), ("stop", 1e-4)])
+def test_edge_rays(cuda, tag, es):
+    g = load("edge_d4")
+    _check_rays(tree_from(g), g["origins"], g["dirs"], 1, g, f"{tag}_", es)
+
+
+@pytest.mark.parametrize("clip", [False, True])
+def test_segments_bit_exact(cuda, clip):
+    g = load("edge_d4")
+    tree = tree_from(g)
+    args = (0.3, 1.7) if clip else (0.0, 1e30)
+    start, leaf, t0, t1 = vv.collect_segments(tree, g["origins"], g["dirs"], *args)
+    p = "clip_" if clip else ""
+    _exact(start, g[p + "seg_start"], "starts")
+    _exact(leaf, g[p + "seg_leaf"], "leaves")
+    _exact(t0, g[p + "seg_t0"], "t0")
+    _exact(t1, g[p + "seg_t1"], "t1")
+    cnt = vv.count_segments(tree, g["origins"], g["dirs"], *args)
+    _exact(cnt, np.diff(g[p + "seg_start"]), "counts")
+
+
+def test_ray_segments_api(cuda):
+    g = load("scalar_d2")
+    tree = tree_from(g)
+    o, d = g["origins"], g["dirs"]
+    for r in range(len(o)):
+        segs = tree.ray_segments(o[r], d[r])
+        s0, s1 = g["seg_start"][r], g["seg_start"][r + 1]
+        assert [s.leaf for s in segs] == list(g["seg_leaf"][s0:s1])
+        assert [s.t_enter for s in segs] == list(g["seg_t0"][s0:s1])
+
+
+@pytest.mark.parametrize("frame", [0, 2])
+def test_cache_bitwise_and_slice(cuda, frame):
+    g = load("cache_d3")
+    tree = tree_from(g)
+    o, d = g["origins"], g["dirs"]
+    p, a, t, st = _check_rays(tree, o, d, frame, g, f"f{frame}_")
+    cache = vv.build_frame_cache(tree, frame)
+    pc, ac, tc, stc = vv.render_rays(tree, o, d, frame, cache=cache, stats=True)
+    _exact(pc, p, "cached premult")
+    _exact(ac, a, "cached alpha")
+    _exact(tc, t, "cached tbar")
+    _exact(stc["sample_count"], st["sample_count"], "cached counts")
+    _exact(cache.sigma.cpu().numpy(), g[f"f{frame}_slice_sigma"], "slice sigma")
+    assert np.abs(cache.q.cpu().numpy() - g[f"f{frame}_slice_q"]).max() < 1e-5
+    cam = camera_from(g)
+    plain = vv.render(tree, cam, frame)
+    cached = vv.render(tree, cam, frame, cache=cache)
+    for x, y in zip((plain.rgb, plain.alpha, plain.depth), (cached.rgb, cached.alpha, cached.depth)):
+        _exact(x, y, "cached image")
+    assert np.abs(plain.rgb - g[f"f{frame}_rgb"]).max() < TOL
+    assert np.abs(plain.alpha - g[f"f{frame}_alpha_img"]).max() < TOL
+    hit = g[f"f{frame}_alpha_img"] >= 1e-3
+    assert np.abs(plain.depth[hit] - g[f"f{frame}_depth"][hit]).max() < TOL
+    assert np.all(plain.depth[~hit] == 1e9)
+
+
+def test_cache_frame_mismatch(cuda):
+    g = load("cache_d3")
+    tree = tree_from(g)
+    cache = vv.build_frame_cache(tree, 0)
+    with pytest.raises(ValueError, match="cache built for frame 0"):
+        vv.render_rays(tree, g["origins"], g["dirs"], 2, cache=cache)
+
+
+def test_frame_out_of_range(cuda):
+    g = load("cache_d3")
+    tree = tree_from(g)
+    with pytest.raises(ValueError, match="frame 99"):
+        vv.render(tree, camera_from(g), 99)
+    with pytest.raises(ValueError, match="out of range"):
+        vv.build_frame_cache(tree, -1)
+
+
+def test_config1(cuda):
+    g = load("cfg1")
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    _check_rays(tree, g["origins"], g["dirs"], int(g["frame"]), g)
+    cam = synthetic.bench_camera(64, 64)
+    layer = vv.render(tree, cam, int(g["frame"]))
+    assert np.abs(layer.rgb - g["rgb"]).max() < TOL
+    assert np.abs(layer.alpha - g["alpha_img"]).max() < TOL
+    hit = g["alpha_img"] >= 1e-3
+    assert np.abs(layer.depth[hit] - g["depth"][hit]).max() < TOL
+    start, leaf, t0, t1 = vv.collect_segments(tree, g["origins"], g["dirs"])
+    _exact(leaf, g["seg_leaf"])
+    _exact(t0, g["seg_t0"])
+
+
+@pytest.mark.parametrize("frame", [0, 2])
+@pytest.mark.parametrize("ew", [1.0, 0.4])
+def test_edits(cuda, frame, ew):
+    g = load("edits_d3")
+    tree = tree_from(g)
+    p, a, t = vv.render_rays(tree, g["origins"], g["dirs"], frame, vv.RenderOptions(edit_weight=ew))
+    pre = f"f{frame}_w{int(ew * 10)}_"
+    assert np.abs(a - g[pre + "alpha"]).max() <= 1e-12
+    assert np.abs(t - g[pre + "tbar"]).max() <= 1e-9
+    assert np.abs(p - g[pre + "premult"]).max() <= TOL
+
+
+@pytest.mark.parametrize("n_max", [0, 3])
+def test_other_truncations(cuda, n_max):
+    g = load(f"nmax{n_max}")
+    _check_rays(tree_from(g), g["origins"], g["dirs"], int(g["frame"]), g)
+
+
+def test_scene_against_reference(cuda):
+    g = load("scene")
+    ta, tb = tree_from(g, "ta_"), tree_from(g, "tb_")
+    cam = camera_from(g)
+
+    def tr(x, y, z):
+        m = np.eye(4)
+        m[:3, 3] = [x, y, z]
+        return m
+
+    scale = np.diag([1.3, 1.3, 1.3, 1.0]) @ tr(-0.3, 0.1, 0.0)
+    insts = [
+        vv.SceneInstance(name="a", tree=ta, affine=tr(0.0, 0.0, 0.0)),
+        vv.SceneInstance(name="b", tree=tb, affine=tr(1.2, 0.3, 0.0), timemap=vv.TimeMap.parse("shift(2)")),
+        vv.SceneInstance(name="c", tree=ta, affine=scale, timemap=vv.TimeMap.parse("reverse")),
+        vv.SceneInstance(name="d", tree=tb, affine=tr(-1.1, 0.4, 0.2), yaw_rate=15.0),
+    ]
+    scene = vv.Scene(instances=insts, background=np.array([0.1, 0.12, 0.2]))
+    for gf in (0, 3):
+        img = vv.render_scene(scene, cam, gf)
+        assert np.abs(img - g[f"g{gf}_image"]).max() < TOL
+        img2, blended, layers = vv.render_scene(scene, cam, gf, want_layers=True)
+        assert np.abs(img2 - g[f"g{gf}_image"]).max() < TOL
+        for i, l in enumerate(layers):
+            assert np.abs(np.asarray(l.alpha) - g[f"g{gf}_layer{i}_alpha"]).max() < TOL
+    single = vv.Scene(instances=[insts[2]], background=np.array([0.1, 0.12, 0.2]))
+    assert np.abs(vv.render_scene(single, cam, 1) - g["single_image"]).max() < TOL
+
+
+@pytest.mark.parametrize("depth,fill,seed", [(5, 0.3, 1), (6, 0.05, 2), (4, 0.9, 3)])
+def test_random_trees_vs_oracle(cuda, depth, fill, seed):
+    rng = np.random.default_rng(seed)
+    res = 1 << depth
+    coords = np.argwhere(rng.random((res, res, res)) < fill)
+    k = 14
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 7 + 3 * k)).astype(np.float32)
+    data[:, 0] = rng.uniform(0.5, 60.0, len(coords))
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(5, 7), 2, depth=depth)
+    n = 4000
+    o = rng.uniform(-1.0, 2.0, (n, 3))
+    tgt = rng.uniform(0.1, 0.9, (n, 3))
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ref = oracle.render_rays(tree, o, d, 3, visits=True)
+    used, start, leaf = vv.render_ray_visits(tree, o, d, 3)
+    _exact(used, ref["used"])
+    _exact(leaf, ref["visit_leaf"])
+    p, a, t, st = vv.render_rays(tree, o, d, 3, stats=True)
+    _exact(st["node_pops"], ref["pops"], "node pops")
+    _exact(st["shaded"], ref["shaded"], "shaded")
+    assert np.abs(a - ref["alpha"]).max() <= 1e-12
+    assert np.abs(p - ref["premult"]).max() <= TOL
+
+
+def test_deep_tree_wide_stack(cuda):
+    """depth 11 (> 9) exercises the 16-byte stack entries."""
+    rng = np.random.default_rng(9)
+    depth = 11
+    res = 1 << depth
+    centers = rng.integers(0, res - 64, (6, 3))
+    coords = np.unique(np.concatenate([c + rng.integers(0, 64, (3000, 3)) for c in centers]), axis=0)
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 3 + 3 * 5)).astype(np.float32)
+    data[:, 0] = rng.uniform(100.0, 3000.0, len(coords))
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(4, 3), 1, depth=depth)
+    n = 3000
+    o = rng.uniform(-0.5, 1.5, (n, 3))
+    tgt = (centers[rng.integers(0, 6, n)] + 32) / res
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ref = oracle.render_rays(tree, o, d, 1, visits=True)
+    used, start, leaf = vv.render_ray_visits(tree, o, d, 1)
+    assert ref["used"].sum() > 1000
+    _exact(used, ref["used"])
+    _exact(leaf, ref["visit_leaf"])
+    start_g, leaf_g, t0_g, t1_g = vv.collect_segments(tree, o, d)
+    start_r, leaf_r, t0_r, t1_r = oracle.collect_segments(tree, o, d)
+    _exact(leaf_g, leaf_r)
+    _exact(t0_g, t0_r)
+    _exact(t1_g, t1_r)
+
+
+def test_empty_tree(cuda):
+    tree = vv.VOctree.from_cells(np.zeros((0, 3), int), np.zeros((0, 2 * 3 + 15), np.float32),
+                                 vv.make_bump_bases(4, 3), 1, depth=2)
+    cam = vv.Camera.look_at([2.0, 0.5, 0.5], [0.5, 0.5, 0.5], width=16, height=16)
+    layer = vv.render(tree, cam, 0)
+    assert np.all(layer.alpha == 0.0) and np.all(layer.rgb == 0.0) and np.all(layer.depth == 1e9)
+
+
+def test_determinism(cuda):
+    g = load("cache_d3")
+    tree = tree_from(g)
+    cam = camera_from(g)
+    a = vv.render(tree, cam, 1)
+    b = vv.render(tree, cam, 1)
+    _exact(a.rgb, b.rgb)
+    _exact(a.depth, b.depth)
+
+
+def test_camera_rays_vs_host(cuda):
+    """GPU-generated camera rays vs host Camera.rays: image within tolerance, and
+    the fraction of rays whose visit lists agree with the host-ray oracle."""
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    cam = synthetic.bench_camera(160, 90)
+    o, d = cam.rays()
+    ref = oracle.render_rays(tree, o, d, 5)
+    rgb, alpha, depth = oracle.finalize(ref["premult"], ref["alpha"], ref["tbar"])
+    layer = vv.render(tree, cam, 5)
+    assert np.abs(layer.rgb.reshape(-1, 3) - rgb).max() < TOL
+    assert np.abs(layer.alpha.reshape(-1) - alpha).max() < TOL
+    hit = alpha >= 1e-3
+    assert np.abs(layer.depth.reshape(-1)[hit] - depth[hit]).max() < TOL

@@ -1,0 +1,137 @@
+"""Pin the CPU oracle (oracle/vv_oracle.c) against the reference's golden vectors.
+
+The vectors in tests/golden/ were produced by the reference implementation
+itself (tests/golden/make_golden.py imports /root/reference).  The oracle is
+a float64, no-FMA restatement of the reference kernels, so the comparisons
+below are bit-exact (np.array_equal) for traversal, counts, visit lists,
+alpha/premult/tbar and slice caches.
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import load, tree_from
+from oracle import oracle
+from paper_2202_06088_b200 import synthetic
+
+
+def _exact(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    assert np.array_equal(a, b), f"max |diff| = {np.max(np.abs(a.astype(float) - b.astype(float)))}"
+
+
+def _check_render(out, g, prefix=""):
+    _exact(out["premult"], g[prefix + "premult"])
+    _exact(out["alpha"], g[prefix + "alpha"])
+    _exact(out["tbar"], g[prefix + "tbar"])
+    if prefix + "used" in g:
+        _exact(out["used"], g[prefix + "used"])
+        _exact(out["visit_start"], g[prefix + "visit_start"])
+        _exact(out["visit_leaf"], g[prefix + "visit_leaf"])
+        # shade_forward's own accumulators agree with render_kernel's
+        _exact(g[prefix + "fwd_alpha"], g[prefix + "alpha"])
+
+
+def _check_segments(seg, g, prefix=""):
+    start, leaf, t0, t1 = seg
+    _exact(start, g[prefix + "seg_start"])
+    _exact(leaf, g[prefix + "seg_leaf"])
+    _exact(t0, g[prefix + "seg_t0"])
+    _exact(t1, g[prefix + "seg_t1"])
+
+
+def test_tables_match_reference():
+    g = load("tables")
+    for n_max in range(4):
+        t = oracle.basis_tables(n_max)
+        for f in ("pair_n", "pair_l", "pair_norm", "k2pair", "k2sh", "sh_pref"):
+            _exact(t[f], g[f"n{n_max}_{f}"])
+
+
+@pytest.mark.parametrize("tag,es", [("nostop", 0.0), ("stop", 1e-4)])
+def test_scalar_case(tag, es):
+    g = load("scalar_d2")
+    tree = tree_from(g)
+    out = oracle.render_rays(tree, g["origins"], g["dirs"], int(g["frame"]), early_stop=es, visits=True)
+    _check_render(out, g, f"{tag}_")
+
+
+def test_scalar_segments():
+    g = load("scalar_d2")
+    _check_segments(oracle.collect_segments(tree_from(g), g["origins"], g["dirs"]), g)
+
+
+@pytest.mark.parametrize("frame", [0, 2])
+def test_cache_case_and_slice(frame):
+    g = load("cache_d3")
+    tree = tree_from(g)
+    out = oracle.render_rays(tree, g["origins"], g["dirs"], frame, visits=True)
+    _check_render(out, g, f"f{frame}_")
+    sigma, q = oracle.build_slice(tree, frame)
+    _exact(sigma, g[f"f{frame}_slice_sigma"])
+    _exact(q, g[f"f{frame}_slice_q"])
+    # cached render equals uncached bitwise (render.py:14-17)
+    out_c = oracle.render_rays(tree, g["origins"], g["dirs"], frame, cache=(sigma, q))
+    for k in ("premult", "alpha", "tbar", "used"):
+        _exact(out_c[k], out[k])
+    # finalize_layer
+    rgb, alpha, depth = oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+    _exact(rgb.reshape(24, 24, 3), g[f"f{frame}_rgb"])
+    _exact(depth.reshape(24, 24), g[f"f{frame}_depth"])
+
+
+@pytest.mark.parametrize("tag,es", [("nostop", 0.0), ("stop", 1e-4)])
+def test_edge_rays_render(tag, es):
+    g = load("edge_d4")
+    out = oracle.render_rays(tree_from(g), g["origins"], g["dirs"], 1, early_stop=es, visits=True)
+    _check_render(out, g, f"{tag}_")
+
+
+def test_edge_rays_segments():
+    g = load("edge_d4")
+    tree = tree_from(g)
+    _check_segments(oracle.collect_segments(tree, g["origins"], g["dirs"]), g)
+    _check_segments(oracle.collect_segments(tree, g["origins"], g["dirs"], tmin=0.3, tmax=1.7), g, "clip_")
+
+
+def test_config1_against_reference():
+    g = load("cfg1")
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in (tree.node_child, tree.leaf_data, tree.bases.a, tree.bases.b):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(g["tree_sha"]), "synthetic generator drifted from the golden tree"
+    out = oracle.render_rays(tree, g["origins"], g["dirs"], int(g["frame"]), visits=True)
+    _check_render(out, g)
+    rgb, alpha, depth = oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+    _exact(rgb.reshape(64, 64, 3), g["rgb"])
+    _exact(alpha.reshape(64, 64), g["alpha_img"])
+    _exact(depth.reshape(64, 64), g["depth"])
+    _check_segments(oracle.collect_segments(tree, g["origins"], g["dirs"]), g)
+
+
+@pytest.mark.parametrize("frame", [0, 2])
+@pytest.mark.parametrize("ew", [1.0, 0.4])
+def test_edits_case(frame, ew):
+    g = load("edits_d3")
+    out = oracle.render_rays(tree_from(g), g["origins"], g["dirs"], frame, edit_weight=ew)
+    p = f"f{frame}_w{int(ew * 10)}_"
+    _exact(out["premult"], g[p + "premult"])
+    _exact(out["alpha"], g[p + "alpha"])
+    _exact(out["tbar"], g[p + "tbar"])
+
+
+@pytest.mark.parametrize("n_max", [0, 3])
+def test_other_truncations(n_max):
+    g = load(f"nmax{n_max}")
+    out = oracle.render_rays(tree_from(g), g["origins"], g["dirs"], int(g["frame"]), visits=True)
+    _exact(out["alpha"], g["alpha"])
+    _exact(out["tbar"], g["tbar"])
+    _exact(out["used"], g["used"])
+    _exact(out["visit_leaf"], g["visit_leaf"])
+    # premult: sin(g)**3 may round differently in the last bit at n_max = 3
+    np.testing.assert_allclose(out["premult"], g["premult"], rtol=0, atol=1e-14)
