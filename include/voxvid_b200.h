@@ -70,7 +70,17 @@ typedef struct {
     double edit_weight;
     double tmin;
     double tmax;
+    /* Leaf decode strategy when no cache is passed (results are bitwise
+     * identical either way, as for the reference's FrameSlice):
+     * VV_SLICE_AUTO picks per call, VV_SLICE_PER_SAMPLE decodes each visited
+     * leaf inside the render kernel (render_kernel's uncached branch),
+     * VV_SLICE_PER_FRAME first decodes every leaf once into a transient
+     * stream-ordered slice, then renders from it. */
+    int32_t frame_slice;
+    int32_t reserved;
 } vv_render_opts;
+
+enum { VV_SLICE_AUTO = 0, VV_SLICE_PER_SAMPLE = 1, VV_SLICE_PER_FRAME = 2 };
 
 /* Pinhole camera (render.py:42-125): intrinsics in pixels, row-major c2w. */
 typedef struct {

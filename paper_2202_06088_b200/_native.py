@@ -28,6 +28,8 @@ __all__ = [
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvoxvid_b200.so"
+if os.environ.get("VV_LIB_PATH"):  # A/B experiments with alternative in-tree builds (tools/build_variants.sh)
+    LIB_PATH = Path(os.environ["VV_LIB_PATH"]).resolve()
 
 VV_OK = 0
 VV_E_INVALID = -1
@@ -103,6 +105,8 @@ class RenderOpts(ctypes.Structure):
         ("edit_weight", ctypes.c_double),
         ("tmin", ctypes.c_double),
         ("tmax", ctypes.c_double),
+        ("frame_slice", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

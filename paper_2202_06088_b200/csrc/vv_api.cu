@@ -1,5 +1,5 @@
-// vv_kernels.cu -- sm_100a kernels and the device half of the C ABI
-// (include/voxvid_b200.h).
+// vv_api.cu -- the C ABI (include/voxvid_b200.h): tree replicas, slices and
+// the render entry points.  Kernels: vv_kernels.cuh / vv_launch_*.cu.
 //
 // Kernels (all one-thread-per-ray/pixel, shared-memory traversal stacks):
 //   k_render_rays    render_kernel (kernels.py:410-652) over explicit rays
@@ -12,6 +12,7 @@
 //   k_repack         payload rows -> padded [w_sigma] / [w_gamma | w_hh] planes
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -19,10 +20,10 @@
 #include <vector>
 
 #include "../../include/voxvid_b200.h"
-#include "vv_device.cuh"
-#include "vv_host_common.h"
+#include "vv_kernels.cuh"
 
 using namespace vv;
+using namespace vvk;
 
 struct vv_tree {
     int device;
@@ -56,9 +57,6 @@ struct vv_slice {
     } while (0)
 
 namespace {
-
-constexpr int kBlock = 128;
-constexpr int kMaxInst = 16;
 
 struct DeviceGuard {
     int prev = -1;
@@ -100,381 +98,6 @@ CamView make_cam(const vv_camera &c) {
     return v;
 }
 
-// cooperative load of the frame's A/B rows (kernels read them for every leaf)
-__device__ __forceinline__ void load_rows(const TreeView &T, int frame, float *sA, float *sB) {
-    for (int c = threadIdx.x; c < kMaxC; c += blockDim.x) {
-        const bool in = c < T.C;
-        sA[c] = in ? T.basis_a[(size_t)frame * T.C + c] : 0.0f;
-        sB[c] = in ? T.basis_b[(size_t)frame * T.C + c] : 0.0f;
-    }
-}
-
-// ------------------------------------------------------------------ rays
-struct RaysParams {
-    TreeView T;
-    SliceView S;
-    Consts K;
-    int frame;
-    double early_stop, edit_weight, tmin, tmax;
-    const double *origins, *dirs;
-    int64_t n;
-    double *premult, *alpha, *tbar;
-    int32_t *used, *pops, *shaded;
-    const int64_t *visit_start;
-    int64_t *visit_leaf;
-};
-
-template <int NMAX, bool CACHED, bool EDITS, class Entry, bool VISITS>
-__global__ void __launch_bounds__(kBlock) k_render_rays(const __grid_constant__ RaysParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ float sA[kMaxC], sB[kMaxC];
-    load_rows(p.T, p.frame, sA, sB);
-    __syncthreads();
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= p.n) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
-    const double ox = p.origins[3 * r], oy = p.origins[3 * r + 1], oz = p.origins[3 * r + 2];
-    const double dx = p.dirs[3 * r], dy = p.dirs[3 * r + 1], dz = p.dirs[3 * r + 2];
-    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
-    Shader<NMAX, CACHED, EDITS, VISITS> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
-    if (VISITS) sh.visit = p.visit_leaf + p.visit_start[r];
-    Ray ray;
-    if (ray_setup(p.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
-        traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
-    if (VISITS) return;
-    p.premult[3 * r + 0] = sh.acc0;
-    p.premult[3 * r + 1] = sh.acc1;
-    p.premult[3 * r + 2] = sh.acc2;
-    p.alpha[r] = sh.aacc;
-    p.tbar[r] = sh.tacc;
-    if (p.used) p.used[r] = sh.used;
-    if (p.pops) p.pops[r] = sh.pops;
-    if (p.shaded) p.shaded[r] = sh.shaded;
-}
-
-// ------------------------------------------------------------------ camera
-struct CamParams {
-    TreeView T;
-    SliceView S;
-    Consts K;
-    CamView cam;
-    int frame;
-    double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
-    float *rgb, *alpha, *depth;
-    // tile mode (packed != null)
-    float *packed;
-    int tile, shard, n_shards, tiles_x;
-};
-
-// block = 16x8 pixels; warp = 16x2 pixels (spatially coherent rays)
-__device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    ix = bx * 16 + (lane & 15);
-    iy = by * 8 + w * 2 + (lane >> 4);
-}
-
-template <int NMAX, bool CACHED, bool EDITS, class Entry>
-__global__ void __launch_bounds__(kBlock) k_render_camera(const __grid_constant__ CamParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ float sA[kMaxC], sB[kMaxC];
-    load_rows(p.T, p.frame, sA, sB);
-    __syncthreads();
-    int ix, iy;
-    int64_t slot = -1;  // tile mode: packed output slot
-    if (p.packed) {
-        const int sub_per_tile = (p.tile / 16) * (p.tile / 8);
-        const int my_tile = blockIdx.x / sub_per_tile;
-        const int sub = blockIdx.x % sub_per_tile;
-        const int tile_id = my_tile * p.n_shards + p.shard;
-        const int tx0 = (tile_id % p.tiles_x) * p.tile, ty0 = (tile_id / p.tiles_x) * p.tile;
-        int lx, ly;
-        block_pixel(sub % (p.tile / 16), sub / (p.tile / 16), lx, ly);
-        ix = tx0 + lx;
-        iy = ty0 + ly;
-        slot = (int64_t)my_tile * p.tile * p.tile + (int64_t)ly * p.tile + lx;
-    } else {
-        block_pixel(blockIdx.x, blockIdx.y, ix, iy);
-    }
-    const bool inside = ix < p.cam.width && iy < p.cam.height;
-    float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
-    if (inside) {
-        double dx, dy, dz;
-        camera_ray(p.cam, ix, iy, dx, dy, dz);
-        Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
-        FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
-        Shader<NMAX, CACHED, EDITS, false> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
-        Ray ray;
-        if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
-            traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
-        finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane,
-                 r, g, b, a, d);
-    }
-    if (p.packed) {
-        float *o = p.packed + slot * 5;
-        o[0] = r; o[1] = g; o[2] = b; o[3] = a; o[4] = d;
-        return;
-    }
-    if (!inside) return;
-    const int64_t pix = (int64_t)iy * p.cam.width + ix;
-    if (p.rgb) {
-        p.rgb[3 * pix + 0] = r;
-        p.rgb[3 * pix + 1] = g;
-        p.rgb[3 * pix + 2] = b;
-    }
-    if (p.alpha) p.alpha[pix] = a;
-    if (p.depth) p.depth[pix] = d;
-}
-
-__global__ void k_unpack_tiles(const float *__restrict__ packed, int width, int height, int tile,
-                               int n_shards, int tiles_x, int tiles_total, float *rgb, float *alpha,
-                               float *depth) {
-    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pix >= (int64_t)width * height) return;
-    const int ix = (int)(pix % width), iy = (int)(pix / width);
-    const int tid = (iy / tile) * tiles_x + (ix / tile);
-    const int shard = tid % n_shards, k = tid / n_shards;
-    const int per_shard = (tiles_total + n_shards - 1) / n_shards;
-    const int64_t slot = ((int64_t)shard * per_shard + k) * tile * tile + (int64_t)(iy % tile) * tile + (ix % tile);
-    const float *s = packed + slot * 5;
-    if (rgb) {
-        rgb[3 * pix + 0] = s[0];
-        rgb[3 * pix + 1] = s[1];
-        rgb[3 * pix + 2] = s[2];
-    }
-    if (alpha) alpha[pix] = s[3];
-    if (depth) depth[pix] = s[4];
-}
-
-// ------------------------------------------------------------------ scene
-struct InstView {
-    TreeView T;
-    CamView cam;      // mode 0: pulled-back pose
-    double inv[12];   // mode 1: rows of inv(affine)[:3, :4]
-    int frame, mode;
-};
-
-struct SceneParams {
-    Consts K;
-    CamView cam;
-    InstView inst[kMaxInst];
-    int n_inst;
-    double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
-    double bg0, bg1, bg2;
-    float *image, *alpha, *depth;
-};
-
-template <int NMAX, class Entry>
-__global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__ SceneParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
-    for (int i = 0; i < p.n_inst; ++i) load_rows(p.inst[i].T, p.inst[i].frame, sA[i], sB[i]);
-    __syncthreads();
-    int ix, iy;
-    block_pixel(blockIdx.x, blockIdx.y, ix, iy);
-    if (ix >= p.cam.width || iy >= p.cam.height) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
-    double cdx, cdy, cdz;
-    camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
-    // blended state (compose.py:386-405): I (3), D, A
-    double I0 = 0, I1 = 0, I2 = 0, D = 0, A = 0;
-    for (int i = 0; i < p.n_inst; ++i) {
-        const InstView &v = p.inst[i];
-        double ox, oy, oz, dx, dy, dz, scale = 1.0;
-        bool scaled = false;
-        if (v.mode == 0) {
-            camera_ray(v.cam, ix, iy, dx, dy, dz);
-            ox = v.cam.ox;
-            oy = v.cam.oy;
-            oz = v.cam.oz;
-        } else {
-            // o_t = o @ inv3^T + t ; d_raw = d @ inv3^T ; d_t = d_raw/|d_raw|
-            const double *m = v.inv;
-            ox = xadd(xadd(xadd(xmul(p.cam.ox, m[0]), xmul(p.cam.oy, m[1])), xmul(p.cam.oz, m[2])), m[3]);
-            oy = xadd(xadd(xadd(xmul(p.cam.ox, m[4]), xmul(p.cam.oy, m[5])), xmul(p.cam.oz, m[6])), m[7]);
-            oz = xadd(xadd(xadd(xmul(p.cam.ox, m[8]), xmul(p.cam.oy, m[9])), xmul(p.cam.oz, m[10])), m[11]);
-            const double r0 = xadd(xadd(xmul(cdx, m[0]), xmul(cdy, m[1])), xmul(cdz, m[2]));
-            const double r1 = xadd(xadd(xmul(cdx, m[4]), xmul(cdy, m[5])), xmul(cdz, m[6]));
-            const double r2 = xadd(xadd(xmul(cdx, m[8]), xmul(cdy, m[9])), xmul(cdz, m[10]));
-            const double nrm = sqrt(xadd(xadd(xmul(r0, r0), xmul(r1, r1)), xmul(r2, r2)));
-            dx = xdiv(r0, nrm);
-            dy = xdiv(r1, nrm);
-            dz = xdiv(r2, nrm);
-            scale = xdiv(1.0, nrm);
-            scaled = true;
-        }
-        FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight};
-        SliceView S{nullptr, nullptr, 0};
-        Shader<NMAX, false, true, false> sh(v.T, S, F, p.K, (float)dx, (float)dy, (float)dz);
-        Ray ray;
-        if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
-            traverse<Entry>(v.T.child, v.T.depth, ray, stk, blockDim.x, sh);
-        // finalize_layer in float64
-        const double al = sh.aacc;
-        const double safe = al > 1e-300 ? al : 1e-300;
-        double li0 = 0, li1 = 0, li2 = 0;
-        if (al > 0.0) {
-            li0 = xdiv(sh.acc0, safe);
-            li1 = xdiv(sh.acc1, safe);
-            li2 = xdiv(sh.acc2, safe);
-        }
-        double t = xdiv(sh.tacc, safe);
-        if (scaled) t = xmul(t, scale);
-        const double ld = al >= p.alpha_floor ? t : p.far_plane;
-        if (i == 0) {
-            I0 = li0; I1 = li1; I2 = li2; D = ld; A = al;
-        } else {
-            // Algorithm 1 (compose.py:393-404); ties go to the incoming layer
-            const double om_ai = xsub(1.0, al), om_a = xsub(1.0, A);
-            if (ld <= D) {
-                I0 = xadd(xmul(al, li0), xmul(xmul(om_ai, A), I0));
-                I1 = xadd(xmul(al, li1), xmul(xmul(om_ai, A), I1));
-                I2 = xadd(xmul(al, li2), xmul(xmul(om_ai, A), I2));
-                D = ld;
-            } else {
-                I0 = xadd(xmul(A, I0), xmul(xmul(om_a, al), li0));
-                I1 = xadd(xmul(A, I1), xmul(xmul(om_a, al), li1));
-                I2 = xadd(xmul(A, I2), xmul(xmul(om_a, al), li2));
-            }
-            A = xadd(A, xmul(al, om_a));
-        }
-    }
-    if (p.n_inst > 1) {  // unpremultiply the blend (compose.py:457-460)
-        const double safe = A > 1e-300 ? A : 1e-300;
-        if (A > 0.0) {
-            I0 = xdiv(I0, safe);
-            I1 = xdiv(I1, safe);
-            I2 = xdiv(I2, safe);
-        } else {
-            I0 = I1 = I2 = 0.0;
-        }
-    }
-    // composite_background: a * rgb + (1 - a) * bg (render.py:243-251)
-    const double om = xsub(1.0, A);
-    const int64_t pix = (int64_t)iy * p.cam.width + ix;
-    p.image[3 * pix + 0] = (float)xadd(xmul(A, I0), xmul(om, p.bg0));
-    p.image[3 * pix + 1] = (float)xadd(xmul(A, I1), xmul(om, p.bg1));
-    p.image[3 * pix + 2] = (float)xadd(xmul(A, I2), xmul(om, p.bg2));
-    if (p.alpha) p.alpha[pix] = (float)A;
-    if (p.depth) p.depth[pix] = (float)D;
-}
-
-// ------------------------------------------------------------------ slice
-struct SliceParams {
-    TreeView T;
-    Consts K;
-    int frame;
-    int64_t n_leaves;
-    double *sigma;
-    float4 *q;
-    int q4;
-};
-
-template <int NMAX>
-__global__ void __launch_bounds__(256) k_build_slice(const __grid_constant__ SliceParams p) {
-    __shared__ float sA[kMaxC], sB[kMaxC];
-    load_rows(p.T, p.frame, sA, sB);
-    __syncthreads();
-    const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (L >= p.n_leaves) return;
-    constexpr int Q4 = Basis<NMAX>::Q4;
-    float q[4 * Q4];
-#pragma unroll
-    for (int i = 0; i < 4 * Q4; ++i) q[i] = 0.0f;
-    double sigma;
-    slice_leaf<NMAX>(p.T, (uint32_t)L, sA, sB, p.K, sigma, q);
-    p.sigma[L] = sigma;
-    float4 *o = p.q + L * p.q4;
-#pragma unroll
-    for (int i = 0; i < Q4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
-}
-
-// ------------------------------------------------------------------ traversal only
-struct SegParams {
-    TreeView T;
-    const double *origins, *dirs;
-    int64_t n;
-    double tmin, tmax;
-    int64_t *count;
-    const int64_t *ray_start;
-    int64_t *seg_leaf;
-    double *seg_t0, *seg_t1;
-};
-
-template <class Entry, bool COLLECT>
-__global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ SegParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= p.n) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
-    Ray ray;
-    const bool hit = ray_setup(p.T, p.origins[3 * r], p.origins[3 * r + 1], p.origins[3 * r + 2],
-                               p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
-    if (COLLECT) {
-        const int64_t b = p.ray_start[r];
-        CollectVisitor v{p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
-        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
-    } else {
-        CountVisitor v;
-        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
-        p.count[r] = v.count;
-    }
-}
-
-// ------------------------------------------------------------------ repack
-// leaf rows (P = 2C + 3K floats) -> sig plane (sig4 float4 per row) and
-// rest plane ([w_gamma pad to 4 | w_hh pad to 4], rest4 float4 per row)
-__global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int sig4,
-                         int rest4, int hh_off4, float *sig, float *rest) {
-    const int sigw = 4 * sig4, restw = 4 * rest4;
-    const int64_t total = rows * (int64_t)(sigw + restw);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / (sigw + restw);
-        const int j = (int)(i % (sigw + restw));
-        const float *s = src + row * P;
-        if (j < sigw) {
-            sig[row * sigw + j] = j < C ? s[j] : 0.0f;
-        } else {
-            const int k = j - sigw;
-            float v = 0.0f;
-            if (k < C) v = s[C + k];
-            else if (k >= 4 * hh_off4 && k < 4 * hh_off4 + K3) v = s[2 * C + (k - 4 * hh_off4)];
-            rest[row * restw + k] = v;
-        }
-    }
-}
-
-// ------------------------------------------------------------------ dispatch helpers
-template <class F>
-int with_nmax(int nmax, F &&f) {
-    switch (nmax) {
-        case 0: return f(std::integral_constant<int, 0>());
-        case 1: return f(std::integral_constant<int, 1>());
-        case 2: return f(std::integral_constant<int, 2>());
-        case 3: return f(std::integral_constant<int, 3>());
-        default: return set_error(VV_E_UNSUPPORTED, "n_max %d not supported on device (max 3)", nmax);
-    }
-}
-
-size_t stack_bytes(int depth, bool wide) {
-    return (size_t)stack_cap(depth) * kBlock * (wide ? sizeof(EntryW) : sizeof(EntryN));
-}
-
-template <class Kern>
-int prep_smem(Kern k, size_t smem) {
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return set_error(VV_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
-    }
-    return VV_OK;
-}
-
-int check_launch(const char *what) {
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return set_error(VV_E_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
-    return VV_OK;
-}
-
 int check_frame(const vv_tree *t, int frame) {
     if (frame < 0 || frame >= t->frames)
         return set_error(VV_E_INVALID, "frame %d out of range [0, %d)", frame, t->frames);
@@ -496,6 +119,8 @@ vv_render_opts default_opts() {
     o.edit_weight = 1.0;
     o.tmin = 0.0;
     o.tmax = 1e30;
+    o.frame_slice = VV_SLICE_AUTO;
+    o.reserved = 0;
     return o;
 }
 
@@ -507,6 +132,71 @@ SliceView slice_view(const vv_slice *c) {
         s.q4 = c->q4;
     }
     return s;
+}
+
+int launch_build_slice(const vv_tree *t, int frame, double *sigma, float4 *q, int q4, cudaStream_t st) {
+    if (t->n_leaves == 0) return VV_OK;
+    SliceParams p;
+    p.T = t->view;
+    p.K = make_consts(t->n_max);
+    p.frame = frame;
+    p.n_leaves = t->n_leaves;
+    p.sigma = sigma;
+    p.q = q;
+    p.q4 = q4;
+    const unsigned grid = (unsigned)((t->n_leaves + 255) / 256);
+    return launch_slice(t->n_max, p, grid, st);
+}
+
+// Transient per-frame slice in the device's stream-ordered pool; freed
+// (stream-ordered) when the render call returns.
+struct Transient {
+    void *mem = nullptr;
+    cudaStream_t st = nullptr;
+    Transient() = default;
+    Transient(const Transient &) = delete;
+    ~Transient() {
+        if (mem) cudaFreeAsync(mem, st);
+    }
+};
+
+void pool_setup(int device) {
+    static std::once_flag flags[64];
+    std::call_once(flags[device & 63], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;  // keep freed slices cached in the pool
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+// VV_SLICE_AUTO: decode every leaf once per frame when the frame's rays would
+// visit a comparable number of leaves anyway (each visited leaf is shared by
+// several neighbouring rays); otherwise decode per visited sample.
+bool want_slice(const vv_tree *t, int64_t n_rays, int policy) {
+    if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return false;
+    if (policy == VV_SLICE_PER_FRAME) return true;
+    return t->n_leaves <= 2 * n_rays;
+}
+
+int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr) {
+    pool_setup(t->device);
+    const int q4 = (3 * t->S + 3) / 4;
+    const size_t sig_b = ((size_t)t->n_leaves * sizeof(double) + 255) & ~(size_t)255;
+    const size_t bytes = sig_b + (size_t)t->n_leaves * q4 * sizeof(float4);
+    cudaError_t e = cudaMallocAsync(&tr.mem, bytes, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        tr.mem = nullptr;
+        return set_error(VV_E_NOMEM, "transient slice allocation (%zu bytes) failed: %s", bytes,
+                         cudaGetErrorString(e));
+    }
+    tr.st = st;
+    sv.sigma = reinterpret_cast<double *>(tr.mem);
+    sv.q = reinterpret_cast<float4 *>(reinterpret_cast<char *>(tr.mem) + sig_b);
+    sv.q4 = q4;
+    return launch_build_slice(t, frame, const_cast<double *>(sv.sigma), const_cast<float4 *>(sv.q), q4, st);
 }
 
 int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool host_src) {
@@ -597,12 +287,12 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
                 }
                 src = stage;
             }
-            k_repack<<<1184, 256>>>(src, rows, P, C, K3, sig4, rest4, hh_off4,
-                                    reinterpret_cast<float *>(t->d_sig + r0 * sig4),
-                                    reinterpret_cast<float *>(t->d_rest + r0 * rest4));
-            if ((e = cudaGetLastError()) != cudaSuccess) {
+            const int lrc = launch_repack(src, rows, P, C, K3, sig4, rest4, hh_off4,
+                                          reinterpret_cast<float *>(t->d_sig + r0 * sig4),
+                                          reinterpret_cast<float *>(t->d_rest + r0 * rest4), nullptr);
+            if (lrc) {
                 if (stage) cudaFree(stage);
-                return fail(set_error(VV_E_CUDA, "repack launch failed: %s", cudaGetErrorString(e)));
+                return fail(lrc);
             }
         }
         e = cudaDeviceSynchronize();
@@ -697,25 +387,10 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
         vv_slice_free(s);
         return set_error(VV_E_NOMEM, "slice allocation failed");
     }
-    if (t->n_leaves > 0) {
-        SliceParams p;
-        p.T = t->view;
-        p.K = make_consts(t->n_max);
-        p.frame = frame;
-        p.n_leaves = t->n_leaves;
-        p.sigma = s->d_sigma;
-        p.q = s->d_q;
-        p.q4 = s->q4;
-        const unsigned grid = (unsigned)((t->n_leaves + 255) / 256);
-        cudaStream_t st = (cudaStream_t)stream;
-        rc = with_nmax(t->n_max, [&](auto N) {
-            k_build_slice<decltype(N)::value><<<grid, 256, 0, st>>>(p);
-            return check_launch("build_slice");
-        });
-        if (rc) {
-            vv_slice_free(s);
-            return rc;
-        }
+    rc = launch_build_slice(t, frame, s->d_sigma, s->d_q, s->q4, (cudaStream_t)stream);
+    if (rc) {
+        vv_slice_free(s);
+        return rc;
     }
     *out = s;
     return VV_OK;
@@ -787,32 +462,13 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
     const size_t smem = stack_bytes(t->depth, wide);
     const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     cudaStream_t st = (cudaStream_t)stream;
-    const bool cached = cache != nullptr, edits = t->has_edits;
-    return with_nmax(t->n_max, [&](auto N) {
-        constexpr int NM = decltype(N)::value;
-        auto launch = [&](auto kern) {
-            int r = prep_smem(kern, smem);
-            if (r) return r;
-            kern<<<grid, kBlock, smem, st>>>(p);
-            return check_launch("render_rays");
-        };
-#define VV_RAYS_DISPATCH(ENTRY, VIS)                                                              \
-    if (cached) {                                                                                 \
-        if (edits) return launch(k_render_rays<NM, true, true, ENTRY, VIS>);                      \
-        return launch(k_render_rays<NM, true, false, ENTRY, VIS>);                                \
-    } else {                                                                                      \
-        if (edits) return launch(k_render_rays<NM, false, true, ENTRY, VIS>);                     \
-        return launch(k_render_rays<NM, false, false, ENTRY, VIS>);                               \
+    Transient tr;
+    if (!cache && want_slice(t, n, opts.frame_slice)) {
+        int r = build_transient(t, frame, st, p.S, tr);
+        if (r) return r;
     }
-        if (wide) {
-            if (visits) { VV_RAYS_DISPATCH(EntryW, true) }
-            else { VV_RAYS_DISPATCH(EntryW, false) }
-        } else {
-            if (visits) { VV_RAYS_DISPATCH(EntryN, true) }
-            else { VV_RAYS_DISPATCH(EntryN, false) }
-        }
-#undef VV_RAYS_DISPATCH
-    });
+    const bool cached = p.S.sigma != nullptr, edits = t->has_edits;
+    return launch_rays(t->n_max, cached, edits, wide, visits, p, grid, smem, st);
 }
 
 int vv_render_rays(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -858,7 +514,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.rgb = rgb;
     p.alpha = alpha;
     p.depth = depth;
-    dim3 grid;
+    unsigned grid_blocks = 0;
     if (packed) {
         p.packed = packed;
         p.tile = tile;
@@ -869,34 +525,22 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         const int total = p.tiles_x * tiles_y;
         const int mine = total > shard ? (total - shard + n_shards - 1) / n_shards : 0;
         if (mine == 0) return VV_OK;
-        grid = dim3((unsigned)(mine * (tile / 16) * (tile / 8)));
+        if (tile % kTW || tile % kTH) return set_error(VV_E_INVALID, "tile must be a multiple of %d", kTW);
+        grid_blocks = (unsigned)mine * (unsigned)((tile / kTW) * (tile / kTH));
     } else {
-        grid = dim3((unsigned)((cam->width + 15) / 16), (unsigned)((cam->height + 7) / 8));
+        p.blocks_x = (cam->width + kTW - 1) / kTW;
+        grid_blocks = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
     }
     const bool wide = t->depth > kNarrowDepth;
     const size_t smem = stack_bytes(t->depth, wide);
     cudaStream_t st = (cudaStream_t)stream;
-    const bool cached = cache != nullptr, edits = t->has_edits;
-    return with_nmax(t->n_max, [&](auto N) {
-        constexpr int NM = decltype(N)::value;
-        auto launch = [&](auto kern) {
-            int r = prep_smem(kern, smem);
-            if (r) return r;
-            kern<<<grid, kBlock, smem, st>>>(p);
-            return check_launch("render_camera");
-        };
-#define VV_CAM_DISPATCH(ENTRY)                                                                    \
-    if (cached) {                                                                                 \
-        if (edits) return launch(k_render_camera<NM, true, true, ENTRY>);                         \
-        return launch(k_render_camera<NM, true, false, ENTRY>);                                   \
-    } else {                                                                                      \
-        if (edits) return launch(k_render_camera<NM, false, true, ENTRY>);                        \
-        return launch(k_render_camera<NM, false, false, ENTRY>);                                  \
+    Transient tr;
+    if (!cache && want_slice(t, (int64_t)cam->width * cam->height, opts.frame_slice)) {
+        int r = build_transient(t, frame, st, p.S, tr);
+        if (r) return r;
     }
-        if (wide) { VV_CAM_DISPATCH(EntryW) }
-        else { VV_CAM_DISPATCH(EntryN) }
-#undef VV_CAM_DISPATCH
-    });
+    const bool cached = p.S.sigma != nullptr, edits = t->has_edits;
+    return launch_camera(t->n_max, cached, edits, wide, p, grid_blocks, smem, st);
 }
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -918,9 +562,9 @@ int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int3
         return set_error(VV_E_INVALID, "bad unpack arguments");
     const int tiles_x = (width + tile - 1) / tile, tiles_y = (height + tile - 1) / tile;
     const int64_t npix = (int64_t)width * height;
-    k_unpack_tiles<<<(unsigned)((npix + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        packed_all, width, height, tile, n_shards, tiles_x, tiles_x * tiles_y, rgb, alpha, depth);
-    return check_launch("unpack_tiles");
+    (void)npix;
+    return launch_unpack(packed_all, width, height, tile, n_shards, tiles_x, tiles_x * tiles_y, rgb, alpha, depth,
+                         (cudaStream_t)stream);
 }
 
 int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
@@ -973,17 +617,20 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
     const size_t smem = stack_bytes(max_depth, wide);
     dim3 grid((unsigned)((cam->width + 15) / 16), (unsigned)((cam->height + 7) / 8));
     cudaStream_t st = (cudaStream_t)stream;
-    return with_nmax(t0->n_max, [&](auto N) {
-        constexpr int NM = decltype(N)::value;
-        auto launch = [&](auto kern) {
-            int r = prep_smem(kern, smem);
+    Transient tr[kMaxInst];
+    for (int i = 0; i < n_inst; ++i) {
+        p.inst[i].S = SliceView{nullptr, nullptr, 0};
+        int same = -1;
+        for (int j = 0; j < i; ++j)
+            if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.sigma) same = j;
+        if (same >= 0) {
+            p.inst[i].S = p.inst[same].S;
+        } else if (want_slice(inst[i].tree, (int64_t)cam->width * cam->height, opts.frame_slice)) {
+            int r = build_transient(inst[i].tree, inst[i].frame, st, p.inst[i].S, tr[i]);
             if (r) return r;
-            kern<<<grid, kBlock, smem, st>>>(p);
-            return check_launch("render_scene");
-        };
-        if (wide) return launch(k_render_scene<NM, EntryW>);
-        return launch(k_render_scene<NM, EntryN>);
-    });
+        }
+    }
+    return launch_scene(t0->n_max, wide, p, grid, smem, st);
 }
 
 static int segments_impl(const vv_tree *t, const double *origins, const double *dirs, int64_t n, double tmin,
@@ -1008,15 +655,8 @@ static int segments_impl(const vv_tree *t, const double *origins, const double *
     const size_t smem = stack_bytes(t->depth, wide);
     const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     cudaStream_t st = (cudaStream_t)stream;
-    auto launch = [&](auto kern) {
-        int r = prep_smem(kern, smem);
-        if (r) return r;
-        kern<<<grid, kBlock, smem, st>>>(p);
-        return check_launch("segments");
-    };
     const bool collect = seg_leaf != nullptr;
-    if (wide) return collect ? launch(k_segments<EntryW, true>) : launch(k_segments<EntryW, false>);
-    return collect ? launch(k_segments<EntryN, true>) : launch(k_segments<EntryN, false>);
+    return launch_segments(wide, collect, p, grid, smem, st);
 }
 
 int vv_count_segments(const vv_tree *t, const double *origins, const double *dirs, int64_t n, double tmin,

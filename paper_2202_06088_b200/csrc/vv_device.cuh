@@ -74,6 +74,9 @@ __device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a,
 // Python builtin max/min of two floats (first argument wins ties)
 __device__ __forceinline__ double pmax(double a, double b) { return (b > a) ? b : a; }
 __device__ __forceinline__ double pmin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 // exact 2^-k for 0 <= k <= 1022
 __device__ __forceinline__ double pow2neg(int k) {
     return __longlong_as_double((long long)(1023 - k) << 52);
@@ -158,127 +161,175 @@ __host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 :
 
 // ------------------------------------------------------------ traversal
 // Visitor interface:
-//   bool leaf(uint32_t row, double tin, double tout)  -> true = stop the ray
-//   void pop()                                         -> one internal-node pop
+//   void pop()                                   one internal-node pop
+//   bool batch(int32_t cp[4], double st[5], int keep)
+//        the <= 4 leaf segments of one last-level node, near to far:
+//        segment s (keep bit s set) is leaf row cp[s] over [st[s], st[s+1]];
+//        returns true to stop the ray (early termination).  May clobber
+//        its arguments.
+//
+// Structure ("while-while"): a lane walks internal nodes until it holds one
+// last-level node's leaf batch, then all lanes of the warp shade their
+// batches together -- the shading code runs with the warp converged instead
+// of interleaving with other lanes' node expansions.
+//
+// Node step (kernels.py:600-647 restated): the reference walks the pierced
+// children by repeatedly taking the smallest not-yet-crossed mid-plane
+// crossing (ties x, y, z) until it reaches the node's exit.  That is a
+// stable sort of the (up to three) uncrossed crossings: a 3-element
+// compare-exchange network with strict '<' swaps yields the same order and
+// the same boundary values st[k] = min(k-th crossing, t_out); step k exists
+// iff st[k] < t_out, which the 'st[k+1] > st[k]' segment test already
+// implies.  Node corners are tracked as exact doubles so crossings need no
+// int->double conversion: p_mid = x_lo + h/2 is the same double as the
+// reference's (2c+1) * 2^-(L+1).
+__device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) {
+    const bool sw = kb < ka;
+    const double tk = sw ? kb : ka;
+    kb = sw ? ka : kb;
+    ka = tk;
+    const int ta = sw ? ab : aa;
+    ab = sw ? aa : ab;
+    aa = ta;
+}
+
+// Resumable traversal state of one ray (persistent kernels keep it across
+// refills of other lanes).
+struct Trav {
+    uint32_t ptr, cx, cy, cz;
+    int L, top;
+    double xl, yl, zl, h;  // node low corner and size (exact)
+    double tin, tout;
+    bool need_pop;
+    __device__ __forceinline__ void init(const Ray &r) {
+        ptr = cx = cy = cz = 0;
+        L = top = 0;
+        xl = yl = zl = 0.0;
+        h = 1.0;
+        tin = r.rt_in;
+        tout = r.rt_out;
+        need_pop = false;
+    }
+};
+
+// Advance the walk until the next last-level node with kept leaves; fills
+// cp/st/keep and returns true, or returns false when the tree is exhausted.
 template <class Entry, class Visitor>
-__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth,
-                                         const Ray &r, Entry *stk, int sstride, Visitor &vis) {
-    uint32_t ptr = 0, cx = 0, cy = 0, cz = 0;
-    int L = 0;
-    double tin = r.rt_in, tout = r.rt_out;
-    int top = 0;
+__device__ __forceinline__ bool trav_next(Trav &t, const int32_t *__restrict__ child, int depth, const Ray &r,
+                                          Entry *stk, int sstride, Visitor &vis, int32_t *cp, double *st,
+                                          int &keep) {
     const double o0 = r.o0, o1 = r.o1, o2 = r.o2, i0 = r.i0, i1 = r.i1, i2 = r.i2;
     const int mirror = r.mirror;
     while (true) {
-        vis.pop();
-        // mid-plane crossings of the current node (kernels.py:603-606)
-        const double hm = pow2neg(L + 1);
-        const double txm = xmul(xsub(xmul((double)(2u * cx + 1u), hm), o0), i0);
-        const double tym = xmul(xsub(xmul((double)(2u * cy + 1u), hm), o1), i1);
-        const double tzm = xmul(xsub(xmul((double)(2u * cz + 1u), hm), o2), i2);
-        int b = 0;
-        if (txm < tin) b |= 1;
-        if (tym < tin) b |= 2;
-        if (tzm < tin) b |= 4;
-        // walk the <= 4 pierced children near to far (kernels.py:614-638)
-        // step s covers [st[s], st[s+1]) in child sb[s]; at most 4 steps
-        // (each step sets one more bit; the reference loops until
-        // t_out >= node t_out, which happens by the 4th step for tmax < 1e301)
-        int sb[4];
-        double st[5];
-        int ns = 0;
-        bool walking = true;
-        st[0] = tin;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            sb[s] = b;
-            st[s + 1] = tout;
-            if (walking) {
-                const double tx = (b & 1) ? 1e301 : txm;
-                const double ty = (b & 2) ? 1e301 : tym;
-                const double tz = (b & 4) ? 1e301 : tzm;
-                const double tt = pmin(pmin(tx, ty), pmin(tz, tout));
-                st[s + 1] = tt;
-                ns = s + 1;
-                if (tt >= tout) {
-                    walking = false;
-                } else if (tx <= ty && tx <= tz) {
-                    b |= 1;
-                } else if (ty <= tz) {
-                    b |= 2;
-                } else {
-                    b |= 4;
-                }
-            }
+        if (t.need_pop) {
+            if (t.top == 0) return false;
+            --t.top;
+            stk[t.top * sstride].get(t.ptr, t.L, t.cx, t.cy, t.cz);
+            // recompute the popped cell's interval from its six faces
+            t.h = pow2neg(t.L);
+            t.xl = xmul((double)t.cx, t.h);
+            t.yl = xmul((double)t.cy, t.h);
+            t.zl = xmul((double)t.cz, t.h);
+            const double xh = xadd(t.xl, t.h), yh = xadd(t.yl, t.h), zh = xadd(t.zl, t.h);
+            t.tin = pmax(pmax(r.rt_in, xmul(xsub(t.xl, o0), i0)),
+                         pmax(xmul(xsub(t.yl, o1), i1), xmul(xsub(t.zl, o2), i2)));
+            t.tout = pmin(pmin(r.rt_out, xmul(xsub(xh, o0), i0)),
+                          pmin(xmul(xsub(yh, o1), i1), xmul(xsub(zh, o2), i2)));
+            t.need_pop = false;
         }
-        // child pointers: independent loads
-        const int32_t *row = child + (size_t)ptr * 8u;
-        int32_t cp[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) cp[s] = (s < ns) ? __ldg(row + (sb[s] ^ mirror)) : -1;
-        int keep = 0;
+        vis.pop();
+        const double tin = t.tin, tout = t.tout;
+        const double hh = xmul(t.h, 0.5);
+        const double txm = xmul(xsub(xadd(t.xl, hh), o0), i0);
+        const double tym = xmul(xsub(xadd(t.yl, hh), o1), i1);
+        const double tzm = xmul(xsub(xadd(t.zl, hh), o2), i2);
+        const bool bx = txm < tin, by = tym < tin, bz = tzm < tin;
+        const int b0 = (bx ? 1 : 0) | (by ? 2 : 0) | (bz ? 4 : 0);
+        double k0 = bx ? 1e301 : txm, k1 = by ? 1e301 : tym, k2 = bz ? 1e301 : tzm;
+        int a0 = 1, a1 = 2, a2 = 4;
+        cswap(k0, a0, k1, a1);
+        cswap(k1, a1, k2, a2);
+        cswap(k0, a0, k1, a1);
+        const int c0 = b0, c1 = c0 | a0, c2 = c1 | a1, c3 = c2 | a2;
+        st[0] = tin;
+        st[1] = pmin(k0, tout);
+        st[2] = pmin(k1, tout);
+        st[3] = pmin(k2, tout);
+        st[4] = tout;
+        // child pointers: four independent loads from the same 32-byte row
+        const int32_t *row = child + (size_t)t.ptr * 8u;
+        cp[0] = __ldg(row + (c0 ^ mirror));
+        cp[1] = __ldg(row + (c1 ^ mirror));
+        cp[2] = __ldg(row + (c2 ^ mirror));
+        cp[3] = __ldg(row + (c3 ^ mirror));
+        keep = 0;
 #pragma unroll
         for (int s = 0; s < 4; ++s)
             if (cp[s] >= 0 && st[s + 1] > st[s]) keep |= 1 << s;
-
-        if (L + 1 == depth) {
-            // children are leaf payload rows: shade near to far
-            bool stop = false;
-#pragma unroll 1
-            for (int s = 0; s < 4; ++s) {
-                if (keep & (1 << s)) {
-                    const int32_t lp = s == 0 ? cp[0] : s == 1 ? cp[1] : s == 2 ? cp[2] : cp[3];
-                    const double a = s == 0 ? st[0] : s == 1 ? st[1] : s == 2 ? st[2] : st[3];
-                    const double c = s == 0 ? st[1] : s == 1 ? st[2] : s == 2 ? st[3] : st[4];
-                    if (vis.leaf((uint32_t)lp, a, c)) { stop = true; break; }
-                }
-            }
-            if (stop) return;
-        } else if (keep) {
-            const int f = __ffs(keep) - 1;
-            // push the farther kept children far -> near (kernels.py:639-647)
-#pragma unroll
-            for (int s = 3; s >= 1; --s) {
-                if ((keep & (1 << s)) && s > f) {
-                    const int bs = sb[s];
-                    stk[top * sstride] = Entry::make((uint32_t)cp[s], L + 1, 2u * cx + (bs & 1),
-                                                     2u * cy + ((bs >> 1) & 1), 2u * cz + ((bs >> 2) & 1));
-                    ++top;
-                }
-            }
-            // continue with the nearest kept child in registers
-            const int bf = f == 0 ? sb[0] : f == 1 ? sb[1] : f == 2 ? sb[2] : sb[3];
-            const double a = f == 0 ? st[0] : f == 1 ? st[1] : f == 2 ? st[2] : st[3];
-            const double c = f == 0 ? st[1] : f == 1 ? st[2] : f == 2 ? st[3] : st[4];
-            ptr = (uint32_t)(f == 0 ? cp[0] : f == 1 ? cp[1] : f == 2 ? cp[2] : cp[3]);
-            cx = 2u * cx + (bf & 1);
-            cy = 2u * cy + ((bf >> 1) & 1);
-            cz = 2u * cz + ((bf >> 2) & 1);
-            ++L;
-            tin = a;
-            tout = c;
+        if (t.L + 1 == depth) {
+            t.need_pop = true;
+            if (keep) return true;
             continue;
         }
-        // pop the next pending cell; recompute its interval from its faces
-        if (top == 0) return;
-        --top;
-        stk[top * sstride].get(ptr, L, cx, cy, cz);
-        const double h = pow2neg(L);
-        const double xl = xmul((double)cx, h), xh = xmul((double)(cx + 1u), h);
-        const double yl = xmul((double)cy, h), yh = xmul((double)(cy + 1u), h);
-        const double zl = xmul((double)cz, h), zh = xmul((double)(cz + 1u), h);
-        tin = pmax(pmax(r.rt_in, xmul(xsub(xl, o0), i0)),
-                   pmax(xmul(xsub(yl, o1), i1), xmul(xsub(zl, o2), i2)));
-        tout = pmin(pmin(r.rt_out, xmul(xsub(xh, o0), i0)),
-                    pmin(xmul(xsub(yh, o1), i1), xmul(xsub(zh, o2), i2)));
+        if (!keep) {
+            t.need_pop = true;
+            continue;
+        }
+        // push the farther kept children far -> near (kernels.py:639-647);
+        // continue with the nearest kept child in registers
+        const int cb[4] = {c0, c1, c2, c3};
+        uint32_t nptr = 0;
+        int nb = 0;
+        double ntin = 0.0, ntout = 0.0;
+        bool found = false;
+#pragma unroll
+        for (int s = 3; s >= 0; --s) {
+            if (keep & (1 << s)) {
+                if (found) {
+                    stk[t.top * sstride] = Entry::make(nptr, t.L + 1, 2u * t.cx + (nb & 1),
+                                                       2u * t.cy + ((nb >> 1) & 1), 2u * t.cz + ((nb >> 2) & 1));
+                    ++t.top;
+                }
+                found = true;
+                nptr = (uint32_t)cp[s];
+                nb = cb[s];
+                ntin = st[s];
+                ntout = st[s + 1];
+            }
+        }
+        t.ptr = nptr;
+        t.cx = 2u * t.cx + (nb & 1);
+        t.cy = 2u * t.cy + ((nb >> 1) & 1);
+        t.cz = 2u * t.cz + ((nb >> 2) & 1);
+        if (nb & 1) t.xl = xadd(t.xl, hh);
+        if (nb & 2) t.yl = xadd(t.yl, hh);
+        if (nb & 4) t.zl = xadd(t.zl, hh);
+        t.h = hh;
+        ++t.L;
+        t.tin = ntin;
+        t.tout = ntout;
     }
 }
 
+// Whole-ray traversal: walk -> shade batch -> walk ... until exhausted or stopped.
+template <class Entry, class Visitor>
+__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth, const Ray &r, Entry *stk,
+                                         int sstride, Visitor &vis) {
+    Trav t;
+    t.init(r);
+    int32_t cp[4];
+    double st[5];
+    int keep;
+    while (trav_next(t, child, depth, r, stk, sstride, vis, cp, st, keep))
+        if (vis.batch(cp, st, keep)) return;
+}
+
 // ------------------------------------------------------------ fp32 basis
+__device__ __forceinline__ float frcp_fast(float x) { return __fdividef(1.0f, x); }
+// fp32 logistic; MUFU exp + fast reciprocal (abs error ~1e-7, well inside
+// the 1e-4 colour tolerance).  exp(-x) overflowing to inf gives exactly 0.
 __device__ __forceinline__ float sigmoidf_(float x) {
-    if (x >= 0.0f) return __frcp_rn(1.0f + __expf(-x));
-    const float e = __expf(x);
-    return __fdiv_rn(e, 1.0f + e);
+    return frcp_fast(1.0f + __expf(-x));
 }
 
 // Real SH stack at a unit direction, kernels.py:127-164 (fp32)
@@ -287,8 +338,9 @@ __device__ __forceinline__ void sh_basis(float dx, float dy, float dz, const Con
     const float rxy = sqrtf(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)));
     float cphi = 1.0f, sphi = 0.0f;
     if (rxy > 0.0f) {
-        cphi = __fdiv_rn(dx, rxy);
-        sphi = __fdiv_rn(dy, rxy);
+        const float ir = frcp_fast(rxy);
+        cphi = dx * ir;
+        sphi = dy * ir;
     }
     const float z = dz;
     float cm = 1.0f, sm = 0.0f, pmm = 1.0f;
@@ -457,7 +509,9 @@ struct FrameCtx {
     double edit_weight;
 };
 
-template <int NMAX, bool CACHED, bool EDITS, bool VISITS>
+// CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
+// run time by S.sigma != nullptr (scene kernel, per-instance slices).
+template <int NMAX, int CACHED, bool EDITS, bool VISITS>
 struct Shader {
     const TreeView &T;
     const SliceView &S;
@@ -477,12 +531,60 @@ struct Shader {
 
     __device__ __forceinline__ void pop() { ++pops; }
 
-    __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout) {
+    __device__ __forceinline__ void reset(float dx_, float dy_, float dz_) {
+        dx = dx_;
+        dy = dy_;
+        dz = dz_;
+        trans = 1.0;
+        acc0 = acc1 = acc2 = aacc = tacc = 0.0;
+        used = pops = shaded = 0;
+        y_ready = false;
+    }
+
+    __device__ __forceinline__ bool is_cached() const { return CACHED == 1 || (CACHED == 2 && S.sigma != nullptr); }
+
+    // one last-level node's leaves: sigma of the whole batch is loaded up
+    // front (independent loads), then the segments are composited in order,
+    // shifting the batch down one slot per segment (no dynamic indexing)
+    __device__ __forceinline__ bool batch(int32_t *cp, double *st, int keep) {
+        double sg[4] = {0.0, 0.0, 0.0, 0.0};
+        if (is_cached()) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+                if (keep & (1 << s)) {
+                    sg[s] = __ldg(S.sigma + cp[s]);
+                    // warm L1 with the batch's sliced-SH rows (112 B at n_max 2)
+                    const char *q = reinterpret_cast<const char *>(S.q + (size_t)cp[s] * S.q4);
+                    prefetch_l1(q);
+                    prefetch_l1(q + 16 * S.q4 - 1);
+                }
+        }
+#pragma unroll 1
+        for (int s = 0; s < 4 && keep; ++s) {
+            if (keep & 1)
+                if (leaf((uint32_t)cp[0], st[0], st[1], sg[0])) return true;
+            keep >>= 1;
+            cp[0] = cp[1];
+            cp[1] = cp[2];
+            cp[2] = cp[3];
+            st[0] = st[1];
+            st[1] = st[2];
+            st[2] = st[3];
+            st[3] = st[4];
+            sg[0] = sg[1];
+            sg[1] = sg[2];
+            sg[2] = sg[3];
+        }
+        return false;
+    }
+
+    __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout, double sigma_cached) {
         if (VISITS) visit[used] = (int64_t)L;
         ++used;
+        const bool cached = is_cached();
         double sigma;
-        if (CACHED) {
-            sigma = __ldg(S.sigma + L);
+        if (cached) {
+            sigma = sigma_cached;
         } else {
             const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, F.sA, T.C);
             sigma = sp > 0.0 ? sp : 0.0;
@@ -506,7 +608,7 @@ struct Shader {
         }
         // colour: c_ch = sigmoid(sum_j y_j q_j,ch)
         float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        if (CACHED) {
+        if (cached) {
             constexpr int Q4 = Basis<NMAX>::Q4;
             const float4 *qr = S.q + (size_t)L * S.q4;
             float q[4 * Q4];
@@ -571,20 +673,28 @@ struct Shader {
 struct CountVisitor {
     int64_t count = 0;
     __device__ __forceinline__ void pop() {}
-    __device__ __forceinline__ bool leaf(uint32_t, double, double) { ++count; return false; }
+    __device__ __forceinline__ bool batch(int32_t *, double *, int keep) {
+        count += __popc(keep);
+        return false;
+    }
 };
 struct CollectVisitor {
     int64_t *leaf_out;
     double *t0_out, *t1_out;
     int64_t count, cap;
     __device__ __forceinline__ void pop() {}
-    __device__ __forceinline__ bool leaf(uint32_t L, double a, double b) {
-        if (count < cap) {
-            leaf_out[count] = (int64_t)L;
-            t0_out[count] = a;
-            t1_out[count] = b;
+    __device__ __forceinline__ bool batch(int32_t *cp, double *st, int keep) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (keep & (1 << s)) {
+                if (count < cap) {
+                    leaf_out[count] = (int64_t)cp[s];
+                    t0_out[count] = st[s];
+                    t1_out[count] = st[s + 1];
+                }
+                ++count;
+            }
         }
-        ++count;
         return false;
     }
 };

@@ -1,0 +1,433 @@
+// vv_kernels.cuh -- kernel templates and their parameter blocks.
+//
+// Kernels (one thread per ray/pixel, shared-memory traversal stacks):
+//   k_render_rays    render_kernel (kernels.py:410-652) over explicit rays
+//   k_render_camera  Camera.rays + render_kernel + finalize_layer, fused
+//                    (render.py:74-83, 218-240); also the tile-sharded form
+//   k_render_scene   render_instance x L + Algorithm 1 + background
+//                    (compose.py:373-475, render.py:243-251), fused per pixel
+//   k_build_slice    build_slice_kernel (kernels.py:397-407)
+//   k_segments       count/collect_segments_kernel (kernels.py:313-367)
+//   k_repack         payload rows -> padded [w_sigma] / [w_gamma | w_hh] planes
+//   k_unpack_tiles   tile slabs (multi-GPU gather) -> images
+// Instantiations live in vv_launch_*.cu (compiled in parallel); the C ABI in
+// vv_api.cu calls the launch_* entry points declared at the bottom.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include "../../include/voxvid_b200.h"
+#include "vv_device.cuh"
+#include "vv_host_common.h"
+
+namespace vvk {
+using namespace vv;
+
+constexpr int kBlock = 128;
+constexpr int kMaxInst = 16;
+#ifndef VV_CAM_MINB
+#define VV_CAM_MINB 4  // min resident 128-thread blocks per SM for the render kernels
+#endif
+
+// cooperative load of the frame's A/B rows (kernels read them for every leaf)
+__device__ __forceinline__ void load_rows(const TreeView &T, int frame, float *sA, float *sB) {
+    for (int c = threadIdx.x; c < kMaxC; c += blockDim.x) {
+        const bool in = c < T.C;
+        sA[c] = in ? T.basis_a[(size_t)frame * T.C + c] : 0.0f;
+        sB[c] = in ? T.basis_b[(size_t)frame * T.C + c] : 0.0f;
+    }
+}
+
+// ------------------------------------------------------------------ rays
+struct RaysParams {
+    TreeView T;
+    SliceView S;
+    Consts K;
+    int frame;
+    double early_stop, edit_weight, tmin, tmax;
+    const double *origins, *dirs;
+    int64_t n;
+    double *premult, *alpha, *tbar;
+    int32_t *used, *pops, *shaded;
+    const int64_t *visit_start;
+    int64_t *visit_leaf;
+};
+
+template <int NMAX, int CACHED, bool EDITS, class Entry, bool VISITS>
+__global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_rays(const __grid_constant__ RaysParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame, sA, sB);
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= p.n) return;
+    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    const double ox = p.origins[3 * r], oy = p.origins[3 * r + 1], oz = p.origins[3 * r + 2];
+    const double dx = p.dirs[3 * r], dy = p.dirs[3 * r + 1], dz = p.dirs[3 * r + 2];
+    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
+    Shader<NMAX, CACHED, EDITS, VISITS> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+    if (VISITS) sh.visit = p.visit_leaf + p.visit_start[r];
+    Ray ray;
+    if (ray_setup(p.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
+        traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
+    if (VISITS) return;
+    p.premult[3 * r + 0] = sh.acc0;
+    p.premult[3 * r + 1] = sh.acc1;
+    p.premult[3 * r + 2] = sh.acc2;
+    p.alpha[r] = sh.aacc;
+    p.tbar[r] = sh.tacc;
+    if (p.used) p.used[r] = sh.used;
+    if (p.pops) p.pops[r] = sh.pops;
+    if (p.shaded) p.shaded[r] = sh.shaded;
+}
+
+// ------------------------------------------------------------------ camera
+struct CamParams {
+    TreeView T;
+    SliceView S;
+    Consts K;
+    CamView cam;
+    int frame;
+    double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
+    float *rgb, *alpha, *depth;
+    // tile mode (packed != null)
+    float *packed;
+    int tile, shard, n_shards, tiles_x;
+    int blocks_x;                 // tiles per row (image mode)
+};
+
+// block = 16x8 pixels; warp = 16x2 pixels (spatially coherent rays)
+__device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    ix = bx * 16 + (lane & 15);
+    iy = by * 8 + w * 2 + (lane >> 4);
+}
+
+// Block work unit: a kTW x kTH pixel tile (one ray per thread); warps take
+// VV_CHUNK_W-wide chunks of it.
+constexpr int kTW = 16, kTH = 8, kTileRays = kTW * kTH;
+
+// block -> tile origin (image mode: row-major tiles; tile mode: sub-tiles of
+// this shard's tiles); local ray id -> pixel and output slot
+__device__ __forceinline__ void block_origin(const CamParams &p, int &x0, int &y0, long long &my_tile, int &lx0,
+                                             int &ly0) {
+    if (p.packed) {
+        const int subs_x = p.tile / kTW, subs = subs_x * (p.tile / kTH);
+        my_tile = blockIdx.x / subs;
+        const int sub = blockIdx.x % subs;
+        lx0 = (sub % subs_x) * kTW;
+        ly0 = (sub / subs_x) * kTH;
+        const long long tile_id = my_tile * p.n_shards + p.shard;
+        x0 = (int)(tile_id % p.tiles_x) * p.tile + lx0;
+        y0 = (int)(tile_id / p.tiles_x) * p.tile + ly0;
+    } else {
+        my_tile = 0;
+        lx0 = ly0 = 0;
+        x0 = (int)(blockIdx.x % p.blocks_x) * kTW;
+        y0 = (int)(blockIdx.x / p.blocks_x) * kTH;
+    }
+}
+
+#ifndef VV_CHUNK_W
+#define VV_CHUNK_W 8  // warp chunk = VV_CHUNK_W x (32 / VV_CHUNK_W) pixels
+#endif
+__device__ __forceinline__ void local_pixel(int rid, int &dx, int &dy) {
+    constexpr int CW = VV_CHUNK_W, CH = 32 / VV_CHUNK_W;
+    const int chunk = rid >> 5, l = rid & 31;
+    dx = (chunk % (kTW / CW)) * CW + (l % CW);
+    dy = (chunk / (kTW / CW)) * CH + (l / CW);
+}
+
+__device__ __forceinline__ void cam_write(const CamParams &p, int ix, int iy, long long slot, float r, float g,
+                                          float b, float a, float d) {
+    if (p.packed) {
+        float *o = p.packed + slot * 5;
+        o[0] = r; o[1] = g; o[2] = b; o[3] = a; o[4] = d;
+        return;
+    }
+    if (ix >= p.cam.width || iy >= p.cam.height) return;
+    if (p.rgb) {
+        p.rgb[3 * slot + 0] = r;
+        p.rgb[3 * slot + 1] = g;
+        p.rgb[3 * slot + 2] = b;
+    }
+    if (p.alpha) p.alpha[slot] = a;
+    if (p.depth) p.depth[slot] = d;
+}
+
+// Camera kernel: one thread per pixel; a block renders one 16x8-pixel tile
+// (each warp an 8x4-pixel chunk), so the block's warps stay on neighbouring
+// pixels (L1 reuse of node rows and slice rows).  Refill-on-finish
+// (persistent) variants were measured slower: see DESIGN.md.
+template <int NMAX, int CACHED, bool EDITS, class Entry>
+__global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __grid_constant__ CamParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame, sA, sB);
+    __syncthreads();
+    int x0, y0, lx0, ly0;
+    long long my_tile;
+    block_origin(p, x0, y0, my_tile, lx0, ly0);
+    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
+#pragma unroll 1
+    for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
+        const int rid = pass * kBlock + (int)threadIdx.x;
+        int dx_, dy_;
+        local_pixel(rid, dx_, dy_);
+        const int ix = x0 + dx_, iy = y0 + dy_;
+        const long long slot = p.packed ? my_tile * p.tile * p.tile + (long long)(ly0 + dy_) * p.tile + (lx0 + dx_)
+                                        : (long long)iy * p.cam.width + ix;
+        float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
+        if (ix < p.cam.width && iy < p.cam.height) {
+            double dx, dy, dz;
+            camera_ray(p.cam, ix, iy, dx, dy, dz);
+            Shader<NMAX, CACHED, EDITS, false> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+            Ray ray;
+            if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
+                traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
+            finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
+                     a, d);
+        }
+        cam_write(p, ix, iy, slot, r, g, b, a, d);
+    }
+}
+
+// ------------------------------------------------------------------ scene
+struct InstView {
+    TreeView T;
+    SliceView S;      // per-instance frame slice (sigma == null: decode per sample)
+    CamView cam;      // mode 0: pulled-back pose
+    double inv[12];   // mode 1: rows of inv(affine)[:3, :4]
+    int frame, mode;
+};
+
+struct SceneParams {
+    Consts K;
+    CamView cam;
+    InstView inst[kMaxInst];
+    int n_inst;
+    double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
+    double bg0, bg1, bg2;
+    float *image, *alpha, *depth;
+};
+
+template <int NMAX, class Entry>
+__global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__ SceneParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
+    for (int i = 0; i < p.n_inst; ++i) load_rows(p.inst[i].T, p.inst[i].frame, sA[i], sB[i]);
+    __syncthreads();
+    int ix, iy;
+    block_pixel(blockIdx.x, blockIdx.y, ix, iy);
+    if (ix >= p.cam.width || iy >= p.cam.height) return;
+    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    double cdx, cdy, cdz;
+    camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
+    // blended state (compose.py:386-405): I (3), D, A
+    double I0 = 0, I1 = 0, I2 = 0, D = 0, A = 0;
+    for (int i = 0; i < p.n_inst; ++i) {
+        const InstView &v = p.inst[i];
+        double ox, oy, oz, dx, dy, dz, scale = 1.0;
+        bool scaled = false;
+        if (v.mode == 0) {
+            camera_ray(v.cam, ix, iy, dx, dy, dz);
+            ox = v.cam.ox;
+            oy = v.cam.oy;
+            oz = v.cam.oz;
+        } else {
+            // o_t = o @ inv3^T + t ; d_raw = d @ inv3^T ; d_t = d_raw/|d_raw|
+            const double *m = v.inv;
+            ox = xadd(xadd(xadd(xmul(p.cam.ox, m[0]), xmul(p.cam.oy, m[1])), xmul(p.cam.oz, m[2])), m[3]);
+            oy = xadd(xadd(xadd(xmul(p.cam.ox, m[4]), xmul(p.cam.oy, m[5])), xmul(p.cam.oz, m[6])), m[7]);
+            oz = xadd(xadd(xadd(xmul(p.cam.ox, m[8]), xmul(p.cam.oy, m[9])), xmul(p.cam.oz, m[10])), m[11]);
+            const double r0 = xadd(xadd(xmul(cdx, m[0]), xmul(cdy, m[1])), xmul(cdz, m[2]));
+            const double r1 = xadd(xadd(xmul(cdx, m[4]), xmul(cdy, m[5])), xmul(cdz, m[6]));
+            const double r2 = xadd(xadd(xmul(cdx, m[8]), xmul(cdy, m[9])), xmul(cdz, m[10]));
+            const double nrm = sqrt(xadd(xadd(xmul(r0, r0), xmul(r1, r1)), xmul(r2, r2)));
+            dx = xdiv(r0, nrm);
+            dy = xdiv(r1, nrm);
+            dz = xdiv(r2, nrm);
+            scale = xdiv(1.0, nrm);
+            scaled = true;
+        }
+        FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight};
+        Shader<NMAX, 2, true, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
+        Ray ray;
+        if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
+            traverse<Entry>(v.T.child, v.T.depth, ray, stk, blockDim.x, sh);
+        // finalize_layer in float64
+        const double al = sh.aacc;
+        const double safe = al > 1e-300 ? al : 1e-300;
+        double li0 = 0, li1 = 0, li2 = 0;
+        if (al > 0.0) {
+            li0 = xdiv(sh.acc0, safe);
+            li1 = xdiv(sh.acc1, safe);
+            li2 = xdiv(sh.acc2, safe);
+        }
+        double t = xdiv(sh.tacc, safe);
+        if (scaled) t = xmul(t, scale);
+        const double ld = al >= p.alpha_floor ? t : p.far_plane;
+        if (i == 0) {
+            I0 = li0; I1 = li1; I2 = li2; D = ld; A = al;
+        } else {
+            // Algorithm 1 (compose.py:393-404); ties go to the incoming layer
+            const double om_ai = xsub(1.0, al), om_a = xsub(1.0, A);
+            if (ld <= D) {
+                I0 = xadd(xmul(al, li0), xmul(xmul(om_ai, A), I0));
+                I1 = xadd(xmul(al, li1), xmul(xmul(om_ai, A), I1));
+                I2 = xadd(xmul(al, li2), xmul(xmul(om_ai, A), I2));
+                D = ld;
+            } else {
+                I0 = xadd(xmul(A, I0), xmul(xmul(om_a, al), li0));
+                I1 = xadd(xmul(A, I1), xmul(xmul(om_a, al), li1));
+                I2 = xadd(xmul(A, I2), xmul(xmul(om_a, al), li2));
+            }
+            A = xadd(A, xmul(al, om_a));
+        }
+    }
+    if (p.n_inst > 1) {  // unpremultiply the blend (compose.py:457-460)
+        const double safe = A > 1e-300 ? A : 1e-300;
+        if (A > 0.0) {
+            I0 = xdiv(I0, safe);
+            I1 = xdiv(I1, safe);
+            I2 = xdiv(I2, safe);
+        } else {
+            I0 = I1 = I2 = 0.0;
+        }
+    }
+    // composite_background: a * rgb + (1 - a) * bg (render.py:243-251)
+    const double om = xsub(1.0, A);
+    const int64_t pix = (int64_t)iy * p.cam.width + ix;
+    p.image[3 * pix + 0] = (float)xadd(xmul(A, I0), xmul(om, p.bg0));
+    p.image[3 * pix + 1] = (float)xadd(xmul(A, I1), xmul(om, p.bg1));
+    p.image[3 * pix + 2] = (float)xadd(xmul(A, I2), xmul(om, p.bg2));
+    if (p.alpha) p.alpha[pix] = (float)A;
+    if (p.depth) p.depth[pix] = (float)D;
+}
+
+// ------------------------------------------------------------------ slice
+struct SliceParams {
+    TreeView T;
+    Consts K;
+    int frame;
+    int64_t n_leaves;
+    double *sigma;
+    float4 *q;
+    int q4;
+};
+
+template <int NMAX>
+__global__ void __launch_bounds__(256) k_build_slice(const __grid_constant__ SliceParams p) {
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame, sA, sB);
+    __syncthreads();
+    const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (L >= p.n_leaves) return;
+    constexpr int Q4 = Basis<NMAX>::Q4;
+    float q[4 * Q4];
+#pragma unroll
+    for (int i = 0; i < 4 * Q4; ++i) q[i] = 0.0f;
+    double sigma;
+    slice_leaf<NMAX>(p.T, (uint32_t)L, sA, sB, p.K, sigma, q);
+    p.sigma[L] = sigma;
+    float4 *o = p.q + L * p.q4;
+#pragma unroll
+    for (int i = 0; i < Q4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+}
+
+// ------------------------------------------------------------------ traversal only
+struct SegParams {
+    TreeView T;
+    const double *origins, *dirs;
+    int64_t n;
+    double tmin, tmax;
+    int64_t *count;
+    const int64_t *ray_start;
+    int64_t *seg_leaf;
+    double *seg_t0, *seg_t1;
+};
+
+template <class Entry, bool COLLECT>
+__global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ SegParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= p.n) return;
+    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    Ray ray;
+    const bool hit = ray_setup(p.T, p.origins[3 * r], p.origins[3 * r + 1], p.origins[3 * r + 2],
+                               p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
+    if (COLLECT) {
+        const int64_t b = p.ray_start[r];
+        CollectVisitor v{p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
+        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
+    } else {
+        CountVisitor v;
+        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
+        p.count[r] = v.count;
+    }
+}
+
+// ------------------------------------------------------------------ dispatch helpers
+template <class F>
+inline int with_nmax(int nmax, F &&f) {
+    switch (nmax) {
+        case 0: return f(std::integral_constant<int, 0>());
+        case 1: return f(std::integral_constant<int, 1>());
+        case 2: return f(std::integral_constant<int, 2>());
+        case 3: return f(std::integral_constant<int, 3>());
+        default: return set_error(VV_E_UNSUPPORTED, "n_max %d not supported on device (max 3)", nmax);
+    }
+}
+
+inline size_t stack_bytes(int depth, bool wide) {
+    return (size_t)stack_cap(depth) * kBlock * (wide ? sizeof(EntryW) : sizeof(EntryN));
+}
+
+template <class Kern>
+inline int prep_smem(Kern k, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return set_error(VV_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+    }
+    return VV_OK;
+}
+
+inline int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(VV_E_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return VV_OK;
+}
+
+// resident-grid size of a persistent kernel on the current device
+template <class Kern>
+inline unsigned persistent_grid(Kern k, int block, size_t smem, unsigned max_blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    const unsigned resident = (unsigned)(sms * per_sm);
+    return max_blocks < resident ? max_blocks : resident;
+}
+
+// ------------------------------------------------------------------ launchers
+int launch_rays(int nmax, bool cached, bool edits, bool wide, bool visits, const RaysParams &p, unsigned grid,
+                size_t smem, cudaStream_t st);
+// one block per 32x16 tile (max_blocks = tile count)
+int launch_camera(int nmax, bool cached, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
+                  cudaStream_t st);
+int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
+int launch_slice(int nmax, const SliceParams &p, unsigned grid, cudaStream_t st);
+int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
+int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
+                  float *rest, cudaStream_t st);
+int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,
+                  float *rgb, float *alpha, float *depth, cudaStream_t st);
+
+}  // namespace vvk

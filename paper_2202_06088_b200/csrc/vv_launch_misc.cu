@@ -1,0 +1,86 @@
+// vv_launch_misc.cu -- slice build, traversal-only, repack and tile-unpack launches.
+#include "vv_kernels.cuh"
+
+namespace vvk {
+
+__global__ void k_unpack_tiles(const float *__restrict__ packed, int width, int height, int tile,
+                               int n_shards, int tiles_x, int tiles_total, float *rgb, float *alpha,
+                               float *depth) {
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (int64_t)width * height) return;
+    const int ix = (int)(pix % width), iy = (int)(pix / width);
+    const int tid = (iy / tile) * tiles_x + (ix / tile);
+    const int shard = tid % n_shards, k = tid / n_shards;
+    const int per_shard = (tiles_total + n_shards - 1) / n_shards;
+    const int64_t slot = ((int64_t)shard * per_shard + k) * tile * tile + (int64_t)(iy % tile) * tile + (ix % tile);
+    const float *s = packed + slot * 5;
+    if (rgb) {
+        rgb[3 * pix + 0] = s[0];
+        rgb[3 * pix + 1] = s[1];
+        rgb[3 * pix + 2] = s[2];
+    }
+    if (alpha) alpha[pix] = s[3];
+    if (depth) depth[pix] = s[4];
+}
+
+// ------------------------------------------------------------------ repack
+// leaf rows (P = 2C + 3K floats) -> sig plane (sig4 float4 per row) and
+// rest plane ([w_gamma pad to 4 | w_hh pad to 4], rest4 float4 per row)
+__global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int sig4,
+                         int rest4, int hh_off4, float *sig, float *rest) {
+    const int sigw = 4 * sig4, restw = 4 * rest4;
+    const int64_t total = rows * (int64_t)(sigw + restw);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / (sigw + restw);
+        const int j = (int)(i % (sigw + restw));
+        const float *s = src + row * P;
+        if (j < sigw) {
+            sig[row * sigw + j] = j < C ? s[j] : 0.0f;
+        } else {
+            const int k = j - sigw;
+            float v = 0.0f;
+            if (k < C) v = s[C + k];
+            else if (k >= 4 * hh_off4 && k < 4 * hh_off4 + K3) v = s[2 * C + (k - 4 * hh_off4)];
+            rest[row * restw + k] = v;
+        }
+    }
+}
+
+
+int launch_slice(int nmax, const SliceParams &p, unsigned grid, cudaStream_t st) {
+    return with_nmax(nmax, [&](auto N) {
+        k_build_slice<decltype(N)::value><<<grid, 256, 0, st>>>(p);
+        return check_launch("build_slice");
+    });
+}
+
+template <class Entry, bool COLLECT>
+static int go_seg(const SegParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    auto kern = k_segments<Entry, COLLECT>;
+    int r = prep_smem(kern, smem);
+    if (r) return r;
+    kern<<<grid, kBlock, smem, st>>>(p);
+    return check_launch("segments");
+}
+
+int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    if (wide) return collect ? go_seg<EntryW, true>(p, grid, smem, st) : go_seg<EntryW, false>(p, grid, smem, st);
+    return collect ? go_seg<EntryN, true>(p, grid, smem, st) : go_seg<EntryN, false>(p, grid, smem, st);
+}
+
+int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
+                  float *rest, cudaStream_t st) {
+    k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, sig4, rest4, hh_off4, sig, rest);
+    return check_launch("repack");
+}
+
+int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,
+                  float *rgb, float *alpha, float *depth, cudaStream_t st) {
+    const int64_t npix = (int64_t)width * height;
+    k_unpack_tiles<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(packed, width, height, tile, n_shards, tiles_x,
+                                                                      tiles_total, rgb, alpha, depth);
+    return check_launch("unpack_tiles");
+}
+
+}  // namespace vvk

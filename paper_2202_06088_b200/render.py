@@ -148,12 +148,26 @@ class LayerImages:
         return LayerImages(c(self.rgb), c(self.alpha), c(self.depth))
 
 
+_SLICE_MODES = {"auto": 0, "per_sample": 1, "per_frame": 2}
+
+
 @dataclass(frozen=True)
 class RenderOptions:
+    """render.py:148-153, plus ``frame_slice``: how leaves are decoded when no
+    FrameSlice is passed -- "per_sample" (inside the render kernel, like the
+    reference's uncached branch), "per_frame" (one coalesced pass over all
+    leaves into a transient device slice, then render from it) or "auto".
+    All three are bitwise identical."""
+
     early_stop: float = 1e-4
     far_plane: float = 1e9
     alpha_floor: float = 1e-3
     edit_weight: float = 1.0
+    frame_slice: str = "auto"
+
+    def __post_init__(self):
+        if self.frame_slice not in _SLICE_MODES:
+            raise ValueError(f"frame_slice must be one of {sorted(_SLICE_MODES)}, got {self.frame_slice!r}")
 
     def c_struct(self, tmin: float = 0.0, tmax: float = 1e30) -> _native.RenderOpts:
         o = _native.RenderOpts()
@@ -163,6 +177,7 @@ class RenderOptions:
         o.edit_weight = float(self.edit_weight)
         o.tmin = float(tmin)
         o.tmax = float(tmax)
+        o.frame_slice = _SLICE_MODES[self.frame_slice]
         return o
 
 
