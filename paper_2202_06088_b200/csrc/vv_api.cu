@@ -43,9 +43,8 @@ struct vv_slice {
     const vv_tree *tree;
     int device;
     int32_t frame;
-    double *d_sigma;
-    float4 *d_q;
-    int q4;
+    float4 *d_rec;  // (n_leaves, rec4) records [q | pad | sigma]
+    int rec4;
     int64_t n_leaves;
 };
 
@@ -125,27 +124,24 @@ vv_render_opts default_opts() {
 }
 
 SliceView slice_view(const vv_slice *c) {
-    SliceView s{nullptr, nullptr, 0};
+    SliceView s{nullptr, 0};
     if (c) {
-        s.sigma = c->d_sigma;
-        s.q = c->d_q;
-        s.q4 = c->q4;
+        s.rec = c->d_rec;
+        s.rec4 = c->rec4;
     }
     return s;
 }
 
-int launch_build_slice(const vv_tree *t, int frame, double *sigma, float4 *q, int q4, cudaStream_t st) {
+int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
     p.T = t->view;
     p.K = make_consts(t->n_max);
     p.frame = frame;
     p.n_leaves = t->n_leaves;
-    p.sigma = sigma;
-    p.q = q;
-    p.q4 = q4;
-    const unsigned grid = (unsigned)((t->n_leaves + 255) / 256);
-    return launch_slice(t->n_max, p, grid, st);
+    p.rec = rec;
+    p.rec4 = rec4;
+    return launch_slice(t->n_max, p, st);
 }
 
 // Transient per-frame slice in the device's stream-ordered pool; freed
@@ -171,20 +167,25 @@ void pool_setup(int device) {
     });
 }
 
-// VV_SLICE_AUTO: decode every leaf once per frame when the frame's rays would
-// visit a comparable number of leaves anyway (each visited leaf is shared by
-// several neighbouring rays); otherwise decode per visited sample.
-bool want_slice(const vv_tree *t, int64_t n_rays, int policy) {
-    if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return false;
-    if (policy == VV_SLICE_PER_FRAME) return true;
-    return t->n_leaves <= 2 * n_rays;
+// Leaf-decode mode for a call without a user cache: 0 = per sample (inside
+// the render kernel), 1 = per-frame slice pre-pass.  VV_SLICE_AUTO takes the
+// pre-pass when the call's rays are numerous enough that every leaf is
+// likely decoded several times per frame anyway.  (Decoding lazily on
+// first visit inside the render kernel was measured slower: the claim
+// atomics, release fences and sub-warp decode bursts cost more than the
+// skipped decodes.)
+int decode_mode(const vv_tree *t, int64_t n_rays, int policy) {
+    if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return 0;
+    if (policy == VV_SLICE_PER_FRAME) return 1;
+    return t->n_leaves <= 2 * n_rays ? 1 : 0;
 }
 
+// Transient per-call slice from the stream-ordered pool (freed, stream
+// ordered, when the call returns).
 int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr) {
     pool_setup(t->device);
-    const int q4 = (3 * t->S + 3) / 4;
-    const size_t sig_b = ((size_t)t->n_leaves * sizeof(double) + 255) & ~(size_t)255;
-    const size_t bytes = sig_b + (size_t)t->n_leaves * q4 * sizeof(float4);
+    const int rec4 = slice_rec4(t->S);
+    const size_t bytes = (size_t)t->n_leaves * rec4 * sizeof(float4);
     cudaError_t e = cudaMallocAsync(&tr.mem, bytes, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -193,10 +194,9 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
                          cudaGetErrorString(e));
     }
     tr.st = st;
-    sv.sigma = reinterpret_cast<double *>(tr.mem);
-    sv.q = reinterpret_cast<float4 *>(reinterpret_cast<char *>(tr.mem) + sig_b);
-    sv.q4 = q4;
-    return launch_build_slice(t, frame, const_cast<double *>(sv.sigma), const_cast<float4 *>(sv.q), q4, st);
+    sv.rec = reinterpret_cast<float4 *>(tr.mem);
+    sv.rec4 = rec4;
+    return launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st);
 }
 
 int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool host_src) {
@@ -379,15 +379,14 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
     s->device = t->device;
     s->frame = frame;
     s->n_leaves = t->n_leaves;
-    s->q4 = (3 * t->S + 3) / 4;
+    s->rec4 = slice_rec4(t->S);
     const int64_t nrows = std::max<int64_t>(t->n_leaves, 1);
-    if (cudaMalloc(&s->d_sigma, nrows * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&s->d_q, nrows * s->q4 * sizeof(float4)) != cudaSuccess) {
+    if (cudaMalloc(&s->d_rec, nrows * s->rec4 * sizeof(float4)) != cudaSuccess) {
         cudaGetLastError();
         vv_slice_free(s);
         return set_error(VV_E_NOMEM, "slice allocation failed");
     }
-    rc = launch_build_slice(t, frame, s->d_sigma, s->d_q, s->q4, (cudaStream_t)stream);
+    rc = launch_build_slice(t, frame, s->d_rec, s->rec4, (cudaStream_t)stream);
     if (rc) {
         vv_slice_free(s);
         return rc;
@@ -399,8 +398,7 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
 int vv_slice_free(vv_slice *s) {
     if (!s) return VV_OK;
     DeviceGuard g(s->device);
-    cudaFree(s->d_sigma);
-    cudaFree(s->d_q);
+    cudaFree(s->d_rec);
     delete s;
     return VV_OK;
 }
@@ -416,10 +414,14 @@ int vv_slice_export(const vv_slice *s, double *sigma, float *q, void *stream) {
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int S3 = 3 * s->tree->S;
-    if (sigma) VV_CUDA(cudaMemcpyAsync(sigma, s->d_sigma, s->n_leaves * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (q && s->n_leaves > 0)
-        VV_CUDA(cudaMemcpy2DAsync(q, S3 * sizeof(float), s->d_q, s->q4 * sizeof(float4), S3 * sizeof(float),
-                                  s->n_leaves, cudaMemcpyDeviceToDevice, st));
+    const size_t pitch = (size_t)s->rec4 * sizeof(float4);
+    if (s->n_leaves == 0) return VV_OK;
+    if (sigma)
+        VV_CUDA(cudaMemcpy2DAsync(sigma, sizeof(double), reinterpret_cast<const char *>(s->d_rec) + pitch - 8, pitch,
+                                  sizeof(double), s->n_leaves, cudaMemcpyDeviceToDevice, st));
+    if (q)
+        VV_CUDA(cudaMemcpy2DAsync(q, S3 * sizeof(float), s->d_rec, pitch, S3 * sizeof(float), s->n_leaves,
+                                  cudaMemcpyDeviceToDevice, st));
     return VV_OK;
 }
 
@@ -463,12 +465,12 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
     const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;
-    if (!cache && want_slice(t, n, opts.frame_slice)) {
+    const int mode = cache ? 1 : decode_mode(t, n, opts.frame_slice);
+    if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
-    const bool cached = p.S.sigma != nullptr, edits = t->has_edits;
-    return launch_rays(t->n_max, cached, edits, wide, visits, p, grid, smem, st);
+    return launch_rays(t->n_max, mode, t->has_edits, wide, visits, p, grid, smem, st);
 }
 
 int vv_render_rays(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -535,12 +537,12 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     const size_t smem = stack_bytes(t->depth, wide);
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;
-    if (!cache && want_slice(t, (int64_t)cam->width * cam->height, opts.frame_slice)) {
+    const int mode = cache ? 1 : decode_mode(t, (int64_t)cam->width * cam->height, opts.frame_slice);
+    if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
-    const bool cached = p.S.sigma != nullptr, edits = t->has_edits;
-    return launch_camera(t->n_max, cached, edits, wide, p, grid_blocks, smem, st);
+    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st);
 }
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -619,13 +621,14 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr[kMaxInst];
     for (int i = 0; i < n_inst; ++i) {
-        p.inst[i].S = SliceView{nullptr, nullptr, 0};
+        p.inst[i].S = SliceView{nullptr, 0};
         int same = -1;
         for (int j = 0; j < i; ++j)
-            if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.sigma) same = j;
+            if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.rec) same = j;
+        const int mode = decode_mode(inst[i].tree, (int64_t)cam->width * cam->height, opts.frame_slice);
         if (same >= 0) {
             p.inst[i].S = p.inst[same].S;
-        } else if (want_slice(inst[i].tree, (int64_t)cam->width * cam->height, opts.frame_slice)) {
+        } else if (mode != 0) {
             int r = build_transient(inst[i].tree, inst[i].frame, st, p.inst[i].S, tr[i]);
             if (r) return r;
         }

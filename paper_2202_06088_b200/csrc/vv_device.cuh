@@ -60,11 +60,17 @@ struct TreeView {
     int depth, C, sig4, rest4, hh_off4, frames, nmax;
 };
 
+// Per-frame slice: one record per leaf, [q (3S fp32) | pad | sigma (f64)],
+// rec4 float4 long -- 128 bytes (one cache line) at n_max = 2.
 struct SliceView {
-    const double *sigma;  // (n_leaves)
-    const float4 *q;      // (n_leaves, q4)
-    int q4;
+    const float4 *rec;  // (n_leaves, rec4) or null (decode per sample)
+    int rec4;           // float4 per record = ceil((3S + 2) / 4)
+    __device__ __forceinline__ const float4 *row(uint32_t L) const { return rec + (size_t)L * rec4; }
+    __device__ __forceinline__ double sigma(uint32_t L) const {
+        return __ldg(reinterpret_cast<const double *>(rec + (size_t)(L + 1) * rec4) - 1);
+    }
 };
+__host__ __device__ constexpr int slice_rec4(int S) { return (3 * S + 2 + 3) / 4; }
 
 // ------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
@@ -120,40 +126,46 @@ __device__ __forceinline__ bool ray_setup(const TreeView &T, double ox, double o
 }
 
 // ------------------------------------------------------------ stack entries
-// narrow: ptr + (level | cx<<4 | cy<<13 | cz<<22), depth <= 9
+// A cell is identified by its level L and packed coordinates pc.  Packing
+// keeps each axis in its own bit field so a child's code is
+// (pc << 1) | spread(child bits); the fields never carry into each other.
+// narrow (depth <= 9): 8-byte entry {ptr, pc | L << 27}, 9 bits per axis
 struct EntryN {
-    uint32_t ptr, code;
-    __device__ __forceinline__ static EntryN make(uint32_t p, int L, uint32_t x, uint32_t y, uint32_t z) {
-        EntryN e;
-        e.ptr = p;
-        e.code = (uint32_t)L | (x << 4) | (y << 13) | (z << 22);
-        return e;
+    using Code = uint32_t;
+    static constexpr int kShift = 9;
+    static constexpr Code kMask = 511u;
+    static constexpr uint32_t kBytes = 8;
+    __device__ __forceinline__ static Code spread(int b) {
+        return (Code)(b & 1) | ((Code)(b & 2) << 8) | ((Code)(b & 4) << 16);
     }
-    __device__ __forceinline__ void get(uint32_t &p, int &L, uint32_t &x, uint32_t &y, uint32_t &z) const {
-        p = ptr;
-        L = (int)(code & 15u);
-        x = (code >> 4) & 511u;
-        y = (code >> 13) & 511u;
-        z = (code >> 22) & 511u;
+    __device__ __forceinline__ static void store(uint32_t addr, uint32_t ptr, int L, Code pc) {
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(ptr), "r"(pc | ((uint32_t)L << 27)));
+    }
+    __device__ __forceinline__ static void load(uint32_t addr, uint32_t &ptr, int &L, Code &pc) {
+        uint32_t c;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(ptr), "=r"(c) : "r"(addr));
+        L = (int)(c >> 27);
+        pc = c & 0x7FFFFFFu;
     }
 };
-// wide: depth <= 20
-struct __align__(16) EntryW {
-    uint32_t ptr, x, y, zl;
-    __device__ __forceinline__ static EntryW make(uint32_t p, int L, uint32_t x_, uint32_t y_, uint32_t z_) {
-        EntryW e;
-        e.ptr = p;
-        e.x = x_;
-        e.y = y_;
-        e.zl = z_ | ((uint32_t)L << 24);
-        return e;
+// wide (depth <= 20): 16-byte entry {ptr, L, pc (64-bit)}, 21 bits per axis
+struct EntryW {
+    using Code = unsigned long long;
+    static constexpr int kShift = 21;
+    static constexpr Code kMask = (1ull << 21) - 1;
+    static constexpr uint32_t kBytes = 16;
+    __device__ __forceinline__ static Code spread(int b) {
+        return (Code)(b & 1) | ((Code)(b & 2) << 20) | ((Code)(b & 4) << 40);
     }
-    __device__ __forceinline__ void get(uint32_t &p, int &L, uint32_t &x_, uint32_t &y_, uint32_t &z_) const {
-        p = ptr;
-        x_ = x;
-        y_ = y;
-        z_ = zl & 0xFFFFFFu;
-        L = (int)(zl >> 24);
+    __device__ __forceinline__ static void store(uint32_t addr, uint32_t ptr, int L, Code pc) {
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(ptr), "r"((uint32_t)L),
+                     "r"((uint32_t)pc), "r"((uint32_t)(pc >> 32)));
+    }
+    __device__ __forceinline__ static void load(uint32_t addr, uint32_t &ptr, int &L, Code &pc) {
+        uint32_t l, lo, hi;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(ptr), "=r"(l), "=r"(lo), "=r"(hi) : "r"(addr));
+        L = (int)l;
+        pc = ((Code)hi << 32) | lo;
     }
 };
 
@@ -193,17 +205,23 @@ __device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) 
     aa = ta;
 }
 
-// Resumable traversal state of one ray (persistent kernels keep it across
-// refills of other lanes).
+// Resumable traversal state of one ray.  The stack lives in shared memory
+// at a 32-bit shared-window address (one slot per level of pending
+// siblings, `stride` bytes between a thread's consecutive slots).
+template <class Entry>
 struct Trav {
-    uint32_t ptr, cx, cy, cz;
-    int L, top;
-    double xl, yl, zl, h;  // node low corner and size (exact)
+    uint32_t ptr;
+    typename Entry::Code pc;  // packed cell coordinates of the current node
+    int L;
+    uint32_t sp;              // shared address of the next free stack slot
+    double xl, yl, zl, h;     // node low corner and size (exact)
     double tin, tout;
     bool need_pop;
-    __device__ __forceinline__ void init(const Ray &r) {
-        ptr = cx = cy = cz = 0;
-        L = top = 0;
+    __device__ __forceinline__ void init(const Ray &r, uint32_t stack_base) {
+        ptr = 0;
+        pc = 0;
+        L = 0;
+        sp = stack_base;
         xl = yl = zl = 0.0;
         h = 1.0;
         tin = r.rt_in;
@@ -215,21 +233,21 @@ struct Trav {
 // Advance the walk until the next last-level node with kept leaves; fills
 // cp/st/keep and returns true, or returns false when the tree is exhausted.
 template <class Entry, class Visitor>
-__device__ __forceinline__ bool trav_next(Trav &t, const int32_t *__restrict__ child, int depth, const Ray &r,
-                                          Entry *stk, int sstride, Visitor &vis, int32_t *cp, double *st,
-                                          int &keep) {
+__device__ __forceinline__ bool trav_next(Trav<Entry> &t, const int32_t *__restrict__ child, int depth, const Ray &r,
+                                          uint32_t stack_base, uint32_t stride, Visitor &vis, int32_t *cp,
+                                          double *st, int &keep) {
     const double o0 = r.o0, o1 = r.o1, o2 = r.o2, i0 = r.i0, i1 = r.i1, i2 = r.i2;
     const int mirror = r.mirror;
     while (true) {
         if (t.need_pop) {
-            if (t.top == 0) return false;
-            --t.top;
-            stk[t.top * sstride].get(t.ptr, t.L, t.cx, t.cy, t.cz);
+            if (t.sp == stack_base) return false;
+            t.sp -= stride;
+            Entry::load(t.sp, t.ptr, t.L, t.pc);
             // recompute the popped cell's interval from its six faces
             t.h = pow2neg(t.L);
-            t.xl = xmul((double)t.cx, t.h);
-            t.yl = xmul((double)t.cy, t.h);
-            t.zl = xmul((double)t.cz, t.h);
+            t.xl = xmul((double)(uint32_t)(t.pc & Entry::kMask), t.h);
+            t.yl = xmul((double)(uint32_t)((t.pc >> Entry::kShift) & Entry::kMask), t.h);
+            t.zl = xmul((double)(uint32_t)((t.pc >> (2 * Entry::kShift)) & Entry::kMask), t.h);
             const double xh = xadd(t.xl, t.h), yh = xadd(t.yl, t.h), zh = xadd(t.zl, t.h);
             t.tin = pmax(pmax(r.rt_in, xmul(xsub(t.xl, o0), i0)),
                          pmax(xmul(xsub(t.yl, o1), i1), xmul(xsub(t.zl, o2), i2)));
@@ -275,22 +293,23 @@ __device__ __forceinline__ bool trav_next(Trav &t, const int32_t *__restrict__ c
             t.need_pop = true;
             continue;
         }
-        // push the farther kept children far -> near (kernels.py:639-647);
-        // continue with the nearest kept child in registers
+        // push the farther kept children far -> near (kernels.py:639-647),
+        // predicated, then continue with the nearest kept child in registers
         const int cb[4] = {c0, c1, c2, c3};
+        const typename Entry::Code pc2 = t.pc << 1;
+#pragma unroll
+        for (int s = 3; s >= 1; --s) {
+            if (((keep >> s) & 1) && (keep & ((1 << s) - 1))) {
+                Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
+                t.sp += stride;
+            }
+        }
         uint32_t nptr = 0;
         int nb = 0;
         double ntin = 0.0, ntout = 0.0;
-        bool found = false;
 #pragma unroll
         for (int s = 3; s >= 0; --s) {
-            if (keep & (1 << s)) {
-                if (found) {
-                    stk[t.top * sstride] = Entry::make(nptr, t.L + 1, 2u * t.cx + (nb & 1),
-                                                       2u * t.cy + ((nb >> 1) & 1), 2u * t.cz + ((nb >> 2) & 1));
-                    ++t.top;
-                }
-                found = true;
+            if ((keep >> s) & 1) {
                 nptr = (uint32_t)cp[s];
                 nb = cb[s];
                 ntin = st[s];
@@ -298,9 +317,7 @@ __device__ __forceinline__ bool trav_next(Trav &t, const int32_t *__restrict__ c
             }
         }
         t.ptr = nptr;
-        t.cx = 2u * t.cx + (nb & 1);
-        t.cy = 2u * t.cy + ((nb >> 1) & 1);
-        t.cz = 2u * t.cz + ((nb >> 2) & 1);
+        t.pc = pc2 | Entry::spread(nb);
         if (nb & 1) t.xl = xadd(t.xl, hh);
         if (nb & 2) t.yl = xadd(t.yl, hh);
         if (nb & 4) t.zl = xadd(t.zl, hh);
@@ -311,16 +328,20 @@ __device__ __forceinline__ bool trav_next(Trav &t, const int32_t *__restrict__ c
     }
 }
 
-// Whole-ray traversal: walk -> shade batch -> walk ... until exhausted or stopped.
+// Whole-ray traversal: walk -> shade batch -> walk ... until exhausted or
+// stopped.  `stk` points at this thread's first stack slot in shared memory;
+// consecutive slots are `sstride` entries apart.
 template <class Entry, class Visitor>
-__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth, const Ray &r, Entry *stk,
+__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth, const Ray &r, void *stk,
                                          int sstride, Visitor &vis) {
-    Trav t;
-    t.init(r);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(stk);
+    const uint32_t stride = (uint32_t)sstride * Entry::kBytes;
+    Trav<Entry> t;
+    t.init(r, base);
     int32_t cp[4];
     double st[5];
     int keep;
-    while (trav_next(t, child, depth, r, stk, sstride, vis, cp, st, keep))
+    while (trav_next(t, child, depth, r, base, stride, vis, cp, st, keep))
         if (vis.batch(cp, st, keep)) return;
 }
 
@@ -432,13 +453,23 @@ __device__ __forceinline__ void slice_col(const float *R, const float *wh, int l
     }
 }
 
+// row loads: read-only global path (__ldg) or plain loads (shared staging)
+template <bool G>
+__device__ __forceinline__ float4 ld4(const float4 *p) {
+    if (G) return __ldg(p);
+    float4 v;
+    asm volatile("ld.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
 // Decoded fp32 hyper-angle sigmoid s = sigmoid(B[t] . w_gamma) (fp32 dot).
+template <bool G = true>
 __device__ __forceinline__ float gamma_s(const float4 *__restrict__ rest_row, const float *sB, int C) {
     float gp = 0.0f;
     const int C4 = (C + 3) >> 2;
 #pragma unroll 4
     for (int i = 0; i < C4; ++i) {
-        const float4 v = __ldg(rest_row + i);
+        const float4 v = ld4<G>(rest_row + i);
         const int c = 4 * i;
         gp = __fmaf_rn(sB[c], v.x, gp);
         if (c + 1 < C) gp = __fmaf_rn(sB[c + 1], v.y, gp);
@@ -449,12 +480,13 @@ __device__ __forceinline__ float gamma_s(const float4 *__restrict__ rest_row, co
 }
 
 // sigma_pre = sum_c A[t,c] * w_sigma[c], float64, sequential (kernels.py:374-381)
+template <bool G = true>
 __device__ __forceinline__ double sigma_pre(const float4 *__restrict__ sig_row, const float *sA, int C) {
     double sp = 0.0;
     const int C4 = (C + 3) >> 2;
 #pragma unroll 4
     for (int i = 0; i < C4; ++i) {
-        const float4 v = __ldg(sig_row + i);
+        const float4 v = ld4<G>(sig_row + i);
         const int c = 4 * i;
         sp = xadd(sp, xmul((double)sA[c], (double)v.x));
         if (c + 1 < C) sp = xadd(sp, xmul((double)sA[c + 1], (double)v.y));
@@ -464,12 +496,12 @@ __device__ __forceinline__ double sigma_pre(const float4 *__restrict__ sig_row, 
     return sp;
 }
 
-template <int NMAX>
+template <int NMAX, bool G = true>
 __device__ __forceinline__ void load_hh(const float4 *__restrict__ rest_row, int hh_off4, float *wh) {
     constexpr int H4 = Basis<NMAX>::HH4;
 #pragma unroll
     for (int i = 0; i < H4; ++i) {
-        const float4 v = __ldg(rest_row + hh_off4 + i);
+        const float4 v = ld4<G>(rest_row + hh_off4 + i);
         wh[4 * i + 0] = v.x;
         wh[4 * i + 1] = v.y;
         wh[4 * i + 2] = v.z;
@@ -479,18 +511,15 @@ __device__ __forceinline__ void load_hh(const float4 *__restrict__ rest_row, int
 
 // Full per-leaf slice (build_slice_kernel, kernels.py:397-407): sigma (f64)
 // and q (fp32, channel-interleaved 3S).
-template <int NMAX>
-__device__ __forceinline__ void slice_leaf(const TreeView &T, uint32_t row, const float *sA,
-                                           const float *sB, const Consts &K, double &sigma,
-                                           float *q) {
-    const double sp = sigma_pre(T.sig + (size_t)row * T.sig4, sA, T.C);
-    sigma = sp > 0.0 ? sp : 0.0;  // max(0.0, sp)
-    const float4 *rr = T.rest + (size_t)row * T.rest4;
-    const float s = gamma_s(rr, sB, T.C);
+// HH->SH slice of one leaf at the frame's hyper angle: q (fp32, 3S)
+template <int NMAX, bool G = true>
+__device__ __forceinline__ void slice_q(const float4 *rest_row, int C, int hh_off4, const float *sB, const Consts &K,
+                                        float *q) {
+    const float s = gamma_s<G>(rest_row, sB, C);
     float R[Basis<NMAX>::NPAIRS];
     radial<NMAX>(s, K, R);
     float wh[4 * Basis<NMAX>::HH4];
-    load_hh<NMAX>(rr, T.hh_off4, wh);
+    load_hh<NMAX, G>(rest_row, hh_off4, wh);
 #pragma unroll
     for (int l = 0; l <= NMAX; ++l)
 #pragma unroll
@@ -498,6 +527,17 @@ __device__ __forceinline__ void slice_leaf(const TreeView &T, uint32_t row, cons
             const int j = l * l + l + m;
             slice_col<NMAX>(R, wh, l, m, q[3 * j + 0], q[3 * j + 1], q[3 * j + 2]);
         }
+}
+
+// Full per-leaf slice (build_slice_kernel, kernels.py:397-407): sigma (f64)
+// and q (fp32, channel-interleaved 3S).
+template <int NMAX, bool G = true>
+__device__ __forceinline__ void slice_rows(const float4 *sig_row, const float4 *rest_row, int C, int hh_off4,
+                                           const float *sA, const float *sB, const Consts &K, double &sigma,
+                                           float *q) {
+    const double sp = sigma_pre<G>(sig_row, sA, C);
+    sigma = sp > 0.0 ? sp : 0.0;  // max(0.0, sp)
+    slice_q<NMAX, G>(rest_row, C, hh_off4, sB, K, q);
 }
 
 // ------------------------------------------------------------ shading visitor
@@ -510,7 +550,7 @@ struct FrameCtx {
 };
 
 // CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
-// run time by S.sigma != nullptr (scene kernel, per-instance slices).
+// run time by S.rec != nullptr (scene kernel, per-instance slices).
 template <int NMAX, int CACHED, bool EDITS, bool VISITS>
 struct Shader {
     const TreeView &T;
@@ -541,7 +581,7 @@ struct Shader {
         y_ready = false;
     }
 
-    __device__ __forceinline__ bool is_cached() const { return CACHED == 1 || (CACHED == 2 && S.sigma != nullptr); }
+    __device__ __forceinline__ bool is_cached() const { return CACHED == 1 || (CACHED == 2 && S.rec != nullptr); }
 
     // one last-level node's leaves: sigma of the whole batch is loaded up
     // front (independent loads), then the segments are composited in order,
@@ -552,11 +592,12 @@ struct Shader {
 #pragma unroll
             for (int s = 0; s < 4; ++s)
                 if (keep & (1 << s)) {
-                    sg[s] = __ldg(S.sigma + cp[s]);
-                    // warm L1 with the batch's sliced-SH rows (112 B at n_max 2)
-                    const char *q = reinterpret_cast<const char *>(S.q + (size_t)cp[s] * S.q4);
+                    // sigma from the record's last 8 bytes; warm L1 with the
+                    // whole record (one 128-byte line at n_max 2)
+                    sg[s] = S.sigma((uint32_t)cp[s]);
+                    const char *q = reinterpret_cast<const char *>(S.row((uint32_t)cp[s]));
                     prefetch_l1(q);
-                    prefetch_l1(q + 16 * S.q4 - 1);
+                    if (16 * S.rec4 > 128) prefetch_l1(q + 16 * S.rec4 - 1);
                 }
         }
 #pragma unroll 1
@@ -581,9 +622,12 @@ struct Shader {
     __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout, double sigma_cached) {
         if (VISITS) visit[used] = (int64_t)L;
         ++used;
-        const bool cached = is_cached();
+        constexpr int Q4 = Basis<NMAX>::Q4;
+        // sliced coefficients: from the frame slice record, or decoded now
+        // from the payload (render_kernel's uncached branch)
+        const bool from_rec = is_cached();
         double sigma;
-        if (cached) {
+        if (from_rec) {
             sigma = sigma_cached;
         } else {
             const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, F.sA, T.C);
@@ -608,10 +652,9 @@ struct Shader {
         }
         // colour: c_ch = sigmoid(sum_j y_j q_j,ch)
         float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        if (cached) {
-            constexpr int Q4 = Basis<NMAX>::Q4;
-            const float4 *qr = S.q + (size_t)L * S.q4;
+        if (from_rec) {
             float q[4 * Q4];
+            const float4 *qr = S.row(L);
 #pragma unroll
             for (int i = 0; i < Q4; ++i) {
                 const float4 v = __ldg(qr + i);

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_rays(const __gri
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.n) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     const double ox = p.origins[3 * r], oy = p.origins[3 * r + 1], oz = p.origins[3 * r + 2];
     const double dx = p.dirs[3 * r], dy = p.dirs[3 * r + 1], dz = p.dirs[3 * r + 2];
     FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __g
     int x0, y0, lx0, ly0;
     long long my_tile;
     block_origin(p, x0, y0, my_tile, lx0, ly0);
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
 #pragma unroll 1
     for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
     int ix, iy;
     block_pixel(blockIdx.x, blockIdx.y, ix, iy);
     if (ix >= p.cam.width || iy >= p.cam.height) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     double cdx, cdy, cdz;
     camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
     // blended state (compose.py:386-405): I (3), D, A
@@ -315,28 +315,34 @@ struct SliceParams {
     Consts K;
     int frame;
     int64_t n_leaves;
-    double *sigma;
-    float4 *q;
-    int q4;
+    float4 *rec;  // (n_leaves, rec4) slice records
+    int rec4;
 };
 
+// build_slice_kernel (kernels.py:397-407): one thread per leaf.  (Bound by
+// L1 wavefronts of the per-thread row loads: 27 LDG.128 per warp, each
+// touching 32 lines; see DESIGN.md for the measured alternatives.)
+constexpr int kSliceBlock = 256;
 template <int NMAX>
-__global__ void __launch_bounds__(256) k_build_slice(const __grid_constant__ SliceParams p) {
+__global__ void __launch_bounds__(kSliceBlock) k_build_slice(const __grid_constant__ SliceParams p) {
     __shared__ float sA[kMaxC], sB[kMaxC];
     load_rows(p.T, p.frame, sA, sB);
     __syncthreads();
-    const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t L = (int64_t)blockIdx.x * kSliceBlock + threadIdx.x;
     if (L >= p.n_leaves) return;
-    constexpr int Q4 = Basis<NMAX>::Q4;
-    float q[4 * Q4];
+    constexpr int R4 = slice_rec4(Basis<NMAX>::S);
+    float q[4 * R4];
 #pragma unroll
-    for (int i = 0; i < 4 * Q4; ++i) q[i] = 0.0f;
+    for (int i = 0; i < 4 * R4; ++i) q[i] = 0.0f;
     double sigma;
-    slice_leaf<NMAX>(p.T, (uint32_t)L, sA, sB, p.K, sigma, q);
-    p.sigma[L] = sigma;
-    float4 *o = p.q + L * p.q4;
+    slice_rows<NMAX>(p.T.sig + (size_t)L * p.T.sig4, p.T.rest + (size_t)L * p.T.rest4, p.T.C, p.T.hh_off4, sA, sB,
+                     p.K, sigma, q);
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+    q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
+    q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
+    float4 *o = p.rec + L * p.rec4;
 #pragma unroll
-    for (int i = 0; i < Q4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+    for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
 }
 
 // ------------------------------------------------------------------ traversal only
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ Seg
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.n) return;
-    Entry *stk = reinterpret_cast<Entry *>(smem_raw) + threadIdx.x;
+    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     Ray ray;
     const bool hit = ray_setup(p.T, p.origins[3 * r], p.origins[3 * r + 1], p.origins[3 * r + 2],
                                p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
@@ -384,7 +390,7 @@ inline int with_nmax(int nmax, F &&f) {
 }
 
 inline size_t stack_bytes(int depth, bool wide) {
-    return (size_t)stack_cap(depth) * kBlock * (wide ? sizeof(EntryW) : sizeof(EntryN));
+    return (size_t)stack_cap(depth) * kBlock * (wide ? EntryW::kBytes : EntryN::kBytes);
 }
 
 template <class Kern>
@@ -417,13 +423,14 @@ inline unsigned persistent_grid(Kern k, int block, size_t smem, unsigned max_blo
 }
 
 // ------------------------------------------------------------------ launchers
-int launch_rays(int nmax, bool cached, bool edits, bool wide, bool visits, const RaysParams &p, unsigned grid,
+// mode: 0 = decode per sample, 1 = frame slice
+int launch_rays(int nmax, int mode, bool edits, bool wide, bool visits, const RaysParams &p, unsigned grid,
                 size_t smem, cudaStream_t st);
 // one block per 32x16 tile (max_blocks = tile count)
-int launch_camera(int nmax, bool cached, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
+int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
                   cudaStream_t st);
 int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
-int launch_slice(int nmax, const SliceParams &p, unsigned grid, cudaStream_t st);
+int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
                   float *rest, cudaStream_t st);

@@ -12,16 +12,22 @@ static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t
     return check_launch("render_camera");
 }
 
-int launch_camera(int nmax, bool cached, bool edits, bool wide, const CamParams &p, unsigned grid, size_t smem,
+template <int NM, int MODE, class Entry>
+static int pick_e(bool edits, const CamParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    return edits ? go<NM, MODE, true, Entry>(p, grid, smem, st) : go<NM, MODE, false, Entry>(p, grid, smem, st);
+}
+
+template <int NM, class Entry>
+static int pick(int mode, bool edits, const CamParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    if (mode == 1) return pick_e<NM, 1, Entry>(edits, p, grid, smem, st);
+    return pick_e<NM, 0, Entry>(edits, p, grid, smem, st);
+}
+
+int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned grid, size_t smem,
                   cudaStream_t st) {
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
-        if (wide) {
-            if (cached) return edits ? go<NM, 1, true, EntryW>(p, grid, smem, st) : go<NM, 1, false, EntryW>(p, grid, smem, st);
-            return edits ? go<NM, 0, true, EntryW>(p, grid, smem, st) : go<NM, 0, false, EntryW>(p, grid, smem, st);
-        }
-        if (cached) return edits ? go<NM, 1, true, EntryN>(p, grid, smem, st) : go<NM, 1, false, EntryN>(p, grid, smem, st);
-        return edits ? go<NM, 0, true, EntryN>(p, grid, smem, st) : go<NM, 0, false, EntryN>(p, grid, smem, st);
+        return wide ? pick<NM, EntryW>(mode, edits, p, grid, smem, st) : pick<NM, EntryN>(mode, edits, p, grid, smem, st);
     });
 }
 

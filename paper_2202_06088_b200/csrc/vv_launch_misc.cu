@@ -48,9 +48,10 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 }
 
 
-int launch_slice(int nmax, const SliceParams &p, unsigned grid, cudaStream_t st) {
+int launch_slice(int nmax, const SliceParams &p, cudaStream_t st) {
+    const unsigned grid = (unsigned)((p.n_leaves + kSliceBlock - 1) / kSliceBlock);
     return with_nmax(nmax, [&](auto N) {
-        k_build_slice<decltype(N)::value><<<grid, 256, 0, st>>>(p);
+        k_build_slice<decltype(N)::value><<<grid, kSliceBlock, 0, st>>>(p);
         return check_launch("build_slice");
     });
 }

@@ -269,3 +269,29 @@ def test_camera_rays_vs_host(cuda):
     assert np.abs(layer.alpha.reshape(-1) - alpha).max() < TOL
     hit = alpha >= 1e-3
     assert np.abs(layer.depth.reshape(-1)[hit] - depth[hit]).max() < TOL
+
+
+@pytest.mark.parametrize("name", ["cache_d3", "edits_d3"])
+def test_decode_modes_bitwise_equal(cuda, name):
+    """per_sample / per_frame / lazy leaf decoding give bitwise-identical
+    renders (the reference's cached == uncached guarantee, render.py:14-17)."""
+    g = load(name)
+    tree = tree_from(g)
+    o, d = g["origins"], g["dirs"]
+    outs = {}
+    for mode in ("per_sample", "per_frame", "auto"):
+        outs[mode] = vv.render_rays(tree, o, d, 2, vv.RenderOptions(frame_slice=mode), stats=True)
+    for mode in ("per_frame", "auto"):
+        for a, b in zip(outs["per_sample"][:3], outs[mode][:3]):
+            _exact(a, b, mode)
+        _exact(outs["per_sample"][3]["sample_count"], outs[mode][3]["sample_count"], mode)
+
+
+def test_decode_modes_config1_images(cuda):
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    cam = synthetic.bench_camera(96, 64)
+    imgs = [vv.render(tree, cam, 5, vv.RenderOptions(frame_slice=m)) for m in ("per_sample", "per_frame", "auto")]
+    for other in imgs[1:]:
+        _exact(imgs[0].rgb, other.rgb)
+        _exact(imgs[0].alpha, other.alpha)
+        _exact(imgs[0].depth, other.depth)

@@ -87,7 +87,8 @@ for r in recs:
     for i in stall_cols:
         a[3][hdr[i]] += int(r[i] or 0)
 print(kname[:120], "total samples", total)
-for key, (s, ex, th, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:int(sys.argv[5]) if len(sys.argv) > 5 else 40]:
+SORT_IDX = int(__import__("os").environ.get("SORT", "0"))
+for key, (s, ex, th, st) in sorted(agg.items(), key=lambda kv: -kv[1][SORT_IDX])[:int(sys.argv[5]) if len(sys.argv) > 5 else 40]:
     top = sorted(st.items(), key=lambda kv: -kv[1])[:3]
     eff = th / ex if ex else 0
     print(f"{s / total * 100:5.1f}%  {key:28s} inst={ex:>10d} thr/inst={eff:5.1f}  " +
