@@ -159,7 +159,19 @@ def algorithmic_bytes(tree, cam, frames, device):
         V = st["sample_count"].to(torch.int64).sum().item()
         S = st["shaded"].to(torch.int64).sum().item()
         n = o.shape[0]
-        out[f] = dict(P=P, V=V, S=S, bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * n)
+        s_sh = (tree.n_max + 1) ** 2
+        out[f] = dict(
+            P=P, V=V, S=S,
+            # uncached path (render_kernel decoding every visited leaf)
+            bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * n,
+            # sliced path actually executed: render kernel reads a node row per
+            # pop, the f64 sigma per visited leaf and the 3S fp32 sliced SH
+            # coefficients per shaded leaf, writes 20 B per pixel ...
+            render_bytes=32 * P + 8 * V + 12 * s_sh * S + 20 * n,
+            # ... after the per-frame slice pass read every payload row and
+            # wrote sigma + q per leaf
+            slice_bytes=tree.n_leaves * (4 * (2 * c + 3 * k) + 8 + 12 * s_sh),
+        )
     return out
 
 
@@ -265,9 +277,19 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     tiles = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev) if world > 1 else None
 
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    cur = {"mid": None}
+
     def step(f):
+        # identical work to render(tree, cam, f): per-frame slice pass, then the
+        # fused ray-gen/traversal/shading/finalize kernel -- split here so the
+        # dominant kernel's own duration is measured (roofline)
         if tiles is None:
-            vv.render_into(tree, cam, f, rgb, alpha, depth)
+            fs = vv.build_frame_cache(tree, f)
+            if cur["mid"] is not None:
+                cur["mid"].record(stream)
+            vv.render_into(tree, cam, f, rgb, alpha, depth, cache=fs)
+            del fs
         else:
             tiles.render_slab(tree, cam, f)
             tiles.gather()
@@ -292,8 +314,10 @@ def run_ours(args, rank, world, local_rank):
     for i, f in enumerate(step_frames):
         flush.zero_()
         starts[i].record(stream)
+        cur["mid"] = mids[i]
         step(f)
         ends[i].record(stream)
+    cur["mid"] = None
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     if world > 1:
@@ -301,6 +325,8 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop() if clocks else None
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
+    render_ms = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) if tiles is None else None
+    slice_ms = sum(s.elapsed_time(m) for s, m in zip(starts, mids)) if tiles is None else None
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -348,9 +374,17 @@ def run_ours(args, rank, world, local_rank):
     # roofline of the dominant kernel (k_render_camera), reference-defined bytes
     ab = algorithmic_bytes(tree, cam, sorted(set(step_frames)), dev)
     bytes_per_step = [ab[f]["bytes"] for f in step_frames]
-    kernel_s = total_ms / 1e3
-    achieved = sum(bytes_per_step) / kernel_s / 1e9 if world == 1 else sum(bytes_per_step) / kernel_s / 1e9 / world
     peak, peak_kind = measured_peak()
+    if render_ms is not None:
+        rbytes = sum(ab[f]["render_bytes"] for f in step_frames)
+        sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
+        achieved = rbytes / (render_ms / 1e3) / 1e9
+        slice_gbs = sbytes / (slice_ms / 1e3) / 1e9
+        frame_gbs = (rbytes + sbytes) / (total_ms / 1e3) / 1e9
+        uncached_gbs = sum(bytes_per_step) / (total_ms / 1e3) / 1e9
+    else:
+        achieved = sum(ab[f]["render_bytes"] + ab[f]["slice_bytes"] for f in step_frames) / (total_ms / 1e3) / 1e9
+        slice_gbs = frame_gbs = uncached_gbs = None
     mean_ab = {k: float(np.mean([ab[f][k] for f in step_frames]) / n_rays) for k in ("P", "V", "S")}
 
     # CPU baseline: oracle port on a bounded sample (rank 0, N = 1 only)
@@ -381,10 +415,20 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
                      "peak_kind": peak_kind, "kernel": "k_render_camera",
-                     "bytes_per_frame": float(np.mean(bytes_per_step))},
+                     "kernel_ms": round(render_ms / len(step_frames), 4) if render_ms is not None else None,
+                     "bytes_per_launch": float(np.mean([ab[f]["render_bytes"] for f in step_frames])),
+                     "bytes_formula": "sum_rays 32 P + 8 V + 12 S_sh S + 20 (sliced path; P/V/S reference counts)",
+                     "slice_pass": {"kernel": "k_build_slice",
+                                    "ms": round(slice_ms / len(step_frames), 4) if slice_ms is not None else None,
+                                    "achieved": round(slice_gbs, 1) if slice_gbs else None,
+                                    "frac": round(slice_gbs / peak, 4) if slice_gbs else None,
+                                    "bytes_per_launch": float(ab[step_frames[0]]["slice_bytes"])},
+                     "frame_achieved": round(frame_gbs, 1) if frame_gbs else None,
+                     "uncached_formula_achieved": round(uncached_gbs, 1) if uncached_gbs else None,
+                     "uncached_bytes_per_frame": float(np.mean(bytes_per_step))},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": len(step_frames) * (1 if world == 1 else 2),
+        "gpu_launches": len(step_frames) * 2,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -130,6 +130,9 @@ int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, in
  * uncached path); the sliced SH coefficients are stored as fp32.
  * Error: frame outside [0, T) -> VV_E_INVALID ("frame F out of range"). */
 int vv_slice_build(const vv_tree *tree, int32_t frame, void *stream, vv_slice **out);
+/* The slice is allocated stream-ordered on `stream` (the device's default
+ * memory pool) and released stream-ordered on the same stream: work already
+ * queued on that stream may still read it. */
 int vv_slice_free(vv_slice *slice);
 /* Copies the cache to caller device buffers: sigma (n_leaves) f64,
  * q (n_leaves, 3S) f32. */

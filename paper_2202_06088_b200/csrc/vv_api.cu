@@ -46,6 +46,7 @@ struct vv_slice {
     float4 *d_rec;  // (n_leaves, rec4) records [q | pad | sigma]
     int rec4;
     int64_t n_leaves;
+    cudaStream_t stream;  // stream-ordered allocation: freed on this stream
 };
 
 #define VV_CUDA(call)                                                                          \
@@ -381,8 +382,11 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
     s->n_leaves = t->n_leaves;
     s->rec4 = slice_rec4(t->S);
     const int64_t nrows = std::max<int64_t>(t->n_leaves, 1);
-    if (cudaMalloc(&s->d_rec, nrows * s->rec4 * sizeof(float4)) != cudaSuccess) {
+    s->stream = (cudaStream_t)stream;
+    pool_setup(t->device);
+    if (cudaMallocAsync(&s->d_rec, nrows * s->rec4 * sizeof(float4), s->stream) != cudaSuccess) {
         cudaGetLastError();
+        s->d_rec = nullptr;
         vv_slice_free(s);
         return set_error(VV_E_NOMEM, "slice allocation failed");
     }
@@ -398,7 +402,7 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
 int vv_slice_free(vv_slice *s) {
     if (!s) return VV_OK;
     DeviceGuard g(s->device);
-    cudaFree(s->d_rec);
+    if (s->d_rec) cudaFreeAsync(s->d_rec, s->stream);
     delete s;
     return VV_OK;
 }

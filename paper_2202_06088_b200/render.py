@@ -227,6 +227,41 @@ class FrameSlice:
             self._handle = None
 
 
+class _PinnedPool:
+    """Reusable pinned host buffers for device->host results.
+
+    A buffer is handed out again only after every numpy array viewing it has
+    been garbage-collected (tracked with a weakref to the base array), so
+    results never alias while avoiding a cudaHostAlloc per call.
+    """
+
+    def __init__(self):
+        self._free = {}  # nbytes -> list of (tensor, weakref or None)
+        self._lock = __import__("threading").Lock()
+
+    def get(self, n_floats: int):
+        import weakref
+
+        torch = require_cuda()
+        with self._lock:
+            lst = self._free.setdefault(n_floats, [])
+            for i, (t, ref) in enumerate(lst):
+                if ref is None or ref() is None:
+                    arr = t.numpy()
+                    lst[i] = (t, weakref.ref(arr))
+                    return t, arr
+            t = torch.empty(n_floats, dtype=torch.float32, pin_memory=True)
+            arr = t.numpy()
+            lst.append((t, weakref.ref(arr)))
+            if len(lst) > 8:  # drop the oldest idle buffers beyond a small cap
+                lst[:] = [e for e in lst if e[1] is not None and e[1]() is not None] + \
+                    [e for e in lst if e[1] is None or e[1]() is None][:4]
+            return t, arr
+
+
+_PINNED = _PinnedPool()
+
+
 def _frame_index(frame) -> int:
     if isinstance(frame, (float, np.floating)) and not float(frame).is_integer():
         return int(round(float(frame)))  # continuous t -> nearest frame (SPEC.md:218)
@@ -402,10 +437,9 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
     render_into(tree, cam, frame, rgb, alpha, depth, opts, cache)
     if out == "torch":
         return LayerImages(rgb, alpha, depth)
-    host = torch.empty(5 * h * w, dtype=torch.float32, pin_memory=True)
+    host, a = _PINNED.get(5 * h * w)
     host.copy_(buf, non_blocking=True)
     torch.cuda.current_stream(dev).synchronize()
-    a = host.numpy()
     return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
                        a[4 * h * w:].reshape(h, w))
 
