@@ -28,6 +28,7 @@ from .render import (
     finalize_layer,
     render,
     render_into,
+    render_sequence,
     render_ray_visits,
     render_rays,
 )
@@ -35,7 +36,7 @@ from .temporal import TemporalBases, make_bump_bases
 
 __all__ = [
     "VOctree", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
-    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into",
+    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
     "render_instance", "render_scene", "duplicate", "TemporalBases", "make_bump_bases",

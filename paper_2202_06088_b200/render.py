@@ -34,6 +34,7 @@ __all__ = [
     "FrameSlice",
     "render",
     "render_into",
+    "render_sequence",
     "render_rays",
     "render_ray_visits",
     "finalize_layer",
@@ -442,6 +443,64 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
     torch.cuda.current_stream(dev).synchronize()
     return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
                        a[4 * h * w:].reshape(h, w))
+
+
+def render_sequence(tree, cam: Camera, frames, opts: RenderOptions = RenderOptions(), *, device=None):
+    """Playback: render `frames` in order, yielding numpy LayerImages (fp32).
+
+    Double-buffered: frame i renders on the current stream while frame i-1's
+    20 B/pixel result is copied device->host on a side stream into pinned
+    memory, so a sequence runs at max(render, copy) per frame instead of
+    their sum.  Each yielded frame is complete on the host.
+    """
+    torch = require_cuda()
+    dev = torch_device(device)
+    h, w = int(cam.height), int(cam.width)
+    n = 5 * h * w
+    caller = torch.cuda.current_stream(dev)
+    comp = torch.cuda.Stream(dev)  # dedicated streams: the legacy default stream would serialise
+    copy = torch.cuda.Stream(dev)
+    comp.wait_stream(caller)
+    bufs = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)]
+    for b in bufs:
+        b.record_stream(copy)
+        b.record_stream(comp)
+    # warm the pinned pool for the frames in flight (2 pending + 1 held by the caller)
+    warm = [_PINNED.get(n) for _ in range(3)]
+    del warm
+    copied = [None, None]
+    pending = []
+
+    def views(a):
+        return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
+                           a[4 * h * w:].reshape(h, w))
+
+    for i, f in enumerate(frames):
+        b = i % 2
+        if copied[b] is not None:
+            comp.wait_event(copied[b])  # buffer b's previous frame has left the device
+        buf = bufs[b]
+        with torch.cuda.stream(comp):
+            render_into(tree, cam, f, buf[: 3 * h * w].view(h, w, 3), buf[3 * h * w: 4 * h * w].view(h, w),
+                        buf[4 * h * w:].view(h, w), opts)
+        rendered = torch.cuda.Event()
+        rendered.record(comp)
+        host, arr = _PINNED.get(n)
+        copy.wait_event(rendered)
+        with torch.cuda.stream(copy):
+            host.copy_(buf, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(copy)
+        copied[b] = done
+        pending.append((done, arr))
+        if len(pending) > 1:
+            ev, a = pending.pop(0)
+            ev.synchronize()
+            yield views(a)
+    while pending:
+        ev, a = pending.pop(0)
+        ev.synchronize()
+        yield views(a)
 
 
 def composite_background(layer: LayerImages, bg) -> np.ndarray:

@@ -295,3 +295,16 @@ def test_decode_modes_config1_images(cuda):
         _exact(imgs[0].rgb, other.rgb)
         _exact(imgs[0].alpha, other.alpha)
         _exact(imgs[0].depth, other.depth)
+
+
+def test_render_sequence_matches_render(cuda):
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    cam = synthetic.bench_camera(80, 48)
+    frames = [3, 4, 5, 9, 0]
+    seq = [l for l in vv.render_sequence(tree, cam, frames)]
+    assert len(seq) == len(frames)
+    for f, l in zip(frames, seq):
+        ref = vv.render(tree, cam, f)
+        _exact(l.rgb, ref.rgb)
+        _exact(l.alpha, ref.alpha)
+        _exact(l.depth, ref.depth)
