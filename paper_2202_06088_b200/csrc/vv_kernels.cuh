@@ -319,30 +319,87 @@ struct SliceParams {
     int rec4;
 };
 
-// build_slice_kernel (kernels.py:397-407): one thread per leaf.  (Bound by
-// L1 wavefronts of the per-thread row loads: 27 LDG.128 per warp, each
-// touching 32 lines; see DESIGN.md for the measured alternatives.)
-constexpr int kSliceBlock = 256;
+// build_slice_kernel (kernels.py:397-407).  Persistent warps, each owning a
+// double-buffered shared-memory stage: one lane issues two TMA bulk copies
+// (cp.async.bulk, completed on an mbarrier) per chunk of 32 consecutive
+// leaves -- their w_sigma rows and their [w_gamma | w_hh] rows are
+// contiguous in HBM -- while the warp slices the previous chunk, one leaf
+// per lane, from shared memory.  Rows reach shared memory without
+// touching registers or the L1 wavefront path that bounds per-thread row
+// loads; the next chunk streams in during the fp64 sigma chains.
+constexpr int kSliceWarps = 4;
+constexpr int kSliceChunk = 32;
+
+__host__ __device__ inline size_t slice_stage_floats4(int sig4, int rest4) {
+    return (size_t)kSliceChunk * (sig4 + rest4);
+}
+__host__ __device__ inline size_t slice_smem_bytes(int sig4, int rest4) {
+    // per warp: 2 stages + 2 mbarriers (16 B)
+    return (size_t)kSliceWarps * (2 * slice_stage_floats4(sig4, rest4) * 16 + 16);
+}
+
 template <int NMAX>
-__global__ void __launch_bounds__(kSliceBlock) k_build_slice(const __grid_constant__ SliceParams p) {
+__global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_constant__ SliceParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[kMaxC], sB[kMaxC];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sig4 = p.T.sig4, rest4 = p.T.rest4;
+    const size_t stage4 = slice_stage_floats4(sig4, rest4);
+    float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 1);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
     load_rows(p.T, p.frame, sA, sB);
     __syncthreads();
-    const int64_t L = (int64_t)blockIdx.x * kSliceBlock + threadIdx.x;
-    if (L >= p.n_leaves) return;
+    const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
+    const int64_t wstride = (int64_t)gridDim.x * kSliceWarps;
+    const int64_t c0 = (int64_t)blockIdx.x * kSliceWarps + warp;
+    auto issue = [&](int64_t c, int stg) {
+        const int64_t base = c * kSliceChunk;
+        const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
+        float4 *dst = wbase + stg * stage4;
+        const uint32_t sb = (uint32_t)rows * sig4 * 16, rb = (uint32_t)rows * rest4 * 16;
+        mbar_expect_tx(&bar[stg], sb + rb);
+        bulk_g2s(dst, p.T.sig + base * sig4, sb, &bar[stg]);
+        bulk_g2s(dst + (size_t)kSliceChunk * sig4, p.T.rest + base * rest4, rb, &bar[stg]);
+    };
+    if (lane == 0) {
+        if (c0 < n_chunks) issue(c0, 0);
+        if (c0 + wstride < n_chunks) issue(c0 + wstride, 1);
+    }
     constexpr int R4 = slice_rec4(Basis<NMAX>::S);
-    float q[4 * R4];
+    int k = 0;
+    for (int64_t c = c0; c < n_chunks; c += wstride, ++k) {
+        const int stg = k & 1;
+        mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
+        const int64_t base = c * kSliceChunk;
+        const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
+        const float4 *ssig = wbase + stg * stage4;
+        const float4 *srest = ssig + (size_t)kSliceChunk * sig4;
+        if (lane < rows) {
+            float q[4 * R4];
 #pragma unroll
-    for (int i = 0; i < 4 * R4; ++i) q[i] = 0.0f;
-    double sigma;
-    slice_rows<NMAX>(p.T.sig + (size_t)L * p.T.sig4, p.T.rest + (size_t)L * p.T.rest4, p.T.C, p.T.hh_off4, sA, sB,
-                     p.K, sigma, q);
-    const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
-    q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
-    q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
-    float4 *o = p.rec + L * p.rec4;
+            for (int i = 0; i < 4 * R4; ++i) q[i] = 0.0f;
+            double sigma;
+            slice_rows<NMAX, false>(ssig + lane * sig4, srest + lane * rest4, p.T.C, p.T.hh_off4, sA, sB, p.K,
+                                    sigma, q);
+            const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+            q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
+            q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
+            float4 *o = p.rec + (base + lane) * p.rec4;
 #pragma unroll
-    for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+            for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+        }
+        __syncwarp();
+        // stage consumed: refill it with the chunk two steps ahead
+        if (lane == 0 && c + 2 * wstride < n_chunks) {
+            fence_proxy_async();
+            issue(c + 2 * wstride, stg);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ traversal only

@@ -49,9 +49,15 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st) {
-    const unsigned grid = (unsigned)((p.n_leaves + kSliceBlock - 1) / kSliceBlock);
+    const size_t smem = slice_smem_bytes(p.T.sig4, p.T.rest4);
     return with_nmax(nmax, [&](auto N) {
-        k_build_slice<decltype(N)::value><<<grid, kSliceBlock, 0, st>>>(p);
+        auto kern = k_build_slice<decltype(N)::value>;
+        int r = prep_smem(kern, smem);
+        if (r) return r;
+        const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
+        const unsigned want = (unsigned)((chunks + kSliceWarps - 1) / kSliceWarps);
+        const unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
+        kern<<<grid, kSliceWarps * 32, smem, st>>>(p);
         return check_launch("build_slice");
     });
 }
