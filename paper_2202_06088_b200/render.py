@@ -445,28 +445,64 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
                        a[4 * h * w:].reshape(h, w))
 
 
+_PLAYBACK = {}
+
+
+def _playback_state(torch, dev, n: int):
+    """Per-device playback streams and double buffers, kept across calls.
+
+    Dedicated streams (the legacy default stream would serialise render and
+    copy), and the SAME streams every call: the frame slice is allocated
+    stream-ordered (cudaMallocAsync) on the render stream, and the pool only
+    recycles a block on the stream that freed it -- a fresh stream per call
+    re-maps ~1.9 GB of slice memory on its first frame (tens of ms).
+    """
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), n)
+    st = _PLAYBACK.get(key)
+    if st is None or st[3][0]:
+        comp, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        with torch.cuda.stream(comp):
+            bufs = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)]
+        for b in bufs:
+            b.record_stream(copy)
+        fresh = (comp, copy, bufs, [False])
+        if st is not None:
+            return fresh  # another playback is live on this device: private state, not cached
+        for k in [k for k in _PLAYBACK if k[0] == key[0]]:
+            del _PLAYBACK[k]  # one resolution per device at a time
+        st = _PLAYBACK[key] = fresh
+    st[0].wait_stream(st[1])  # an abandoned playback may still be copying out of the buffers
+    return st
+
+
 def render_sequence(tree, cam: Camera, frames, opts: RenderOptions = RenderOptions(), *, device=None):
     """Playback: render `frames` in order, yielding numpy LayerImages (fp32).
 
-    Double-buffered: frame i renders on the current stream while frame i-1's
-    20 B/pixel result is copied device->host on a side stream into pinned
-    memory, so a sequence runs at max(render, copy) per frame instead of
-    their sum.  Each yielded frame is complete on the host.
+    Double-buffered: frame i renders on a per-device render stream (ordered
+    after the caller's current stream) while frame i-1's 20 B/pixel result is
+    copied device->host on a side stream into pinned memory, so a sequence
+    runs at max(render, copy) per frame instead of their sum.  Each yielded
+    frame is complete on the host.
     """
     torch = require_cuda()
     dev = torch_device(device)
     h, w = int(cam.height), int(cam.width)
     n = 5 * h * w
     caller = torch.cuda.current_stream(dev)
-    comp = torch.cuda.Stream(dev)  # dedicated streams: the legacy default stream would serialise
-    copy = torch.cuda.Stream(dev)
+    comp, copy, bufs, busy = _playback_state(torch, dev, n)
     comp.wait_stream(caller)
-    bufs = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)]
-    for b in bufs:
-        b.record_stream(copy)
-        b.record_stream(comp)
-    # warm the pinned pool for the frames in flight (2 pending + 1 held by the caller)
-    warm = [_PINNED.get(n) for _ in range(3)]
+    busy[0] = True
+    try:
+        yield from _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n)
+    finally:
+        busy[0] = False
+
+
+def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
+    # warm the pinned pool for the frames in flight (2 pending + the caller's
+    # current and previous frame): a 41 MB cudaHostAlloc costs 25-100 ms, so
+    # grow the pool once up front instead of stalling mid-sequence
+    warm = [_PINNED.get(n) for _ in range(4)]
     del warm
     copied = [None, None]
     pending = []

@@ -308,3 +308,28 @@ def test_render_sequence_matches_render(cuda):
         _exact(l.rgb, ref.rgb)
         _exact(l.alpha, ref.alpha)
         _exact(l.depth, ref.depth)
+
+
+def test_render_sequence_reuse_interleave_abandon(cuda):
+    """Cached playback state: repeated calls, an abandoned generator and two
+    interleaved generators on one device all still yield render()'s images."""
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=1)
+    cam = synthetic.bench_camera(64, 40)
+    ref = {f: vv.render(tree, cam, f) for f in range(8)}
+
+    def same(l, f):
+        _exact(l.rgb, ref[f].rgb)
+        _exact(l.alpha, ref[f].alpha)
+        _exact(l.depth, ref[f].depth)
+
+    g = vv.render_sequence(tree, cam, [0, 1, 2, 3])
+    same(next(g), 0)
+    del g  # abandoned with a copy possibly in flight
+    for _ in range(2):
+        for f, l in zip([4, 5, 6], vv.render_sequence(tree, cam, [4, 5, 6])):
+            same(l, f)
+    a = vv.render_sequence(tree, cam, [0, 2, 4, 6])
+    b = vv.render_sequence(tree, cam, [1, 3, 5, 7])
+    for (fa, la), (fb, lb) in zip(zip([0, 2, 4, 6], a), zip([1, 3, 5, 7], b)):
+        same(la, fa)
+        same(lb, fb)
