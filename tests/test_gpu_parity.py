@@ -186,7 +186,8 @@ def test_scene_against_reference(cuda):
     assert np.abs(vv.render_scene(single, cam, 1) - g["single_image"]).max() < TOL
 
 
-@pytest.mark.parametrize("depth,fill,seed", [(5, 0.3, 1), (6, 0.05, 2), (4, 0.9, 3)])
+@pytest.mark.parametrize("depth,fill,seed", [(5, 0.3, 1), (6, 0.05, 2), (4, 0.9, 3), (3, 0.5, 4), (2, 0.6, 5),
+                                             (1, 0.7, 6), (7, 0.02, 7)])
 def test_random_trees_vs_oracle(cuda, depth, fill, seed):
     rng = np.random.default_rng(seed)
     res = 1 << depth

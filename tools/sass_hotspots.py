@@ -49,7 +49,7 @@ with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=td, capture_output=True)
     dis = ""
     for cub in Path(td).glob("*.cubin"):
-        d = subprocess.run(["nvdisasm", "-g", "-c", str(cub)], capture_output=True, text=True).stdout
+        d = subprocess.run(["nvdisasm", "-gi", "-c", str(cub)], capture_output=True, text=True).stdout
         if re.search(kre, d):
             dis = d
             break
@@ -63,14 +63,31 @@ for f in funcs:
         break
 if target is None:
     sys.exit(f"kernel {kre} not found in cubin")
+HELPER_MAX_LINE = int(__import__("os").environ.get("HELPER_MAX_LINE", "100"))
+
+
+def _is_helper(fname, line):
+    return fname.endswith(".hpp") or fname.endswith(".h") or (fname == "vv_device.cuh" and line < HELPER_MAX_LINE)
+
+
 line_of = {}
 cur = None
+in_chain = False
 for ln in target.split("\n"):
-    m = re.search(r"//## File \"([^\"]+)\", line (\d+)", ln)
+    m = re.search(r"//## File \"([^\"]+)\", line (\d+)(?: inlined at \"([^\"]+)\", line (\d+))?", ln)
     if m:
+        # nvdisasm -gi prints the inline chain innermost -> outermost: keep the first
+        if in_chain:
+            continue
+        in_chain = True
         cur = f"{Path(m.group(1)).name}:{m.group(2)}"
+        # tiny helpers (fp64 wrappers, intrinsics headers) -> their call site
+        if m.group(3) and (_is_helper(Path(m.group(1)).name, int(m.group(2)))):
+            cur = f"{Path(m.group(3)).name}:{m.group(4)}"
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+    if m:
+        in_chain = False
     if m and cur:
         line_of[int(m.group(1), 16)] = cur
 agg = defaultdict(lambda: [0, 0, 0, defaultdict(int)])
@@ -87,6 +104,28 @@ for r in recs:
     for i in stall_cols:
         a[3][hdr[i]] += int(r[i] or 0)
 print(kname[:120], "total samples", total)
+REGIONS = __import__("os").environ.get("REGIONS")  # "name:lo-hi,name:lo-hi" over vv_device.cuh lines
+if REGIONS:
+    buckets = defaultdict(lambda: [0, 0])
+    tot_wait = sum(a[3].get("stall_wait", 0) for a in agg.values())
+    for key, (s_, ex, th, st) in agg.items():
+        f, _, ln = key.partition(":")
+        name = "other:" + f
+        if f == "vv_device.cuh" and ln.isdigit():
+            for spec in REGIONS.split(","):
+                nm, rng = spec.split(":")
+                lo_, hi_ = (int(x) for x in rng.split("-"))
+                if lo_ <= int(ln) <= hi_:
+                    name = nm
+                    break
+        buckets[name][0] += ex
+        buckets[name][1] += s_
+        buckets[name].append(st.get("stall_wait", 0))
+    tot_ex = sum(v[0] for v in buckets.values())
+    for nm, vals in sorted(buckets.items(), key=lambda kv: -kv[1][0]):
+        ex, s_, w = vals[0], vals[1], sum(vals[2:])
+        print(f"  region {nm:24s} inst={ex:>11d} ({ex / tot_ex * 100:5.1f}%)  samples {s_ / total * 100:5.1f}%"
+              f"  wait {w:6d} ({w / max(tot_wait, 1) * 100:4.1f}% of wait)")
 SORT_IDX = int(__import__("os").environ.get("SORT", "0"))
 for key, (s, ex, th, st) in sorted(agg.items(), key=lambda kv: -kv[1][SORT_IDX])[:int(sys.argv[5]) if len(sys.argv) > 5 else 40]:
     top = sorted(st.items(), key=lambda kv: -kv[1])[:3]
