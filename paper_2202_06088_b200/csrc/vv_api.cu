@@ -465,7 +465,7 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
     p.visit_start = visit_start;
     p.visit_leaf = visit_leaf;
     const bool wide = t->depth > kNarrowDepth;
-    const size_t smem = stack_bytes(t->depth, wide);
+    const size_t smem = stack_bytes(t->depth, wide, true);
     const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;

@@ -204,11 +204,11 @@ __host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 :
 // ------------------------------------------------------------ traversal
 // Visitor interface:
 //   void pop()                                   one internal-node pop
-//   bool batch(int32_t cp[4], double st[5], int keep)
-//        the <= 4 leaf segments of one last-level node, near to far:
-//        segment s (keep bit s set) is leaf row cp[s] over [st[s], st[s+1]];
-//        returns true to stop the ray (early termination).  May clobber
-//        its arguments.
+//   int pop_count()                              pops so far (stats)
+//   bool batch(const SegBuf &seg, int n)
+//        the next n queued leaf segments, near to far: leaf row
+//        seg.leaf_at(s) over [seg.t0_at(s), seg.t1_at(s)]; returns true to
+//        stop the ray (early termination).
 //
 // Structure ("while-while"): a lane walks internal nodes until it holds one
 // last-level node's leaf batch, then all lanes of the warp shade their
@@ -260,17 +260,77 @@ struct Trav {
     }
 };
 
-// Advance the walk until the next last-level node with kept leaves; fills
-// cp/st/keep and returns true, or returns false when the tree is exhausted.
+// Leaf segments queued for shading live in shared memory, structure of
+// arrays per slot (consecutive threads -> consecutive words, conflict-free):
+// t0, t1, leaf rows, node-visit counts.  A walk queues >= kSegMin segments
+// (one last-level node adds up to 4) before the warp shades; the walk may
+// so run ahead of an early termination, and the visit count queued with
+// each segment restores the reference's count at the terminating one.
+#ifndef VV_SEG_MIN
+#define VV_SEG_MIN 6
+#endif
+#ifndef VV_SEG_SLOTS
+#define VV_SEG_SLOTS (VV_SEG_MIN + 3)
+#endif
+constexpr int kSegMin = VV_SEG_MIN;
+constexpr int kSegSlots = VV_SEG_SLOTS;
+static_assert(kSegSlots >= kSegMin + 3, "a last-level node queues up to 4 segments");
+// (the visit counts only for visitors that report them, kPops)
+__host__ __device__ constexpr uint32_t seg_bytes_per_thread(bool pops) { return kSegSlots * (pops ? 24u : 20u); }
+struct SegBuf {
+    uint32_t t0, t1, leaf, pops;  // shared addresses of this thread's slot 0
+    uint32_t sl, sd;              // slot strides (bytes) of the int and double arrays
+    __device__ __forceinline__ void init(uint32_t base, int nthreads, int tid) {
+        sl = 4u * nthreads;
+        sd = 8u * nthreads;
+        t0 = base + 8u * tid;
+        t1 = t0 + kSegSlots * sd;
+        leaf = base + 2 * kSegSlots * sd + 4u * tid;
+        pops = leaf + kSegSlots * sl;
+    }
+    template <bool POPS>
+    __device__ __forceinline__ void put(int s, int32_t L, double a, double b, int np) const {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(leaf + s * sl), "r"(L));
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(t0 + s * sd), "d"(a));
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(t1 + s * sd), "d"(b));
+        if (POPS) asm volatile("st.shared.u32 [%0], %1;" ::"r"(pops + s * sl), "r"(np));
+    }
+    __device__ __forceinline__ int pops_at(int s) const {
+        int v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(pops + s * sl));
+        return v;
+    }
+    __device__ __forceinline__ int32_t leaf_at(int s) const {
+        int32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(leaf + s * sl));
+        return v;
+    }
+    __device__ __forceinline__ double t0_at(int s) const {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(t0 + s * sd));
+        return v;
+    }
+    __device__ __forceinline__ double t1_at(int s) const {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(t1 + s * sd));
+        return v;
+    }
+};
+
+// Advance the walk, queueing the kept leaves of the last-level nodes it
+// passes, until >= kSegMin segments are queued or the tree is exhausted;
+// returns the number queued (0: done).
 template <class Entry, class Visitor>
-__device__ __forceinline__ bool trav_next(Trav<Entry> &t, const int32_t *__restrict__ child, int depth, const Ray &r,
-                                          uint32_t stack_base, uint32_t stride, Visitor &vis, int32_t *cp,
-                                          double *st, int &keep) {
+__device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restrict__ child, int depth, const Ray &r,
+                                         uint32_t stack_base, uint32_t stride, Visitor &vis, const SegBuf &seg) {
+    int n = 0;
+    int32_t cp[4];
+    double st[5];
     const double o0 = r.o0, o1 = r.o1, o2 = r.o2, i0 = r.i0, i1 = r.i1, i2 = r.i2;
     const int mirror = r.mirror;
     while (true) {
         if (t.need_pop) {
-            if (t.sp == stack_base) return false;
+            if (t.sp == stack_base) return n;
             t.sp -= stride;
             Entry::load(t.sp, t.ptr, t.L, t.pc);
             // recompute the popped cell's interval from its six faces
@@ -310,13 +370,16 @@ __device__ __forceinline__ bool trav_next(Trav<Entry> &t, const int32_t *__restr
         cp[1] = __ldg(row + (c1 ^ mirror));
         cp[2] = __ldg(row + (c2 ^ mirror));
         cp[3] = __ldg(row + (c3 ^ mirror));
-        keep = 0;
+        int keep = 0;
 #pragma unroll
         for (int s = 0; s < 4; ++s)
             if (cp[s] >= 0 && st[s + 1] > st[s]) keep |= 1 << s;
         if (t.L + 1 == depth) {
             t.need_pop = true;
-            if (keep) return true;
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+                if ((keep >> s) & 1) seg.put<Visitor::kPops>(n++, cp[s], st[s], st[s + 1], vis.pop_count());
+            if (n >= kSegMin) return n;
             continue;
         }
         if (!keep) {
@@ -358,21 +421,40 @@ __device__ __forceinline__ bool trav_next(Trav<Entry> &t, const int32_t *__restr
     }
 }
 
-// Whole-ray traversal: walk -> shade batch -> walk ... until exhausted or
-// stopped.  `stk` points at this thread's first stack slot in shared memory;
-// consecutive slots are `sstride` entries apart.
+// Whole-ray traversal: walk -> shade queue -> walk ... until exhausted or
+// stopped.  `smem` is the block's dynamic shared memory: the segment
+// queues (seg_bytes_per_thread per thread), then the stacks (one slot per
+// pending sibling, consecutive slots blockDim.x entries apart).
+//
+// Warp-synchronous while-while: the lanes that entered together walk and
+// shade in lock step (finished lanes idle), so every shading round runs
+// converged; queueing >= kSegMin segments per round keeps the walks of the
+// lanes similar in length.  (One last-level node per round shaded in
+// lock step wasted the walkers' time; letting the compiler interleave walk
+// and shade per lane shaded in partial warps -- both measured slower.)
 template <class Entry, class Visitor>
-__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth, const Ray &r, void *stk,
-                                         int sstride, Visitor &vis) {
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(stk);
-    const uint32_t stride = (uint32_t)sstride * Entry::kBytes;
+__device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int depth, const Ray &r,
+                                         unsigned char *smem, Visitor &vis) {
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const int nt = blockDim.x, tid = threadIdx.x;
+    SegBuf seg;
+    seg.init(sbase, nt, tid);
+    const uint32_t base = sbase + seg_bytes_per_thread(Visitor::kPops) * nt + (uint32_t)tid * Entry::kBytes;
+    const uint32_t stride = (uint32_t)nt * Entry::kBytes;
     Trav<Entry> t;
     t.init(r, base);
-    int32_t cp[4];
-    double st[5];
-    int keep;
-    while (trav_next(t, child, depth, r, base, stride, vis, cp, st, keep))
-        if (vis.batch(cp, st, keep)) return;
+    const unsigned mask = __activemask();
+    bool alive = true;
+    while (true) {
+        int n = 0;
+        if (alive) {
+            n = trav_next(t, child, depth, r, base, stride, vis, seg);
+            alive = n >= kSegMin;  // fewer: the walk is exhausted
+        }
+        __syncwarp(mask);
+        if (n && vis.batch(seg, n)) alive = false;
+        if (!__any_sync(mask, alive)) break;
+    }
 }
 
 // ------------------------------------------------------------ fp32 basis
@@ -581,8 +663,9 @@ struct FrameCtx {
 
 // CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
 // run time by S.rec != nullptr (scene kernel, per-instance slices).
-template <int NMAX, int CACHED, bool EDITS, bool VISITS>
+template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false>
 struct Shader {
+    static constexpr bool kPops = POPS;  // exact node-pop counts (stats)
     const TreeView &T;
     const SliceView &S;
     const FrameCtx &F;
@@ -600,6 +683,7 @@ struct Shader {
           acc2(0.0), aacc(0.0), tacc(0.0), used(0), pops(0), shaded(0), y_ready(false), visit(nullptr) {}
 
     __device__ __forceinline__ void pop() { ++pops; }
+    __device__ __forceinline__ int pop_count() const { return pops; }
 
     __device__ __forceinline__ void reset(float dx_, float dy_, float dz_) {
         dx = dx_;
@@ -613,38 +697,26 @@ struct Shader {
 
     __device__ __forceinline__ bool is_cached() const { return CACHED == 1 || (CACHED == 2 && S.rec != nullptr); }
 
-    // one last-level node's leaves: sigma of the whole batch is loaded up
-    // front (independent loads), then the segments are composited in order,
-    // shifting the batch down one slot per segment (no dynamic indexing)
-    __device__ __forceinline__ bool batch(int32_t *cp, double *st, int keep) {
-        double sg[4] = {0.0, 0.0, 0.0, 0.0};
+    // one round of queued segments: warm L1 with every queued record first
+    // (independent prefetches; one 128-byte line per record at n_max 2,
+    // sigma in its last 8 bytes), then composite them in order
+    __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
         if (is_cached()) {
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-                if (keep & (1 << s)) {
-                    // sigma from the record's last 8 bytes; warm L1 with the
-                    // whole record (one 128-byte line at n_max 2)
-                    sg[s] = S.sigma((uint32_t)cp[s]);
-                    const char *q = reinterpret_cast<const char *>(S.row((uint32_t)cp[s]));
-                    prefetch_l1(q);
-                    if (16 * S.rec4 > 128) prefetch_l1(q + 16 * S.rec4 - 1);
-                }
+#pragma unroll 1
+            for (int s = 0; s < n; ++s) {
+                const char *q = reinterpret_cast<const char *>(S.row((uint32_t)seg.leaf_at(s)));
+                prefetch_l1(q);
+                if (16 * S.rec4 > 128) prefetch_l1(q + 16 * S.rec4 - 1);
+            }
         }
 #pragma unroll 1
-        for (int s = 0; s < 4 && keep; ++s) {
-            if (keep & 1)
-                if (leaf((uint32_t)cp[0], st[0], st[1], sg[0])) return true;
-            keep >>= 1;
-            cp[0] = cp[1];
-            cp[1] = cp[2];
-            cp[2] = cp[3];
-            st[0] = st[1];
-            st[1] = st[2];
-            st[2] = st[3];
-            st[3] = st[4];
-            sg[0] = sg[1];
-            sg[1] = sg[2];
-            sg[2] = sg[3];
+        for (int s = 0; s < n; ++s) {
+            const uint32_t L = (uint32_t)seg.leaf_at(s);
+            const double sg = is_cached() ? S.sigma(L) : 0.0;
+            if (leaf(L, seg.t0_at(s), seg.t1_at(s), sg)) {
+                if (POPS) pops = seg.pops_at(s);  // the walk may have run ahead
+                return true;
+            }
         }
         return false;
     }
@@ -744,29 +816,30 @@ struct Shader {
 
 // Traversal-only visitors (count / collect, kernels.py:313-367)
 struct CountVisitor {
+    static constexpr bool kPops = false;
     int64_t count = 0;
     __device__ __forceinline__ void pop() {}
-    __device__ __forceinline__ bool batch(int32_t *, double *, int keep) {
-        count += __popc(keep);
+    __device__ __forceinline__ int pop_count() const { return 0; }
+    __device__ __forceinline__ bool batch(const SegBuf &, int n) {
+        count += n;
         return false;
     }
 };
 struct CollectVisitor {
+    static constexpr bool kPops = false;
     int64_t *leaf_out;
     double *t0_out, *t1_out;
     int64_t count, cap;
     __device__ __forceinline__ void pop() {}
-    __device__ __forceinline__ bool batch(int32_t *cp, double *st, int keep) {
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            if (keep & (1 << s)) {
-                if (count < cap) {
-                    leaf_out[count] = (int64_t)cp[s];
-                    t0_out[count] = st[s];
-                    t1_out[count] = st[s + 1];
-                }
-                ++count;
+    __device__ __forceinline__ int pop_count() const { return 0; }
+    __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
+        for (int s = 0; s < n; ++s) {
+            if (count < cap) {
+                leaf_out[count] = (int64_t)seg.leaf_at(s);
+                t0_out[count] = seg.t0_at(s);
+                t1_out[count] = seg.t1_at(s);
             }
+            ++count;
         }
         return false;
     }

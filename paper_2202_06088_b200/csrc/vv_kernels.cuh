@@ -64,15 +64,14 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_rays(const __gri
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.n) return;
-    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     const double ox = p.origins[3 * r], oy = p.origins[3 * r + 1], oz = p.origins[3 * r + 2];
     const double dx = p.dirs[3 * r], dy = p.dirs[3 * r + 1], dz = p.dirs[3 * r + 2];
     FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
-    Shader<NMAX, CACHED, EDITS, VISITS> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+    Shader<NMAX, CACHED, EDITS, VISITS, true> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
     if (VISITS) sh.visit = p.visit_leaf + p.visit_start[r];
     Ray ray;
     if (ray_setup(p.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
-        traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
+        traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
     if (VISITS) return;
     p.premult[3 * r + 0] = sh.acc0;
     p.premult[3 * r + 1] = sh.acc1;
@@ -171,7 +170,6 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __g
     int x0, y0, lx0, ly0;
     long long my_tile;
     block_origin(p, x0, y0, my_tile, lx0, ly0);
-    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
 #pragma unroll 1
     for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
@@ -188,7 +186,7 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __g
             Shader<NMAX, CACHED, EDITS, false> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
             Ray ray;
             if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
-                traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, sh);
+                traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
         }
@@ -224,7 +222,6 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
     int ix, iy;
     block_pixel(blockIdx.x, blockIdx.y, ix, iy);
     if (ix >= p.cam.width || iy >= p.cam.height) return;
-    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     double cdx, cdy, cdz;
     camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
     // blended state (compose.py:386-405): I (3), D, A
@@ -258,7 +255,7 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
         Shader<NMAX, 2, true, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
         Ray ray;
         if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
-            traverse<Entry>(v.T.child, v.T.depth, ray, stk, blockDim.x, sh);
+            traverse<Entry>(v.T.child, v.T.depth, ray, smem_raw, sh);
         // finalize_layer in float64
         const double al = sh.aacc;
         const double safe = al > 1e-300 ? al : 1e-300;
@@ -419,17 +416,16 @@ __global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ Seg
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.n) return;
-    unsigned char *stk = smem_raw + threadIdx.x * Entry::kBytes;
     Ray ray;
     const bool hit = ray_setup(p.T, p.origins[3 * r], p.origins[3 * r + 1], p.origins[3 * r + 2],
                                p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
     if (COLLECT) {
         const int64_t b = p.ray_start[r];
         CollectVisitor v{p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
-        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
+        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, v);
     } else {
         CountVisitor v;
-        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, stk, blockDim.x, v);
+        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, v);
         p.count[r] = v.count;
     }
 }
@@ -446,8 +442,11 @@ inline int with_nmax(int nmax, F &&f) {
     }
 }
 
-inline size_t stack_bytes(int depth, bool wide) {
-    return (size_t)stack_cap(depth) * kBlock * (wide ? EntryW::kBytes : EntryN::kBytes);
+// traversal shared memory per block: segment queues + stacks (traverse());
+// pops: the visitor queues node-visit counts (k_render_rays)
+inline size_t stack_bytes(int depth, bool wide, bool pops = false) {
+    return (size_t)kBlock *
+           (seg_bytes_per_thread(pops) + (size_t)stack_cap(depth) * (wide ? EntryW::kBytes : EntryN::kBytes));
 }
 
 template <class Kern>

@@ -25,6 +25,7 @@ static int pick(int mode, bool edits, const CamParams &p, unsigned grid, size_t 
 
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned grid, size_t smem,
                   cudaStream_t st) {
+    smem = stack_bytes(p.T.depth, wide);  // this TU's queue geometry (A/B builds vary it)
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
         return wide ? pick<NM, EntryW>(mode, edits, p, grid, smem, st) : pick<NM, EntryN>(mode, edits, p, grid, smem, st);

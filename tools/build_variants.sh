@@ -7,6 +7,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 CS=$ROOT/paper_2202_06088_b200/csrc
 make -s -C $CS
 NVCC=/usr/local/cuda/bin/nvcc
+BASEFLAGS=${BASEFLAGS:-}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 OBJ=$ROOT/paper_2202_06088_b200/_lib/obj
 while [ $# -gt 1 ]; do
