@@ -336,8 +336,8 @@ def run_ours(args, rank, world, local_rank):
     # end-to-end through the public API: render() -> host numpy images
     e2e = None
     if world == 1:
-        for f in warm_frames[:2]:
-            vv.render(tree, cam, f)
+        for f in warm_frames[:3]:  # two results alive at once in the loop below: warm both pinned buffers
+            layer = vv.render(tree, cam, f)
         torch.cuda.synchronize()
         # single-call latency: render() -> numpy, one frame at a time
         te = time.perf_counter()
