@@ -205,6 +205,21 @@ int vv_collect_segments(const vv_tree *tree, const double *origins, const double
                         int64_t n, double tmin, double tmax, const int64_t *ray_start,
                         int64_t *seg_leaf, double *seg_t0, double *seg_t1, void *stream);
 
+/* ---- paint / termination voxel ---------------------------------------------
+ * Replaces the per-pixel loop of compose.paint (compose.py:482-532): for
+ * each ray, walk every leaf segment (ray_segments, octree.py:296-326, no
+ * early stop), accumulate alpha with sigma = max(0, w_sigma . A[frame]) and
+ * delta = (t1 - t0) * norms[r], and write the first leaf row where the
+ * accumulated alpha reaches alpha_threshold, or -1.  Device pointers;
+ * norms[r] = |dirs[r]| as the caller computed it (np.linalg.norm). */
+int vv_termination_leaves(const vv_tree *tree, int32_t frame, const double *origins,
+                          const double *dirs, const double *norms, int64_t n,
+                          double alpha_threshold, int64_t *out_leaf, void *stream);
+/* Replace a replica's edit channels (VOctree.edit_rgb / edit_t, octree.py:
+ * 84-108, written by paint) from HOST arrays of n_leaves rows, without
+ * re-uploading the payload; both NULL removes them.  Synchronous. */
+int vv_tree_set_edits(vv_tree *tree, const float *edit_rgb, const int32_t *edit_t);
+
 /* ---- .voct codec (host) ----------------------------------------------------
  * Replaces the node-table loops of VOctree.to_bytes / from_bytes
  * (octree.py:383-394, 440-455).  parse: reads n_internal BFS records

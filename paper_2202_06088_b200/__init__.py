@@ -6,7 +6,18 @@ Camera, RenderOptions, LayerImages, Scene, SceneInstance, render_scene, ...)
 backed by hand-written sm_100a CUDA kernels in libvoxvid_b200.so.
 """
 
-from .compose import Light, Scene, SceneInstance, TimeMap, blend_layers, duplicate, render_instance, render_scene
+from .compose import (
+    Light,
+    Scene,
+    SceneInstance,
+    TimeMap,
+    blend_layers,
+    duplicate,
+    paint,
+    render_instance,
+    render_scene,
+    termination_leaves,
+)
 from .octree import (
     BadMagicError,
     ChecksumError,
@@ -39,5 +50,6 @@ __all__ = [
     "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
-    "render_instance", "render_scene", "duplicate", "TemporalBases", "make_bump_bases",
+    "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "TemporalBases",
+    "make_bump_bases",
 ]

@@ -64,6 +64,8 @@ EXPORTED_SYMBOLS = (
     "vv_render_scene",
     "vv_count_segments",
     "vv_collect_segments",
+    "vv_termination_leaves",
+    "vv_tree_set_edits",
     "vv_voct_parse_nodes",
     "vv_voct_encode_nodes",
     "vv_crc32",
@@ -174,6 +176,8 @@ _SIGNATURES = {
     ),
     "vv_count_segments": (ctypes.c_int, [_P, _P, _P, _I64, _D, _D, _P, _P]),
     "vv_collect_segments": (ctypes.c_int, [_P, _P, _P, _I64, _D, _D, _P, _P, _P, _P, _P]),
+    "vv_termination_leaves": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _I64, _D, _P, _P]),
+    "vv_tree_set_edits": (ctypes.c_int, [_P, _P, _P]),
     "vv_voct_parse_nodes": (ctypes.c_int, [_P, ctypes.c_size_t, _I64, _P, ctypes.POINTER(ctypes.c_size_t)]),
     "vv_voct_encode_nodes": (ctypes.c_int, [_P, _I64, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "vv_crc32": (ctypes.c_uint32, [ctypes.c_uint32, _P, ctypes.c_size_t]),

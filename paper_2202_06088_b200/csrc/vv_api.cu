@@ -679,4 +679,65 @@ int vv_collect_segments(const vv_tree *t, const double *origins, const double *d
     return segments_impl(t, origins, dirs, n, tmin, tmax, nullptr, ray_start, seg_leaf, seg_t0, seg_t1, stream);
 }
 
+int vv_termination_leaves(const vv_tree *t, int32_t frame, const double *origins, const double *dirs,
+                          const double *norms, int64_t n, double alpha_threshold, int64_t *out_leaf, void *stream) {
+    if (!t) return set_error(VV_E_INVALID, "null tree");
+    if (n == 0) return VV_OK;
+    if (!origins || !dirs || !norms || !out_leaf) return set_error(VV_E_INVALID, "null argument");
+    int rc = check_frame(t, frame);
+    if (rc) return rc;
+    DeviceGuard g(t->device);
+    TermParams p;
+    p.T = t->view;
+    p.frame = frame;
+    p.origins = origins;
+    p.dirs = dirs;
+    p.norms = norms;
+    p.n = n;
+    p.thr = alpha_threshold;
+    p.out_leaf = out_leaf;
+    const bool wide = t->depth > kNarrowDepth;
+    const size_t smem = stack_bytes(t->depth, wide);
+    const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
+    return launch_terminate(wide, p, grid, smem, (cudaStream_t)stream);
+}
+
+int vv_tree_set_edits(vv_tree *t, const float *edit_rgb, const int32_t *edit_t) {
+    if (!t) return set_error(VV_E_INVALID, "null tree");
+    if ((edit_rgb == nullptr) != (edit_t == nullptr))
+        return set_error(VV_E_INVALID, "edit_rgb and edit_t must both be set or both be NULL");
+    DeviceGuard g(t->device);
+    const int64_t nl = t->n_leaves;
+    if (!edit_rgb || nl == 0) {
+        cudaDeviceSynchronize();  // no kernel may still read the old channels
+        cudaFree(t->d_edit_rgb);
+        cudaFree(t->d_edit_t);
+        if (t->d_edit_rgb) t->bytes -= nl * (int64_t)(sizeof(float4) + sizeof(int2));
+        t->d_edit_rgb = nullptr;
+        t->d_edit_t = nullptr;
+        t->has_edits = false;
+        t->view.edit_rgb = nullptr;
+        t->view.edit_t = nullptr;
+        return VV_OK;
+    }
+    if (!t->d_edit_rgb) {
+        if (cudaMalloc(&t->d_edit_rgb, (size_t)nl * sizeof(float4)) != cudaSuccess ||
+            cudaMalloc(&t->d_edit_t, (size_t)nl * sizeof(int2)) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(t->d_edit_rgb);
+            t->d_edit_rgb = nullptr;
+            t->d_edit_t = nullptr;
+            return set_error(VV_E_NOMEM, "edit channel allocation failed");
+        }
+        t->bytes += nl * (int64_t)(sizeof(float4) + sizeof(int2));
+    }
+    cudaDeviceSynchronize();  // stream-ordered renders may still read the old values
+    VV_CUDA(cudaMemcpy(t->d_edit_rgb, edit_rgb, (size_t)nl * sizeof(float4), cudaMemcpyHostToDevice));
+    VV_CUDA(cudaMemcpy(t->d_edit_t, edit_t, (size_t)nl * sizeof(int2), cudaMemcpyHostToDevice));
+    t->has_edits = true;
+    t->view.edit_rgb = t->d_edit_rgb;
+    t->view.edit_t = t->d_edit_t;
+    return VV_OK;
+}
+
 }  // extern "C"

@@ -430,6 +430,68 @@ __global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ Seg
     }
 }
 
+// ------------------------------------------------------------------ paint query
+// Termination voxel of compose.paint (compose.py:482-532): walk all leaf
+// segments of the ray (ray_segments, octree.py:296-326) and return the
+// first leaf where accumulated alpha reaches the threshold, else -1.
+// sigma = max(0, w_sigma . A[frame]) in f64 (sequential; the reference
+// uses numpy's matmul -- equal to within an ulp), delta = (t1 - t0) * |d|
+// with |d| from the host (np.linalg.norm, as ray_segments).
+struct TermParams {
+    TreeView T;
+    int frame;
+    const double *origins, *dirs, *norms;
+    int64_t n;
+    double thr;
+    int64_t *out_leaf;
+};
+
+struct TerminateVisitor {
+    static constexpr bool kPops = false;
+    const TreeView &T;
+    const float *sA;
+    double norm, thr;
+    double acc = 0.0, trans = 1.0;
+    int64_t hit = -1;
+    __device__ __forceinline__ TerminateVisitor(const TreeView &T_, const float *sA_, double norm_, double thr_)
+        : T(T_), sA(sA_), norm(norm_), thr(thr_) {}
+    __device__ __forceinline__ void pop() {}
+    __device__ __forceinline__ int pop_count() const { return 0; }
+    __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
+        for (int s = 0; s < n; ++s) {
+            const uint32_t L = (uint32_t)seg.leaf_at(s);
+            const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, sA, T.C);
+            const double sigma = sp > 0.0 ? sp : 0.0;
+            const double delta = xmul(xsub(seg.t1_at(s), seg.t0_at(s)), norm);
+            const double a = xsub(1.0, exp(xmul(-sigma, delta)));
+            acc = xadd(acc, xmul(trans, a));
+            trans = xmul(trans, xsub(1.0, a));
+            if (acc >= thr) {
+                hit = (int64_t)L;
+                return true;
+            }
+        }
+        return false;
+    }
+};
+
+template <class Entry>
+__global__ void __launch_bounds__(kBlock) k_terminate(const __grid_constant__ TermParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxC];
+    for (int c = threadIdx.x; c < kMaxC; c += blockDim.x)
+        sA[c] = c < p.T.C ? p.T.basis_a[(size_t)p.frame * p.T.C + c] : 0.0f;
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= p.n) return;
+    Ray ray;
+    const bool hit = ray_setup(p.T, p.origins[3 * r], p.origins[3 * r + 1], p.origins[3 * r + 2],
+                               p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], 0.0, 1e30, ray);
+    TerminateVisitor v(p.T, sA, p.norms[r], p.thr);
+    if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, v);
+    p.out_leaf[r] = v.hit;
+}
+
 // ------------------------------------------------------------------ dispatch helpers
 template <class F>
 inline int with_nmax(int nmax, F &&f) {
@@ -488,6 +550,7 @@ int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p,
 int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
+int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
                   float *rest, cudaStream_t st);
 int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,

@@ -76,6 +76,19 @@ int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, 
     return collect ? go_seg<EntryN, true>(p, grid, smem, st) : go_seg<EntryN, false>(p, grid, smem, st);
 }
 
+template <class Entry>
+static int go_term(const TermParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    auto kern = k_terminate<Entry>;
+    int r = prep_smem(kern, smem);
+    if (r) return r;
+    kern<<<grid, kBlock, smem, st>>>(p);
+    return check_launch("terminate");
+}
+
+int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st) {
+    return wide ? go_term<EntryW>(p, grid, smem, st) : go_term<EntryN>(p, grid, smem, st);
+}
+
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
                   float *rest, cudaStream_t st) {
     k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, sig4, rest4, hh_off4, sig, rest);

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native
 
-__all__ = ["DeviceTree", "replica", "invalidate", "torch_device", "stream_ptr", "require_cuda"]
+__all__ = ["DeviceTree", "replica", "invalidate", "sync_edits", "torch_device", "stream_ptr", "require_cuda"]
 
 _lock = threading.Lock()
 
@@ -159,3 +159,26 @@ def invalidate(tree) -> None:
     cache = getattr(tree, "_vv_replicas", None)
     if cache:
         cache.clear()
+
+
+def sync_edits(tree) -> None:
+    """Push ``tree``'s host edit channels (edit_rgb / edit_t) to its cached
+    replicas in place (vv_tree_set_edits) -- after paint -- instead of
+    re-uploading the payload."""
+    cache = getattr(tree, "_vv_replicas", None)
+    if not cache:
+        return
+    er = getattr(tree, "edit_rgb", None)
+    et = getattr(tree, "edit_t", None)
+    lib = _native.lib()
+    with _lock:
+        for dev, (_, rep) in list(cache.items()):
+            if er is None or et is None:
+                _native.check(lib.vv_tree_set_edits(rep.handle, None, None))
+            else:
+                rgb = np.ascontiguousarray(er, dtype=np.float32)
+                t = np.ascontiguousarray(et, dtype=np.int32)
+                if rgb.shape != (rep.n_leaves, 4) or t.shape != (rep.n_leaves, 2):
+                    raise ValueError(f"edit arrays must be ({rep.n_leaves}, 4) / ({rep.n_leaves}, 2)")
+                _native.check(lib.vv_tree_set_edits(rep.handle, rgb.ctypes.data, t.ctypes.data))
+            cache[dev] = (_key(tree), rep)

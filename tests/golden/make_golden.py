@@ -15,7 +15,11 @@ frame, options) and the reference outputs:
 * full segment lists from count/collect_segments_kernel (kernels.py:313-367);
 * build_frame_cache sigma/q (kernels.py:397-407);
 * LayerImages from render() and images from compose.render_scene;
-* .voct bytes from VOctree.to_bytes.
+* .voct bytes from VOctree.to_bytes;
+* compose.paint results (edit channels, skipped pixels) and the per-ray
+  termination leaves of its loop (compose.py:508-522).
+
+    python tests/golden/make_golden.py [case ...]   # default: every case
 """
 
 from __future__ import annotations
@@ -37,7 +41,7 @@ sys.path.insert(0, str(REPO))
 from voxvid import hh as rhh  # noqa: E402
 from voxvid import kernels as rk  # noqa: E402
 from voxvid import temporal as rt  # noqa: E402
-from voxvid.compose import Scene, SceneInstance, TimeMap, render_scene  # noqa: E402
+from voxvid.compose import Scene, SceneInstance, TimeMap, paint, render_scene  # noqa: E402
 from voxvid.octree import VOctree  # noqa: E402
 from voxvid.render import Camera, RenderOptions, build_frame_cache, render, render_rays  # noqa: E402
 from voxvid.train import TrainConfig, Trainer  # noqa: E402
@@ -311,7 +315,44 @@ def main():
             c[f"n{n_max}_{f}"] = getattr(tab, f)
     cases["tables"] = c
 
+    # J. paint (compose.py:482-532)
+    rng = np.random.default_rng(71)
+    tree = random_payload_tree(rng, depth=4, fill=0.3, frames=6, n_max=1, sigma_scale=12.0)
+    cam = Camera.look_at([2.2, -0.8, 1.4], [0.5, 0.5, 0.5], width=24, height=20)
+    c = dict(tree_arrays(tree), cam_c2w=cam.c2w, cam_wh=np.array([cam.width, cam.height]),
+             cam_f=np.array([cam.fx, cam.fy, cam.cx, cam.cy]))
+    # per-ray termination leaves at frame 1, threshold 0.9: the loop of
+    # compose.py:508-522 over the reference's own ray_segments and sigma
+    o, d = cam.rays()
+    sig = np.maximum(0.0, tree.leaf_data[:, :tree.coeff_count].astype(np.float64)
+                     @ tree.bases.a[1].astype(np.float64))
+    term = np.full(len(o), -1, np.int64)
+    for r in range(len(o)):
+        acc, trans = 0.0, 1.0
+        for seg in tree.ray_segments(o[r], d[r]):
+            a = 1.0 - math.exp(-sig[seg.leaf] * seg.delta)
+            acc += trans * a
+            trans *= 1.0 - a
+            if acc >= 0.9:
+                term[r] = seg.leaf
+                break
+    c.update(origins=o, dirs=d, term_leaf=term)
+    mask = rng.random((cam.height, cam.width)) < 0.5
+    res = paint(tree, cam, mask, (0.9, 0.2, 0.1), (1, 4), alpha_threshold=0.9)
+    c.update(p1_mask=mask, p1_edited=np.int64(res["edited_voxels"]),
+             p1_skipped=np.array(res["skipped_pixels"], np.int64).reshape(-1, 2),
+             p1_edit_rgb=tree.edit_rgb.copy(), p1_edit_t=tree.edit_t.copy())
+    pix = np.array([[3, 4], [10, 2], [23, 19], [0, 0], [12, 10], [15, 9]])
+    res = paint(tree, cam, pix, (0.1, 0.8, 0.3), (2, 5), alpha_threshold=0.5, target_density=7.5, frame=3)
+    c.update(p2_pixels=pix, p2_edited=np.int64(res["edited_voxels"]),
+             p2_skipped=np.array(res["skipped_pixels"], np.int64).reshape(-1, 2),
+             p2_edit_rgb=tree.edit_rgb.copy(), p2_edit_t=tree.edit_t.copy())
+    cases["paint"] = c
+
+    want = set(sys.argv[1:])
     for name, arrays in cases.items():
+        if want and name not in want:
+            continue
         path = HERE / f"{name}.npz"
         np.savez_compressed(path, **arrays)
         print(f"{path.name}: {path.stat().st_size / 1024:.0f} KiB")

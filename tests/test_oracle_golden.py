@@ -135,3 +135,13 @@ def test_other_truncations(n_max):
     _exact(out["visit_leaf"], g["visit_leaf"])
     # premult: sin(g)**3 may round differently in the last bit at n_max = 3
     np.testing.assert_allclose(out["premult"], g["premult"], rtol=0, atol=1e-14)
+
+
+def test_paint_termination_leaves_oracle():
+    """compose.paint's termination voxel per ray (compose.py:508-522) vs the
+    reference's own loop over ray_segments."""
+    g = load("paint")
+    tree = tree_from(g)
+    got = oracle.termination_leaves(tree, g["origins"], g["dirs"], 1, 0.9)
+    assert np.array_equal(got, g["term_leaf"])
+    assert (got >= 0).sum() > 10
