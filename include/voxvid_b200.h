@@ -231,6 +231,21 @@ int vv_voct_parse_nodes(const uint8_t *buf, size_t len, int64_t n_internal,
                         int32_t *node_child, size_t *consumed);
 int vv_voct_encode_nodes(const int32_t *node_child, int64_t n_internal, uint8_t *buf,
                          size_t cap, size_t *used);
+/* Whole .voct stream -> device replica, no host arrays (octree.py:371-510,
+ * VOctree.from_bytes + upload): validates in the reference's order with its
+ * error classes (VV_E_TRUNCATED / VV_E_MAGIC / VV_E_VERSION / VV_E_CHECKSUM /
+ * VV_E_FORMAT for a non-cube bbox, trailing bytes or a K that is no HH
+ * count), checks the CRC (host threads), parses the node table and streams
+ * the payload block from buf through the device repack; edit channels are
+ * unpacked from the 5 extra columns.  info (optional) receives the header. */
+typedef struct {
+    int32_t version, flags, depth, frames, coeff_count, basis_count, n_max;
+    int32_t reserved;
+    int64_t n_internal, n_leaves;
+    double bbox_lo[3];
+    double side;
+} vv_voct_info;
+int vv_voct_upload(const uint8_t *buf, size_t len, int device, vv_tree **out, vv_voct_info *info);
 /* CRC-32 (zlib polynomial) of buf, continuing from crc. */
 uint32_t vv_crc32(uint32_t crc, const uint8_t *buf, size_t len);
 

@@ -18,6 +18,7 @@ from .compose import (
     render_scene,
     termination_leaves,
 )
+from .device import DeviceTree, load_device
 from .octree import (
     BadMagicError,
     ChecksumError,
@@ -46,7 +47,7 @@ from .render import (
 from .temporal import TemporalBases, make_bump_bases
 
 __all__ = [
-    "VOctree", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
+    "VOctree", "DeviceTree", "load_device", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
     "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",

@@ -21,6 +21,7 @@ __all__ = [
     "check",
     "VVError",
     "TreeDesc",
+    "VoctInfo",
     "RenderOpts",
     "CameraDesc",
     "InstanceDesc",
@@ -69,6 +70,7 @@ EXPORTED_SYMBOLS = (
     "vv_voct_parse_nodes",
     "vv_voct_encode_nodes",
     "vv_crc32",
+    "vv_voct_upload",
 )
 
 
@@ -96,6 +98,25 @@ class TreeDesc(ctypes.Structure):
         ("basis_b", ctypes.c_void_p),
         ("edit_rgb", ctypes.c_void_p),
         ("edit_t", ctypes.c_void_p),
+    ]
+
+
+class VoctInfo(ctypes.Structure):
+    """vv_voct_info: header of an uploaded .voct stream."""
+
+    _fields_ = [
+        ("version", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("depth", ctypes.c_int32),
+        ("frames", ctypes.c_int32),
+        ("coeff_count", ctypes.c_int32),
+        ("basis_count", ctypes.c_int32),
+        ("n_max", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("n_internal", ctypes.c_int64),
+        ("n_leaves", ctypes.c_int64),
+        ("bbox_lo", ctypes.c_double * 3),
+        ("side", ctypes.c_double),
     ]
 
 
@@ -181,6 +202,7 @@ _SIGNATURES = {
     "vv_voct_parse_nodes": (ctypes.c_int, [_P, ctypes.c_size_t, _I64, _P, ctypes.POINTER(ctypes.c_size_t)]),
     "vv_voct_encode_nodes": (ctypes.c_int, [_P, _I64, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "vv_crc32": (ctypes.c_uint32, [ctypes.c_uint32, _P, ctypes.c_size_t]),
+    "vv_voct_upload": (ctypes.c_int, [_P, ctypes.c_size_t, ctypes.c_int, _P, _P]),
 }
 
 _lib = None

@@ -200,7 +200,9 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     return launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st);
 }
 
-int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool host_src) {
+// src_stride: floats per source payload row (0: 2C + 3K; .voct rows with
+// edit channels carry 5 more, vv_voct_upload)
+int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool host_src, int64_t src_stride = 0) {
     if (!d || !out) return set_error(VV_E_INVALID, "null argument");
     if (d->depth < 1 || d->depth > kMaxDepth)
         return set_error(VV_E_UNSUPPORTED, "depth %d outside [1, %d]", d->depth, kMaxDepth);
@@ -269,7 +271,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     }
     // payload rows -> padded planes, chunked through a device staging buffer
     if (nl > 0) {
-        const int64_t row_b = (int64_t)P * sizeof(float);
+        const int64_t stride = src_stride > 0 ? src_stride : P;
+        const int64_t row_b = stride * (int64_t)sizeof(float);
         const int64_t chunk = host_src ? std::max<int64_t>(1, std::min<int64_t>(nl, (256ll << 20) / row_b)) : nl;
         float *stage = nullptr;
         if (host_src) {
@@ -280,7 +283,7 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
         }
         for (int64_t r0 = 0; r0 < nl; r0 += chunk) {
             const int64_t rows = std::min(chunk, nl - r0);
-            const float *src = d->leaf_data + r0 * P;
+            const float *src = d->leaf_data + r0 * stride;
             if (host_src) {
                 if ((e = cudaMemcpy(stage, src, rows * row_b, cudaMemcpyHostToDevice)) != cudaSuccess) {
                     cudaFree(stage);
@@ -288,7 +291,7 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
                 }
                 src = stage;
             }
-            const int lrc = launch_repack(src, rows, P, C, K3, sig4, rest4, hh_off4,
+            const int lrc = launch_repack(src, rows, (int)stride, C, K3, sig4, rest4, hh_off4,
                                           reinterpret_cast<float *>(t->d_sig + r0 * sig4),
                                           reinterpret_cast<float *>(t->d_rest + r0 * rest4), nullptr);
             if (lrc) {
@@ -737,6 +740,117 @@ int vv_tree_set_edits(vv_tree *t, const float *edit_rgb, const int32_t *edit_t) 
     t->has_edits = true;
     t->view.edit_rgb = t->d_edit_rgb;
     t->view.edit_t = t->d_edit_t;
+    return VV_OK;
+}
+
+int vv_voct_upload(const uint8_t *buf, size_t len, int device, vv_tree **out, vv_voct_info *info) {
+    if (!buf || !out) return set_error(VV_E_INVALID, "null argument");
+    // checks in the order of VOctree.from_bytes (octree.py:440-510)
+    if (len < 4) return set_error(VV_E_TRUNCATED, "stream of %zu bytes is shorter than the magic", len);
+    if (memcmp(buf, "VOCT", 4) != 0) {
+        char m[64];
+        int k = 0;
+        for (int i = 0; i < 4; ++i) {
+            const unsigned c = buf[i];
+            k += (c >= 32 && c < 127 && c != '\\' && c != '\'') ? snprintf(m + k, sizeof(m) - k, "%c", c)
+                                                                   : snprintf(m + k, sizeof(m) - k, "\\x%02x", c);
+        }
+        return set_error(VV_E_MAGIC, "bad magic b'%s', expected b'VOCT'", m);
+    }
+    if (len < 8) return set_error(VV_E_TRUNCATED, "stream ends inside the header");
+    auto u32 = [&](size_t off) {
+        uint32_t v;
+        memcpy(&v, buf + off, 4);
+        return v;
+    };
+    if (u32(4) != 1u) return set_error(VV_E_VERSION, "unsupported .voct version %u", u32(4));
+    if (len < 4 + 24 + 48 + 8 + 4) return set_error(VV_E_TRUNCATED, "stream ends inside the header");
+    const size_t body = len - 4;
+    if (vv_crc32(0, buf, body) != u32(body)) return set_error(VV_E_CHECKSUM, "crc32 mismatch: stream corrupted");
+    const uint32_t flags = u32(8), depth = u32(12), T = u32(16), C = u32(20), K = u32(24);
+    double bbox[6];
+    memcpy(bbox, buf + 28, sizeof(bbox));
+    const uint32_t n_internal = u32(76), n_leaves = u32(80);
+    double sides[3], smin = 1e308, smax = -1e308;
+    for (int i = 0; i < 3; ++i) {
+        sides[i] = bbox[3 + i] - bbox[i];
+        smin = std::min(smin, sides[i]);
+        smax = std::max(smax, sides[i]);
+    }
+    if (smax - smin > 1e-9 * std::max(1.0, fabs(sides[0])))
+        return set_error(VV_E_FORMAT, "bbox is not a cube: sides [%.17g %.17g %.17g]", sides[0], sides[1], sides[2]);
+    std::vector<int32_t> node_child((size_t)std::max<uint32_t>(n_internal, 1) * 8, -1);
+    size_t off = 84, used = 0;
+    int rc = vv_voct_parse_nodes(buf + off, body - off, n_internal, node_child.data(), &used);
+    if (rc) return rc;
+    off += used;
+    const bool edits = (flags & 1u) != 0;
+    const int64_t P = 2 * (int64_t)C + 3 * (int64_t)K, plen = P + (edits ? 5 : 0);
+    const size_t need = (size_t)n_leaves * plen * 4 + 2 * (size_t)T * C * 4;
+    if (off + need > body) return set_error(VV_E_TRUNCATED, "stream ends inside the payload block");
+    if (off + need != body) return set_error(VV_E_FORMAT, "%zu trailing bytes after payload", body - off - need);
+    int n_max = -1;
+    for (int n = 0, k = 0; n <= 64; ++n) {  // _n_max_from_k: K = sum_{n' <= n} (n'+1)^2
+        k += (n + 1) * (n + 1);
+        if ((uint32_t)k == K) {
+            n_max = n;
+            break;
+        }
+        if ((uint32_t)k > K) break;
+    }
+    if (n_max < 0) return set_error(VV_E_FORMAT, "basis count %u is not a hyperspherical-harmonic count", K);
+    const uint8_t *payload = buf + off;
+    const uint8_t *a_ptr = payload + (size_t)n_leaves * plen * 4;
+    std::vector<float> edit_rgb;
+    std::vector<int32_t> edit_t;
+    vv_tree_desc d;
+    memset(&d, 0, sizeof(d));
+    d.depth = (int32_t)depth;
+    d.n_max = n_max;
+    d.frames = (int32_t)T;
+    d.coeff_count = (int32_t)C;
+    d.n_internal = std::max<uint32_t>(n_internal, 1);
+    d.n_leaves = n_leaves;
+    d.bbox_lo[0] = bbox[0];
+    d.bbox_lo[1] = bbox[1];
+    d.bbox_lo[2] = bbox[2];
+    d.side = sides[0];
+    d.node_child = node_child.data();
+    d.leaf_data = n_leaves ? reinterpret_cast<const float *>(payload) : nullptr;  // rows of plen floats
+    d.basis_a = reinterpret_cast<const float *>(a_ptr);
+    d.basis_b = reinterpret_cast<const float *>(a_ptr + (size_t)T * C * 4);
+    if (edits && n_leaves) {  // [w | rgb(4) | packed u16 range]
+        edit_rgb.resize((size_t)n_leaves * 4);
+        edit_t.resize((size_t)n_leaves * 2);
+        for (size_t r = 0; r < n_leaves; ++r) {
+            const uint8_t *row = payload + r * plen * 4;
+            memcpy(&edit_rgb[4 * r], row + (size_t)P * 4, 16);
+            uint32_t packed;
+            memcpy(&packed, row + (size_t)(P + 4) * 4, 4);
+            edit_t[2 * r] = (int32_t)(packed & 0xFFFFu);
+            edit_t[2 * r + 1] = (int32_t)(packed >> 16);
+        }
+        d.edit_rgb = edit_rgb.data();
+        d.edit_t = edit_t.data();
+    }
+    rc = tree_alloc_common(&d, device, out, true, plen);
+    if (rc) return rc;
+    if (info) {
+        memset(info, 0, sizeof(*info));
+        info->version = 1;
+        info->flags = (int32_t)flags;
+        info->depth = (int32_t)depth;
+        info->frames = (int32_t)T;
+        info->coeff_count = (int32_t)C;
+        info->basis_count = (int32_t)K;
+        info->n_max = n_max;
+        info->n_internal = n_internal;
+        info->n_leaves = n_leaves;
+        info->bbox_lo[0] = bbox[0];
+        info->bbox_lo[1] = bbox[1];
+        info->bbox_lo[2] = bbox[2];
+        info->side = sides[0];
+    }
     return VV_OK;
 }
 

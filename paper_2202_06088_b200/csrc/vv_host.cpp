@@ -3,6 +3,11 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #include "../../include/voxvid_b200.h"
 #include "vv_host_common.h"
 
@@ -157,9 +162,11 @@ int vv_voct_encode_nodes(const int32_t *node_child, int64_t n_internal, uint8_t 
     return VV_OK;
 }
 
-// CRC-32 (reflected 0xEDB88320), slicing-by-8.
+// CRC-32 (reflected 0xEDB88320), slicing-by-8; buffers >= 64 MB are split
+// across host threads and the chunk CRCs joined with the GF(2) shift
+// operator (the zlib crc32_combine construction).
 static uint32_t g_crc_tab[8][256];
-static bool g_crc_init = false;
+static std::once_flag g_crc_once;
 
 static void crc_init() {
     for (uint32_t i = 0; i < 256; ++i) {
@@ -174,11 +181,9 @@ static void crc_init() {
             g_crc_tab[t][i] = c;
         }
     }
-    g_crc_init = true;
 }
 
-uint32_t vv_crc32(uint32_t crc, const uint8_t *buf, size_t len) {
-    if (!g_crc_init) crc_init();
+static uint32_t crc_serial(uint32_t crc, const uint8_t *buf, size_t len) {
     uint32_t c = ~crc;
     while (len >= 8) {
         uint32_t lo, hi;
@@ -193,6 +198,63 @@ uint32_t vv_crc32(uint32_t crc, const uint8_t *buf, size_t len) {
     }
     while (len--) c = g_crc_tab[0][(c ^ *buf++) & 0xFF] ^ (c >> 8);
     return ~c;
+}
+
+// 32x32 GF(2) matrices as 32 column words
+static uint32_t gf2_times(const uint32_t *mat, uint32_t vec) {
+    uint32_t sum = 0;
+    for (int i = 0; vec; ++i, vec >>= 1)
+        if (vec & 1) sum ^= mat[i];
+    return sum;
+}
+static void gf2_square(uint32_t *sq, const uint32_t *mat) {
+    for (int n = 0; n < 32; ++n) sq[n] = gf2_times(mat, mat[n]);
+}
+
+// crc(A || B) from crc(A), crc(B) and |B|
+static uint32_t crc_combine(uint32_t crc1, uint32_t crc2, size_t len2) {
+    if (len2 == 0) return crc1;
+    uint32_t even[32], odd[32];
+    odd[0] = 0xEDB88320u;  // operator for one zero bit
+    uint32_t row = 1;
+    for (int n = 1; n < 32; ++n) {
+        odd[n] = row;
+        row <<= 1;
+    }
+    gf2_square(even, odd);  // two zero bits
+    gf2_square(odd, even);  // four zero bits
+    do {  // apply len2 zero bytes to crc1
+        gf2_square(even, odd);
+        if (len2 & 1) crc1 = gf2_times(even, crc1);
+        len2 >>= 1;
+        if (!len2) break;
+        gf2_square(odd, even);
+        if (len2 & 1) crc1 = gf2_times(odd, crc1);
+        len2 >>= 1;
+    } while (len2);
+    return crc1 ^ crc2;
+}
+
+uint32_t vv_crc32(uint32_t crc, const uint8_t *buf, size_t len) {
+    std::call_once(g_crc_once, crc_init);
+    const size_t kPar = 64u << 20;
+    unsigned nt = std::thread::hardware_concurrency();
+    if (len < kPar || nt < 2) return crc_serial(crc, buf, len);
+    nt = std::min<unsigned>(nt, 32u);
+    const size_t chunk = (len + nt - 1) / nt;
+    std::vector<uint32_t> part(nt, 0);
+    std::vector<size_t> plen(nt, 0);
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nt; ++i) {
+        const size_t b = (size_t)i * chunk, e = std::min(len, b + chunk);
+        if (b >= e) break;
+        plen[i] = e - b;
+        th.emplace_back([&, i, b, e] { part[i] = crc_serial(i == 0 ? crc : 0u, buf + b, e - b); });
+    }
+    for (auto &x : th) x.join();
+    uint32_t c = part[0];
+    for (unsigned i = 1; i < th.size(); ++i) c = crc_combine(c, part[i], plen[i]);
+    return c;
 }
 
 }  // extern "C"

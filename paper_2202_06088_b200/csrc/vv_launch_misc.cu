@@ -27,7 +27,7 @@ __global__ void k_unpack_tiles(const float *__restrict__ packed, int width, int 
 // leaf rows (P = 2C + 3K floats) -> sig plane (sig4 float4 per row) and
 // rest plane ([w_gamma pad to 4 | w_hh pad to 4], rest4 float4 per row)
 __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int sig4,
-                         int rest4, int hh_off4, float *sig, float *rest) {
+                         int rest4, int hh_off4, float *sig, float *rest) {  // P: source row stride (floats)
     const int sigw = 4 * sig4, restw = 4 * rest4;
     const int64_t total = rows * (int64_t)(sigw + restw);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;

@@ -23,7 +23,8 @@ import numpy as np
 
 from . import _native
 
-__all__ = ["DeviceTree", "replica", "invalidate", "sync_edits", "torch_device", "stream_ptr", "require_cuda"]
+__all__ = ["DeviceTree", "load_device", "replica", "invalidate", "sync_edits", "torch_device", "stream_ptr",
+           "require_cuda"]
 
 _lock = threading.Lock()
 
@@ -123,6 +124,48 @@ class DeviceTree:
         _native.check(lib.vv_tree_info(handle, None, None, None, None, ctypes.byref(nb)))
         self.device_bytes = int(nb.value)
 
+    @classmethod
+    def from_voct(cls, data, device=None) -> "DeviceTree":
+        """A .voct stream straight to the device (vv_voct_upload): the same
+        checks and exception classes as VOctree.from_bytes (octree.py:
+        413-501), no host VOctree arrays.  ``data``: bytes-like or path."""
+        from . import octree as _oct
+
+        torch = require_cuda()
+        if not isinstance(data, (bytes, bytearray, memoryview, np.ndarray)):
+            data = np.fromfile(str(data), dtype=np.uint8)
+        buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+        buf = np.ascontiguousarray(buf, dtype=np.uint8)
+        self = cls.__new__(cls)
+        self.device = torch_device(device)
+        lib = _native.lib()
+        handle = ctypes.c_void_p()
+        info = _native.VoctInfo()
+        rc = lib.vv_voct_upload(buf.ctypes.data if buf.size else None, buf.size, self.device.index,
+                                ctypes.byref(handle), ctypes.byref(info))
+        if rc != _native.VV_OK:
+            exc = {_native.VV_E_TRUNCATED: _oct.TruncatedStreamError, _native.VV_E_MAGIC: _oct.BadMagicError,
+                   _native.VV_E_VERSION: _oct.UnsupportedVersionError, _native.VV_E_CHECKSUM: _oct.ChecksumError,
+                   _native.VV_E_FORMAT: _oct.VoctError}.get(rc)
+            if exc is not None:
+                raise exc(_native.last_error())
+            _native.check(rc)
+        self.handle = handle
+        self.n_leaves = int(info.n_leaves)
+        self.n_internal = int(max(info.n_internal, 1))
+        self.depth = int(info.depth)
+        self.frames = int(info.frames)
+        self.coeff_count = int(info.coeff_count)
+        self.n_max = int(info.n_max)
+        self.s = (self.n_max + 1) ** 2
+        self.bbox_lo = np.array(info.bbox_lo[:], dtype=np.float64)
+        self.side = float(info.side)
+        self.has_edits = bool(info.flags & 1)
+        nb = ctypes.c_int64()
+        _native.check(lib.vv_tree_info(handle, None, None, None, None, ctypes.byref(nb)))
+        self.device_bytes = int(nb.value)
+        return self
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
@@ -182,3 +225,8 @@ def sync_edits(tree) -> None:
                     raise ValueError(f"edit arrays must be ({rep.n_leaves}, 4) / ({rep.n_leaves}, 2)")
                 _native.check(lib.vv_tree_set_edits(rep.handle, rgb.ctypes.data, t.ctypes.data))
             cache[dev] = (_key(tree), rep)
+
+
+def load_device(path, device=None) -> DeviceTree:
+    """``VOctree.load`` straight to a device replica (vv_voct_upload)."""
+    return DeviceTree.from_voct(path, device)

@@ -334,3 +334,27 @@ def test_render_sequence_reuse_interleave_abandon(cuda):
     for (fa, la), (fb, lb) in zip(zip([0, 2, 4, 6], a), zip([1, 3, 5, 7], b)):
         same(la, fa)
         same(lb, fb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["voct", "voct_edits"])
+def test_load_device_matches_host_path(cuda, key):
+    """.voct straight to the device (vv_voct_upload) renders bitwise like
+    VOctree.from_bytes + upload, edits included."""
+    g = load("voct")
+    data = bytes(g[key])
+    host = vv.VOctree.from_bytes(data)
+    dev = vv.DeviceTree.from_voct(data)
+    assert (dev.n_leaves, dev.depth, dev.frames, dev.has_edits) == (host.n_leaves, host.depth, host.frames,
+                                                                    host.has_edits)
+    cam = vv.Camera.look_at([2.1, -0.7, 1.5], [0.5, 0.5, 0.5], width=24, height=20)
+    for f in (0, 2):
+        a = vv.render(host, cam, f)
+        b = vv.render(dev, cam, f)
+        _exact(a.rgb, b.rgb)
+        _exact(a.alpha, b.alpha)
+        _exact(a.depth, b.depth)
+    with pytest.raises(vv.ChecksumError):
+        bad = bytearray(data)
+        bad[300] ^= 4
+        vv.DeviceTree.from_voct(bytes(bad))

@@ -260,3 +260,55 @@ def test_effective_affine_yaw():
     c = np.array([0.5, 0.5, 0.5, 1.0])
     np.testing.assert_allclose(m @ c, c, atol=1e-12)
     assert math.isclose(m[0, 1], -1.0, abs_tol=1e-12)
+
+
+def test_crc32_parallel_matches_zlib():
+    """vv_crc32 splits >= 64 MB buffers across threads (zlib crc32_combine)."""
+    import zlib
+
+    rng = np.random.default_rng(3)
+    buf = rng.integers(0, 256, (64 << 20) + 12345, dtype=np.uint8)
+    lib = _native.lib()
+    assert lib.vv_crc32(0, buf.ctypes.data, buf.size) == zlib.crc32(buf.tobytes()) & 0xFFFFFFFF
+    head = 1000
+    c0 = lib.vv_crc32(0, buf.ctypes.data, head)
+    assert lib.vv_crc32(c0, buf[head:].ctypes.data, buf.size - head) == zlib.crc32(buf.tobytes()) & 0xFFFFFFFF
+
+
+def test_voct_upload_error_classes():
+    """vv_voct_upload validates like VOctree.from_bytes (octree.py:413-501);
+    every check runs before any CUDA call."""
+    import ctypes
+    import struct
+    import zlib
+
+    from golden_util import load
+
+    good = bytes(load("voct")["voct"])
+    lib = _native.lib()
+
+    def rc_of(data):
+        b = np.frombuffer(data, dtype=np.uint8).copy()
+        h = ctypes.c_void_p()
+        return lib.vv_voct_upload(b.ctypes.data if b.size else None, b.size, 0, ctypes.byref(h), None)
+
+    def recrc(body):
+        return body + struct.pack("<I", zlib.crc32(body) & 0xFFFFFFFF)
+
+    assert rc_of(good[:3]) == _native.VV_E_TRUNCATED
+    assert rc_of(b"XXXX" + good[4:]) == _native.VV_E_MAGIC
+    assert "bad magic b'XXXX'" in _native.last_error()
+    assert rc_of(good[:6]) == _native.VV_E_TRUNCATED
+    assert rc_of(good[:4] + struct.pack("<I", 9) + good[8:]) == _native.VV_E_VERSION
+    assert rc_of(good[:40]) == _native.VV_E_TRUNCATED
+    bad = bytearray(good)
+    bad[200] ^= 1
+    assert rc_of(bytes(bad)) == _native.VV_E_CHECKSUM
+    body = good[:-4]
+    assert rc_of(recrc(body + b"\0\0\0\0")) == _native.VV_E_FORMAT
+    assert "trailing bytes" in _native.last_error()
+    assert rc_of(recrc(body[:-100])) == _native.VV_E_TRUNCATED
+    cube = bytearray(body)
+    struct.pack_into("<d", cube, 28 + 3 * 8, 2.0)  # hi.x: not a cube
+    assert rc_of(recrc(bytes(cube))) == _native.VV_E_FORMAT
+    assert "not a cube" in _native.last_error()
