@@ -190,7 +190,9 @@ int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int3
  * (blend_layers, compose.py:373-406), unpremultiplied (compose.py:457-460)
  * and composited over `background` (composite_background,
  * render.py:243-251).  Outputs (device fp32): image (H, W, 3); optional
- * blended alpha (H, W) and depth (H, W). */
+ * blended alpha (H, W) and depth (H, W).  background = NULL: image gets the
+ * blended, unpremultiplied layer rgb instead (input of the lighting passes,
+ * vv_scene_lighting); image may then be NULL too (alpha/depth only). */
 int vv_render_scene(const vv_instance *instances, int32_t n_instances,
                     const vv_render_opts *opts, const vv_camera *cam, const double *background,
                     float *image, float *alpha, float *depth, void *stream);
@@ -204,6 +206,38 @@ int vv_count_segments(const vv_tree *tree, const double *origins, const double *
 int vv_collect_segments(const vv_tree *tree, const double *origins, const double *dirs,
                         int64_t n, double tmin, double tmax, const int64_t *ray_start,
                         int64_t *seg_leaf, double *seg_t0, double *seg_t1, void *stream);
+
+/* ---- lighting passes (compose.py:539-619) ---------------------------------
+ * One point light: falloff scale clamp(r0^2 / (r0^2 + d^2), min, 1) on the
+ * blended colour where alpha > 0 (falloff_pass, compose.py:606-619), and a
+ * ground-plane shadow factor 1 - strength * occ on the background, occ
+ * sampled bilinearly (map_coordinates order 1, mode "constant") from the
+ * light's blurred alpha map through its camera (ShadowMap.background_factor
+ * / factor_at_points, compose.py:547-582).  w2c: row-major 3x4 of
+ * inv(light_cam.c2w) as the host computed it. */
+typedef struct {
+    double position[3];
+    double ground_plane[4];
+    double shadow_strength, falloff_r0, falloff_min_scale;
+    int32_t cast_shadows, falloff_enabled;
+    const double *shadow_map; /* (res, res) device f64, row = y */
+    int32_t shadow_res, reserved;
+    double w2c[12];
+    double fx, fy, cx, cy;    /* light camera intrinsics */
+} vv_light;
+/* shadow_pass's blur (compose.py:590-602): scipy gaussian_filter, mode
+ * "constant", truncate 4 -- weights (2 radius + 1, host, normalised as
+ * scipy's _gaussian_kernel1d) correlated along rows then columns in
+ * scipy's symmetric summation order, f64.  alpha: (res, res) device fp32
+ * joint alpha; tmp, out: (res, res) device f64.  radius 0: plain copy. */
+int vv_shadow_blur(const float *alpha, int32_t res, const double *weights, int32_t radius, double *tmp,
+                   double *out, void *stream);
+/* Lights applied in order to the blended layer (vv_render_scene with
+ * background NULL), then composite_background over `background`
+ * (render_scene, compose.py:462-471).  Device fp32 images; at most 16 lights. */
+int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
+                      const double *background, const vv_light *lights, int32_t n_lights, float *image,
+                      void *stream);
 
 /* ---- paint / termination voxel ---------------------------------------------
  * Replaces the per-pixel loop of compose.paint (compose.py:482-532): for

@@ -25,6 +25,7 @@ __all__ = [
     "RenderOpts",
     "CameraDesc",
     "InstanceDesc",
+    "LightDesc",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -63,6 +64,8 @@ EXPORTED_SYMBOLS = (
     "vv_render_camera_tiles",
     "vv_unpack_tiles",
     "vv_render_scene",
+    "vv_shadow_blur",
+    "vv_scene_lighting",
     "vv_count_segments",
     "vv_collect_segments",
     "vv_termination_leaves",
@@ -145,6 +148,28 @@ class CameraDesc(ctypes.Structure):
     ]
 
 
+class LightDesc(ctypes.Structure):
+    """vv_light (include/voxvid_b200.h)."""
+
+    _fields_ = [
+        ("position", ctypes.c_double * 3),
+        ("ground_plane", ctypes.c_double * 4),
+        ("shadow_strength", ctypes.c_double),
+        ("falloff_r0", ctypes.c_double),
+        ("falloff_min_scale", ctypes.c_double),
+        ("cast_shadows", ctypes.c_int32),
+        ("falloff_enabled", ctypes.c_int32),
+        ("shadow_map", ctypes.c_void_p),
+        ("shadow_res", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("w2c", ctypes.c_double * 12),
+        ("fx", ctypes.c_double),
+        ("fy", ctypes.c_double),
+        ("cx", ctypes.c_double),
+        ("cy", ctypes.c_double),
+    ]
+
+
 class InstanceDesc(ctypes.Structure):
     _fields_ = [
         ("tree", ctypes.c_void_p),
@@ -190,6 +215,8 @@ _SIGNATURES = {
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _I32, _I32, _I32, _P, _P],
     ),
     "vv_unpack_tiles": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
+    "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),
     "vv_render_scene": (
         ctypes.c_int,
         [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),

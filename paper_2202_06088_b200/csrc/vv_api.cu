@@ -578,7 +578,9 @@ int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int3
 
 int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
                     const double *background, float *image, float *alpha, float *depth, void *stream) {
-    if (!inst || !cam || !image || !background) return set_error(VV_E_INVALID, "null argument");
+    if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
+    if (!image && !alpha && !depth) return set_error(VV_E_INVALID, "no output");
+    if (background && !image) return set_error(VV_E_INVALID, "background given without an image output");
     if (n_inst < 1) return set_error(VV_E_INVALID, "scene has no visible instances");
     if (n_inst > kMaxInst) return set_error(VV_E_UNSUPPORTED, "at most %d instances per fused scene", kMaxInst);
     const vv_tree *t0 = inst[0].tree;
@@ -616,9 +618,10 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
     p.tmax = opts.tmax;
     p.far_plane = opts.far_plane;
     p.alpha_floor = opts.alpha_floor;
-    p.bg0 = background[0];
-    p.bg1 = background[1];
-    p.bg2 = background[2];
+    p.composite = background != nullptr;
+    p.bg0 = background ? background[0] : 0.0;
+    p.bg1 = background ? background[1] : 0.0;
+    p.bg2 = background ? background[2] : 0.0;
     p.image = image;
     p.alpha = alpha;
     p.depth = depth;
@@ -680,6 +683,57 @@ int vv_collect_segments(const vv_tree *t, const double *origins, const double *d
                         void *stream) {
     if (!ray_start || !seg_leaf || !seg_t0 || !seg_t1) return set_error(VV_E_INVALID, "null output");
     return segments_impl(t, origins, dirs, n, tmin, tmax, nullptr, ray_start, seg_leaf, seg_t0, seg_t1, stream);
+}
+
+int vv_shadow_blur(const float *alpha, int32_t res, const double *weights, int32_t radius, double *tmp, double *out,
+                   void *stream) {
+    if (!alpha || !out || res < 0 || radius < 0) return set_error(VV_E_INVALID, "bad argument");
+    if (radius > 0 && (!weights || !tmp)) return set_error(VV_E_INVALID, "null weights / scratch");
+    double *dw = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (radius > 0) {  // the 2r+1 host weights ride along stream-ordered
+        VV_CUDA(cudaMallocAsync(&dw, (size_t)(2 * radius + 1) * sizeof(double), st));
+        VV_CUDA(cudaMemcpyAsync(dw, weights, (size_t)(2 * radius + 1) * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    const int rc = launch_shadow_blur(alpha, res, dw, radius, tmp, out, st);
+    if (dw) cudaFreeAsync(dw, st);
+    return rc;
+}
+
+int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
+                      const double *background, const vv_light *lights, int32_t n_lights, float *image,
+                      void *stream) {
+    if (!cam || !rgb || !alpha || !depth || !background || !image || (n_lights > 0 && !lights))
+        return set_error(VV_E_INVALID, "null argument");
+    if (n_lights < 0 || n_lights > kMaxLights)
+        return set_error(VV_E_UNSUPPORTED, "%d lights (at most %d per pass)", n_lights, kMaxLights);
+    LightView L[kMaxLights];
+    for (int i = 0; i < n_lights; ++i) {
+        const vv_light &s = lights[i];
+        if (s.cast_shadows && (!s.shadow_map || s.shadow_res < 1))
+            return set_error(VV_E_INVALID, "light %d casts shadows without a shadow map", i);
+        L[i].px = s.position[0];
+        L[i].py = s.position[1];
+        L[i].pz = s.position[2];
+        L[i].ga = s.ground_plane[0];
+        L[i].gb = s.ground_plane[1];
+        L[i].gc = s.ground_plane[2];
+        L[i].gd = s.ground_plane[3];
+        L[i].strength = s.shadow_strength;
+        L[i].r0sq = s.falloff_r0 * s.falloff_r0;
+        L[i].min_scale = s.falloff_min_scale;
+        L[i].cast_shadows = s.cast_shadows;
+        L[i].falloff_enabled = s.falloff_enabled;
+        L[i].map = s.shadow_map;
+        L[i].res = s.shadow_res;
+        memcpy(L[i].w2c, s.w2c, sizeof(L[i].w2c));
+        L[i].fx = s.fx;
+        L[i].fy = s.fy;
+        L[i].cx = s.cx;
+        L[i].cy = s.cy;
+    }
+    return launch_scene_light(make_cam(*cam), rgb, alpha, depth, background[0], background[1], background[2], L,
+                              n_lights, image, (cudaStream_t)stream);
 }
 
 int vv_termination_leaves(const vv_tree *t, int32_t frame, const double *origins, const double *dirs,

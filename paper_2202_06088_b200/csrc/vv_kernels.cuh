@@ -210,6 +210,7 @@ struct SceneParams {
     int n_inst;
     double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
     double bg0, bg1, bg2;
+    int composite;  // 1: image = composite over bg; 0: image = blended (unpremultiplied) rgb
     float *image, *alpha, *depth;
 };
 
@@ -296,12 +297,18 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
             I0 = I1 = I2 = 0.0;
         }
     }
-    // composite_background: a * rgb + (1 - a) * bg (render.py:243-251)
-    const double om = xsub(1.0, A);
     const int64_t pix = (int64_t)iy * p.cam.width + ix;
-    p.image[3 * pix + 0] = (float)xadd(xmul(A, I0), xmul(om, p.bg0));
-    p.image[3 * pix + 1] = (float)xadd(xmul(A, I1), xmul(om, p.bg1));
-    p.image[3 * pix + 2] = (float)xadd(xmul(A, I2), xmul(om, p.bg2));
+    if (p.image && p.composite) {
+        // composite_background: a * rgb + (1 - a) * bg (render.py:243-251)
+        const double om = xsub(1.0, A);
+        p.image[3 * pix + 0] = (float)xadd(xmul(A, I0), xmul(om, p.bg0));
+        p.image[3 * pix + 1] = (float)xadd(xmul(A, I1), xmul(om, p.bg1));
+        p.image[3 * pix + 2] = (float)xadd(xmul(A, I2), xmul(om, p.bg2));
+    } else if (p.image) {  // the blended layer, for the lighting passes
+        p.image[3 * pix + 0] = (float)I0;
+        p.image[3 * pix + 1] = (float)I1;
+        p.image[3 * pix + 2] = (float)I2;
+    }
     if (p.alpha) p.alpha[pix] = (float)A;
     if (p.depth) p.depth[pix] = (float)D;
 }
@@ -551,6 +558,21 @@ int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t sm
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);
+int launch_shadow_blur(const float *alpha, int res, const double *weights, int radius, double *tmp, double *out,
+                       cudaStream_t st);
+constexpr int kMaxLights = 16;
+struct LightView {  // vv_light (include/voxvid_b200.h)
+    double px, py, pz;
+    double ga, gb, gc, gd;
+    double strength, r0sq, min_scale;
+    int cast_shadows, falloff_enabled;
+    const double *map;
+    int res;
+    double w2c[12];
+    double fx, fy, cx, cy;
+};
+int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha, const float *depth, double bg0,
+                       double bg1, double bg2, const LightView *lights, int n_lights, float *image, cudaStream_t st);
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
                   float *rest, cudaStream_t st);
 int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,

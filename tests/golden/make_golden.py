@@ -41,7 +41,16 @@ sys.path.insert(0, str(REPO))
 from voxvid import hh as rhh  # noqa: E402
 from voxvid import kernels as rk  # noqa: E402
 from voxvid import temporal as rt  # noqa: E402
-from voxvid.compose import Scene, SceneInstance, TimeMap, paint, render_scene  # noqa: E402
+from voxvid.compose import (  # noqa: E402
+    Light,
+    Scene,
+    SceneInstance,
+    TimeMap,
+    falloff_pass,
+    paint,
+    render_scene,
+    shadow_pass,
+)
 from voxvid.octree import VOctree  # noqa: E402
 from voxvid.render import Camera, RenderOptions, build_frame_cache, render, render_rays  # noqa: E402
 from voxvid.train import TrainConfig, Trainer  # noqa: E402
@@ -348,6 +357,41 @@ def main():
              p2_skipped=np.array(res["skipped_pixels"], np.int64).reshape(-1, 2),
              p2_edit_rgb=tree.edit_rgb.copy(), p2_edit_t=tree.edit_t.copy())
     cases["paint"] = c
+
+    # K. lighting passes (compose.py:539-619): shadow maps, falloff, lit render_scene
+    rng = np.random.default_rng(81)
+    tree_a = random_payload_tree(rng, depth=3, fill=0.5, frames=6, sigma_scale=8.0)
+    tree_b = random_payload_tree(rng, depth=2, fill=0.7, frames=6, sigma_scale=6.0)
+
+    def tr(x, y, z):
+        m = np.eye(4)
+        m[:3, 3] = [x, y, z]
+        return m
+
+    insts = [SceneInstance(name="a", tree=tree_a, affine=tr(0.0, 0.0, 0.6)),
+             SceneInstance(name="b", tree=tree_b, affine=tr(1.3, 0.2, 0.4), timemap=TimeMap.parse("shift(1)"))]
+    lights = [Light(position=(0.9, 0.4, 3.5), blur_sigma=1.5, shadow_resolution=96, falloff_enabled=True,
+                    falloff_r0=2.5, falloff_min_scale=0.2),
+              Light(position=(-0.5, 1.5, 2.0), cast_shadows=False, falloff_enabled=True, falloff_r0=1.5),
+              Light(position=(2.0, -1.0, 2.5), blur_sigma=0.0, shadow_resolution=64, shadow_strength=0.5)]
+    scene = Scene(instances=insts, lights=lights, background=np.array([0.6, 0.65, 0.7]))
+    cam = Camera.look_at([0.8, -3.0, 2.2], [0.8, 0.5, 0.3], width=28, height=22)
+    c = dict(tree_arrays(tree_a, "ta_"), **tree_arrays(tree_b, "tb_"), cam_c2w=cam.c2w,
+             cam_wh=np.array([cam.width, cam.height]), cam_f=np.array([cam.fx, cam.fy, cam.cx, cam.cy]))
+    for g in (0, 2):
+        img, blended, _ = render_scene(scene, cam, g, want_layers=True)
+        c[f"g{g}_image"] = img
+        c[f"g{g}_blended_rgb"] = blended.rgb
+        c[f"g{g}_blended_alpha"] = blended.alpha
+        c[f"g{g}_blended_depth"] = blended.depth
+        sm = shadow_pass(insts, lights[0], g)
+        c[f"g{g}_shadow0"] = sm.alpha
+        c[f"g{g}_shadow0_c2w"] = sm.cam.c2w
+        c[f"g{g}_bgfac0"] = sm.background_factor(cam)
+        sm2 = shadow_pass(insts, lights[2], g)
+        c[f"g{g}_shadow2"] = sm2.alpha
+        c[f"g{g}_falloff1"] = falloff_pass(blended, cam, lights[1])
+    cases["lights"] = c
 
     want = set(sys.argv[1:])
     for name, arrays in cases.items():
