@@ -520,8 +520,13 @@ inline size_t stack_bytes(int depth, bool wide, bool pops = false) {
 
 template <class Kern>
 inline int prep_smem(Kern k, size_t smem) {
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // opt in beyond 48 KB per block: the limit covers static + dynamic
+    // shared memory (the scene kernel stages 8 KB of basis rows statically)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return set_error(VV_E_CUDA, "function attributes: %s", cudaGetErrorString(e));
+    if (smem + fa.sharedSizeBytes > 48 * 1024 && (int)smem > fa.maxDynamicSharedSizeBytes) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_error(VV_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     }
     return VV_OK;

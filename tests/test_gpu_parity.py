@@ -358,3 +358,25 @@ def test_load_device_matches_host_path(cuda, key):
         bad = bytearray(data)
         bad[300] ^= 4
         vv.DeviceTree.from_voct(bytes(bad))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("depth", [9, 11])
+def test_deep_scene_launch(cuda, depth):
+    """Deep trees in the fused scene kernel: traversal shared memory + the
+    8 KB of staged basis rows exceed 48 KB per block (opt-in path)."""
+    rng = np.random.default_rng(depth)
+    res = 1 << depth
+    coords = np.unique(rng.integers(res // 4, 3 * res // 4, (3000, 3)), axis=0)
+    k = 14
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 7 + 3 * k)).astype(np.float32)
+    data[:, 0] = rng.uniform(50.0, 400.0, len(coords))
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(4, 7), 2, depth=depth)
+    m = np.eye(4)
+    m[:3, 3] = [0.4, 0.1, 0.0]
+    scene = vv.Scene(instances=[vv.SceneInstance(name="a", tree=tree),
+                                vv.SceneInstance(name="b", tree=tree, affine=m)])
+    cam = vv.Camera.look_at([0.6, -2.5, 1.2], [0.6, 0.5, 0.5], width=40, height=32)
+    fused = vv.render_scene(scene, cam, 1)
+    host, _, _ = vv.render_scene(scene, cam, 1, want_layers=True)
+    assert np.abs(fused - host).max() < 1e-4
