@@ -170,15 +170,63 @@ void pool_setup(int device) {
 
 // Leaf-decode mode for a call without a user cache: 0 = per sample (inside
 // the render kernel), 1 = per-frame slice pre-pass.  VV_SLICE_AUTO takes the
-// pre-pass when the call's rays are numerous enough that every leaf is
-// likely decoded several times per frame anyway.  (Decoding lazily on
-// first visit inside the render kernel was measured slower: the claim
-// atomics, release fences and sub-warp decode bursts cost more than the
-// skipped decodes.)
-int decode_mode(const vv_tree *t, int64_t n_rays, int policy) {
+// pre-pass when the rays that can reach the tree are numerous enough that
+// every leaf is likely decoded several times per frame anyway: n_leaves <=
+// 3 x rays (measured: a full-screen 1080p tree at leaves/rays 1.7 renders
+// 2.4x faster sliced; the cfg4 performers, each seen by ~280 k of the 2 M
+// rays, 2x faster per sample).  (Decoding lazily on first visit inside the
+// render kernel was measured slower: the claim atomics, release fences and
+// sub-warp decode bursts cost more than the skipped decodes.)
+int decode_mode(const vv_tree *t, double n_rays, int policy) {
     if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return 0;
     if (policy == VV_SLICE_PER_FRAME) return 1;
-    return t->n_leaves <= 2 * n_rays ? 1 : 0;
+    return (double)t->n_leaves <= 3.0 * n_rays ? 1 : 0;
+}
+
+// Rays of `cam` that can reach a tree: the screen rectangle bounding its
+// cube (corners lo + side {0,1}^3, mapped by the 3x4 affine A when given)
+// projected through the camera; every pixel when a corner is not in front
+// of the eye.
+double cube_footprint(const vv_camera &cam, const double lo[3], double side, const double *A) {
+    const double npix = (double)cam.width * cam.height;
+    const double *m = cam.c2w;  // row-major 4x4: columns 0..2 = camera axes
+    double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+    for (int c = 0; c < 8; ++c) {
+        double p[3] = {lo[0] + ((c & 1) ? side : 0.0), lo[1] + ((c & 2) ? side : 0.0), lo[2] + ((c & 4) ? side : 0.0)};
+        if (A) {
+            double q[3];
+            for (int r = 0; r < 3; ++r) q[r] = A[4 * r] * p[0] + A[4 * r + 1] * p[1] + A[4 * r + 2] * p[2] + A[4 * r + 3];
+            p[0] = q[0];
+            p[1] = q[1];
+            p[2] = q[2];
+        }
+        const double d[3] = {p[0] - m[3], p[1] - m[7], p[2] - m[11]};
+        double cc[3];
+        for (int k = 0; k < 3; ++k) cc[k] = m[k] * d[0] + m[4 + k] * d[1] + m[8 + k] * d[2];  // R^T d
+        if (!(cc[2] > 1e-9)) return npix;
+        const double px = cam.fx * cc[0] / cc[2] + cam.cx, py = cam.fy * cc[1] / cc[2] + cam.cy;
+        x0 = std::min(x0, px);
+        x1 = std::max(x1, px);
+        y0 = std::min(y0, py);
+        y1 = std::max(y1, py);
+    }
+    const double w = std::max(0.0, std::min(x1, (double)cam.width) - std::max(x0, 0.0));
+    const double h = std::max(0.0, std::min(y1, (double)cam.height) - std::max(y0, 0.0));
+    return std::min(npix, w * h);
+}
+
+// Affine A (3x4) from its inverse's 3x4 rows (scene instances in mode 1).
+void affine_from_inverse(const double *inv, double *A) {
+    const double a = inv[0], b = inv[1], c = inv[2], d = inv[4], e = inv[5], f = inv[6], g = inv[8], h = inv[9],
+                 i = inv[10];
+    const double det = a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+    const double M[9] = {(e * i - f * h) / det, (c * h - b * i) / det, (b * f - c * e) / det,
+                         (f * g - d * i) / det, (a * i - c * g) / det, (c * d - a * f) / det,
+                         (d * h - e * g) / det, (b * g - a * h) / det, (a * e - b * d) / det};
+    for (int r = 0; r < 3; ++r) {
+        for (int k = 0; k < 3; ++k) A[4 * r + k] = M[3 * r + k];
+        A[4 * r + 3] = -(M[3 * r] * inv[3] + M[3 * r + 1] * inv[7] + M[3 * r + 2] * inv[11]);
+    }
 }
 
 // Transient per-call slice from the stream-ordered pool (freed, stream
@@ -472,7 +520,7 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
     const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;
-    const int mode = cache ? 1 : decode_mode(t, n, opts.frame_slice);
+    const int mode = cache ? 1 : decode_mode(t, (double)n, opts.frame_slice);
     if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
@@ -524,6 +572,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.alpha = alpha;
     p.depth = depth;
     unsigned grid_blocks = 0;
+    double share = 1.0;  // fraction of the frame's pixels this call renders
     if (packed) {
         p.packed = packed;
         p.tile = tile;
@@ -536,6 +585,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         if (mine == 0) return VV_OK;
         if (tile % kTW || tile % kTH) return set_error(VV_E_INVALID, "tile must be a multiple of %d", kTW);
         grid_blocks = (unsigned)mine * (unsigned)((tile / kTW) * (tile / kTH));
+        share = (double)mine / (double)total;
     } else {
         p.blocks_x = (cam->width + kTW - 1) / kTW;
         grid_blocks = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
@@ -544,7 +594,9 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     const size_t smem = stack_bytes(t->depth, wide);
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;
-    const int mode = cache ? 1 : decode_mode(t, (int64_t)cam->width * cam->height, opts.frame_slice);
+    const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
+    const int mode =
+        cache ? 1 : decode_mode(t, share * cube_footprint(*cam, lo, t->view.side, nullptr), opts.frame_slice);
     if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
@@ -635,7 +687,24 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
         int same = -1;
         for (int j = 0; j < i; ++j)
             if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.rec) same = j;
-        const int mode = decode_mode(inst[i].tree, (int64_t)cam->width * cam->height, opts.frame_slice);
+        // rays that can reach this tree at this frame, over every instance sharing it
+        double reach = 0.0;
+        for (int j = 0; j < n_inst; ++j) {
+            if (inst[j].tree != inst[i].tree || inst[j].frame != inst[i].frame) continue;
+            const vv_tree *tj = inst[j].tree;
+            const double lo[3] = {tj->view.lo0, tj->view.lo1, tj->view.lo2};
+            if (inst[j].mode == 0) {  // rigid: the pulled-back camera in the tree's frame
+                vv_camera c2 = *cam;
+                memcpy(c2.c2w, inst[j].pose, sizeof(c2.c2w));
+                reach += cube_footprint(c2, lo, tj->view.side, nullptr);
+            } else {
+                double A[12];
+                affine_from_inverse(inst[j].inv, A);
+                reach += cube_footprint(*cam, lo, tj->view.side, A);
+            }
+        }
+        reach = std::min(reach, (double)cam->width * cam->height);
+        const int mode = decode_mode(inst[i].tree, reach, opts.frame_slice);
         if (same >= 0) {
             p.inst[i].S = p.inst[same].S;
         } else if (mode != 0) {
