@@ -9,10 +9,13 @@ finalize kernel).  One step = one full 1080p frame; steps sweep frames
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: every rank holds a full tree replica and
-renders its interleaved 64x64 tiles of the same frame, then one NCCL
-all-gather per frame assembles the image (strong scaling: fixed work per
-step).  The reference arm (--impl reference) times the reference's own CPU
+N > 1 runs under torchrun as batched playback (the north star's "by frame
+for batched playback"): every rank holds a full tree replica and renders
+frames f = rank, rank + N, ... of the sweep -- one full frame per rank per
+step, no data-path collective (weak scaling; the timed region is the max
+over ranks).  The single-frame tile path (64x64 tiles interleaved over the
+ranks, one NCCL all-gather, unpack) is timed as well and reported under
+"tile_frame".  The reference arm (--impl reference) times the reference's own CPU
 renderer (voxvid from baseline/_ref, numba, all host threads) or, if that
 is not installed, the C oracle port (OpenMP, all host threads).
 """
@@ -268,15 +271,16 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     log(f"[bench] rank {rank}: upload {time.time() - t0:.2f}s, {rep.device_bytes / 1e9:.3f} GB on device")
 
+    # batched playback: frame f is rendered by rank f mod world (full replica
+    # per GPU, frames independent -> no data-path collective, weak scaling)
     frames_total = FRAMES if args.config != 3 else 60
-    step_frames = [(args.warmup + i) % frames_total for i in range(args.steps)]
-    warm_frames = [i % frames_total for i in range(args.warmup)]
+    step_frames = [(args.warmup * world + i * world + rank) % frames_total for i in range(args.steps)]
+    warm_frames = [(i * world + rank) % frames_total for i in range(args.warmup)]
 
     rgb = torch.empty((HEIGHT, WIDTH, 3), dtype=torch.float32, device=dev)
     alpha = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
     depth = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-    tiles = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev) if world > 1 else None
 
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     cur = {"mid": None}
@@ -285,17 +289,11 @@ def run_ours(args, rank, world, local_rank):
         # identical work to render(tree, cam, f): per-frame slice pass, then the
         # fused ray-gen/traversal/shading/finalize kernel -- split here so the
         # dominant kernel's own duration is measured (roofline)
-        if tiles is None:
-            fs = vv.build_frame_cache(tree, f)
-            if cur["mid"] is not None:
-                cur["mid"].record(stream)
-            vv.render_into(tree, cam, f, rgb, alpha, depth, cache=fs)
-            del fs
-        else:
-            tiles.render_slab(tree, cam, f)
-            tiles.gather()
-            if rank == 0:
-                tiles.unpack(rgb, alpha, depth)
+        fs = vv.build_frame_cache(tree, f)
+        if cur["mid"] is not None:
+            cur["mid"].record(stream)
+        vv.render_into(tree, cam, f, rgb, alpha, depth, cache=fs)
+        del fs
 
     for f in warm_frames:
         step(f)
@@ -326,64 +324,80 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop() if clocks else None
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
-    render_ms = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) if tiles is None else None
-    slice_ms = sum(s.elapsed_time(m) for s, m in zip(starts, mids)) if tiles is None else None
+    render_ms = sum(m.elapsed_time(e) for m, e in zip(mids, ends))
+    slice_ms = sum(s.elapsed_time(m) for s, m in zip(starts, mids))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
 
-    # end-to-end through the public API: render() -> host numpy images
-    e2e = None
-    if world == 1:
-        for f in warm_frames[:3]:  # two results alive at once in the loop below: warm both pinned buffers
-            layer = vv.render(tree, cam, f)
-        torch.cuda.synchronize()
-        # single-call latency: render() -> numpy, one frame at a time
-        te = time.perf_counter()
-        for f in step_frames[:10]:
-            layer = vv.render(tree, cam, f)
-        single_ms = (time.perf_counter() - te) / len(step_frames[:10]) * 1e3
-        assert layer.rgb.shape == (HEIGHT, WIDTH, 3)
-        del layer
-        # steady-state playback: pinned result pool and render streams warm
-        # (a 41 MB cudaHostAlloc costs 25-100 ms; none may land in the timed run)
-        for _ in range(2):
-            collections.deque(vv.render_sequence(tree, cam, warm_frames), maxlen=0)  # holds no frame
-        torch.cuda.synchronize()
-        # playback through the public API: every frame complete on the host
-        te = time.perf_counter()
-        got = 0
-        for layer in vv.render_sequence(tree, cam, step_frames):
-            got += 1
-        e2e_s = time.perf_counter() - te
-        assert got == len(step_frames) and layer.rgb.shape == (HEIGHT, WIDTH, 3)
-        e2e = {"value": round(n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
-               "h2d_bytes_per_step": 168 + 48, "d2h_bytes_per_step": 5 * 4 * n_rays,
-               "api": "paper_2202_06088_b200.render_sequence(tree, cam, frames) -> numpy LayerImages (fp32) "
-                      "per frame, render of frame i overlapped with the D2H of frame i-1",
-               "single_render_call_ms": round(single_ms, 3)}
-    else:
-        # tiles -> all-gather -> rank 0 unpack -> D2H on rank 0
-        host = torch.empty(5 * n_rays, dtype=torch.float32, pin_memory=True) if rank == 0 else None
+    # end-to-end through the public API: every frame complete on the host
+    for f in warm_frames[:3]:  # two results alive at once in the loop below: warm both pinned buffers
+        layer = vv.render(tree, cam, f)
+    torch.cuda.synchronize()
+    # single-call latency: render() -> numpy, one frame at a time
+    te = time.perf_counter()
+    for f in step_frames[:10]:
+        layer = vv.render(tree, cam, f)
+    single_ms = (time.perf_counter() - te) / len(step_frames[:10]) * 1e3
+    assert layer.rgb.shape == (HEIGHT, WIDTH, 3)
+    del layer
+    # steady-state playback: pinned result pool and render streams warm
+    # (a 41 MB cudaHostAlloc costs 25-100 ms; none may land in the timed run)
+    for _ in range(2):
+        collections.deque(vv.render_sequence(tree, cam, warm_frames), maxlen=0)  # holds no frame
+    torch.cuda.synchronize()
+    if world > 1:
         dist.barrier()
-        te = time.perf_counter()
-        for f in step_frames:
-            step(f)
-            if rank == 0:
-                host[: 3 * n_rays].copy_(rgb.view(-1), non_blocking=True)
-                host[3 * n_rays: 4 * n_rays].copy_(alpha.view(-1), non_blocking=True)
-                host[4 * n_rays:].copy_(depth.view(-1), non_blocking=True)
-                torch.cuda.current_stream(dev).synchronize()
-        torch.cuda.synchronize()
-        dist.barrier()
-        e2e_s = time.perf_counter() - te
+    te = time.perf_counter()
+    got = 0
+    for layer in vv.render_sequence(tree, cam, step_frames):  # this rank's frames, to this rank's host
+        got += 1
+    e2e_s = time.perf_counter() - te
+    assert got == len(step_frames) and layer.rgb.shape == (HEIGHT, WIDTH, 3)
+    del layer
+    if world > 1:
         et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_s = float(et.item())
-        e2e = {"value": round(n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
-               "h2d_bytes_per_step": 168 + 48, "d2h_bytes_per_step": 5 * 4 * n_rays,
-               "api": "TileRenderer.render_slab + NCCL all_gather + unpack -> pinned host (rank 0)"}
+    e2e = {"value": round(world * n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
+           "h2d_bytes_per_step": (168 + 48) * world, "d2h_bytes_per_step": 5 * 4 * n_rays * world,
+           "api": "paper_2202_06088_b200.render_sequence(tree, cam, frames) -> numpy LayerImages (fp32) "
+                  "per frame on every rank, render of frame i overlapped with the D2H of frame i-1",
+           "single_render_call_ms": round(single_ms, 3)}
+
+    # single-frame latency across the ranks: 64x64 tiles interleaved over the
+    # GPUs, one NCCL all-gather of the packed slabs, unpack on rank 0
+    tile_frame = None
+    if world > 1:
+        tiles = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev)
+
+        def tile_step(f):
+            tiles.render_slab(tree, cam, f)
+            tiles.gather()
+            if rank == 0:
+                tiles.unpack(rgb, alpha, depth)
+
+        for f in warm_frames:
+            tile_step(f)
+        torch.cuda.synchronize()
+        nt = min(10, len(step_frames))
+        ts, tend = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        ts.record(stream)
+        for f in step_frames[:nt]:
+            flush.zero_()
+            tile_step(f)
+        tend.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([ts.elapsed_time(tend) / nt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tile_frame = {"ms_per_frame": round(float(tt.item()), 4),
+                      "mrays": round(n_rays / float(tt.item()) / 1e3, 3),
+                      "parallelism": f"64x64 tiles interleaved over {world} GPUs + NCCL all_gather + unpack",
+                      "note": "one frame split across all GPUs (strong scaling; includes a 252 MiB L2 flush "
+                              "memset per frame)"}
 
     if rank != 0:
         return
@@ -392,16 +406,13 @@ def run_ours(args, rank, world, local_rank):
     ab = algorithmic_bytes(tree, cam, sorted(set(step_frames)), dev)
     bytes_per_step = [ab[f]["bytes"] for f in step_frames]
     peak, peak_kind = measured_peak()
-    if render_ms is not None:
-        rbytes = sum(ab[f]["render_bytes"] for f in step_frames)
-        sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
-        achieved = rbytes / (render_ms / 1e3) / 1e9
-        slice_gbs = sbytes / (slice_ms / 1e3) / 1e9
-        frame_gbs = (rbytes + sbytes) / (total_ms / 1e3) / 1e9
-        uncached_gbs = sum(bytes_per_step) / (total_ms / 1e3) / 1e9
-    else:
-        achieved = sum(ab[f]["render_bytes"] + ab[f]["slice_bytes"] for f in step_frames) / (total_ms / 1e3) / 1e9
-        slice_gbs = frame_gbs = uncached_gbs = None
+    # per GPU (rank 0's kernels; every rank does the same per-frame work)
+    rbytes = sum(ab[f]["render_bytes"] for f in step_frames)
+    sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
+    achieved = rbytes / (render_ms / 1e3) / 1e9
+    slice_gbs = sbytes / (slice_ms / 1e3) / 1e9
+    frame_gbs = (rbytes + sbytes) / (total_ms / 1e3) / 1e9
+    uncached_gbs = sum(bytes_per_step) / (total_ms / 1e3) / 1e9
     mean_ab = {k: float(np.mean([ab[f][k] for f in step_frames]) / n_rays) for k in ("P", "V", "S")}
 
     # CPU baseline: oracle port on a bounded sample (rank 0, N = 1 only)
@@ -414,29 +425,30 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"{len(sample_frames)} full 1080p frame(s) {sample_frames}, host ray gen + render + finalize"}
 
     ms = total_ms / len(step_frames)
-    value = n_rays * len(step_frames) / (total_ms / 1e3) / 1e6
+    value = world * n_rays * len(step_frames) / (total_ms / 1e3) / 1e6  # whole job
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "fps": round(1e3 / ms, 2),
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "fps": round(world * 1e3 / ms, 2),
         "config": {
             "workload": "cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached "
                         "render (ray gen + traversal + HH shading + compositing + finalize), frame sweep",
-            "rays_per_step": n_rays, "frames": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
+            "rays_per_step": n_rays * world, "frames_rank0": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
             "l2": "inputs larger than L2 (1.54 GB tree) and L2 flushed between steps (252 MiB memset outside "
                   "the per-step CUDA events)",
-            "parallelism": f"tile{world}" if world > 1 else "single",
+            "parallelism": f"frames x {world} GPUs (frame f on rank f mod {world}, full replica each)"
+                           if world > 1 else "single",
             "per_ray": mean_ab, "wall_ms_timed_region": round(wall * 1e3, 3),
             "dtype_note": "f64 traversal/sigma/compositing, fp32 HH colour",
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
                      "peak_kind": peak_kind, "kernel": "k_render_camera",
-                     "kernel_ms": round(render_ms / len(step_frames), 4) if render_ms is not None else None,
+                     "kernel_ms": round(render_ms / len(step_frames), 4),
                      "bytes_per_launch": float(np.mean([ab[f]["render_bytes"] for f in step_frames])),
                      "bytes_formula": "sum_rays 32 P + 8 V + 12 S_sh S + 20 (sliced path; P/V/S reference counts)",
                      "slice_pass": {"kernel": "k_build_slice",
-                                    "ms": round(slice_ms / len(step_frames), 4) if slice_ms is not None else None,
+                                    "ms": round(slice_ms / len(step_frames), 4),
                                     "achieved": round(slice_gbs, 1) if slice_gbs else None,
                                     "frac": round(slice_gbs / peak, 4) if slice_gbs else None,
                                     "bytes_per_launch": float(ab[step_frames[0]]["slice_bytes"])},
@@ -445,7 +457,8 @@ def run_ours(args, rank, world, local_rank):
                      "uncached_bytes_per_frame": float(np.mean(bytes_per_step))},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": len(step_frames) * 2,
+        "gpu_launches": len(step_frames) * 2 * world,
+        "tile_frame": tile_frame,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -474,8 +487,16 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("VV_BENCH_FUNCTIONAL_GLOO"):
+            # functional check of the N > 1 code on a box with fewer GPUs:
+            # ranks share devices, gloo carries the host-side collectives; the
+            # printed numbers are NOT measurements (GPUs are shared)
+            local_rank = local_rank % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -113,8 +113,10 @@ class TileRenderer:
 
         if self.world == 1:
             self.all[0].copy_(self.slab)
-        else:
+        elif dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(self.all.view(-1), self.slab.view(-1), group=self.group)
+        else:  # gloo (functional runs): list form
+            dist.all_gather(list(self.all.unbind(0)), self.slab, group=self.group)
         return self.all
 
     def unpack(self, rgb, alpha, depth):
