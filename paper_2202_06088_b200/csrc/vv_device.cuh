@@ -235,6 +235,10 @@ __device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) 
     aa = ta;
 }
 
+#ifndef VV_BRANCHFREE_PUSH
+#define VV_BRANCHFREE_PUSH 1
+#endif
+
 // Resumable traversal state of one ray.  The stack lives in shared memory
 // at a 32-bit shared-window address (one slot per level of pending
 // siblings, `stride` bytes between a thread's consecutive slots).
@@ -392,10 +396,20 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         const typename Entry::Code pc2 = t.pc << 1;
 #pragma unroll
         for (int s = 3; s >= 1; --s) {
+#if VV_BRANCHFREE_PUSH
+            // branch-free: the entry always goes to the top slot and the top
+            // moves only for a real push (a slot above the top is scratch;
+            // at a level-L node the stack holds <= 3L entries, so the slot
+            // is <= 3(depth-2)+2 < stack_cap)
+            const bool push = ((keep >> s) & 1) && (keep & ((1 << s) - 1));
+            Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
+            t.sp += push ? stride : 0u;
+#else
             if (((keep >> s) & 1) && (keep & ((1 << s) - 1))) {
                 Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
                 t.sp += stride;
             }
+#endif
         }
         uint32_t nptr = 0;
         int nb = 0;
