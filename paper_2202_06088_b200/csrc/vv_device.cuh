@@ -238,6 +238,9 @@ __device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) 
 #ifndef VV_BRANCHFREE_PUSH
 #define VV_BRANCHFREE_PUSH 1
 #endif
+#ifndef VV_BRANCHFREE_QUEUE
+#define VV_BRANCHFREE_QUEUE 1
+#endif
 
 // Resumable traversal state of one ray.  The stack lives in shared memory
 // at a 32-bit shared-window address (one slot per level of pending
@@ -381,8 +384,16 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         if (t.L + 1 == depth) {
             t.need_pop = true;
 #pragma unroll
-            for (int s = 0; s < 4; ++s)
+            for (int s = 0; s < 4; ++s) {
+#if VV_BRANCHFREE_QUEUE
+                // branch-free: write slot n, keep it only for a kept leaf
+                // (n < kSegMin before this node, so n + 3 < kSegSlots)
+                seg.put<Visitor::kPops>(n, cp[s], st[s], st[s + 1], vis.pop_count());
+                n += (keep >> s) & 1;
+#else
                 if ((keep >> s) & 1) seg.put<Visitor::kPops>(n++, cp[s], st[s], st[s + 1], vis.pop_count());
+#endif
+            }
             if (n >= kSegMin) return n;
             continue;
         }
