@@ -241,6 +241,9 @@ __device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) 
 #ifndef VV_BRANCHFREE_QUEUE
 #define VV_BRANCHFREE_QUEUE 1
 #endif
+#ifndef VV_RANK_SORT
+#define VV_RANK_SORT 1
+#endif
 
 // Resumable traversal state of one ray.  The stack lives in shared memory
 // at a 32-bit shared-window address (one slot per level of pending
@@ -361,11 +364,28 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         const bool bx = txm < tin, by = tym < tin, bz = tzm < tin;
         const int b0 = (bx ? 1 : 0) | (by ? 2 : 0) | (bz ? 4 : 0);
         double k0 = bx ? 1e301 : txm, k1 = by ? 1e301 : tym, k2 = bz ? 1e301 : tzm;
+#if VV_RANK_SORT
+        // stable rank sort: the three comparisons are independent (the
+        // network below chains them); rank_i = #{j: k_j < k_i} + #{j < i:
+        // k_j == k_i} -- the same order, ties to the earlier axis
+        const bool l10 = k1 < k0, l20 = k2 < k0, l21 = k2 < k1;
+        const int r0 = (int)l10 + (int)l20, r1 = (int)!l10 + (int)l21;
+        const double s0 = r0 == 0 ? k0 : (r1 == 0 ? k1 : k2);
+        const double s1 = r0 == 1 ? k0 : (r1 == 1 ? k1 : k2);
+        const double s2 = r0 == 2 ? k0 : (r1 == 2 ? k1 : k2);
+        const int a0 = r0 == 0 ? 1 : (r1 == 0 ? 2 : 4);
+        const int a1 = r0 == 1 ? 1 : (r1 == 1 ? 2 : 4);
+        k0 = s0;
+        k1 = s1;
+        k2 = s2;
+        const int c0 = b0, c1 = c0 | a0, c2 = c1 | a1, c3 = 7;  // every axis crossed
+#else
         int a0 = 1, a1 = 2, a2 = 4;
         cswap(k0, a0, k1, a1);
         cswap(k1, a1, k2, a2);
         cswap(k0, a0, k1, a1);
         const int c0 = b0, c1 = c0 | a0, c2 = c1 | a1, c3 = c2 | a2;
+#endif
         st[0] = tin;
         st[1] = pmin(k0, tout);
         st[2] = pmin(k1, tout);
