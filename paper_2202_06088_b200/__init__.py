@@ -10,12 +10,15 @@ from .compose import (
     Light,
     Scene,
     SceneInstance,
+    ShadowMap,
     TimeMap,
     blend_layers,
     duplicate,
+    falloff_pass,
     paint,
     render_instance,
     render_scene,
+    shadow_pass,
     termination_leaves,
 )
 from .device import DeviceTree, load_device
@@ -51,6 +54,7 @@ __all__ = [
     "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
-    "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "TemporalBases",
+    "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "ShadowMap", "shadow_pass",
+    "falloff_pass", "TemporalBases",
     "make_bump_bases",
 ]
