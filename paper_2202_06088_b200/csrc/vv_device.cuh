@@ -210,40 +210,20 @@ __host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 :
 //        seg.leaf_at(s) over [seg.t0_at(s), seg.t1_at(s)]; returns true to
 //        stop the ray (early termination).
 //
-// Structure ("while-while"): a lane walks internal nodes until it holds one
-// last-level node's leaf batch, then all lanes of the warp shade their
-// batches together -- the shading code runs with the warp converged instead
-// of interleaving with other lanes' node expansions.
+// Structure (queued "while-while", see traverse()): a lane walks internal
+// nodes, queueing the kept leaves of the last-level nodes it passes, until
+// it holds >= kSegMin segments; then the warp shades in lock step.
 //
 // Node step (kernels.py:600-647 restated): the reference walks the pierced
 // children by repeatedly taking the smallest not-yet-crossed mid-plane
 // crossing (ties x, y, z) until it reaches the node's exit.  That is a
-// stable sort of the (up to three) uncrossed crossings: a 3-element
-// compare-exchange network with strict '<' swaps yields the same order and
-// the same boundary values st[k] = min(k-th crossing, t_out); step k exists
+// stable sort of the (up to three) uncrossed crossings, done here as a rank
+// sort with independent comparisons, which yields the same order and the
+// same boundary values st[k] = min(k-th crossing, t_out); step k exists
 // iff st[k] < t_out, which the 'st[k+1] > st[k]' segment test already
 // implies.  Node corners are tracked as exact doubles so crossings need no
 // int->double conversion: p_mid = x_lo + h/2 is the same double as the
 // reference's (2c+1) * 2^-(L+1).
-__device__ __forceinline__ void cswap(double &ka, int &aa, double &kb, int &ab) {
-    const bool sw = kb < ka;
-    const double tk = sw ? kb : ka;
-    kb = sw ? ka : kb;
-    ka = tk;
-    const int ta = sw ? ab : aa;
-    ab = sw ? aa : ab;
-    aa = ta;
-}
-
-#ifndef VV_BRANCHFREE_PUSH
-#define VV_BRANCHFREE_PUSH 1
-#endif
-#ifndef VV_BRANCHFREE_QUEUE
-#define VV_BRANCHFREE_QUEUE 1
-#endif
-#ifndef VV_RANK_SORT
-#define VV_RANK_SORT 1
-#endif
 
 // Resumable traversal state of one ray.  The stack lives in shared memory
 // at a 32-bit shared-window address (one slot per level of pending
@@ -364,7 +344,6 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         const bool bx = txm < tin, by = tym < tin, bz = tzm < tin;
         const int b0 = (bx ? 1 : 0) | (by ? 2 : 0) | (bz ? 4 : 0);
         double k0 = bx ? 1e301 : txm, k1 = by ? 1e301 : tym, k2 = bz ? 1e301 : tzm;
-#if VV_RANK_SORT
         // stable rank sort: the three comparisons are independent (the
         // network below chains them); rank_i = #{j: k_j < k_i} + #{j < i:
         // k_j == k_i} -- the same order, ties to the earlier axis
@@ -379,13 +358,6 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         k1 = s1;
         k2 = s2;
         const int c0 = b0, c1 = c0 | a0, c2 = c1 | a1, c3 = 7;  // every axis crossed
-#else
-        int a0 = 1, a1 = 2, a2 = 4;
-        cswap(k0, a0, k1, a1);
-        cswap(k1, a1, k2, a2);
-        cswap(k0, a0, k1, a1);
-        const int c0 = b0, c1 = c0 | a0, c2 = c1 | a1, c3 = c2 | a2;
-#endif
         st[0] = tin;
         st[1] = pmin(k0, tout);
         st[2] = pmin(k1, tout);
@@ -405,14 +377,10 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
             t.need_pop = true;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-#if VV_BRANCHFREE_QUEUE
                 // branch-free: write slot n, keep it only for a kept leaf
                 // (n < kSegMin before this node, so n + 3 < kSegSlots)
                 seg.put<Visitor::kPops>(n, cp[s], st[s], st[s + 1], vis.pop_count());
                 n += (keep >> s) & 1;
-#else
-                if ((keep >> s) & 1) seg.put<Visitor::kPops>(n++, cp[s], st[s], st[s + 1], vis.pop_count());
-#endif
             }
             if (n >= kSegMin) return n;
             continue;
@@ -427,7 +395,6 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
         const typename Entry::Code pc2 = t.pc << 1;
 #pragma unroll
         for (int s = 3; s >= 1; --s) {
-#if VV_BRANCHFREE_PUSH
             // branch-free: the entry always goes to the top slot and the top
             // moves only for a real push (a slot above the top is scratch;
             // at a level-L node the stack holds <= 3L entries, so the slot
@@ -435,12 +402,6 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
             const bool push = ((keep >> s) & 1) && (keep & ((1 << s) - 1));
             Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
             t.sp += push ? stride : 0u;
-#else
-            if (((keep >> s) & 1) && (keep & ((1 << s) - 1))) {
-                Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
-                t.sp += stride;
-            }
-#endif
         }
         uint32_t nptr = 0;
         int nb = 0;
