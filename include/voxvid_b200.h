@@ -183,6 +183,20 @@ int vv_render_camera_tiles(const vv_tree *tree, int32_t frame, const vv_slice *c
 int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int32_t tile,
                     int32_t n_shards, float *rgb, float *alpha, float *depth, void *stream);
 
+/* The leaf-decode mode VV_SLICE_AUTO picks for a camera render of this tree
+ * (1 = per-frame slice pass, 0 = decode per sample): slice when the leaves
+ * number <= 3 x the rays that can reach the tree (its projected footprint). */
+int vv_camera_decode_mode(const vv_tree *tree, const vv_camera *cam, const vv_render_opts *opts, int32_t *mode);
+/* Playback: n_frames (2..4) frames of ONE camera in one walk -- the rays and
+ * therefore the traversal are frame-independent, so one walk serves every
+ * frame; each frame keeps its own slice (caches[k], required, built for
+ * frames[k]), accumulators and early termination.  Per-frame outputs are
+ * bitwise identical to vv_render_camera(frames[k]).  rgb/alpha/depth:
+ * arrays of n_frames device pointers (entries may be NULL). */
+int vv_render_camera_multi(const vv_tree *tree, int32_t n_frames, const int32_t *frames,
+                           const vv_slice *const *caches, const vv_render_opts *opts, const vv_camera *cam,
+                           float *const *rgb, float *const *alpha, float *const *depth, void *stream);
+
 /* ---- multi-instance scene -------------------------------------------------
  * Replaces render_scene (compose.py:443-475) without lights: per pixel,
  * every instance is rendered through its pulled-back ray (render_instance,

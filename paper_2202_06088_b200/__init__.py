@@ -42,6 +42,7 @@ from .render import (
     count_segments,
     finalize_layer,
     render,
+    render_frames_into,
     render_into,
     render_sequence,
     render_ray_visits,
@@ -51,7 +52,7 @@ from .temporal import TemporalBases, make_bump_bases
 
 __all__ = [
     "VOctree", "DeviceTree", "load_device", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
-    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_sequence",
+    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_frames_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
     "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "ShadowMap", "shadow_pass",

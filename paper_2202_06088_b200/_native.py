@@ -64,6 +64,8 @@ EXPORTED_SYMBOLS = (
     "vv_render_camera_tiles",
     "vv_unpack_tiles",
     "vv_render_scene",
+    "vv_render_camera_multi",
+    "vv_camera_decode_mode",
     "vv_shadow_blur",
     "vv_scene_lighting",
     "vv_count_segments",
@@ -215,6 +217,8 @@ _SIGNATURES = {
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _I32, _I32, _I32, _P, _P],
     ),
     "vv_unpack_tiles": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "vv_camera_decode_mode": (ctypes.c_int, [_P, _P, _P, _P]),
+    "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),
     "vv_render_scene": (

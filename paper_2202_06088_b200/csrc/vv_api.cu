@@ -609,6 +609,53 @@ int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, con
     return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, stream);
 }
 
+int vv_camera_decode_mode(const vv_tree *t, const vv_camera *cam, const vv_render_opts *o, int32_t *mode) {
+    if (!t || !cam || !mode) return set_error(VV_E_INVALID, "null argument");
+    const vv_render_opts opts = o ? *o : default_opts();
+    const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
+    *mode = decode_mode(t, cube_footprint(*cam, lo, t->view.side, nullptr), opts.frame_slice);
+    return VV_OK;
+}
+
+int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
+                           const vv_render_opts *o, const vv_camera *cam, float *const *rgb, float *const *alpha,
+                           float *const *depth, void *stream) {
+    if (!t || !frames || !caches || !cam || !rgb || !alpha || !depth) return set_error(VV_E_INVALID, "null argument");
+    if (n_frames < 2 || n_frames > kMaxMulti)
+        return set_error(VV_E_UNSUPPORTED, "%d frames per walk (2..%d)", n_frames, kMaxMulti);
+    for (int k = 0; k < n_frames; ++k) {
+        int rc = check_frame(t, frames[k]);
+        if (rc) return rc;
+        if (!caches[k]) return set_error(VV_E_INVALID, "frame %d: a slice is required", frames[k]);
+        if ((rc = check_cache(t, caches[k], frames[k]))) return rc;
+    }
+    DeviceGuard g(t->device);
+    const vv_render_opts opts = o ? *o : default_opts();
+    CamMultiParams p;
+    memset(&p, 0, sizeof(p));
+    p.T = t->view;
+    p.K = make_consts(t->n_max);
+    p.cam = make_cam(*cam);
+    for (int k = 0; k < n_frames; ++k) {
+        p.S[k] = slice_view(caches[k]);
+        p.frames[k] = frames[k];
+        p.rgb[k] = rgb[k];
+        p.alpha[k] = alpha[k];
+        p.depth[k] = depth[k];
+    }
+    p.early_stop = opts.early_stop;
+    p.edit_weight = opts.edit_weight;
+    p.tmin = opts.tmin;
+    p.tmax = opts.tmax;
+    p.far_plane = opts.far_plane;
+    p.alpha_floor = opts.alpha_floor;
+    p.blocks_x = (cam->width + kTW - 1) / kTW;
+    const unsigned grid = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
+    if (grid == 0) return VV_OK;
+    return launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid,
+                               (cudaStream_t)stream);
+}
+
 int vv_render_camera_tiles(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
                            const vv_camera *cam, int32_t tile, int32_t shard, int32_t n_shards, float *packed,
                            void *stream) {

@@ -820,6 +820,122 @@ struct Shader {
     }
 };
 
+// Several frames of one camera in one walk (playback): the rays, and so the
+// traversal and the segment list, do not depend on the frame; every frame
+// keeps its own slice, accumulators and early termination, and sees the
+// same segments in the same order as a single-frame render -- identical
+// results.  The walk ends when every frame has terminated.
+constexpr int kMaxMulti = 4;
+template <int NMAX, int KF, bool EDITS>
+struct ShaderMulti {
+    static constexpr bool kPops = false;
+    const TreeView &T;
+    const SliceView *S;  // KF frame slices
+    const int *frames;
+    const Consts &K;
+    double early_stop, edit_weight;
+    float dx, dy, dz;
+    double trans[KF], acc0[KF], acc1[KF], acc2[KF], aacc[KF], tacc[KF];
+    unsigned alive;
+    bool y_ready;
+    float y[Basis<NMAX>::S];
+
+    __device__ __forceinline__ ShaderMulti(const TreeView &T_, const SliceView *S_, const int *frames_, const Consts &K_,
+                                           double es, double ew, float dx_, float dy_, float dz_)
+        : T(T_), S(S_), frames(frames_), K(K_), early_stop(es), edit_weight(ew), dx(dx_), dy(dy_), dz(dz_),
+          alive((1u << KF) - 1u), y_ready(false) {
+#pragma unroll
+        for (int k = 0; k < KF; ++k) {
+            trans[k] = 1.0;
+            acc0[k] = acc1[k] = acc2[k] = aacc[k] = tacc[k] = 0.0;
+        }
+    }
+    __device__ __forceinline__ void pop() {}
+    __device__ __forceinline__ int pop_count() const { return 0; }
+
+    __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
+#pragma unroll 1
+        for (int s = 0; s < n; ++s) {  // records of the live frames to L1
+            const uint32_t L = (uint32_t)seg.leaf_at(s);
+#pragma unroll
+            for (int k = 0; k < KF; ++k)
+                if ((alive >> k) & 1u) prefetch_l1(S[k].row(L));
+        }
+#pragma unroll 1
+        for (int s = 0; s < n; ++s) {
+            const uint32_t L = (uint32_t)seg.leaf_at(s);
+            const double tin = seg.t0_at(s), tout = seg.t1_at(s);
+#pragma unroll
+            for (int k = 0; k < KF; ++k)
+                if (((alive >> k) & 1u) && leaf(k, L, tin, tout)) alive &= ~(1u << k);
+            if (!alive) return true;
+        }
+        return false;
+    }
+
+    // Shader::leaf (kernels.py:539-599) for frame k (a constant after
+    // unrolling: the per-frame arrays stay in registers), sliced path
+    __device__ __forceinline__ bool leaf(int k, uint32_t L, double tin, double tout) {
+        constexpr int Q4 = Basis<NMAX>::Q4;
+        double sigma = S[k].sigma(L);
+        bool edited = false;
+        float4 erg = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (EDITS && T.edit_t != nullptr) {
+            const int2 et = __ldg(T.edit_t + L);
+            if (et.x <= frames[k] && frames[k] <= et.y) {
+                edited = true;
+                erg = __ldg(T.edit_rgb + L);
+                const double sd = (double)erg.w;
+                if (sd >= 0.0) sigma = sd;
+            }
+        }
+        if (sigma == 0.0) return false;
+        if (!y_ready) {
+            sh_basis<NMAX>(dx, dy, dz, K, y);
+            y_ready = true;
+        }
+        float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+        {
+            float q[4 * Q4];
+            const float4 *qr = S[k].row(L);
+#pragma unroll
+            for (int i = 0; i < Q4; ++i) {
+                const float4 v = __ldg(qr + i);
+                q[4 * i + 0] = v.x;
+                q[4 * i + 1] = v.y;
+                q[4 * i + 2] = v.z;
+                q[4 * i + 3] = v.w;
+            }
+#pragma unroll
+            for (int j = 0; j < Basis<NMAX>::S; ++j) {
+                c0 = __fmaf_rn(y[j], q[3 * j + 0], c0);
+                c1 = __fmaf_rn(y[j], q[3 * j + 1], c1);
+                c2 = __fmaf_rn(y[j], q[3 * j + 2], c2);
+            }
+        }
+        double col0 = (double)sigmoidf_(c0);
+        double col1 = (double)sigmoidf_(c1);
+        double col2 = (double)sigmoidf_(c2);
+        if (EDITS && edited) {
+            const double ew = edit_weight, om = xsub(1.0, ew);
+            col0 = xadd(xmul(ew, (double)erg.x), xmul(om, col0));
+            col1 = xadd(xmul(ew, (double)erg.y), xmul(om, col1));
+            col2 = xadd(xmul(ew, (double)erg.z), xmul(om, col2));
+        }
+        const double delta = xsub(tout, tin);
+        const double e = exp(xmul(-sigma, delta));
+        const double a = xsub(1.0, e);
+        const double w = xmul(trans[k], a);
+        acc0[k] = xadd(acc0[k], xmul(w, col0));
+        acc1[k] = xadd(acc1[k], xmul(w, col1));
+        acc2[k] = xadd(acc2[k], xmul(w, col2));
+        aacc[k] = xadd(aacc[k], w);
+        tacc[k] = xadd(tacc[k], xmul(xmul(w, 0.5), xadd(tin, tout)));
+        trans[k] = xmul(trans[k], e);
+        return trans[k] < early_stop;
+    }
+};
+
 // Traversal-only visitors (count / collect, kernels.py:313-367)
 struct CountVisitor {
     static constexpr bool kPops = false;

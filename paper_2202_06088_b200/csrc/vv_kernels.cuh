@@ -313,6 +313,57 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
     if (p.depth) p.depth[pix] = (float)D;
 }
 
+// ------------------------------------------------------------------ playback, several frames
+// k_render_camera for KF frames of one camera in one walk (ShaderMulti):
+// per-frame slices (required), images and results identical to KF
+// single-frame renders.
+struct CamMultiParams {
+    TreeView T;
+    SliceView S[kMaxMulti];
+    int frames[kMaxMulti];
+    Consts K;
+    CamView cam;
+    double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
+    float *rgb[kMaxMulti], *alpha[kMaxMulti], *depth[kMaxMulti];
+    int blocks_x;
+};
+
+template <int NMAX, int KF, bool EDITS, class Entry>
+__global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int bx = blockIdx.x % p.blocks_x, by = blockIdx.x / p.blocks_x;
+    const int x0 = bx * kTW, y0 = by * kTH;
+#pragma unroll 1
+    for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
+        const int rid = pass * kBlock + (int)threadIdx.x;
+        int dx_, dy_;
+        local_pixel(rid, dx_, dy_);
+        const int ix = x0 + dx_, iy = y0 + dy_;
+        if (ix >= p.cam.width || iy >= p.cam.height) continue;
+        double dx, dy, dz;
+        camera_ray(p.cam, ix, iy, dx, dy, dz);
+        ShaderMulti<NMAX, KF, EDITS> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
+                                        (float)dz);
+        Ray ray;
+        if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
+            traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+        const long long slot = (long long)iy * p.cam.width + ix;
+#pragma unroll
+        for (int k = 0; k < KF; ++k) {
+            float r, g, b, a, d;
+            finalize(sh.acc0[k], sh.acc1[k], sh.acc2[k], sh.aacc[k], sh.tacc[k], 1.0, false, p.alpha_floor,
+                     p.far_plane, r, g, b, a, d);
+            if (p.rgb[k]) {
+                p.rgb[k][3 * slot + 0] = r;
+                p.rgb[k][3 * slot + 1] = g;
+                p.rgb[k][3 * slot + 2] = b;
+            }
+            if (p.alpha[k]) p.alpha[k][slot] = a;
+            if (p.depth[k]) p.depth[k][slot] = d;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ slice
 struct SliceParams {
     TreeView T;
@@ -559,6 +610,8 @@ int launch_rays(int nmax, int mode, bool edits, bool wide, bool visits, const Ra
 // one block per 32x16 tile (max_blocks = tile count)
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
                   cudaStream_t st);
+int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
+                        cudaStream_t st);
 int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);

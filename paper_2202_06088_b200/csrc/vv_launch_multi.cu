@@ -1,0 +1,35 @@
+// vv_launch_multi.cu -- instantiations of k_render_camera_multi (playback:
+// several frames of one camera in one walk).
+#include "vv_kernels.cuh"
+
+namespace vvk {
+
+template <int NM, int KF, bool EDITS, class Entry>
+static int go(const CamMultiParams &p, unsigned grid, cudaStream_t st) {
+    auto kern = k_render_camera_multi<NM, KF, EDITS, Entry>;
+    const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes);
+    int r = prep_smem(kern, smem);
+    if (r) return r;
+    kern<<<grid, kBlock, smem, st>>>(p);
+    return check_launch("render_camera_multi");
+}
+
+template <int NM, class Entry>
+static int pick(int kf, bool edits, const CamMultiParams &p, unsigned grid, cudaStream_t st) {
+    switch (kf) {
+        case 2: return edits ? go<NM, 2, true, Entry>(p, grid, st) : go<NM, 2, false, Entry>(p, grid, st);
+        case 3: return edits ? go<NM, 3, true, Entry>(p, grid, st) : go<NM, 3, false, Entry>(p, grid, st);
+        case 4: return edits ? go<NM, 4, true, Entry>(p, grid, st) : go<NM, 4, false, Entry>(p, grid, st);
+        default: return set_error(VV_E_UNSUPPORTED, "%d frames per walk (2..%d)", kf, kMaxMulti);
+    }
+}
+
+int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
+                        cudaStream_t st) {
+    return with_nmax(nmax, [&](auto N) {
+        constexpr int NM = decltype(N)::value;
+        return wide ? pick<NM, EntryW>(kf, edits, p, grid, st) : pick<NM, EntryN>(kf, edits, p, grid, st);
+    });
+}
+
+}  // namespace vvk

@@ -34,6 +34,7 @@ __all__ = [
     "FrameSlice",
     "render",
     "render_into",
+    "render_frames_into",
     "render_sequence",
     "render_rays",
     "render_ray_visits",
@@ -445,14 +446,65 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
                        a[4 * h * w:].reshape(h, w))
 
 
+def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = RenderOptions(), *, stream=None):
+    """Render 1..4 frames of ONE camera into caller-owned CUDA float32
+    tensors ``outs[k] = (rgb, alpha, depth)`` (any may be None).
+
+    The rays -- and so the octree walk and every ray's segment list -- do not
+    depend on the frame, so the frames share one walk
+    (vv_render_camera_multi); each frame has its own slice pass,
+    accumulators and early termination, and its images are bitwise
+    identical to ``render_into`` of that frame.  When the decode policy
+    would decode per sample (a tree small on screen) the frames render one
+    by one instead.  Asynchronous on the current (or given) stream.
+    """
+    torch = require_cuda()
+    frames = [_frame_index(f) for f in frames]
+    if len(frames) != len(outs):
+        raise ValueError(f"{len(frames)} frames but {len(outs)} outputs")
+    if not 1 <= len(frames) <= 4:
+        raise ValueError("1..4 frames per walk")
+    for f in frames:
+        _check_frame(tree, f)
+    ref = next(x for o in outs for x in o if x is not None)
+    dev = ref.device
+    rep = replica(tree, dev)
+    oc = opts.c_struct()
+    cd = cam.desc()
+    mode = ctypes.c_int32(0)
+    _native.check(_native.lib().vv_camera_decode_mode(rep.handle, ctypes.byref(cd), ctypes.byref(oc),
+                                                      ctypes.byref(mode)))
+    if len(frames) == 1 or mode.value == 0:
+        for f, o in zip(frames, outs):
+            render_into(tree, cam, f, *o, opts, stream=stream)
+        return
+    ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream(dev))
+    with ctx:
+        caches = [build_frame_cache(tree, f, device=dev) for f in frames]  # freed stream-ordered after the walk
+        n = len(frames)
+        P = ctypes.c_void_p
+
+        def ptrs(j):
+            return (P * n)(*[o[j].data_ptr() if o[j] is not None else None for o in outs])
+
+        _native.check(_native.lib().vv_render_camera_multi(
+            rep.handle, n, (ctypes.c_int32 * n)(*frames), (P * n)(*[c._handle for c in caches]),
+            ctypes.byref(oc), ctypes.byref(cd), ptrs(0), ptrs(1), ptrs(2), stream_ptr(dev)))
+        del caches
+
+
+# frames per shared walk in playback (measured per-frame render kernel cost
+# at cfg2 for 1/2/3/4 frames: 0.76 / 0.49 / 0.41 / 0.42 ms)
+PLAYBACK_GROUP = 3
+
 _PLAYBACK = {}
 
 
 def _playback_state(torch, dev, n: int):
-    """Per-device playback streams and double buffers, kept across calls.
+    """Per-device playback streams and double-buffered frame groups, kept across calls.
 
     Dedicated streams (the legacy default stream would serialise render and
-    copy), and the SAME streams every call: the frame slice is allocated
+    copy), and the SAME streams every call: the frame slices are allocated
     stream-ordered (cudaMallocAsync) on the render stream, and the pool only
     recycles a block on the stream that freed it -- a fresh stream per call
     re-maps ~1.9 GB of slice memory on its first frame (tens of ms).
@@ -462,9 +514,11 @@ def _playback_state(torch, dev, n: int):
     if st is None or st[3][0]:
         comp, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         with torch.cuda.stream(comp):
-            bufs = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)]
-        for b in bufs:
-            b.record_stream(copy)
+            bufs = [[torch.empty(n, dtype=torch.float32, device=dev) for _ in range(PLAYBACK_GROUP)]
+                    for _ in range(2)]
+        for grp in bufs:
+            for b in grp:
+                b.record_stream(copy)
         fresh = (comp, copy, bufs, [False])
         if st is not None:
             return fresh  # another playback is live on this device: private state, not cached
@@ -478,11 +532,13 @@ def _playback_state(torch, dev, n: int):
 def render_sequence(tree, cam: Camera, frames, opts: RenderOptions = RenderOptions(), *, device=None):
     """Playback: render `frames` in order, yielding numpy LayerImages (fp32).
 
-    Double-buffered: frame i renders on a per-device render stream (ordered
-    after the caller's current stream) while frame i-1's 20 B/pixel result is
-    copied device->host on a side stream into pinned memory, so a sequence
-    runs at max(render, copy) per frame instead of their sum.  Each yielded
-    frame is complete on the host.
+    Frames render in groups of PLAYBACK_GROUP sharing one octree walk
+    (render_frames_into: one camera, so the walk is frame-independent; each
+    frame's images are bitwise identical to ``render``).  Double-buffered:
+    group g renders on a per-device render stream (ordered after the
+    caller's current stream) while group g-1's 20 B/pixel results are copied
+    device->host on a side stream into pinned memory.  Each yielded frame is
+    complete on the host.
     """
     torch = require_cuda()
     dev = torch_device(device)
@@ -499,10 +555,10 @@ def render_sequence(tree, cam: Camera, frames, opts: RenderOptions = RenderOptio
 
 
 def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
-    # warm the pinned pool for the frames in flight (2 pending + the caller's
-    # current and previous frame): a 41 MB cudaHostAlloc costs 25-100 ms, so
-    # grow the pool once up front instead of stalling mid-sequence
-    warm = [_PINNED.get(n) for _ in range(4)]
+    # warm the pinned pool for the frames in flight (two groups pending + the
+    # caller's current and previous frame): a 41 MB cudaHostAlloc costs
+    # 25-100 ms, so grow the pool once up front instead of stalling mid-sequence
+    warm = [_PINNED.get(n) for _ in range(2 * PLAYBACK_GROUP + 2)]
     del warm
     copied = [None, None]
     pending = []
@@ -511,32 +567,41 @@ def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
         return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
                            a[4 * h * w:].reshape(h, w))
 
-    for i, f in enumerate(frames):
-        b = i % 2
+    def split(b):
+        return (b[: 3 * h * w].view(h, w, 3), b[3 * h * w: 4 * h * w].view(h, w), b[4 * h * w:].view(h, w))
+
+    frames = list(frames)
+    for gi, g0 in enumerate(range(0, len(frames), PLAYBACK_GROUP)):
+        group = frames[g0:g0 + PLAYBACK_GROUP]
+        b = gi % 2
         if copied[b] is not None:
-            comp.wait_event(copied[b])  # buffer b's previous frame has left the device
-        buf = bufs[b]
+            comp.wait_event(copied[b])  # group b's previous frames have left the device
+        grp = bufs[b][:len(group)]
         with torch.cuda.stream(comp):
-            render_into(tree, cam, f, buf[: 3 * h * w].view(h, w, 3), buf[3 * h * w: 4 * h * w].view(h, w),
-                        buf[4 * h * w:].view(h, w), opts)
+            render_frames_into(tree, cam, group, [split(x) for x in grp], opts)
         rendered = torch.cuda.Event()
         rendered.record(comp)
-        host, arr = _PINNED.get(n)
         copy.wait_event(rendered)
-        with torch.cuda.stream(copy):
-            host.copy_(buf, non_blocking=True)
+        arrs = []
+        for x in grp:
+            host, arr = _PINNED.get(n)
+            with torch.cuda.stream(copy):
+                host.copy_(x, non_blocking=True)
+            arrs.append(arr)
         done = torch.cuda.Event()
         done.record(copy)
         copied[b] = done
-        pending.append((done, arr))
+        pending.append((done, arrs))
         if len(pending) > 1:
             ev, a = pending.pop(0)
             ev.synchronize()
-            yield views(a)
+            for x in a:
+                yield views(x)
     while pending:
         ev, a = pending.pop(0)
         ev.synchronize()
-        yield views(a)
+        for x in a:
+            yield views(x)
 
 
 def composite_background(layer: LayerImages, bg) -> np.ndarray:

@@ -380,3 +380,66 @@ def test_deep_scene_launch(cuda, depth):
     fused = vv.render_scene(scene, cam, 1)
     host, _, _ = vv.render_scene(scene, cam, 1, want_layers=True)
     assert np.abs(fused - host).max() < 1e-4
+
+
+def _outs(torch, h, w, k):
+    return [(torch.empty((h, w, 3), device="cuda"), torch.empty((h, w), device="cuda"),
+             torch.empty((h, w), device="cuda")) for _ in range(k)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_max,k", [(0, 2), (1, 3), (2, 4), (3, 2), (2, 3)])
+def test_frames_share_one_walk_bitwise(cuda, n_max, k):
+    """render_frames_into (several frames, one walk) == render_into per frame, bitwise."""
+    import torch
+
+    rng = np.random.default_rng(40 + n_max)
+    res = 1 << 6
+    coords = np.argwhere(rng.random((res, res, res)) < 0.08)
+    kk = (n_max + 1) * (n_max + 2) * (2 * n_max + 3) // 6
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 5 + 3 * kk)).astype(np.float32)
+    data[:, 0] = rng.uniform(5.0, 60.0, len(coords))
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(6, 5), n_max, depth=6)
+    cam = vv.Camera.look_at([1.8, -0.9, 1.3], [0.5, 0.5, 0.5], width=96, height=72)
+    frames = [5, 0, 3, 3][:k]  # any order, repeats allowed
+    outs, refs = _outs(torch, 72, 96, k), _outs(torch, 72, 96, k)
+    vv.render_frames_into(tree, cam, frames, outs)
+    for f, r in zip(frames, refs):
+        vv.render_into(tree, cam, f, *r)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        for a, b in zip(o, r):
+            assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_frames_share_one_walk_with_edits(cuda):
+    import torch
+
+    g = load("edits_d3")
+    tree = tree_from(g)
+    cam = vv.Camera.look_at([2.1, -0.7, 1.5], [0.5, 0.5, 0.5], width=40, height=40)
+    frames = [0, 2, 5]  # inside and outside the edit windows
+    for ew in (1.0, 0.4):
+        opts = vv.RenderOptions(edit_weight=ew, frame_slice="per_frame")
+        outs, refs = _outs(torch, 40, 40, 3), _outs(torch, 40, 40, 3)
+        vv.render_frames_into(tree, cam, frames, outs, opts)
+        for f, r in zip(frames, refs):
+            vv.render_into(tree, cam, f, *r, opts)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, b) for o, r in zip(outs, refs) for a, b in zip(o, r))
+
+
+@pytest.mark.gpu
+def test_frames_per_sample_fallback(cuda):
+    """A tree small on screen decodes per sample: frames render one by one, same images."""
+    import torch
+
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=16, seed=0)
+    cam = vv.Camera.look_at([6.0, 5.0, 4.0], [0.5, 0.5, 0.5], width=128, height=96)
+    outs, refs = _outs(torch, 96, 128, 2), _outs(torch, 96, 128, 2)
+    vv.render_frames_into(tree, cam, [1, 7], outs)
+    for f, r in zip([1, 7], refs):
+        vv.render_into(tree, cam, f, *r)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for o, r in zip(outs, refs) for a, b in zip(o, r))

@@ -20,6 +20,6 @@ wait
 for d in $ROOT/variants/*/; do
   [ -f $d/cam.o ] || continue
   $NVCC $ARCH -shared -cudart=static -o $d/libvoxvid_b200.so $OBJ/vv_api.o $OBJ/vv_launch_rays.o $d/cam.o \
-      $OBJ/vv_launch_scene.o $OBJ/vv_launch_misc.o $OBJ/vv_launch_light.o $OBJ/vv_host.o
+      $OBJ/vv_launch_scene.o $OBJ/vv_launch_misc.o $OBJ/vv_launch_light.o $OBJ/vv_launch_multi.o $OBJ/vv_host.o
   echo "$d: $(grep -A2 'k_render_cameraILi2ELi1ELb0EN2vv6EntryN' $d/ptxas.log | grep -E 'registers|spill' | tr '\n' ' ')"
 done
