@@ -595,13 +595,13 @@ def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
         if len(pending) > 1:
             ev, a = pending.pop(0)
             ev.synchronize()
-            for x in a:
-                yield views(x)
+            while a:  # hand frames over without keeping them (their pinned buffers recycle)
+                yield views(a.pop(0))
     while pending:
         ev, a = pending.pop(0)
         ev.synchronize()
-        for x in a:
-            yield views(x)
+        while a:
+            yield views(a.pop(0))
 
 
 def composite_background(layer: LayerImages, bg) -> np.ndarray:
