@@ -443,3 +443,39 @@ def test_frames_per_sample_fallback(cuda):
         vv.render_into(tree, cam, f, *r)
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for o, r in zip(outs, refs) for a, b in zip(o, r))
+
+
+@pytest.mark.gpu
+def test_full_size_config2(cuda):
+    """BASELINE configs[1] at full size (depth 9, 3,557,912 leaves, 1080p):
+    visits / sample counts bit-exact against the oracle on a random pixel
+    sample; the fused camera kernel agrees with render_rays on those pixels;
+    shared-walk playback is bitwise equal to per-frame renders."""
+    import torch
+
+    tree = synthetic.shell_tree()
+    cam = synthetic.bench_camera()
+    o, d = cam.rays()
+    rng = np.random.default_rng(99)
+    idx = np.sort(rng.choice(len(o), 20000, replace=False))
+    frame = 11
+    ref = oracle.render_rays(tree, o[idx], d[idx], frame, visits=True)
+    used, start, leaf = vv.render_ray_visits(tree, o[idx], d[idx], frame)
+    _exact(used, ref["used"], "sample counts")
+    _exact(leaf, ref["visit_leaf"], "visited leaves")
+    assert (used > 0).sum() > 3000
+    p, a, t = vv.render_rays(tree, o[idx], d[idx], frame)
+    assert np.abs(a - ref["alpha"]).max() <= 1e-12
+    assert np.abs(p - ref["premult"]).max() <= TOL
+    layer = vv.render(tree, cam, frame)
+    rgb, alpha, depth = oracle.finalize(p, a, t)
+    assert np.abs(layer.rgb.reshape(-1, 3)[idx] - rgb).max() < TOL
+    assert np.abs(layer.alpha.reshape(-1)[idx] - alpha).max() < TOL
+    hit = alpha >= 1e-3
+    assert np.abs(layer.depth.reshape(-1)[idx][hit] - depth[hit]).max() < TOL
+    seq = list(vv.render_sequence(tree, cam, [frame, 12, 13, 29]))
+    for f, l in zip([frame, 12, 13, 29], seq):
+        r = vv.render(tree, cam, f)
+        _exact(l.rgb, r.rgb)
+        _exact(l.alpha, r.alpha)
+        _exact(l.depth, r.depth)
