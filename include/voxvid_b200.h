@@ -133,6 +133,11 @@ int vv_slice_build(const vv_tree *tree, int32_t frame, void *stream, vv_slice **
 /* The slice is allocated stream-ordered on `stream` (the device's default
  * memory pool) and released stream-ordered on the same stream: work already
  * queued on that stream may still read it. */
+/* Slices of n_frames (1..4) frames from ONE pass over the payload (each
+ * leaf row is read once and sliced per frame): out[k] is frames[k]'s slice,
+ * equal to vv_slice_build(frames[k]).  Playback groups use it. */
+int vv_slice_build_multi(const vv_tree *tree, int32_t n_frames, const int32_t *frames, void *stream,
+                         vv_slice **out);
 int vv_slice_free(vv_slice *slice);
 /* Copies the cache to caller device buffers: sigma (n_leaves) f64,
  * q (n_leaves, 3S) f32. */

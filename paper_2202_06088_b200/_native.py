@@ -65,6 +65,7 @@ EXPORTED_SYMBOLS = (
     "vv_unpack_tiles",
     "vv_render_scene",
     "vv_render_camera_multi",
+    "vv_slice_build_multi",
     "vv_camera_decode_mode",
     "vv_shadow_blur",
     "vv_scene_lighting",
@@ -218,6 +219,7 @@ _SIGNATURES = {
     ),
     "vv_unpack_tiles": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "vv_camera_decode_mode": (ctypes.c_int, [_P, _P, _P, _P]),
+    "vv_slice_build_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),

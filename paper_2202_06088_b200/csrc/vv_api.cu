@@ -136,11 +136,13 @@ SliceView slice_view(const vv_slice *c) {
 int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
+    memset(&p, 0, sizeof(p));
     p.T = t->view;
     p.K = make_consts(t->n_max);
-    p.frame = frame;
+    p.n_frames = 1;
+    p.frame[0] = frame;
     p.n_leaves = t->n_leaves;
-    p.rec = rec;
+    p.rec[0] = rec;
     p.rec4 = rec4;
     return launch_slice(t->n_max, p, st);
 }
@@ -448,6 +450,54 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
     }
     *out = s;
     return VV_OK;
+}
+
+int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, void *stream, vv_slice **out) {
+    if (!t || !frames || !out) return set_error(VV_E_INVALID, "null argument");
+    if (n_frames < 1 || n_frames > kMaxMulti)
+        return set_error(VV_E_UNSUPPORTED, "%d frames per slice pass (1..%d)", n_frames, kMaxMulti);
+    for (int f = 0; f < n_frames; ++f) {
+        int rc = check_frame(t, frames[f]);
+        if (rc) return rc;
+        out[f] = nullptr;
+    }
+    DeviceGuard g(t->device);
+    pool_setup(t->device);
+    SliceParams p;
+    memset(&p, 0, sizeof(p));
+    p.T = t->view;
+    p.K = make_consts(t->n_max);
+    p.n_frames = n_frames;
+    p.n_leaves = t->n_leaves;
+    p.rec4 = slice_rec4(t->S);
+    const int64_t nrows = std::max<int64_t>(t->n_leaves, 1);
+    auto fail = [&](int rc) {
+        for (int f = 0; f < n_frames; ++f) {
+            vv_slice_free(out[f]);
+            out[f] = nullptr;
+        }
+        return rc;
+    };
+    for (int f = 0; f < n_frames; ++f) {
+        vv_slice *s = new vv_slice();
+        s->tree = t;
+        s->device = t->device;
+        s->frame = frames[f];
+        s->n_leaves = t->n_leaves;
+        s->rec4 = p.rec4;
+        s->stream = (cudaStream_t)stream;
+        out[f] = s;
+        if (cudaMallocAsync(&s->d_rec, nrows * s->rec4 * sizeof(float4), s->stream) != cudaSuccess) {
+            cudaGetLastError();
+            s->d_rec = nullptr;
+            return fail(set_error(VV_E_NOMEM, "slice allocation failed"));
+        }
+        p.frame[f] = frames[f];
+        p.rec[f] = s->d_rec;
+    }
+    if (t->n_leaves == 0) return VV_OK;
+    const int rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
+    return rc ? fail(rc) : VV_OK;
 }
 
 int vv_slice_free(vv_slice *s) {

@@ -368,9 +368,10 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera_multi(con
 struct SliceParams {
     TreeView T;
     Consts K;
-    int frame;
+    int n_frames;               // 1..kMaxMulti frames sliced from one read of the payload
+    int frame[kMaxMulti];
     int64_t n_leaves;
-    float4 *rec;  // (n_leaves, rec4) slice records
+    float4 *rec[kMaxMulti];     // (n_leaves, rec4) slice records per frame
     int rec4;
 };
 
@@ -393,10 +394,16 @@ __host__ __device__ inline size_t slice_smem_bytes(int sig4, int rest4) {
     return (size_t)kSliceWarps * (2 * slice_stage_floats4(sig4, rest4) * 16 + 16);
 }
 
-template <int NMAX>
+// KF frames (playback groups) are sliced from ONE read of the payload: a
+// staged row's w_sigma / w_gamma entries are read once and feed KF sigma
+// (f64) and KF gamma (fp32) accumulators side by side -- each frame keeps
+// exactly its single-frame summation order -- and w_hh is loaded once for
+// the KF HH->SH slices.
+template <int NMAX, int KF>
 __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_constant__ SliceParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ float sA[kMaxC], sB[kMaxC];
+    __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
+    __shared__ double dA[KF][kMaxC];  // A rows widened once (the values sigma_pre multiplies)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sig4 = p.T.sig4, rest4 = p.T.rest4;
     const size_t stage4 = slice_stage_floats4(sig4, rest4);
@@ -407,8 +414,12 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
-    load_rows(p.T, p.frame, sA, sB);
+#pragma unroll
+    for (int f = 0; f < KF; ++f) load_rows(p.T, p.frame[f], sA[f], sB[f]);
     __syncthreads();
+    for (int i = threadIdx.x; i < KF * kMaxC; i += blockDim.x) dA[i / kMaxC][i % kMaxC] = (double)sA[i / kMaxC][i % kMaxC];
+    __syncthreads();
+    const int C = p.T.C, C4 = (C + 3) >> 2;
     const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
     const int64_t wstride = (int64_t)gridDim.x * kSliceWarps;
     const int64_t c0 = (int64_t)blockIdx.x * kSliceWarps + warp;
@@ -432,21 +443,59 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kSliceChunk;
         const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
-        const float4 *ssig = wbase + stg * stage4;
-        const float4 *srest = ssig + (size_t)kSliceChunk * sig4;
+        const float4 *ssig = wbase + stg * stage4 + lane * sig4;
+        const float4 *srest = wbase + stg * stage4 + (size_t)kSliceChunk * sig4 + lane * rest4;
         if (lane < rows) {
-            float q[4 * R4];
+            // sigma_pre (kernels.py:374-381, f64, sequential) and the gamma dot
+            // (fp32), every frame at once
+            double sp[KF];
+            float gp[KF];
 #pragma unroll
-            for (int i = 0; i < 4 * R4; ++i) q[i] = 0.0f;
-            double sigma;
-            slice_rows<NMAX, false>(ssig + lane * sig4, srest + lane * rest4, p.T.C, p.T.hh_off4, sA, sB, p.K,
-                                    sigma, q);
-            const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
-            q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
-            q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
-            float4 *o = p.rec + (base + lane) * p.rec4;
+            for (int f = 0; f < KF; ++f) {
+                sp[f] = 0.0;
+                gp[f] = 0.0f;
+            }
+#pragma unroll 2
+            for (int i = 0; i < C4; ++i) {
+                const float4 v = ld4<false>(ssig + i), g = ld4<false>(srest + i);
+                const double w[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+                const float gw[4] = {g.x, g.y, g.z, g.w};
+                const int cc = 4 * i;
 #pragma unroll
-            for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+                for (int e = 0; e < 4; ++e) {
+                    if (cc + e < C) {
+#pragma unroll
+                        for (int f = 0; f < KF; ++f) {
+                            sp[f] = xadd(sp[f], xmul(dA[f][cc + e], w[e]));
+                            gp[f] = __fmaf_rn(sB[f][cc + e], gw[e], gp[f]);
+                        }
+                    }
+                }
+            }
+            float wh[4 * Basis<NMAX>::HH4];
+            load_hh<NMAX, false>(srest, p.T.hh_off4, wh);
+#pragma unroll
+            for (int f = 0; f < KF; ++f) {
+                float q[4 * R4];
+#pragma unroll
+                for (int i = 0; i < 4 * R4; ++i) q[i] = 0.0f;
+                float R[Basis<NMAX>::NPAIRS];
+                radial<NMAX>(sigmoidf_(gp[f]), p.K, R);
+#pragma unroll
+                for (int l = 0; l <= NMAX; ++l)
+#pragma unroll
+                    for (int m = -l; m <= l; ++m) {
+                        const int j = l * l + l + m;
+                        slice_col<NMAX>(R, wh, l, m, q[3 * j + 0], q[3 * j + 1], q[3 * j + 2]);
+                    }
+                const double sigma = sp[f] > 0.0 ? sp[f] : 0.0;  // max(0.0, sp)
+                const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+                q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
+                q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
+                float4 *o = p.rec[f] + (base + lane) * p.rec4;
+#pragma unroll
+                for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+            }
         }
         __syncwarp();
         // stage consumed: refill it with the chunk two steps ahead

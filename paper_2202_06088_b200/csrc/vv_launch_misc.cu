@@ -48,17 +48,29 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 }
 
 
-int launch_slice(int nmax, const SliceParams &p, cudaStream_t st) {
+template <int NM, int KF>
+static int go_slice(const SliceParams &p, cudaStream_t st) {
     const size_t smem = slice_smem_bytes(p.T.sig4, p.T.rest4);
+    auto kern = k_build_slice<NM, KF>;
+    int r = prep_smem(kern, smem);
+    if (r) return r;
+    const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
+    const unsigned want = (unsigned)((chunks + kSliceWarps - 1) / kSliceWarps);
+    const unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
+    kern<<<grid, kSliceWarps * 32, smem, st>>>(p);
+    return check_launch("build_slice");
+}
+
+int launch_slice(int nmax, const SliceParams &p, cudaStream_t st) {
     return with_nmax(nmax, [&](auto N) {
-        auto kern = k_build_slice<decltype(N)::value>;
-        int r = prep_smem(kern, smem);
-        if (r) return r;
-        const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
-        const unsigned want = (unsigned)((chunks + kSliceWarps - 1) / kSliceWarps);
-        const unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
-        kern<<<grid, kSliceWarps * 32, smem, st>>>(p);
-        return check_launch("build_slice");
+        constexpr int NM = decltype(N)::value;
+        switch (p.n_frames) {
+            case 1: return go_slice<NM, 1>(p, st);
+            case 2: return go_slice<NM, 2>(p, st);
+            case 3: return go_slice<NM, 3>(p, st);
+            case 4: return go_slice<NM, 4>(p, st);
+            default: return set_error(VV_E_UNSUPPORTED, "%d frames per slice pass", p.n_frames);
+        }
     });
 }
 

@@ -41,6 +41,7 @@ __all__ = [
     "finalize_layer",
     "composite_background",
     "build_frame_cache",
+    "build_frame_caches",
     "count_segments",
     "collect_segments",
 ]
@@ -298,6 +299,24 @@ def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
     return FrameSlice(frame, handle, rep, dev)
 
 
+def build_frame_caches(tree, frames, device=None) -> list:
+    """Slices of 1..4 frames from ONE pass over the payload (vv_slice_build_multi):
+    each leaf row is read once and sliced per frame; ``[build_frame_cache(tree, f) for f in frames]``
+    with a quarter to a half of the HBM traffic."""
+    frames = [_frame_index(f) for f in frames]
+    for f in frames:
+        _check_frame(tree, f)
+    if not 1 <= len(frames) <= 4:
+        raise ValueError("1..4 frames per slice pass")
+    dev = torch_device(device)
+    rep = replica(tree, dev)
+    n = len(frames)
+    handles = (ctypes.c_void_p * n)()
+    _native.check(_native.lib().vv_slice_build_multi(rep.handle, n, (ctypes.c_int32 * n)(*frames), stream_ptr(dev),
+                                                     handles))
+    return [FrameSlice(f, ctypes.c_void_p(h), rep, dev) for f, h in zip(frames, handles)]
+
+
 def _as_device_rays(x, dev):
     torch = require_cuda()
     if isinstance(x, torch.Tensor):
@@ -480,7 +499,7 @@ def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = Re
         return
     ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream(dev))
     with ctx:
-        caches = [build_frame_cache(tree, f, device=dev) for f in frames]  # freed stream-ordered after the walk
+        caches = build_frame_caches(tree, frames, device=dev)  # one payload pass; freed stream-ordered after the walk
         n = len(frames)
         P = ctypes.c_void_p
 

@@ -479,3 +479,18 @@ def test_full_size_config2(cuda):
         _exact(l.rgb, r.rgb)
         _exact(l.alpha, r.alpha)
         _exact(l.depth, r.depth)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("frames", [[2], [0, 5], [1, 1, 4], [3, 0, 2, 5]])
+def test_slice_pass_several_frames_bitwise(cuda, frames):
+    """build_frame_caches (one payload pass) == build_frame_cache per frame, bitwise."""
+    g = load("cache_d3")
+    tree = tree_from(g)
+    frames = [f % tree.frames for f in frames]
+    many = vv.build_frame_caches(tree, frames)
+    for f, c in zip(frames, many):
+        one = vv.build_frame_cache(tree, f)
+        assert c.frame == f
+        _exact(c.sigma.cpu().numpy(), one.sigma.cpu().numpy())
+        _exact(c.q.cpu().numpy(), one.q.cpu().numpy())
