@@ -494,3 +494,29 @@ def test_slice_pass_several_frames_bitwise(cuda, frames):
         assert c.frame == f
         _exact(c.sigma.cpu().numpy(), one.sigma.cpu().numpy())
         _exact(c.q.cpu().numpy(), one.q.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_frames_share_one_walk_deep_and_empty(cuda):
+    """Shared walk with wide (16-byte) stack entries (depth 11), and an empty tree."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    res = 1 << 11
+    coords = np.unique(rng.integers(res // 3, 2 * res // 3, (4000, 3)), axis=0)
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 5 + 3 * 5)).astype(np.float32)
+    data[:, 0] = rng.uniform(100.0, 900.0, len(coords))
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(4, 5), 1, depth=11)
+    cam = vv.Camera.look_at([0.5, -1.5, 0.6], [0.5, 0.5, 0.5], width=64, height=48)
+    opts = vv.RenderOptions(frame_slice="per_frame")
+    outs, refs = _outs(torch, 48, 64, 3), _outs(torch, 48, 64, 3)
+    vv.render_frames_into(tree, cam, [0, 1, 3], outs, opts)
+    for f, r in zip([0, 1, 3], refs):
+        vv.render_into(tree, cam, f, *r, opts)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for o, r in zip(outs, refs) for a, b in zip(o, r))
+    assert float(outs[0][1].max()) > 0.0
+    empty = vv.VOctree.from_cells(np.zeros((0, 3), np.int64), np.zeros((0, 25), np.float32),
+                                  vv.make_bump_bases(4, 5), 1, depth=3)
+    seq = list(vv.render_sequence(empty, cam, [0, 1, 2, 3]))
+    assert len(seq) == 4 and all(np.all(l.alpha == 0.0) for l in seq)
