@@ -627,37 +627,6 @@ __device__ __forceinline__ void load_hh(const float4 *__restrict__ rest_row, int
     }
 }
 
-// Full per-leaf slice (build_slice_kernel, kernels.py:397-407): sigma (f64)
-// and q (fp32, channel-interleaved 3S).
-// HH->SH slice of one leaf at the frame's hyper angle: q (fp32, 3S)
-template <int NMAX, bool G = true>
-__device__ __forceinline__ void slice_q(const float4 *rest_row, int C, int hh_off4, const float *sB, const Consts &K,
-                                        float *q) {
-    const float s = gamma_s<G>(rest_row, sB, C);
-    float R[Basis<NMAX>::NPAIRS];
-    radial<NMAX>(s, K, R);
-    float wh[4 * Basis<NMAX>::HH4];
-    load_hh<NMAX, G>(rest_row, hh_off4, wh);
-#pragma unroll
-    for (int l = 0; l <= NMAX; ++l)
-#pragma unroll
-        for (int m = -l; m <= l; ++m) {
-            const int j = l * l + l + m;
-            slice_col<NMAX>(R, wh, l, m, q[3 * j + 0], q[3 * j + 1], q[3 * j + 2]);
-        }
-}
-
-// Full per-leaf slice (build_slice_kernel, kernels.py:397-407): sigma (f64)
-// and q (fp32, channel-interleaved 3S).
-template <int NMAX, bool G = true>
-__device__ __forceinline__ void slice_rows(const float4 *sig_row, const float4 *rest_row, int C, int hh_off4,
-                                           const float *sA, const float *sB, const Consts &K, double &sigma,
-                                           float *q) {
-    const double sp = sigma_pre<G>(sig_row, sA, C);
-    sigma = sp > 0.0 ? sp : 0.0;  // max(0.0, sp)
-    slice_q<NMAX, G>(rest_row, C, hh_off4, sB, K, q);
-}
-
 // ------------------------------------------------------------ shading visitor
 struct FrameCtx {
     const float *sA;   // A[t] row in shared memory
