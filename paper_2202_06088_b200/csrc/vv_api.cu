@@ -964,9 +964,10 @@ int vv_tree_set_edits(vv_tree *t, const float *edit_rgb, const int32_t *edit_t) 
 }
 
 int vv_voct_upload(const uint8_t *buf, size_t len, int device, vv_tree **out, vv_voct_info *info) {
-    if (!buf || !out) return set_error(VV_E_INVALID, "null argument");
+    if (!out) return set_error(VV_E_INVALID, "null argument");
     // checks in the order of VOctree.from_bytes (octree.py:440-510)
     if (len < 4) return set_error(VV_E_TRUNCATED, "stream of %zu bytes is shorter than the magic", len);
+    if (!buf) return set_error(VV_E_INVALID, "null argument");
     if (memcmp(buf, "VOCT", 4) != 0) {
         char m[64];
         int k = 0;
