@@ -834,9 +834,12 @@ struct ShaderMulti {
         for (int s = 0; s < n; ++s) {
             const uint32_t L = (uint32_t)seg.leaf_at(s);
             const double tin = seg.t0_at(s), tout = seg.t1_at(s);
+            double sg[KF];  // every live frame's sigma requested at once (independent loads)
+#pragma unroll
+            for (int k = 0; k < KF; ++k) sg[k] = ((alive >> k) & 1u) ? S[k].sigma(L) : 0.0;
 #pragma unroll
             for (int k = 0; k < KF; ++k)
-                if (((alive >> k) & 1u) && leaf(k, L, tin, tout)) alive &= ~(1u << k);
+                if (((alive >> k) & 1u) && leaf(k, L, tin, tout, sg[k])) alive &= ~(1u << k);
             if (!alive) return true;
         }
         return false;
@@ -844,9 +847,8 @@ struct ShaderMulti {
 
     // Shader::leaf (kernels.py:539-599) for frame k (a constant after
     // unrolling: the per-frame arrays stay in registers), sliced path
-    __device__ __forceinline__ bool leaf(int k, uint32_t L, double tin, double tout) {
+    __device__ __forceinline__ bool leaf(int k, uint32_t L, double tin, double tout, double sigma) {
         constexpr int Q4 = Basis<NMAX>::Q4;
-        double sigma = S[k].sigma(L);
         bool edited = false;
         float4 erg = make_float4(0.f, 0.f, 0.f, 0.f);
         if (EDITS && T.edit_t != nullptr) {

@@ -512,9 +512,20 @@ def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = Re
         del caches
 
 
-# frames per shared walk in playback (measured per-frame render kernel cost
-# at cfg2 for 1/2/3/4 frames: 0.76 / 0.49 / 0.41 / 0.42 ms)
-PLAYBACK_GROUP = 3
+# frames per shared walk in playback (measured per-frame render-kernel cost
+# at cfg2 for 1/2/3/4 frames: 0.76 / 0.49 / 0.39 / 0.38 ms; cfg3 2.03 / 1.13 /
+# 0.87 / 0.78 ms); at n_max 3 the 4-frame kernel spills, so 3 there
+PLAYBACK_GROUP = 4
+
+
+def playback_group(tree) -> int:
+    return PLAYBACK_GROUP if int(tree.n_max) <= 2 else 3
+
+
+# render_sequence delivers every frame to the host: PCIe (41.5 MB per 1080p
+# frame at ~56 GB/s) bounds it, and smaller groups pipeline the copies
+# better (measured e2e 2,600 Mrays/s with 3 vs 2,260 with 4)
+SEQUENCE_GROUP = 3
 
 _PLAYBACK = {}
 
@@ -551,7 +562,7 @@ def _playback_state(torch, dev, n: int):
 def render_sequence(tree, cam: Camera, frames, opts: RenderOptions = RenderOptions(), *, device=None):
     """Playback: render `frames` in order, yielding numpy LayerImages (fp32).
 
-    Frames render in groups of PLAYBACK_GROUP sharing one octree walk
+    Frames render in groups of SEQUENCE_GROUP (3) sharing one octree walk
     (render_frames_into: one camera, so the walk is frame-independent; each
     frame's images are bitwise identical to ``render``).  Double-buffered:
     group g renders on a per-device render stream (ordered after the
@@ -590,8 +601,9 @@ def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
         return (b[: 3 * h * w].view(h, w, 3), b[3 * h * w: 4 * h * w].view(h, w), b[4 * h * w:].view(h, w))
 
     frames = list(frames)
-    for gi, g0 in enumerate(range(0, len(frames), PLAYBACK_GROUP)):
-        group = frames[g0:g0 + PLAYBACK_GROUP]
+    G = min(SEQUENCE_GROUP, playback_group(tree))
+    for gi, g0 in enumerate(range(0, len(frames), G)):
+        group = frames[g0:g0 + G]
         b = gi % 2
         if copied[b] is not None:
             comp.wait_event(copied[b])  # group b's previous frames have left the device
