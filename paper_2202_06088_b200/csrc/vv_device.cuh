@@ -684,14 +684,24 @@ struct Shader {
                 if (16 * S.rec4 > 128) prefetch_l1(q + 16 * S.rec4 - 1);
             }
         }
+        // software-pipelined: the next segment's sigma is requested before
+        // the current one shades
+        uint32_t L = (uint32_t)seg.leaf_at(0);
+        double sg = is_cached() ? S.sigma(L) : 0.0;
 #pragma unroll 1
         for (int s = 0; s < n; ++s) {
-            const uint32_t L = (uint32_t)seg.leaf_at(s);
-            const double sg = is_cached() ? S.sigma(L) : 0.0;
+            uint32_t Ln = 0;
+            double sgn = 0.0;
+            if (s + 1 < n) {
+                Ln = (uint32_t)seg.leaf_at(s + 1);
+                if (is_cached()) sgn = S.sigma(Ln);
+            }
             if (leaf(L, seg.t0_at(s), seg.t1_at(s), sg)) {
                 if (POPS) pops = seg.pops_at(s);  // the walk may have run ahead
                 return true;
             }
+            L = Ln;
+            sg = sgn;
         }
         return false;
     }
