@@ -571,12 +571,16 @@ __device__ __forceinline__ void slice_col(const float *R, const float *wh, int l
     }
 }
 
-// row loads: read-only global path (__ldg) or plain loads (shared staging)
+// row loads: read-only global path (__ldg) or the shared-memory staging
+// (ld.shared at a 32-bit shared address; volatile keeps it after the
+// mbarrier wait that published the TMA data)
 template <bool G>
 __device__ __forceinline__ float4 ld4(const float4 *p) {
     if (G) return __ldg(p);
     float4 v;
-    asm volatile("ld.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
     return v;
 }
 
