@@ -188,6 +188,32 @@ int vv_render_camera_tiles(const vv_tree *tree, int32_t frame, const vv_slice *c
 int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int32_t tile,
                     int32_t n_shards, float *rgb, float *alpha, float *depth, void *stream);
 
+/* Fused tile render + gather (no all-gather, no unpack): renders this
+ * shard's tiles (same assignment as vv_render_camera_tiles) straight into
+ * the FULL-image planes rgb (H, W, 3), alpha (H, W), depth (H, W); pixels
+ * of other shards' tiles are not touched.  The planes may be another GPU's
+ * memory mapped with vv_ipc_open (the output rank's frame, written over
+ * NVLink/NVSwitch as the tiles finish); `peer` != 0 then makes the kernel
+ * fence its stores system-wide before it retires, so one stream-ordered
+ * barrier after the launch publishes the frame.  Replaces the per-frame
+ * gather of SURVEY.md section 8(e) (the reference has no multi-device
+ * path: it renders frames sequentially, cli.py:189-200). */
+int vv_render_camera_tiles_direct(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                                  const vv_render_opts *opts, const vv_camera *cam, int32_t tile,
+                                  int32_t shard, int32_t n_shards, float *rgb, float *alpha,
+                                  float *depth, int32_t peer, void *stream);
+
+/* CUDA IPC for the planes above: vv_ipc_alloc (output rank) allocates
+ * `bytes` on `device` and returns its VV_IPC_HANDLE_BYTES-byte handle;
+ * the other ranks of the node map it with vv_ipc_open (a different
+ * process; peer access is enabled lazily), unmap with vv_ipc_close; the
+ * owner releases it with vv_ipc_free. */
+#define VV_IPC_HANDLE_BYTES 64
+int vv_ipc_alloc(int32_t device, size_t bytes, void **ptr, unsigned char *handle);
+int vv_ipc_open(int32_t device, const unsigned char *handle, void **ptr);
+int vv_ipc_close(int32_t device, void *ptr);
+int vv_ipc_free(int32_t device, void *ptr);
+
 /* The leaf-decode mode VV_SLICE_AUTO picks for a camera render of this tree
  * (1 = per-frame slice pass, 0 = decode per sample): slice when the leaves
  * number <= 3 x the rays that can reach the tree (its projected footprint). */

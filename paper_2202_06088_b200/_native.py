@@ -63,6 +63,11 @@ EXPORTED_SYMBOLS = (
     "vv_render_camera",
     "vv_render_camera_tiles",
     "vv_unpack_tiles",
+    "vv_render_camera_tiles_direct",
+    "vv_ipc_alloc",
+    "vv_ipc_open",
+    "vv_ipc_close",
+    "vv_ipc_free",
     "vv_render_scene",
     "vv_render_camera_multi",
     "vv_slice_build_multi",
@@ -218,6 +223,15 @@ _SIGNATURES = {
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _I32, _I32, _I32, _P, _P],
     ),
     "vv_unpack_tiles": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "vv_render_camera_tiles_direct": (
+        ctypes.c_int,
+        [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _I32, _I32, _I32, _P, _P, _P,
+         _I32, _P],
+    ),
+    "vv_ipc_alloc": (ctypes.c_int, [_I32, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), _P]),
+    "vv_ipc_open": (ctypes.c_int, [_I32, _P, ctypes.POINTER(ctypes.c_void_p)]),
+    "vv_ipc_close": (ctypes.c_int, [_I32, _P]),
+    "vv_ipc_free": (ctypes.c_int, [_I32, _P]),
     "vv_camera_decode_mode": (ctypes.c_int, [_P, _P, _P, _P]),
     "vv_slice_build_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),

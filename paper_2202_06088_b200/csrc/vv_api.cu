@@ -595,13 +595,13 @@ int vv_render_rays_visits(const vv_tree *t, int32_t frame, const vv_slice *cache
 
 static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *o,
                               const vv_camera *cam, float *rgb, float *alpha, float *depth, float *packed,
-                              int tile, int shard, int n_shards, void *stream) {
+                              int tile, int shard, int n_shards, int peer, void *stream) {
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
     if ((rc = check_cache(t, cache, frame))) return rc;
     if (cam->width <= 0 || cam->height <= 0) return set_error(VV_E_INVALID, "bad camera size");
-    if (packed && (tile <= 0 || tile % 16 != 0 || n_shards < 1 || shard < 0 || shard >= n_shards))
+    if (tile && (tile <= 0 || tile % 16 != 0 || n_shards < 1 || shard < 0 || shard >= n_shards))
         return set_error(VV_E_INVALID, "bad tile arguments (tile must be a positive multiple of 16)");
     DeviceGuard g(t->device);
     const vv_render_opts opts = o ? *o : default_opts();
@@ -623,7 +623,8 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.depth = depth;
     unsigned grid_blocks = 0;
     double share = 1.0;  // fraction of the frame's pixels this call renders
-    if (packed) {
+    p.peer = peer;
+    if (tile) {
         p.packed = packed;
         p.tile = tile;
         p.shard = shard;
@@ -656,7 +657,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
                      const vv_camera *cam, float *rgb, float *alpha, float *depth, void *stream) {
-    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, stream);
+    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream);
 }
 
 int vv_camera_decode_mode(const vv_tree *t, const vv_camera *cam, const vv_render_opts *o, int32_t *mode) {
@@ -710,8 +711,67 @@ int vv_render_camera_tiles(const vv_tree *t, int32_t frame, const vv_slice *cach
                            const vv_camera *cam, int32_t tile, int32_t shard, int32_t n_shards, float *packed,
                            void *stream) {
     if (!packed) return set_error(VV_E_INVALID, "null packed output");
+    if (tile <= 0) return set_error(VV_E_INVALID, "bad tile arguments (tile must be a positive multiple of 16)");
     return render_camera_impl(t, frame, cache, opts, cam, nullptr, nullptr, nullptr, packed, tile, shard, n_shards,
-                              stream);
+                              0, stream);
+}
+
+int vv_render_camera_tiles_direct(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
+                                  const vv_camera *cam, int32_t tile, int32_t shard, int32_t n_shards, float *rgb,
+                                  float *alpha, float *depth, int32_t peer, void *stream) {
+    if (!rgb && !alpha && !depth) return set_error(VV_E_INVALID, "null image planes");
+    if (tile <= 0) return set_error(VV_E_INVALID, "bad tile arguments (tile must be a positive multiple of 16)");
+    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, tile, shard, n_shards,
+                              peer ? 1 : 0, stream);
+}
+
+// ------------------------------------------------------------ CUDA IPC
+// Image planes shared between the ranks of one node: the output rank
+// allocates, every rank maps the handle and stores its tiles over
+// NVLink/NVSwitch.
+int vv_ipc_alloc(int32_t device, size_t bytes, void **ptr, unsigned char *handle) {
+    if (!ptr || !handle || bytes == 0) return set_error(VV_E_INVALID, "bad ipc_alloc arguments");
+    DeviceGuard g(device);
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(VV_E_NOMEM, "cudaMalloc(%zu) failed", bytes);
+    }
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return set_error(VV_E_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == VV_IPC_HANDLE_BYTES, "ipc handle size");
+    memcpy(handle, &h, sizeof(h));
+    *ptr = p;
+    return VV_OK;
+}
+
+int vv_ipc_open(int32_t device, const unsigned char *handle, void **ptr) {
+    if (!ptr || !handle) return set_error(VV_E_INVALID, "bad ipc_open arguments");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(VV_E_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    }
+    return VV_OK;
+}
+
+int vv_ipc_close(int32_t device, void *ptr) {
+    DeviceGuard g(device);
+    if (ptr && cudaIpcCloseMemHandle(ptr) != cudaSuccess) return set_error(VV_E_CUDA, "cudaIpcCloseMemHandle failed");
+    return VV_OK;
+}
+
+int vv_ipc_free(int32_t device, void *ptr) {
+    DeviceGuard g(device);
+    if (ptr && cudaFree(ptr) != cudaSuccess) return set_error(VV_E_CUDA, "cudaFree failed");
+    return VV_OK;
 }
 
 int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int32_t tile, int32_t n_shards,

@@ -92,9 +92,12 @@ struct CamParams {
     int frame;
     double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
     float *rgb, *alpha, *depth;
-    // tile mode (packed != null)
+    // tile mode (tile > 0): this shard's tiles only, written packed (packed
+    // != null) or straight into the image planes above (which may be a peer
+    // GPU's memory mapped through CUDA IPC)
     float *packed;
     int tile, shard, n_shards, tiles_x;
+    int peer;                     // image planes live on another GPU: fence at exit
     int blocks_x;                 // tiles per row (image mode)
 };
 
@@ -113,7 +116,7 @@ constexpr int kTW = 16, kTH = 8, kTileRays = kTW * kTH;
 // this shard's tiles); local ray id -> pixel and output slot
 __device__ __forceinline__ void block_origin(const CamParams &p, int &x0, int &y0, long long &my_tile, int &lx0,
                                              int &ly0) {
-    if (p.packed) {
+    if (p.tile) {
         const int subs_x = p.tile / kTW, subs = subs_x * (p.tile / kTH);
         my_tile = blockIdx.x / subs;
         const int sub = blockIdx.x % subs;
@@ -192,6 +195,9 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __g
         }
         cam_write(p, ix, iy, slot, r, g, b, a, d);
     }
+    // peer stores: make them visible system-wide before the kernel retires
+    // (the caller's stream-ordered barrier then publishes the frame)
+    if (p.peer) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ scene

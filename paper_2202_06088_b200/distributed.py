@@ -9,6 +9,14 @@ NVLink/NVSwitch) of equal-size slabs brings every rank's slab to the
 output rank, where vv_unpack_tiles scatters them into full images.  This is
 the only exchange step per frame.
 
+``mode="p2p"`` fuses the render and the gather instead: the output rank
+allocates the frame's image planes (two slots) with CUDA IPC
+(vv_ipc_alloc), every rank maps them (vv_ipc_open) and its tile kernel
+(vv_render_camera_tiles_direct) stores each finished pixel straight into
+the output rank's planes over NVLink/NVSwitch -- no slab, no all-gather,
+no unpack kernel.  One stream-ordered barrier per frame (a one-element
+NCCL all-reduce, queued after the kernel on every rank) publishes it.
+
 The host-side layout helpers here are also restated in numpy
 (``unpack_tiles_host``) so the CPU test-suite can check the protocol with
 the gloo backend and world_size 2 without a GPU.
@@ -22,7 +30,8 @@ import numpy as np
 
 from . import _native
 
-__all__ = ["tile_grid", "tiles_of", "slab_tiles", "unpack_tiles_host", "pack_tiles_host", "TileRenderer"]
+__all__ = ["tile_grid", "tiles_of", "slab_tiles", "unpack_tiles_host", "pack_tiles_host", "tile_mask_host",
+           "TileRenderer"]
 
 
 def tile_grid(width: int, height: int, tile: int):
@@ -60,6 +69,17 @@ def pack_tiles_host(img5: np.ndarray, rank: int, world: int, tile: int) -> np.nd
     return out
 
 
+def tile_mask_host(rank: int, world: int, width: int, height: int, tile: int) -> np.ndarray:
+    """(H, W) bool: the pixels `rank`'s tiles cover (what the direct tile
+    kernel writes; the ranks' masks partition the image)."""
+    tx, _, _ = tile_grid(width, height, tile)
+    m = np.zeros((height, width), dtype=bool)
+    for tid in tiles_of(rank, world, width, height, tile):
+        x0, y0 = (tid % tx) * tile, (tid // tx) * tile
+        m[y0:y0 + tile, x0:x0 + tile] = True
+    return m
+
+
 def unpack_tiles_host(packed_all: np.ndarray, width: int, height: int, tile: int, world: int) -> np.ndarray:
     """Numpy restatement of vv_unpack_tiles: (world, per, tile*tile, 5) -> (H, W, 5)."""
     tx, _, total = tile_grid(width, height, tile)
@@ -74,23 +94,142 @@ def unpack_tiles_host(packed_all: np.ndarray, width: int, height: int, tile: int
     return out
 
 
+class _Planes:
+    """A raw device allocation seen by torch (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
 class TileRenderer:
-    """Per-rank tile renderer + NCCL gather for one camera size."""
+    """Per-rank tile renderer for one camera size.
+
+    mode="gather": render_slab + gather (NCCL all-gather) + unpack.
+    mode="p2p": render_frame stores this rank's tiles straight into the
+    output rank's image planes (CUDA IPC over NVLink), then one
+    stream-ordered barrier; see the module docstring.
+    """
 
     def __init__(self, width: int, height: int, tile: int = 64, rank: int = 0, world: int = 1, device=None,
-                 group=None):
+                 group=None, mode: str = "gather", out_rank: int = 0):
         import torch
 
         from .device import torch_device
 
         if tile % 16:
             raise ValueError("tile must be a multiple of 16")
+        if mode not in ("gather", "p2p"):
+            raise ValueError(f"mode must be 'gather' or 'p2p', not {mode!r}")
         self.width, self.height, self.tile = int(width), int(height), int(tile)
         self.rank, self.world, self.group = int(rank), int(world), group
+        self.mode, self.out_rank = mode, int(out_rank)
         self.device = torch_device(device)
         self.per = slab_tiles(world, width, height, tile)
-        self.slab = torch.zeros((self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
-        self.all = torch.empty((world, self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
+        if mode == "gather":
+            self.slab = torch.zeros((self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
+            self.all = torch.empty((world, self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
+        else:
+            self._init_p2p(torch)
+
+    # ------------------------------------------------------------ p2p mode
+    def _init_p2p(self, torch):
+        import torch.distributed as dist
+
+        lib, dev = _native.lib(), self.device.index
+        n = 2 * 5 * self.width * self.height  # two frame slots of [rgb | alpha | depth]
+        self._slot = 0
+        self._owned = self._mapped = None
+        handle = (ctypes.c_ubyte * 64)()
+        base = None
+        if self.rank == self.out_rank:
+            ptr = ctypes.c_void_p()
+            _native.check(lib.vv_ipc_alloc(dev, 4 * n, ctypes.byref(ptr), handle))
+            self._owned = base = ptr.value
+        if self.world > 1:
+            obj = [bytes(handle) if self.rank == self.out_rank else None]
+            dist.broadcast_object_list(obj, src=self.out_rank, group=self.group)
+            if self.rank != self.out_rank:
+                ctypes.memmove(handle, obj[0], 64)
+                ptr = ctypes.c_void_p()
+                _native.check(lib.vv_ipc_open(dev, handle, ctypes.byref(ptr)))
+                self._mapped = base = ptr.value
+            self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._base = base
+        self.planes = None
+        if self.rank == self.out_rank:
+            self.planes = torch.as_tensor(_Planes(base, n), device=self.device).view(2, -1)
+
+    def _slot_ptrs(self, slot):
+        hw = self.width * self.height
+        base = self._base + slot * 5 * hw * 4
+        return base, base + 3 * hw * 4, base + 4 * hw * 4
+
+    def _views(self, slot):
+        from .render import LayerImages
+
+        h, w = self.height, self.width
+        b = self.planes[slot]
+        return LayerImages(b[: 3 * h * w].view(h, w, 3), b[3 * h * w: 4 * h * w].view(h, w), b[4 * h * w:].view(h, w))
+
+    def barrier(self):
+        """Stream-ordered on NCCL (a one-element all-reduce queued after the
+        tile kernel); host-synchronous on gloo (functional runs)."""
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def render_frame(self, tree, cam, frame, opts=None, cache=None):
+        """p2p mode: render this rank's tiles of `frame` into the output
+        rank's planes and publish them.  On the output rank returns device
+        LayerImages views of the frame's slot (valid until the render_frame
+        call after next: two slots); None elsewhere."""
+        from .device import replica, stream_ptr
+        from .render import RenderOptions, _check_cache
+
+        if self.mode != "p2p":
+            raise RuntimeError("render_frame needs mode='p2p' (gather mode: render_slab/gather/unpack)")
+        if (int(cam.width), int(cam.height)) != (self.width, self.height):
+            raise ValueError(f"camera is {cam.width}x{cam.height}, renderer {self.width}x{self.height}")
+        opts = opts or RenderOptions()
+        rep = replica(tree, self.device)
+        ch = _check_cache(cache, int(frame), rep)
+        oc = opts.c_struct()
+        cd = cam.desc()
+        slot = self._slot
+        self._slot ^= 1
+        rgb, alpha, depth = self._slot_ptrs(slot)
+        _native.check(_native.lib().vv_render_camera_tiles_direct(
+            rep.handle, int(frame), ch, ctypes.byref(oc), ctypes.byref(cd), self.tile, self.rank, self.world,
+            rgb, alpha, depth, int(self.rank != self.out_rank), stream_ptr(self.device)))
+        self.barrier()
+        return self._views(slot) if self.rank == self.out_rank else None
+
+    def close(self):
+        """Unmap / free the IPC planes (p2p mode).  Call on every rank once
+        no rank will render into them again."""
+        if self.mode != "p2p":
+            return
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        lib, dev = _native.lib(), self.device.index
+        self.planes = None
+        if self._mapped:
+            _native.check(lib.vv_ipc_close(dev, self._mapped))
+            self._mapped = None
+        if self._owned:
+            _native.check(lib.vv_ipc_free(dev, self._owned))
+            self._owned = None
+
+    # --------------------------------------------------------- gather mode
 
     def render_slab(self, tree, cam, frame, opts=None, cache=None):
         """Render this rank's tiles into self.slab (async on the current stream)."""

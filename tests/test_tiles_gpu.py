@@ -1,0 +1,142 @@
+"""Multi-GPU tile paths on one GPU.
+
+* packed tiles (vv_render_camera_tiles) of every shard, gathered shard-major
+  and scattered by vv_unpack_tiles, reproduce render() bitwise;
+* the fused direct form (vv_render_camera_tiles_direct) writes exactly its
+  shard's pixels of the full image, bitwise equal to render(), and leaves
+  every other pixel untouched;
+* TileRenderer(mode="p2p") end to end with two processes on this GPU (gloo
+  for the handle exchange and the barrier): rank 1 maps rank 0's planes
+  through CUDA IPC and stores its tiles there; rank 0's frame equals
+  render().  Two ranks sharing one GPU only check the plumbing: the peer
+  stores go through the same device's memory, no kernel waits on another.
+"""
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2202_06088_b200 as vv
+from paper_2202_06088_b200 import synthetic
+from paper_2202_06088_b200.distributed import TileRenderer, tile_mask_host
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+W, H, TILE = 208, 144, 64  # ragged: the last tile column/row is partial
+
+
+def _tree():
+    return synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=3)
+
+
+def _np(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def _eq(a, b, what):
+    a, b = _np(a), _np(b)
+    assert a.shape == b.shape, what
+    assert np.array_equal(a, b, equal_nan=False), f"{what}: {np.count_nonzero(a != b)} mismatches"
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_packed_tiles_gather_unpack_bitwise(cuda, world):
+    import torch
+
+    tree, cam = _tree(), synthetic.bench_camera(W, H)
+    ref = vv.render(tree, cam, 5)
+    slabs = []
+    for s in range(world):
+        tr = TileRenderer(W, H, TILE, rank=s, world=world, device=cuda)
+        slabs.append(tr.render_slab(tree, cam, 5).clone())
+    tr.all.copy_(torch.stack(slabs))
+    rgb = torch.full((H, W, 3), float("nan"), device=cuda)
+    alpha = torch.full((H, W), float("nan"), device=cuda)
+    depth = torch.full((H, W), float("nan"), device=cuda)
+    tr.unpack(rgb, alpha, depth)
+    torch.cuda.synchronize()
+    _eq(rgb, ref.rgb, "rgb")
+    _eq(alpha, ref.alpha, "alpha")
+    _eq(depth, ref.depth, "depth")
+
+
+def test_direct_tiles_write_only_their_shard(cuda):
+    import ctypes
+
+    import torch
+
+    from paper_2202_06088_b200 import _native
+    from paper_2202_06088_b200.device import replica, stream_ptr
+
+    tree, cam = _tree(), synthetic.bench_camera(W, H)
+    ref = vv.render(tree, cam, 2)
+    rep = replica(tree, cuda)
+    rgb = torch.full((H, W, 3), float("nan"), device=cuda)
+    alpha = torch.full((H, W), float("nan"), device=cuda)
+    depth = torch.full((H, W), float("nan"), device=cuda)
+    oc, cd = vv.RenderOptions().c_struct(), cam.desc()
+    world = 3
+    covered = np.zeros((H, W), dtype=bool)
+    for s in range(world):
+        _native.check(_native.lib().vv_render_camera_tiles_direct(
+            rep.handle, 2, None, ctypes.byref(oc), ctypes.byref(cd), TILE, s, world, rgb.data_ptr(),
+            alpha.data_ptr(), depth.data_ptr(), 0, stream_ptr(cuda)))
+        torch.cuda.synchronize()
+        covered |= tile_mask_host(s, world, W, H, TILE)
+        a = _np(alpha)
+        assert np.array_equal(np.isnan(a), ~covered), f"shard {s} wrote outside its tiles"
+        _eq(a[covered], _np(ref.alpha)[covered], f"alpha after shard {s}")
+    assert covered.all()
+    _eq(rgb, ref.rgb, "rgb")
+    _eq(depth, ref.depth, "depth")
+    with pytest.raises(ValueError):  # tile not a multiple of 16
+        _native.check(_native.lib().vv_render_camera_tiles_direct(
+            rep.handle, 2, None, ctypes.byref(oc), ctypes.byref(cd), 24, 0, 1, rgb.data_ptr(), None, None, 0,
+            stream_ptr(cuda)))
+
+
+def test_p2p_renderer_world1(cuda):
+    tree, cam = _tree(), synthetic.bench_camera(W, H)
+    tr = TileRenderer(W, H, TILE, rank=0, world=1, device=cuda, mode="p2p")
+    try:
+        for f in (1, 4, 6):  # alternating slots
+            out = tr.render_frame(tree, cam, f)
+            ref = vv.render(tree, cam, f)
+            _eq(out.rgb, ref.rgb, f"rgb frame {f}")
+            _eq(out.alpha, ref.alpha, f"alpha frame {f}")
+            _eq(out.depth, ref.depth, f"depth frame {f}")
+        with pytest.raises(ValueError):
+            tr.render_frame(tree, synthetic.bench_camera(W + 16, H), 0)
+    finally:
+        tr.close()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_p2p_renderer_two_processes_ipc(cuda):
+    port = _free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   PYTHONPATH=str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        procs.append(subprocess.Popen([sys.executable, str(ROOT / "tests" / "p2p_worker.py")], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=300)[0])
+        except subprocess.TimeoutExpired:
+            p.kill()
+            outs.append(p.communicate()[0])
+    for r, (p, o) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0, f"rank {r} failed:\n{o[-3000:]}"
+    assert "P2P_OK" in outs[0], outs[0][-2000:]
