@@ -110,7 +110,15 @@ __device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
 
 // Block work unit: a kTW x kTH pixel tile (one ray per thread); warps take
 // VV_CHUNK_W-wide chunks of it.
-constexpr int kTW = 16, kTH = 8, kTileRays = kTW * kTH;
+#ifndef VV_CHUNK_W
+#define VV_CHUNK_W 8  // warp chunk = VV_CHUNK_W x (32 / VV_CHUNK_W) pixels
+#endif
+#ifndef VV_CAM_TH
+#define VV_CAM_TH 8  // camera block = 16 x VV_CAM_TH pixels, one thread each
+#endif
+constexpr int kTW = 16, kTH = VV_CAM_TH, kTileRays = kTW * kTH;
+constexpr int kCamMinBlocks = VV_CAM_MINB * kBlock / kTileRays;  // same warps per SM for any tile height
+static_assert(kTileRays % 32 == 0 && kTH % (32 / VV_CHUNK_W) == 0, "camera tile must hold whole warp chunks");
 
 // block -> tile origin (image mode: row-major tiles; tile mode: sub-tiles of
 // this shard's tiles); local ray id -> pixel and output slot
@@ -133,9 +141,6 @@ __device__ __forceinline__ void block_origin(const CamParams &p, int &x0, int &y
     }
 }
 
-#ifndef VV_CHUNK_W
-#define VV_CHUNK_W 8  // warp chunk = VV_CHUNK_W x (32 / VV_CHUNK_W) pixels
-#endif
 __device__ __forceinline__ void local_pixel(int rid, int &dx, int &dy) {
     constexpr int CW = VV_CHUNK_W, CH = 32 / VV_CHUNK_W;
     const int chunk = rid >> 5, l = rid & 31;
@@ -165,7 +170,7 @@ __device__ __forceinline__ void cam_write(const CamParams &p, int ix, int iy, lo
 // pixels (L1 reuse of node rows and slice rows).  Refill-on-finish
 // (persistent) variants were measured slower: see DESIGN.md.
 template <int NMAX, int CACHED, bool EDITS, class Entry>
-__global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __grid_constant__ CamParams p) {
+__global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(const __grid_constant__ CamParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxC], sB[kMaxC];
     load_rows(p.T, p.frame, sA, sB);
@@ -174,9 +179,8 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera(const __g
     long long my_tile;
     block_origin(p, x0, y0, my_tile, lx0, ly0);
     FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
-#pragma unroll 1
-    for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
-        const int rid = pass * kBlock + (int)threadIdx.x;
+    {
+        const int rid = (int)threadIdx.x;  // blockDim.x == kTileRays
         int dx_, dy_;
         local_pixel(rid, dx_, dy_);
         const int ix = x0 + dx_, iy = y0 + dy_;
@@ -335,17 +339,16 @@ struct CamMultiParams {
 };
 
 template <int NMAX, int KF, bool EDITS, class Entry>
-__global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
+__global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int bx = blockIdx.x % p.blocks_x, by = blockIdx.x / p.blocks_x;
     const int x0 = bx * kTW, y0 = by * kTH;
-#pragma unroll 1
-    for (int pass = 0; pass < kTileRays / kBlock; ++pass) {
-        const int rid = pass * kBlock + (int)threadIdx.x;
+    {
+        const int rid = (int)threadIdx.x;  // blockDim.x == kTileRays
         int dx_, dy_;
         local_pixel(rid, dx_, dy_);
         const int ix = x0 + dx_, iy = y0 + dy_;
-        if (ix >= p.cam.width || iy >= p.cam.height) continue;
+        if (ix >= p.cam.width || iy >= p.cam.height) return;
         double dx, dy, dz;
         camera_ray(p.cam, ix, iy, dx, dy, dz);
         ShaderMulti<NMAX, KF, EDITS> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
@@ -619,8 +622,8 @@ inline int with_nmax(int nmax, F &&f) {
 
 // traversal shared memory per block: segment queues + stacks (traverse());
 // pops: the visitor queues node-visit counts (k_render_rays)
-inline size_t stack_bytes(int depth, bool wide, bool pops = false) {
-    return (size_t)kBlock *
+inline size_t stack_bytes(int depth, bool wide, bool pops = false, int threads = kBlock) {
+    return (size_t)threads *
            (seg_bytes_per_thread(pops) + (size_t)stack_cap(depth) * (wide ? EntryW::kBytes : EntryN::kBytes));
 }
 

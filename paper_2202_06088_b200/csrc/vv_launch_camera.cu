@@ -8,7 +8,7 @@ static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t
     auto kern = k_render_camera<NM, CACHED, EDITS, Entry>;
     int r = prep_smem(kern, smem);
     if (r) return r;
-    kern<<<max_blocks, kBlock, smem, st>>>(p);
+    kern<<<max_blocks, kTileRays, smem, st>>>(p);
     return check_launch("render_camera");
 }
 
@@ -25,7 +25,7 @@ static int pick(int mode, bool edits, const CamParams &p, unsigned grid, size_t 
 
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned grid, size_t smem,
                   cudaStream_t st) {
-    smem = stack_bytes(p.T.depth, wide);  // this TU's queue geometry (A/B builds vary it)
+    smem = stack_bytes(p.T.depth, wide, false, kTileRays);  // this TU's queue geometry (A/B builds vary it)
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
         return wide ? pick<NM, EntryW>(mode, edits, p, grid, smem, st) : pick<NM, EntryN>(mode, edits, p, grid, smem, st);

@@ -7,10 +7,10 @@ namespace vvk {
 template <int NM, int KF, bool EDITS, class Entry>
 static int go(const CamMultiParams &p, unsigned grid, cudaStream_t st) {
     auto kern = k_render_camera_multi<NM, KF, EDITS, Entry>;
-    const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes);
+    const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes, false, kTileRays);
     int r = prep_smem(kern, smem);
     if (r) return r;
-    kern<<<grid, kBlock, smem, st>>>(p);
+    kern<<<grid, kTileRays, smem, st>>>(p);
     return check_launch("render_camera_multi");
 }
 
