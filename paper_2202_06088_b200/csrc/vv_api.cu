@@ -34,7 +34,7 @@ struct vv_tree {
     int64_t bytes;
     // owned device allocations
     int32_t *d_child;
-    float4 *d_sig, *d_rest, *d_edit_rgb;
+    float4 *d_sig, *d_gam, *d_hh, *d_edit_rgb;
     int2 *d_edit_t;
     float *d_a, *d_b;
 };
@@ -281,9 +281,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     t->has_edits = d->edit_rgb != nullptr;
     const int C = t->C, K3 = 3 * t->K;
     const int P = 2 * C + K3;
-    const int sig4 = (C + 3) / 4;
-    const int hh_off4 = (C + 3) / 4;
-    const int rest4 = hh_off4 + (K3 + 3) / 4;
+    const int c4 = (C + 3) / 4;      // float4 chunks of w_sigma / w_gamma
+    const int hh4 = (K3 + 3) / 4;    // float4 per w_hh row
     const int64_t nl = d->n_leaves, nrows = std::max<int64_t>(nl, 1);
     auto fail = [&](int rc) {
         vv_tree_free(t);
@@ -301,8 +300,9 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     int rc;
     const size_t child_b = (size_t)d->n_internal * 8 * sizeof(int32_t);
     if ((rc = alloc((void **)&t->d_child, child_b))) return fail(rc);
-    if ((rc = alloc((void **)&t->d_sig, (size_t)nrows * sig4 * sizeof(float4)))) return fail(rc);
-    if ((rc = alloc((void **)&t->d_rest, (size_t)nrows * rest4 * sizeof(float4)))) return fail(rc);
+    if ((rc = alloc((void **)&t->d_sig, (size_t)nrows * c4 * sizeof(float4)))) return fail(rc);
+    if ((rc = alloc((void **)&t->d_gam, (size_t)nrows * c4 * sizeof(float4)))) return fail(rc);
+    if ((rc = alloc((void **)&t->d_hh, (size_t)nrows * hh4 * sizeof(float4)))) return fail(rc);
     const size_t ab = (size_t)d->frames * C * sizeof(float);
     if ((rc = alloc((void **)&t->d_a, ab))) return fail(rc);
     if ((rc = alloc((void **)&t->d_b, ab))) return fail(rc);
@@ -341,9 +341,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
                 }
                 src = stage;
             }
-            const int lrc = launch_repack(src, rows, (int)stride, C, K3, sig4, rest4, hh_off4,
-                                          reinterpret_cast<float *>(t->d_sig + r0 * sig4),
-                                          reinterpret_cast<float *>(t->d_rest + r0 * rest4), nullptr);
+            const int lrc = launch_repack(src, rows, (int)stride, C, K3, c4, hh4, nrows, r0, t->d_sig, t->d_gam,
+                                          t->d_hh, nullptr);
             if (lrc) {
                 if (stage) cudaFree(stage);
                 return fail(lrc);
@@ -356,7 +355,9 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     TreeView &v = t->view;
     v.child = t->d_child;
     v.sig = t->d_sig;
-    v.rest = t->d_rest;
+    v.gam = t->d_gam;
+    v.hh = t->d_hh;
+    v.lstride = nrows;
     v.edit_rgb = t->d_edit_rgb;
     v.edit_t = t->d_edit_t;
     v.basis_a = t->d_a;
@@ -367,9 +368,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     v.side = d->side;
     v.depth = d->depth;
     v.C = C;
-    v.sig4 = sig4;
-    v.rest4 = rest4;
-    v.hh_off4 = hh_off4;
+    v.c4 = c4;
+    v.hh4 = hh4;
     v.frames = d->frames;
     v.nmax = d->n_max;
     *out = t;
@@ -403,7 +403,8 @@ int vv_tree_free(vv_tree *t) {
     DeviceGuard g(t->device);
     cudaFree(t->d_child);
     cudaFree(t->d_sig);
-    cudaFree(t->d_rest);
+    cudaFree(t->d_gam);
+    cudaFree(t->d_hh);
     cudaFree(t->d_edit_rgb);
     cudaFree(t->d_edit_t);
     cudaFree(t->d_a);

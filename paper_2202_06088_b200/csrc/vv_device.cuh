@@ -50,15 +50,32 @@ struct Consts {
 // Device view of one uploaded tree.
 struct TreeView {
     const int32_t *child;    // (n_internal, 8)
-    const float4 *sig;       // (n_leaves, sig4): w_sigma padded
-    const float4 *rest;      // (n_leaves, rest4): [w_gamma pad | w_hh pad]
+    // w_sigma / w_gamma chunk-major: float4 chunk j (columns 4j..4j+3, zero
+    // padded) of leaf L at [j * lstride + L] -- a frame whose A (B) row is
+    // zero over a chunk never reads it, and the chunks it does read are
+    // contiguous over consecutive leaves
+    const float4 *sig;       // (c4, lstride)
+    const float4 *gam;       // (c4, lstride)
+    const float4 *hh;        // (n_leaves, hh4): w_hh padded, row-major
     const float4 *edit_rgb;  // (n_leaves) or null
     const int2 *edit_t;      // (n_leaves) or null
     const float *basis_a;    // (T, C)
     const float *basis_b;    // (T, C)
     double lo0, lo1, lo2, side;
-    int depth, C, sig4, rest4, hh_off4, frames, nmax;
+    int64_t lstride;         // leaf rows per chunk plane (>= n_leaves)
+    int depth, C, c4, hh4, frames, nmax;
 };
+
+// Bit j set when the basis row (fp32, C columns) has a nonzero entry among
+// columns 4j..4j+3.  The sigma / gamma sums skip the other chunks: their
+// products are +-0, and adding +-0 to an accumulator that starts at +0 and
+// so is never -0 leaves it bit-identical (finite payloads).
+__device__ __forceinline__ uint32_t nz_chunks(const float *row, int C) {
+    uint32_t m = 0;
+    for (int c = 0; c < C; ++c)
+        if (row[c] != 0.0f) m |= 1u << (c >> 2);
+    return m;
+}
 
 // Per-frame slice: one record per leaf, [q (3S fp32) | pad | sigma (f64)],
 // rec4 float4 long -- 128 bytes (one cache line) at n_max = 2.
@@ -584,14 +601,15 @@ __device__ __forceinline__ float4 ld4(const float4 *p) {
     return v;
 }
 
-// Decoded fp32 hyper-angle sigmoid s = sigmoid(B[t] . w_gamma) (fp32 dot).
+// Decoded fp32 hyper-angle sigmoid s = sigmoid(B[t] . w_gamma) (fp32 dot)
+// over the chunks in `mask` (nz_chunks of B[t]); chunk i at g[i * cs].
 template <bool G = true>
-__device__ __forceinline__ float gamma_s(const float4 *__restrict__ rest_row, const float *sB, int C) {
+__device__ __forceinline__ float gamma_s(const float4 *__restrict__ g, int64_t cs, const float *sB, int C,
+                                         uint32_t mask) {
     float gp = 0.0f;
-    const int C4 = (C + 3) >> 2;
-#pragma unroll 4
-    for (int i = 0; i < C4; ++i) {
-        const float4 v = ld4<G>(rest_row + i);
+    for (uint32_t m = mask; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const float4 v = ld4<G>(g + i * cs);
         const int c = 4 * i;
         gp = __fmaf_rn(sB[c], v.x, gp);
         if (c + 1 < C) gp = __fmaf_rn(sB[c + 1], v.y, gp);
@@ -601,14 +619,15 @@ __device__ __forceinline__ float gamma_s(const float4 *__restrict__ rest_row, co
     return sigmoidf_(gp);
 }
 
-// sigma_pre = sum_c A[t,c] * w_sigma[c], float64, sequential (kernels.py:374-381)
+// sigma_pre = sum_c A[t,c] * w_sigma[c], float64, sequential (kernels.py:374-381),
+// over the chunks in `mask` (nz_chunks of A[t]); chunk i at w[i * cs].
 template <bool G = true>
-__device__ __forceinline__ double sigma_pre(const float4 *__restrict__ sig_row, const float *sA, int C) {
+__device__ __forceinline__ double sigma_pre(const float4 *__restrict__ w, int64_t cs, const float *sA, int C,
+                                            uint32_t mask) {
     double sp = 0.0;
-    const int C4 = (C + 3) >> 2;
-#pragma unroll 4
-    for (int i = 0; i < C4; ++i) {
-        const float4 v = ld4<G>(sig_row + i);
+    for (uint32_t m = mask; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const float4 v = ld4<G>(w + i * cs);
         const int c = 4 * i;
         sp = xadd(sp, xmul((double)sA[c], (double)v.x));
         if (c + 1 < C) sp = xadd(sp, xmul((double)sA[c + 1], (double)v.y));
@@ -619,11 +638,11 @@ __device__ __forceinline__ double sigma_pre(const float4 *__restrict__ sig_row, 
 }
 
 template <int NMAX, bool G = true>
-__device__ __forceinline__ void load_hh(const float4 *__restrict__ rest_row, int hh_off4, float *wh) {
+__device__ __forceinline__ void load_hh(const float4 *__restrict__ hh_row, float *wh) {
     constexpr int H4 = Basis<NMAX>::HH4;
 #pragma unroll
     for (int i = 0; i < H4; ++i) {
-        const float4 v = ld4<G>(rest_row + hh_off4 + i);
+        const float4 v = ld4<G>(hh_row + i);
         wh[4 * i + 0] = v.x;
         wh[4 * i + 1] = v.y;
         wh[4 * i + 2] = v.z;
@@ -638,6 +657,7 @@ struct FrameCtx {
     int frame;
     double early_stop;
     double edit_weight;
+    uint32_t mA, mB;   // nz_chunks of the two rows
 };
 
 // CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
@@ -721,7 +741,7 @@ struct Shader {
         if (from_rec) {
             sigma = sigma_cached;
         } else {
-            const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, F.sA, T.C);
+            const double sp = sigma_pre(T.sig + L, T.lstride, F.sA, T.C, F.mA);
             sigma = sp > 0.0 ? sp : 0.0;
         }
         bool edited = false;
@@ -761,12 +781,11 @@ struct Shader {
                 c2 = __fmaf_rn(y[j], q[3 * j + 2], c2);
             }
         } else {
-            const float4 *rr = T.rest + (size_t)L * T.rest4;
-            const float s = gamma_s(rr, F.sB, T.C);
+            const float s = gamma_s(T.gam + L, T.lstride, F.sB, T.C, F.mB);
             float R[Basis<NMAX>::NPAIRS];
             radial<NMAX>(s, K, R);
             float wh[4 * Basis<NMAX>::HH4];
-            load_hh<NMAX>(rr, T.hh_off4, wh);
+            load_hh<NMAX>(T.hh + (size_t)L * T.hh4, wh);
 #pragma unroll
             for (int l = 0; l <= NMAX; ++l)
 #pragma unroll

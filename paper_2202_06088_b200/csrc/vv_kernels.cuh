@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_rays(const __gri
     if (r >= p.n) return;
     const double ox = p.origins[3 * r], oy = p.origins[3 * r + 1], oz = p.origins[3 * r + 2];
     const double dx = p.dirs[3 * r], dy = p.dirs[3 * r + 1], dz = p.dirs[3 * r + 2];
-    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
+    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight, nz_chunks(sA, p.T.C), nz_chunks(sB, p.T.C)};
     Shader<NMAX, CACHED, EDITS, VISITS, true> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
     if (VISITS) sh.visit = p.visit_leaf + p.visit_start[r];
     Ray ray;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
     int x0, y0, lx0, ly0;
     long long my_tile;
     block_origin(p, x0, y0, my_tile, lx0, ly0);
-    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight};
+    FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight, nz_chunks(sA, p.T.C), nz_chunks(sB, p.T.C)};
     {
         const int rid = (int)threadIdx.x;  // blockDim.x == kTileRays
         int dx_, dy_;
@@ -228,7 +228,13 @@ template <int NMAX, class Entry>
 __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__ SceneParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
+    __shared__ uint32_t sM[kMaxInst][2];
     for (int i = 0; i < p.n_inst; ++i) load_rows(p.inst[i].T, p.inst[i].frame, sA[i], sB[i]);
+    __syncthreads();
+    if ((int)threadIdx.x < p.n_inst) {
+        sM[threadIdx.x][0] = nz_chunks(sA[threadIdx.x], p.inst[threadIdx.x].T.C);
+        sM[threadIdx.x][1] = nz_chunks(sB[threadIdx.x], p.inst[threadIdx.x].T.C);
+    }
     __syncthreads();
     int ix, iy;
     block_pixel(blockIdx.x, blockIdx.y, ix, iy);
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
             scale = xdiv(1.0, nrm);
             scaled = true;
         }
-        FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight};
+        FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight, sM[i][0], sM[i][1]};
         Shader<NMAX, 2, true, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
         Ray ray;
         if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
@@ -385,22 +391,24 @@ struct SliceParams {
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps, each owning a
-// double-buffered shared-memory stage: one lane issues two TMA bulk copies
-// (cp.async.bulk, completed on an mbarrier) per chunk of 32 consecutive
-// leaves -- their w_sigma rows and their [w_gamma | w_hh] rows are
-// contiguous in HBM -- while the warp slices the previous chunk, one leaf
-// per lane, from shared memory.  Rows reach shared memory without
-// touching registers or the L1 wavefront path that bounds per-thread row
-// loads; the next chunk streams in during the fp64 sigma chains.
+// double-buffered shared-memory stage: one lane issues TMA bulk copies
+// (cp.async.bulk, completed on an mbarrier) for a chunk of 32 consecutive
+// leaves -- one per w_sigma / w_gamma float4 chunk the group's A / B rows do
+// not zero out (chunk-major planes: 512 contiguous bytes each) and one for
+// their w_hh rows -- while the warp slices the previous chunk, one leaf per
+// lane, from shared memory.  Chunks whose basis entries are all zero are
+// never read: their products are +-0 and the sums skip them bit-exactly
+// (nz_chunks).  Rows reach shared memory without touching registers; the
+// next chunk streams in during the fp64 sigma chains.
 constexpr int kSliceWarps = 4;
 constexpr int kSliceChunk = 32;
 
-__host__ __device__ inline size_t slice_stage_floats4(int sig4, int rest4) {
-    return (size_t)kSliceChunk * (sig4 + rest4);
+__host__ __device__ inline size_t slice_stage_floats4(int c4, int hh4) {
+    return (size_t)kSliceChunk * (2 * c4 + hh4);  // worst case: every w_sigma / w_gamma chunk needed
 }
-__host__ __device__ inline size_t slice_smem_bytes(int sig4, int rest4) {
+__host__ __device__ inline size_t slice_smem_bytes(int c4, int hh4) {
     // per warp: 2 stages + 2 mbarriers (16 B)
-    return (size_t)kSliceWarps * (2 * slice_stage_floats4(sig4, rest4) * 16 + 16);
+    return (size_t)kSliceWarps * (2 * slice_stage_floats4(c4, hh4) * 16 + 16);
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
@@ -413,9 +421,10 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
     __shared__ double dA[KF][kMaxC];  // A rows widened once (the values sigma_pre multiplies)
+    __shared__ uint32_t sMask[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sig4 = p.T.sig4, rest4 = p.T.rest4;
-    const size_t stage4 = slice_stage_floats4(sig4, rest4);
+    const int hh4 = p.T.hh4;
+    const size_t stage4 = slice_stage_floats4(p.T.c4, hh4);
     float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 1);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
     if (lane == 0) {
@@ -427,19 +436,35 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     for (int f = 0; f < KF; ++f) load_rows(p.T, p.frame[f], sA[f], sB[f]);
     __syncthreads();
     for (int i = threadIdx.x; i < KF * kMaxC; i += blockDim.x) dA[i / kMaxC][i % kMaxC] = (double)sA[i / kMaxC][i % kMaxC];
+    if (threadIdx.x == 0) {  // chunks any frame of the group needs (zero chunks are never read)
+        uint32_t ms = 0, mg = 0;
+        for (int f = 0; f < KF; ++f) {
+            ms |= nz_chunks(sA[f], p.T.C);
+            mg |= nz_chunks(sB[f], p.T.C);
+        }
+        sMask[0] = ms;
+        sMask[1] = mg;
+    }
     __syncthreads();
-    const int C = p.T.C, C4 = (C + 3) >> 2;
+    const uint32_t mS = sMask[0], mG = sMask[1];
+    const int nS = __popc(mS), nG = __popc(mG);
+    const int C = p.T.C;
+    const int64_t ls = p.T.lstride;
     const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
     const int64_t wstride = (int64_t)gridDim.x * kSliceWarps;
     const int64_t c0 = (int64_t)blockIdx.x * kSliceWarps + warp;
+    // stage: [needed w_sigma chunks][32 leaves] | [needed w_gamma chunks][32] | [32 leaves][hh4]
     auto issue = [&](int64_t c, int stg) {
         const int64_t base = c * kSliceChunk;
         const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
         float4 *dst = wbase + stg * stage4;
-        const uint32_t sb = (uint32_t)rows * sig4 * 16, rb = (uint32_t)rows * rest4 * 16;
-        mbar_expect_tx(&bar[stg], sb + rb);
-        bulk_g2s(dst, p.T.sig + base * sig4, sb, &bar[stg]);
-        bulk_g2s(dst + (size_t)kSliceChunk * sig4, p.T.rest + base * rest4, rb, &bar[stg]);
+        const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
+        mbar_expect_tx(&bar[stg], (uint32_t)(nS + nG) * cb + hb);
+        for (uint32_t m = mS; m; m &= m - 1, dst += kSliceChunk)
+            bulk_g2s(dst, p.T.sig + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
+        for (uint32_t m = mG; m; m &= m - 1, dst += kSliceChunk)
+            bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
+        bulk_g2s(dst, p.T.hh + base * hh4, hb, &bar[stg]);
     };
     if (lane == 0) {
         if (c0 < n_chunks) issue(c0, 0);
@@ -452,11 +477,10 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kSliceChunk;
         const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
-        const float4 *ssig = wbase + stg * stage4 + lane * sig4;
-        const float4 *srest = wbase + stg * stage4 + (size_t)kSliceChunk * sig4 + lane * rest4;
+        const float4 *sv = wbase + stg * stage4 + lane;
         if (lane < rows) {
             // sigma_pre (kernels.py:374-381, f64, sequential) and the gamma dot
-            // (fp32), every frame at once
+            // (fp32), every frame at once, over the needed chunks in column order
             double sp[KF];
             float gp[KF];
 #pragma unroll
@@ -464,25 +488,33 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 sp[f] = 0.0;
                 gp[f] = 0.0f;
             }
-#pragma unroll 2
-            for (int i = 0; i < C4; ++i) {
-                const float4 v = ld4<false>(ssig + i), g = ld4<false>(srest + i);
+            for (uint32_t m = mS; m; m &= m - 1, sv += kSliceChunk) {
+                const float4 v = ld4<false>(sv);
                 const double w[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
-                const float gw[4] = {g.x, g.y, g.z, g.w};
-                const int cc = 4 * i;
+                const int cc = 4 * (__ffs(m) - 1);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     if (cc + e < C) {
 #pragma unroll
-                        for (int f = 0; f < KF; ++f) {
-                            sp[f] = xadd(sp[f], xmul(dA[f][cc + e], w[e]));
-                            gp[f] = __fmaf_rn(sB[f][cc + e], gw[e], gp[f]);
-                        }
+                        for (int f = 0; f < KF; ++f) sp[f] = xadd(sp[f], xmul(dA[f][cc + e], w[e]));
                     }
                 }
             }
+            for (uint32_t m = mG; m; m &= m - 1, sv += kSliceChunk) {
+                const float4 g = ld4<false>(sv);
+                const float gw[4] = {g.x, g.y, g.z, g.w};
+                const int cc = 4 * (__ffs(m) - 1);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (cc + e < C) {
+#pragma unroll
+                        for (int f = 0; f < KF; ++f) gp[f] = __fmaf_rn(sB[f][cc + e], gw[e], gp[f]);
+                    }
+                }
+            }
+            const float4 *shh = wbase + stg * stage4 + (size_t)(nS + nG) * kSliceChunk + (size_t)lane * hh4;
             float wh[4 * Basis<NMAX>::HH4];
-            load_hh<NMAX, false>(srest, p.T.hh_off4, wh);
+            load_hh<NMAX, false>(shh, wh);
 #pragma unroll
             for (int f = 0; f < KF; ++f) {
                 float q[4 * R4];
@@ -567,16 +599,17 @@ struct TerminateVisitor {
     const TreeView &T;
     const float *sA;
     double norm, thr;
+    uint32_t mA;
     double acc = 0.0, trans = 1.0;
     int64_t hit = -1;
     __device__ __forceinline__ TerminateVisitor(const TreeView &T_, const float *sA_, double norm_, double thr_)
-        : T(T_), sA(sA_), norm(norm_), thr(thr_) {}
+        : T(T_), sA(sA_), norm(norm_), thr(thr_), mA(nz_chunks(sA_, T_.C)) {}
     __device__ __forceinline__ void pop() {}
     __device__ __forceinline__ int pop_count() const { return 0; }
     __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
         for (int s = 0; s < n; ++s) {
             const uint32_t L = (uint32_t)seg.leaf_at(s);
-            const double sp = sigma_pre(T.sig + (size_t)L * T.sig4, sA, T.C);
+            const double sp = sigma_pre(T.sig + L, T.lstride, sA, T.C, mA);
             const double sigma = sp > 0.0 ? sp : 0.0;
             const double delta = xmul(xsub(seg.t1_at(s), seg.t0_at(s)), norm);
             const double a = xsub(1.0, exp(xmul(-sigma, delta)));
@@ -689,8 +722,8 @@ struct LightView {  // vv_light (include/voxvid_b200.h)
 };
 int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha, const float *depth, double bg0,
                        double bg1, double bg2, const LightView *lights, int n_lights, float *image, cudaStream_t st);
-int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
-                  float *rest, cudaStream_t st);
+int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int c4, int hh4, int64_t lstride,
+                  int64_t r0, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st);
 int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,
                   float *rgb, float *alpha, float *depth, cudaStream_t st);
 

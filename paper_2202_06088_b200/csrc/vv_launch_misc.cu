@@ -24,25 +24,31 @@ __global__ void k_unpack_tiles(const float *__restrict__ packed, int width, int 
 }
 
 // ------------------------------------------------------------------ repack
-// leaf rows (P = 2C + 3K floats) -> sig plane (sig4 float4 per row) and
-// rest plane ([w_gamma pad to 4 | w_hh pad to 4], rest4 float4 per row)
-__global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int sig4,
-                         int rest4, int hh_off4, float *sig, float *rest) {  // P: source row stride (floats)
-    const int sigw = 4 * sig4, restw = 4 * rest4;
-    const int64_t total = rows * (int64_t)(sigw + restw);
+// leaf rows (source stride P floats: [w_sigma (C) | w_gamma (C) | w_hh (K3)])
+// r0 .. r0 + rows - 1 -> chunk-major w_sigma / w_gamma planes (float4 chunk
+// j of row g at [j * lstride + g], zero padded past C) and the row-major
+// w_hh plane (hh4 float4 per row, zero padded past K3)
+__global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int c4, int hh4,
+                         int64_t lstride, int64_t r0, float4 *sig, float4 *gam, float4 *hh) {
+    const int64_t planar = 2 * (int64_t)c4 * rows, total = planar + rows * hh4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / (sigw + restw);
-        const int j = (int)(i % (sigw + restw));
-        const float *s = src + row * P;
-        if (j < sigw) {
-            sig[row * sigw + j] = j < C ? s[j] : 0.0f;
+        float v[4];
+        if (i < planar) {  // row index fastest: coalesced plane writes
+            const int pj = (int)(i / rows);
+            const int64_t r = i % rows;
+            const int j = pj % c4;
+            const float *s = src + r * P + (pj < c4 ? 0 : C);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = 4 * j + e < C ? s[4 * j + e] : 0.0f;
+            (pj < c4 ? sig : gam)[(int64_t)j * lstride + r0 + r] = make_float4(v[0], v[1], v[2], v[3]);
         } else {
-            const int k = j - sigw;
-            float v = 0.0f;
-            if (k < C) v = s[C + k];
-            else if (k >= 4 * hh_off4 && k < 4 * hh_off4 + K3) v = s[2 * C + (k - 4 * hh_off4)];
-            rest[row * restw + k] = v;
+            const int64_t k = i - planar, r = k / hh4;
+            const int q = (int)(k % hh4);
+            const float *s = src + r * P + 2 * C;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = 4 * q + e < K3 ? s[4 * q + e] : 0.0f;
+            hh[(r0 + r) * hh4 + q] = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
 }
@@ -50,7 +56,7 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
-    const size_t smem = slice_smem_bytes(p.T.sig4, p.T.rest4);
+    const size_t smem = slice_smem_bytes(p.T.c4, p.T.hh4);
     auto kern = k_build_slice<NM, KF>;
     int r = prep_smem(kern, smem);
     if (r) return r;
@@ -101,9 +107,9 @@ int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem,
     return wide ? go_term<EntryW>(p, grid, smem, st) : go_term<EntryN>(p, grid, smem, st);
 }
 
-int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int sig4, int rest4, int hh_off4, float *sig,
-                  float *rest, cudaStream_t st) {
-    k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, sig4, rest4, hh_off4, sig, rest);
+int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int c4, int hh4, int64_t lstride,
+                  int64_t r0, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st) {
+    k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, c4, hh4, lstride, r0, sig, gam, hh);
     return check_launch("repack");
 }
 
