@@ -37,7 +37,26 @@ struct vv_tree {
     float4 *d_sig, *d_gam, *d_hh, *d_edit_rgb;
     int2 *d_edit_t;
     float *d_a, *d_b;
+    std::vector<float> h_a, h_b;  // host copies of the basis rows (slice-pass chunk masks)
 };
+
+// float4 chunks of the frame's fp32 A (which = 0) or B (1) row holding a
+// nonzero entry -- the same test as the device's nz_chunks
+static uint32_t host_nz_chunks(const vv_tree *t, int frame, int which) {
+    const float *row = (which ? t->h_b.data() : t->h_a.data()) + (size_t)frame * t->C;
+    uint32_t m = 0;
+    for (int c = 0; c < t->C; ++c)
+        if (row[c] != 0.0f) m |= 1u << (c >> 2);
+    return m;
+}
+
+static void set_slice_masks(const vv_tree *t, SliceParams &p) {
+    p.mS = p.mG = 0;
+    for (int f = 0; f < p.n_frames; ++f) {
+        p.mS |= host_nz_chunks(t, p.frame[f], 0);
+        p.mG |= host_nz_chunks(t, p.frame[f], 1);
+    }
+}
 
 struct vv_slice {
     const vv_tree *tree;
@@ -144,6 +163,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
     p.n_leaves = t->n_leaves;
     p.rec[0] = rec;
     p.rec4 = rec4;
+    set_slice_masks(t, p);
     return launch_slice(t->n_max, p, st);
 }
 
@@ -312,6 +332,11 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
         (e = cudaMemcpy(t->d_a, d->basis_a, ab, kind)) != cudaSuccess ||
         (e = cudaMemcpy(t->d_b, d->basis_b, ab, kind)) != cudaSuccess)
         return fail(set_error(VV_E_CUDA, "tree copy failed: %s", cudaGetErrorString(e)));
+    t->h_a.resize((size_t)d->frames * C);
+    t->h_b.resize((size_t)d->frames * C);
+    if (ab && ((e = cudaMemcpy(t->h_a.data(), t->d_a, ab, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+               (e = cudaMemcpy(t->h_b.data(), t->d_b, ab, cudaMemcpyDeviceToHost)) != cudaSuccess))
+        return fail(set_error(VV_E_CUDA, "basis copy failed: %s", cudaGetErrorString(e)));
     if (t->has_edits && nl > 0) {
         if ((rc = alloc((void **)&t->d_edit_rgb, (size_t)nl * sizeof(float4)))) return fail(rc);
         if ((rc = alloc((void **)&t->d_edit_t, (size_t)nl * sizeof(int2)))) return fail(rc);
@@ -497,6 +522,7 @@ int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *fram
         p.rec[f] = s->d_rec;
     }
     if (t->n_leaves == 0) return VV_OK;
+    set_slice_masks(t, p);
     const int rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
     return rc ? fail(rc) : VV_OK;
 }

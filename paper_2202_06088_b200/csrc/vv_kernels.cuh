@@ -388,6 +388,7 @@ struct SliceParams {
     int64_t n_leaves;
     float4 *rec[kMaxMulti];     // (n_leaves, rec4) slice records per frame
     int rec4;
+    uint32_t mS, mG;            // w_sigma / w_gamma chunks the frames need (union of nz_chunks)
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps, each owning a
@@ -400,15 +401,21 @@ struct SliceParams {
 // never read: their products are +-0 and the sums skip them bit-exactly
 // (nz_chunks).  Rows reach shared memory without touching registers; the
 // next chunk streams in during the fp64 sigma chains.
-constexpr int kSliceWarps = 4;
+#ifndef VV_SLICE_WARPS
+#define VV_SLICE_WARPS 4
+#endif
+#ifndef VV_SLICE_BPS
+#define VV_SLICE_BPS 2  // resident slice blocks per SM (0: as many as fit; 2 measured best)
+#endif
+constexpr int kSliceWarps = VV_SLICE_WARPS;
 constexpr int kSliceChunk = 32;
 
-__host__ __device__ inline size_t slice_stage_floats4(int c4, int hh4) {
-    return (size_t)kSliceChunk * (2 * c4 + hh4);  // worst case: every w_sigma / w_gamma chunk needed
+__host__ __device__ inline size_t slice_stage_floats4(int need, int hh4) {
+    return (size_t)kSliceChunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
 }
-__host__ __device__ inline size_t slice_smem_bytes(int c4, int hh4) {
+__host__ __device__ inline size_t slice_smem_bytes(int need, int hh4) {
     // per warp: 2 stages + 2 mbarriers (16 B)
-    return (size_t)kSliceWarps * (2 * slice_stage_floats4(c4, hh4) * 16 + 16);
+    return (size_t)kSliceWarps * (2 * slice_stage_floats4(need, hh4) * 16 + 16);
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
@@ -421,10 +428,11 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
     __shared__ double dA[KF][kMaxC];  // A rows widened once (the values sigma_pre multiplies)
-    __shared__ uint32_t sMask[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hh4 = p.T.hh4;
-    const size_t stage4 = slice_stage_floats4(p.T.c4, hh4);
+    const uint32_t mS = p.mS, mG = p.mG;  // chunk masks (host: nz_chunks of the group's rows)
+    const int nS = __popc(mS), nG = __popc(mG);
+    const size_t stage4 = slice_stage_floats4(nS + nG, hh4);
     float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 1);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
     if (lane == 0) {
@@ -436,18 +444,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     for (int f = 0; f < KF; ++f) load_rows(p.T, p.frame[f], sA[f], sB[f]);
     __syncthreads();
     for (int i = threadIdx.x; i < KF * kMaxC; i += blockDim.x) dA[i / kMaxC][i % kMaxC] = (double)sA[i / kMaxC][i % kMaxC];
-    if (threadIdx.x == 0) {  // chunks any frame of the group needs (zero chunks are never read)
-        uint32_t ms = 0, mg = 0;
-        for (int f = 0; f < KF; ++f) {
-            ms |= nz_chunks(sA[f], p.T.C);
-            mg |= nz_chunks(sB[f], p.T.C);
-        }
-        sMask[0] = ms;
-        sMask[1] = mg;
-    }
     __syncthreads();
-    const uint32_t mS = sMask[0], mG = sMask[1];
-    const int nS = __popc(mS), nG = __popc(mG);
     const int C = p.T.C;
     const int64_t ls = p.T.lstride;
     const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;

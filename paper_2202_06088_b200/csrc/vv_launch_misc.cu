@@ -1,4 +1,6 @@
 // vv_launch_misc.cu -- slice build, traversal-only, repack and tile-unpack launches.
+#include <algorithm>
+
 #include "vv_kernels.cuh"
 
 namespace vvk {
@@ -56,13 +58,19 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
-    const size_t smem = slice_smem_bytes(p.T.c4, p.T.hh4);
+    const size_t smem = slice_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4);
     auto kern = k_build_slice<NM, KF>;
     int r = prep_smem(kern, smem);
     if (r) return r;
     const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
     const unsigned want = (unsigned)((chunks + kSliceWarps - 1) / kSliceWarps);
-    const unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
+    unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
+    if (VV_SLICE_BPS > 0) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = std::min(grid, (unsigned)(VV_SLICE_BPS * sms));
+    }
     kern<<<grid, kSliceWarps * 32, smem, st>>>(p);
     return check_launch("build_slice");
 }

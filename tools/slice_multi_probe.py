@@ -11,7 +11,7 @@ from paper_2202_06088_b200 import synthetic  # noqa: E402
 tree = synthetic.shell_tree()
 
 
-def timed(fn, n=10):
+def timed(fn, n=20):
     for i in range(3):
         fn(i)
     torch.cuda.synchronize()
@@ -24,8 +24,11 @@ def timed(fn, n=10):
     return s.elapsed_time(e) / n
 
 
+def group(i, k):  # a sweep of consecutive frames, like playback
+    return [(3 + k * i + j) % tree.frames for j in range(k)]
+
+
 for k in (1, 2, 3, 4):
-    fr = list(range(k))
-    t1 = timed(lambda i: [vv.build_frame_cache(tree, f) for f in fr])
-    tk = timed(lambda i: vv.build_frame_caches(tree, fr))
+    t1 = timed(lambda i: [vv.build_frame_cache(tree, f) for f in group(i, k)])
+    tk = timed(lambda i: vv.build_frame_caches(tree, group(i, k)))
     print(f"K={k}: {k} single passes {t1:.3f} ms | one {k}-frame pass {tk:.3f} ms")
