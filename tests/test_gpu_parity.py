@@ -520,3 +520,73 @@ def test_frames_share_one_walk_deep_and_empty(cuda):
                                   vv.make_bump_bases(4, 5), 1, depth=3)
     seq = list(vv.render_sequence(empty, cam, [0, 1, 2, 3]))
     assert len(seq) == 4 and all(np.all(l.alpha == 0.0) for l in seq)
+
+
+def _sparse_bases(rng, frames=7, c=10):
+    """Basis rows exercising the nonzero-chunk skipping (nz_chunks): only the
+    constant column; a zero leading chunk; an all-zero row; a dense row; only
+    the partial last chunk; negative entries; a single zero in each chunk."""
+    a = np.zeros((frames, c), dtype=np.float32)
+    a[0, 0] = 1.0
+    a[1, [5, 9]] = [0.7, -0.4]
+    a[3] = rng.normal(size=c)
+    a[4, [8, 9]] = [0.9, 0.3]
+    a[5, [0, 1, 6]] = [1.0, -0.8, 0.5]
+    a[6] = rng.uniform(0.2, 1.0, c)
+    a[6, [0, 5, 9]] = 0.0
+    b = np.zeros_like(a)
+    b[0] = rng.normal(size=c)
+    b[1, 4] = 0.6
+    b[3, [2, 3]] = [0.5, -0.5]
+    b[4] = rng.normal(size=c)
+    b[5, 9] = 1.2
+    b[6] = rng.normal(size=c)
+    return vv.TemporalBases(a, b)
+
+
+@pytest.mark.parametrize("mode", ["per_sample", "per_frame"])
+def test_sparse_basis_chunks_vs_oracle(cuda, mode):
+    """The sigma / gamma sums skip float4 chunks whose basis entries are all
+    zero: counts and visit lists stay exact, sigma bit-exact, colour within
+    tolerance, against the oracle's full sums -- for every row shape."""
+    rng = np.random.default_rng(11)
+    depth, c, k = 5, 10, 14
+    res = 1 << depth
+    coords = np.argwhere(rng.random((res, res, res)) < 0.25)
+    data = rng.normal(scale=0.6, size=(len(coords), 2 * c + 3 * k)).astype(np.float32)
+    data[:, :c] *= 4.0  # sigma weights of both signs: some leaves dark in some frames
+    bases = _sparse_bases(rng, 7, c)
+    tree = vv.VOctree.from_cells(coords, data, bases, 2, depth=depth)
+    n = 3000
+    o = rng.uniform(-1.0, 2.0, (n, 3))
+    d = rng.uniform(0.1, 0.9, (n, 3)) - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    opts = vv.RenderOptions(frame_slice=mode)
+    for f in range(7):
+        ref = oracle.render_rays(tree, o, d, f)
+        p, a, t, st = vv.render_rays(tree, o, d, f, opts, stats=True)
+        _exact(st["sample_count"], ref["used"], f"frame {f} counts")
+        _exact(st["shaded"], ref["shaded"], f"frame {f} shaded")
+        assert np.abs(a - ref["alpha"]).max() <= 1e-12, f
+        assert np.abs(p - ref["premult"]).max() <= TOL, f
+        sig, q = oracle.build_slice(tree, f)
+        cache = vv.build_frame_cache(tree, f)
+        _exact(cache.sigma.cpu().numpy(), sig, f"frame {f} slice sigma")
+        assert np.abs(cache.q.cpu().numpy() - q).max() < 1e-5, f
+
+
+def test_sparse_basis_multi_frame_slices_bitwise(cuda):
+    """One multi-frame slice pass (union of the frames' chunk masks) gives
+    every frame the records of its own single-frame pass."""
+    rng = np.random.default_rng(12)
+    depth, c, k = 5, 10, 14
+    res = 1 << depth
+    coords = np.argwhere(rng.random((res, res, res)) < 0.3)
+    data = rng.normal(scale=0.6, size=(len(coords), 2 * c + 3 * k)).astype(np.float32)
+    tree = vv.VOctree.from_cells(coords, data, _sparse_bases(rng, 7, c), 2, depth=depth)
+    for group in ([0, 1], [2, 3, 4], [1, 4, 5, 6]):
+        multi = vv.build_frame_caches(tree, group)
+        for f, m in zip(group, multi):
+            one = vv.build_frame_cache(tree, f)
+            _exact(m.sigma.cpu().numpy(), one.sigma.cpu().numpy(), f"group {group} frame {f} sigma")
+            _exact(m.q.cpu().numpy(), one.q.cpu().numpy(), f"group {group} frame {f} q")
