@@ -402,20 +402,23 @@ struct SliceParams {
 // (nz_chunks).  Rows reach shared memory without touching registers; the
 // next chunk streams in during the fp64 sigma chains.
 #ifndef VV_SLICE_WARPS
-#define VV_SLICE_WARPS 4
+#define VV_SLICE_WARPS 4  // max warps per block (fewer when a warp's stages are large)
 #endif
 #ifndef VV_SLICE_BPS
-#define VV_SLICE_BPS 2  // resident slice blocks per SM (0: as many as fit; 2 measured best)
+#define VV_SLICE_BPS 1  // resident slice blocks per SM (0: as many as fit)
 #endif
 constexpr int kSliceWarps = VV_SLICE_WARPS;
-constexpr int kSliceChunk = 32;
+#ifndef VV_SLICE_CHUNK
+#define VV_SLICE_CHUNK 64  // leaves per staged chunk (a multiple of 32; lanes loop over their leaves)
+#endif
+constexpr int kSliceChunk = VV_SLICE_CHUNK;
+static_assert(kSliceChunk % 32 == 0, "slice chunk must be whole warps of leaves");
 
 __host__ __device__ inline size_t slice_stage_floats4(int need, int hh4) {
     return (size_t)kSliceChunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
 }
-__host__ __device__ inline size_t slice_smem_bytes(int need, int hh4) {
-    // per warp: 2 stages + 2 mbarriers (16 B)
-    return (size_t)kSliceWarps * (2 * slice_stage_floats4(need, hh4) * 16 + 16);
+__host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4) {
+    return 2 * slice_stage_floats4(need, hh4) * 16 + 16;  // 2 stages + 2 mbarriers
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
@@ -448,8 +451,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     const int C = p.T.C;
     const int64_t ls = p.T.lstride;
     const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
-    const int64_t wstride = (int64_t)gridDim.x * kSliceWarps;
-    const int64_t c0 = (int64_t)blockIdx.x * kSliceWarps + warp;
+    const int nw = blockDim.x >> 5;  // <= kSliceWarps: the launcher fits the stages in shared memory
+    const int64_t wstride = (int64_t)gridDim.x * nw;
+    const int64_t c0 = (int64_t)blockIdx.x * nw + warp;
     // stage: [needed w_sigma chunks][32 leaves] | [needed w_gamma chunks][32] | [32 leaves][hh4]
     auto issue = [&](int64_t c, int stg) {
         const int64_t base = c * kSliceChunk;
@@ -474,8 +478,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kSliceChunk;
         const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
-        const float4 *sv = wbase + stg * stage4 + lane;
-        if (lane < rows) {
+#pragma unroll 1
+        for (int r = lane; r < rows; r += 32) {
+            const float4 *sv = wbase + stg * stage4 + r;
             // sigma_pre (kernels.py:374-381, f64, sequential) and the gamma dot
             // (fp32), every frame at once, over the needed chunks in column order
             double sp[KF];
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                     }
                 }
             }
-            const float4 *shh = wbase + stg * stage4 + (size_t)(nS + nG) * kSliceChunk + (size_t)lane * hh4;
+            const float4 *shh = wbase + stg * stage4 + (size_t)(nS + nG) * kSliceChunk + (size_t)r * hh4;
             float wh[4 * Basis<NMAX>::HH4];
             load_hh<NMAX, false>(shh, wh);
 #pragma unroll
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
                 q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
                 q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
-                float4 *o = p.rec[f] + (base + lane) * p.rec4;
+                float4 *o = p.rec[f] + (base + r) * p.rec4;
 #pragma unroll
                 for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
             }

@@ -58,20 +58,25 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
-    const size_t smem = slice_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4);
+    const size_t per_warp = slice_warp_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4);
+    const size_t limit = 227 * 1024 - 4096;  // opt-in maximum less the static arrays
+    const int nw = (int)std::min<size_t>(kSliceWarps, limit / per_warp);
+    if (nw < 1)
+        return set_error(VV_E_UNSUPPORTED, "slice stage of %zu bytes per warp exceeds shared memory", per_warp);
+    const size_t smem = (size_t)nw * per_warp;
     auto kern = k_build_slice<NM, KF>;
     int r = prep_smem(kern, smem);
     if (r) return r;
     const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
-    const unsigned want = (unsigned)((chunks + kSliceWarps - 1) / kSliceWarps);
-    unsigned grid = persistent_grid(kern, kSliceWarps * 32, smem, want);
+    const unsigned want = (unsigned)((chunks + nw - 1) / nw);
+    unsigned grid = persistent_grid(kern, nw * 32, smem, want);
     if (VV_SLICE_BPS > 0) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = std::min(grid, (unsigned)(VV_SLICE_BPS * sms));
     }
-    kern<<<grid, kSliceWarps * 32, smem, st>>>(p);
+    kern<<<grid, nw * 32, smem, st>>>(p);
     return check_launch("build_slice");
 }
 
