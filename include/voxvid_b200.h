@@ -138,9 +138,20 @@ int vv_slice_build(const vv_tree *tree, int32_t frame, void *stream, vv_slice **
  * equal to vv_slice_build(frames[k]).  Playback groups use it. */
 int vv_slice_build_multi(const vv_tree *tree, int32_t n_frames, const int32_t *frames, void *stream,
                          vv_slice **out);
+/* vv_slice_build_multi with flags.  VV_SLICE_RENDER_ONLY: slices only for
+ * rendering -- where a chunk of 64 consecutive leaves has sigma 0 in every
+ * frame, only sigma is written, and while chunks stay dark their w_gamma /
+ * w_hh rows are not read.  The renderers never read the colour of a leaf
+ * with sigma 0 (kernels.py:556-559), so images are bitwise the same; q of
+ * such a slice cannot be exported.  Ignored for trees with edits (an edit
+ * can give a dark leaf density).  render()'s transient slices and the
+ * playback groups are built this way. */
+#define VV_SLICE_RENDER_ONLY 1
+int vv_slice_build_frames(const vv_tree *tree, int32_t n_frames, const int32_t *frames, int32_t flags,
+                          void *stream, vv_slice **out);
 int vv_slice_free(vv_slice *slice);
 /* Copies the cache to caller device buffers: sigma (n_leaves) f64,
- * q (n_leaves, 3S) f32. */
+ * q (n_leaves, 3S) f32 (q: VV_E_INVALID for a VV_SLICE_RENDER_ONLY slice). */
 int vv_slice_export(const vv_slice *slice, double *sigma, float *q, void *stream);
 int vv_slice_frame(const vv_slice *slice, int32_t *frame);
 

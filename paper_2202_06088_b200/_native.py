@@ -71,6 +71,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_scene",
     "vv_render_camera_multi",
     "vv_slice_build_multi",
+    "vv_slice_build_frames",
     "vv_camera_decode_mode",
     "vv_shadow_blur",
     "vv_scene_lighting",
@@ -188,6 +189,7 @@ class InstanceDesc(ctypes.Structure):
     ]
 
 
+VV_SLICE_RENDER_ONLY = 1
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -234,6 +236,7 @@ _SIGNATURES = {
     "vv_ipc_free": (ctypes.c_int, [_I32, _P]),
     "vv_camera_decode_mode": (ctypes.c_int, [_P, _P, _P, _P]),
     "vv_slice_build_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
+    "vv_slice_build_frames": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P]),
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),

@@ -64,6 +64,7 @@ struct vv_slice {
     int32_t frame;
     float4 *d_rec;  // (n_leaves, rec4) records [q | pad | sigma]
     int rec4;
+    bool render_only;  // colour omitted where sigma is 0 (VV_SLICE_RENDER_ONLY): not exportable
     int64_t n_leaves;
     cudaStream_t stream;  // stream-ordered allocation: freed on this stream
 };
@@ -152,7 +153,7 @@ SliceView slice_view(const vv_slice *c) {
     return s;
 }
 
-int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st) {
+int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
     memset(&p, 0, sizeof(p));
@@ -163,6 +164,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
     p.n_leaves = t->n_leaves;
     p.rec[0] = rec;
     p.rec4 = rec4;
+    p.skip_dark = render_only && !t->has_edits;
     set_slice_masks(t, p);
     return launch_slice(t->n_max, p, st);
 }
@@ -267,7 +269,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     tr.st = st;
     sv.rec = reinterpret_cast<float4 *>(tr.mem);
     sv.rec4 = rec4;
-    return launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st);
+    return launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st, true);
 }
 
 // src_stride: floats per source payload row (0: 2C + 3K; .voct rows with
@@ -469,7 +471,7 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
         vv_slice_free(s);
         return set_error(VV_E_NOMEM, "slice allocation failed");
     }
-    rc = launch_build_slice(t, frame, s->d_rec, s->rec4, (cudaStream_t)stream);
+    rc = launch_build_slice(t, frame, s->d_rec, s->rec4, (cudaStream_t)stream, false);
     if (rc) {
         vv_slice_free(s);
         return rc;
@@ -479,7 +481,13 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
 }
 
 int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, void *stream, vv_slice **out) {
+    return vv_slice_build_frames(t, n_frames, frames, 0, stream, out);
+}
+
+int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *frames, int32_t flags, void *stream,
+                          vv_slice **out) {
     if (!t || !frames || !out) return set_error(VV_E_INVALID, "null argument");
+    if (flags & ~VV_SLICE_RENDER_ONLY) return set_error(VV_E_INVALID, "unknown slice flags 0x%x", flags);
     if (n_frames < 1 || n_frames > kMaxMulti)
         return set_error(VV_E_UNSUPPORTED, "%d frames per slice pass (1..%d)", n_frames, kMaxMulti);
     for (int f = 0; f < n_frames; ++f) {
@@ -512,6 +520,7 @@ int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *fram
         s->n_leaves = t->n_leaves;
         s->rec4 = p.rec4;
         s->stream = (cudaStream_t)stream;
+        s->render_only = (flags & VV_SLICE_RENDER_ONLY) != 0;
         out[f] = s;
         if (cudaMallocAsync(&s->d_rec, nrows * s->rec4 * sizeof(float4), s->stream) != cudaSuccess) {
             cudaGetLastError();
@@ -522,6 +531,7 @@ int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *fram
         p.rec[f] = s->d_rec;
     }
     if (t->n_leaves == 0) return VV_OK;
+    p.skip_dark = (flags & VV_SLICE_RENDER_ONLY) && !t->has_edits;
     set_slice_masks(t, p);
     const int rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
     return rc ? fail(rc) : VV_OK;
@@ -543,6 +553,9 @@ int vv_slice_frame(const vv_slice *s, int32_t *frame) {
 
 int vv_slice_export(const vv_slice *s, double *sigma, float *q, void *stream) {
     if (!s) return set_error(VV_E_INVALID, "null slice");
+    if (s->render_only && q)
+        return set_error(VV_E_INVALID, "a render-only slice has no colour for dark leaves; build it without "
+                                       "VV_SLICE_RENDER_ONLY to export q");
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int S3 = 3 * s->tree->S;

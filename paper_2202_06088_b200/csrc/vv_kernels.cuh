@@ -389,6 +389,7 @@ struct SliceParams {
     float4 *rec[kMaxMulti];     // (n_leaves, rec4) slice records per frame
     int rec4;
     uint32_t mS, mG;            // w_sigma / w_gamma chunks the frames need (union of nz_chunks)
+    int skip_dark;              // render-internal slice: dark chunks get sigma only (no colour)
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps, each owning a
@@ -408,6 +409,9 @@ struct SliceParams {
 #define VV_SLICE_BPS 1  // resident slice blocks per SM (0: as many as fit)
 #endif
 constexpr int kSliceWarps = VV_SLICE_WARPS;
+#ifndef VV_SLICE_RUNS
+#define VV_SLICE_RUNS 0  // 1: contiguous runs of chunks per warp instead of strided
+#endif
 #ifndef VV_SLICE_CHUNK
 #define VV_SLICE_CHUNK 64  // leaves per staged chunk (a multiple of 32; lanes loop over their leaves)
 #endif
@@ -418,7 +422,7 @@ __host__ __device__ inline size_t slice_stage_floats4(int need, int hh4) {
     return (size_t)kSliceChunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
 }
 __host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4) {
-    return 2 * slice_stage_floats4(need, hh4) * 16 + 16;  // 2 stages + 2 mbarriers
+    return 2 * slice_stage_floats4(need, hh4) * 16 + 32;  // 2 stages + 4 mbarriers
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
@@ -431,16 +435,19 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
     __shared__ double dA[KF][kMaxC];  // A rows widened once (the values sigma_pre multiplies)
+    constexpr int kPer = kSliceChunk / 32;  // leaves per lane per chunk
+    constexpr int R4 = slice_rec4(Basis<NMAX>::S);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hh4 = p.T.hh4;
     const uint32_t mS = p.mS, mG = p.mG;  // chunk masks (host: nz_chunks of the group's rows)
     const int nS = __popc(mS), nG = __popc(mG);
     const size_t stage4 = slice_stage_floats4(nS + nG, hh4);
-    float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 1);
+    float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 2);
+    // bar[0..1]: a stage's staged copies; bar[2..3]: its colour rows fetched late
     uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
     if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) mbar_init(&bar[b], 1);
         mbar_fence_init();
     }
 #pragma unroll
@@ -452,56 +459,112 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     const int64_t ls = p.T.lstride;
     const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
     const int nw = blockDim.x >> 5;  // <= kSliceWarps: the launcher fits the stages in shared memory
-    const int64_t wstride = (int64_t)gridDim.x * nw;
-    const int64_t c0 = (int64_t)blockIdx.x * nw + warp;
-    // stage: [needed w_sigma chunks][32 leaves] | [needed w_gamma chunks][32] | [32 leaves][hh4]
-    auto issue = [&](int64_t c, int stg) {
+    const int64_t n_warps = (int64_t)gridDim.x * nw, wid = (int64_t)blockIdx.x * nw + warp;
+#if VV_SLICE_RUNS
+    // contiguous runs of chunks per warp (the chunk before is a spatial neighbour)
+    const int64_t c_begin = n_chunks * wid / n_warps, c_end = n_chunks * (wid + 1) / n_warps, c_step = 1;
+#else
+    // chunks strided over the warps: the chunks in flight at any time are
+    // neighbours in HBM
+    const int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
+#endif
+    // stage: [needed w_sigma chunks][kSliceChunk leaves] | [needed w_gamma chunks][kSliceChunk] | [leaves][hh4]
+    auto rows_of = [&](int64_t c) { return (int)min((int64_t)kSliceChunk, p.n_leaves - c * kSliceChunk); };
+    auto issue_colour = [&](int64_t c, int stg, uint64_t *b, bool arrive) {
         const int64_t base = c * kSliceChunk;
-        const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
+        const int rows = rows_of(c);
+        float4 *dst = wbase + stg * stage4 + (size_t)nS * kSliceChunk;
+        const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
+        if (arrive) mbar_expect_tx(b, (uint32_t)nG * cb + hb);
+        for (uint32_t m = mG; m; m &= m - 1, dst += kSliceChunk)
+            bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, b);
+        bulk_g2s(dst, p.T.hh + base * hh4, hb, b);
+    };
+    auto issue = [&](int64_t c, int stg, bool colour) {  // lane 0
+        const int64_t base = c * kSliceChunk;
+        const int rows = rows_of(c);
         float4 *dst = wbase + stg * stage4;
         const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
-        mbar_expect_tx(&bar[stg], (uint32_t)(nS + nG) * cb + hb);
+        mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
         for (uint32_t m = mS; m; m &= m - 1, dst += kSliceChunk)
             bulk_g2s(dst, p.T.sig + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
-        for (uint32_t m = mG; m; m &= m - 1, dst += kSliceChunk)
-            bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
-        bulk_g2s(dst, p.T.hh + base * hh4, hb, &bar[stg]);
+        if (colour) issue_colour(c, stg, &bar[stg], false);
     };
+    // colour rows are staged with the sigma chunks while the chunks are
+    // bright; a dark chunk (every leaf's sigma 0 in every frame: the shader
+    // never reads its colour, kernels.py:556-559) only gets its sigma
+    // written, and while chunks stay dark the colour rows are not fetched
+    // (render-internal slices of trees without edits: p.skip_dark)
+    uint32_t colour_in = 3u;  // bit s: stage s was issued with its colour rows
     if (lane == 0) {
-        if (c0 < n_chunks) issue(c0, 0);
-        if (c0 + wstride < n_chunks) issue(c0 + wstride, 1);
+        if (c_begin < c_end) issue(c_begin, 0, true);
+        if (c_begin + c_step < c_end) issue(c_begin + c_step, 1, true);
     }
-    constexpr int R4 = slice_rec4(Basis<NMAX>::S);
+    uint32_t late_par = 0;  // phase parity of bar[2], bar[3]
     int k = 0;
-    for (int64_t c = c0; c < n_chunks; c += wstride, ++k) {
+    for (int64_t c = c_begin; c < c_end; c += c_step, ++k) {
         const int stg = k & 1;
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kSliceChunk;
-        const int rows = (int)min((int64_t)kSliceChunk, p.n_leaves - base);
-#pragma unroll 1
-        for (int r = lane; r < rows; r += 32) {
-            const float4 *sv = wbase + stg * stage4 + r;
-            // sigma_pre (kernels.py:374-381, f64, sequential) and the gamma dot
-            // (fp32), every frame at once, over the needed chunks in column order
-            double sp[KF];
-            float gp[KF];
+        const int rows = rows_of(c);
+        const float4 *st4 = wbase + stg * stage4;
+        // sigma_pre (kernels.py:374-381, f64, sequential), every frame, over
+        // the needed chunks in column order
+        double sp[kPer][KF];
+        bool lit = false;
 #pragma unroll
-            for (int f = 0; f < KF; ++f) {
-                sp[f] = 0.0;
-                gp[f] = 0.0f;
-            }
-            for (uint32_t m = mS; m; m &= m - 1, sv += kSliceChunk) {
-                const float4 v = ld4<false>(sv);
-                const double w[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
-                const int cc = 4 * (__ffs(m) - 1);
+        for (int u = 0; u < kPer; ++u) {
+            const int r = lane + 32 * u;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (cc + e < C) {
+            for (int f = 0; f < KF; ++f) sp[u][f] = 0.0;
+            if (r < rows) {
+                const float4 *sv = st4 + r;
+                for (uint32_t m = mS; m; m &= m - 1, sv += kSliceChunk) {
+                    const float4 v = ld4<false>(sv);
+                    const double w[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+                    const int cc = 4 * (__ffs(m) - 1);
 #pragma unroll
-                        for (int f = 0; f < KF; ++f) sp[f] = xadd(sp[f], xmul(dA[f][cc + e], w[e]));
+                    for (int e = 0; e < 4; ++e) {
+                        if (cc + e < C) {
+#pragma unroll
+                            for (int f = 0; f < KF; ++f) sp[u][f] = xadd(sp[u][f], xmul(dA[f][cc + e], w[e]));
+                        }
                     }
                 }
+#pragma unroll
+                for (int f = 0; f < KF; ++f) lit |= sp[u][f] > 0.0;
             }
+        }
+        const bool bright = !p.skip_dark || __any_sync(0xffffffffu, lit);
+        if (bright && !((colour_in >> stg) & 1u)) {  // mispredicted dark: fetch the colour rows now
+            if (lane == 0) {
+                fence_proxy_async();  // the colour region was last read through the generic proxy
+                issue_colour(c, stg, &bar[2 + stg], true);
+            }
+            mbar_wait(&bar[2 + stg], (late_par >> stg) & 1u);
+            late_par ^= 1u << stg;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int r = lane + 32 * u;
+            if (r >= rows) continue;
+            if (!bright) {  // sigma only: the record's last float4 pair (one sector at even R4)
+#pragma unroll
+                for (int f = 0; f < KF; ++f) {
+                    const double sigma = sp[u][f] > 0.0 ? sp[u][f] : 0.0;
+                    const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+                    float4 *o = p.rec[f] + (base + r) * p.rec4 + (R4 - 1);
+                    if (R4 % 2 == 0) o[-1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    *o = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
+                                     __uint_as_float((unsigned)(sb >> 32)));
+                }
+                continue;
+            }
+            // the gamma dot (fp32), every frame, over the needed chunks
+            float gp[KF];
+#pragma unroll
+            for (int f = 0; f < KF; ++f) gp[f] = 0.0f;
+            const float4 *sv = st4 + (size_t)nS * kSliceChunk + r;
             for (uint32_t m = mG; m; m &= m - 1, sv += kSliceChunk) {
                 const float4 g = ld4<false>(sv);
                 const float gw[4] = {g.x, g.y, g.z, g.w};
@@ -514,7 +577,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                     }
                 }
             }
-            const float4 *shh = wbase + stg * stage4 + (size_t)(nS + nG) * kSliceChunk + (size_t)r * hh4;
+            const float4 *shh = st4 + (size_t)(nS + nG) * kSliceChunk + (size_t)r * hh4;
             float wh[4 * Basis<NMAX>::HH4];
             load_hh<NMAX, false>(shh, wh);
 #pragma unroll
@@ -531,7 +594,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                         const int j = l * l + l + m;
                         slice_col<NMAX>(R, wh, l, m, q[3 * j + 0], q[3 * j + 1], q[3 * j + 2]);
                     }
-                const double sigma = sp[f] > 0.0 ? sp[f] : 0.0;  // max(0.0, sp)
+                const double sigma = sp[u][f] > 0.0 ? sp[u][f] : 0.0;  // max(0.0, sp)
                 const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
                 q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
                 q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
@@ -541,10 +604,12 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
             }
         }
         __syncwarp();
-        // stage consumed: refill it with the chunk two steps ahead
-        if (lane == 0 && c + 2 * wstride < n_chunks) {
+        // stage consumed: refill it with the chunk two ahead, predicting its
+        // colour rows are needed iff this chunk's were
+        colour_in = (colour_in & ~(1u << stg)) | ((uint32_t)bright << stg);
+        if (lane == 0 && c + 2 * c_step < c_end) {
             fence_proxy_async();
-            issue(c + 2 * wstride, stg);
+            issue(c + 2 * c_step, stg, bright);
         }
     }
 }

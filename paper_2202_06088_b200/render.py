@@ -200,24 +200,23 @@ class FrameSlice:
         self._sigma = None
         self._q = None
 
-    def _export(self):
-        torch = require_cuda()
-        n = self._rep.n_leaves
-        self._sigma = torch.empty(n, dtype=torch.float64, device=self._device)
-        self._q = torch.empty((n, 3 * self._rep.s), dtype=torch.float32, device=self._device)
-        _native.check(_native.lib().vv_slice_export(self._handle, self._sigma.data_ptr(), self._q.data_ptr(),
-                                                    stream_ptr(self._device)))
-
     @property
     def sigma(self):
         if self._sigma is None:
-            self._export()
+            torch = require_cuda()
+            sigma = torch.empty(self._rep.n_leaves, dtype=torch.float64, device=self._device)
+            _native.check(_native.lib().vv_slice_export(self._handle, sigma.data_ptr(), None,
+                                                        stream_ptr(self._device)))
+            self._sigma = sigma
         return self._sigma
 
     @property
     def q(self):
         if self._q is None:
-            self._export()
+            torch = require_cuda()
+            q = torch.empty((self._rep.n_leaves, 3 * self._rep.s), dtype=torch.float32, device=self._device)
+            _native.check(_native.lib().vv_slice_export(self._handle, None, q.data_ptr(), stream_ptr(self._device)))
+            self._q = q
         return self._q
 
     def __del__(self):
@@ -299,10 +298,13 @@ def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
     return FrameSlice(frame, handle, rep, dev)
 
 
-def build_frame_caches(tree, frames, device=None) -> list:
+def build_frame_caches(tree, frames, device=None, *, render_only: bool = False) -> list:
     """Slices of 1..4 frames from ONE pass over the payload (vv_slice_build_multi):
     each leaf row is read once and sliced per frame; ``[build_frame_cache(tree, f) for f in frames]``
-    with a quarter to a half of the HBM traffic."""
+    with a quarter to a half of the HBM traffic.  ``render_only``: the
+    colour of leaves dark (sigma 0) in every frame is omitted
+    (VV_SLICE_RENDER_ONLY) -- rendering is bitwise the same, ``q`` cannot be
+    read."""
     frames = [_frame_index(f) for f in frames]
     for f in frames:
         _check_frame(tree, f)
@@ -312,8 +314,9 @@ def build_frame_caches(tree, frames, device=None) -> list:
     rep = replica(tree, dev)
     n = len(frames)
     handles = (ctypes.c_void_p * n)()
-    _native.check(_native.lib().vv_slice_build_multi(rep.handle, n, (ctypes.c_int32 * n)(*frames), stream_ptr(dev),
-                                                     handles))
+    _native.check(_native.lib().vv_slice_build_frames(rep.handle, n, (ctypes.c_int32 * n)(*frames),
+                                                      _native.VV_SLICE_RENDER_ONLY if render_only else 0,
+                                                      stream_ptr(dev), handles))
     return [FrameSlice(f, ctypes.c_void_p(h), rep, dev) for f, h in zip(frames, handles)]
 
 
@@ -499,7 +502,9 @@ def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = Re
         return
     ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream(dev))
     with ctx:
-        caches = build_frame_caches(tree, frames, device=dev)  # one payload pass; freed stream-ordered after the walk
+        # one payload pass (colour skipped where every frame is dark); freed
+        # stream-ordered after the walk
+        caches = build_frame_caches(tree, frames, device=dev, render_only=True)
         n = len(frames)
         P = ctypes.c_void_p
 

@@ -590,3 +590,38 @@ def test_sparse_basis_multi_frame_slices_bitwise(cuda):
             one = vv.build_frame_cache(tree, f)
             _exact(m.sigma.cpu().numpy(), one.sigma.cpu().numpy(), f"group {group} frame {f} sigma")
             _exact(m.q.cpu().numpy(), one.q.cpu().numpy(), f"group {group} frame {f} q")
+
+
+def test_render_only_slices_dark_chunks_bitwise(cuda):
+    """Render-internal slices (VV_SLICE_RENDER_ONLY) leave the colour of
+    all-dark leaf chunks unwritten and skip their colour rows: on the cfg3
+    motion generator (about 90% of leaves dark in any frame) render(),
+    the shared-walk playback and the per-sample path stay bitwise equal to
+    rendering from complete caches; exporting q from such a slice is refused."""
+    import torch
+
+    tree = synthetic.motion_tree(depth=7, frames=12)
+    cam = synthetic.bench_camera(160, 96)
+    h, w = cam.height, cam.width
+    for f in (0, 5, 11):
+        full = vv.build_frame_cache(tree, f)
+        ref = vv.render(tree, cam, f, cache=full)
+        for mode in ("per_frame", "per_sample"):
+            img = vv.render(tree, cam, f, vv.RenderOptions(frame_slice=mode))
+            _exact(img.rgb, ref.rgb, f"{mode} rgb {f}")
+            _exact(img.alpha, ref.alpha, f"{mode} alpha {f}")
+            _exact(img.depth, ref.depth, f"{mode} depth {f}")
+        ro = vv.build_frame_caches(tree, [f], render_only=True)[0]
+        _exact(ro.sigma.cpu().numpy(), full.sigma.cpu().numpy(), f"render-only sigma {f}")
+        with pytest.raises(ValueError):
+            ro.q
+    frames = [2, 3, 4, 9]
+    outs = [(torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda))
+            for _ in frames]
+    vv.render_frames_into(tree, cam, frames, outs)
+    torch.cuda.synchronize()
+    for f, (r, a, d) in zip(frames, outs):
+        ref = vv.render(tree, cam, f, cache=vv.build_frame_cache(tree, f))
+        _exact(r.cpu().numpy(), ref.rgb, f"playback rgb {f}")
+        _exact(a.cpu().numpy(), ref.alpha, f"playback alpha {f}")
+        _exact(d.cpu().numpy(), ref.depth, f"playback depth {f}")

@@ -8,7 +8,9 @@ import torch  # noqa: E402
 import paper_2202_06088_b200 as vv  # noqa: E402
 from paper_2202_06088_b200 import synthetic  # noqa: E402
 
-tree = synthetic.shell_tree()
+import os  # noqa: E402
+
+tree = synthetic.motion_tree() if os.environ.get("VV_PROBE_TREE") == "motion" else synthetic.shell_tree()
 
 
 def timed(fn, n=20):
@@ -32,3 +34,5 @@ for k in (1, 2, 3, 4):
     t1 = timed(lambda i: [vv.build_frame_cache(tree, f) for f in group(i, k)])
     tk = timed(lambda i: vv.build_frame_caches(tree, group(i, k)))
     print(f"K={k}: {k} single passes {t1:.3f} ms | one {k}-frame pass {tk:.3f} ms")
+    tr = timed(lambda i: vv.build_frame_caches(tree, group(i, k), render_only=True))
+    print(f"K={k}: one {k}-frame render-only pass {tr:.3f} ms")
