@@ -75,12 +75,15 @@ typedef struct {
      * VV_SLICE_AUTO picks per call, VV_SLICE_PER_SAMPLE decodes each visited
      * leaf inside the render kernel (render_kernel's uncached branch),
      * VV_SLICE_PER_FRAME first decodes every leaf once into a transient
-     * stream-ordered slice, then renders from it. */
+     * stream-ordered slice, then renders from it.  VV_SLICE_DEFERRED
+     * (vv_render_camera only; others treat it as PER_FRAME): sigma per leaf,
+     * the walk with the compositing weights, the colour of the leaves some
+     * ray shades, then colour per ray -- see DESIGN.md. */
     int32_t frame_slice;
     int32_t reserved;
 } vv_render_opts;
 
-enum { VV_SLICE_AUTO = 0, VV_SLICE_PER_SAMPLE = 1, VV_SLICE_PER_FRAME = 2 };
+enum { VV_SLICE_AUTO = 0, VV_SLICE_PER_SAMPLE = 1, VV_SLICE_PER_FRAME = 2, VV_SLICE_DEFERRED = 3 };
 
 /* Pinhole camera (render.py:42-125): intrinsics in pixels, row-major c2w. */
 typedef struct {

@@ -21,6 +21,7 @@
 
 #include "../../include/voxvid_b200.h"
 #include "vv_kernels.cuh"
+#include "vv_deferred.cuh"
 
 using namespace vv;
 using namespace vvk;
@@ -38,6 +39,10 @@ struct vv_tree {
     int2 *d_edit_t;
     float *d_a, *d_b;
     std::vector<float> h_a, h_b;  // host copies of the basis rows (slice-pass chunk masks)
+    // deferred renders: per-leaf stamp (== epoch: shaded in the current
+    // render), allocated on first use
+    mutable uint32_t *d_stamp = nullptr;
+    mutable uint32_t epoch = 0;
 };
 
 // float4 chunks of the frame's fp32 A (which = 0) or B (1) row holding a
@@ -204,6 +209,7 @@ void pool_setup(int device) {
 int decode_mode(const vv_tree *t, double n_rays, int policy) {
     if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return 0;
     if (policy == VV_SLICE_PER_FRAME) return 1;
+    if (policy == VV_SLICE_DEFERRED) return 2;
     return (double)t->n_leaves <= 3.0 * n_rays ? 1 : 0;
 }
 
@@ -432,6 +438,7 @@ int vv_tree_free(vv_tree *t) {
     cudaFree(t->d_sig);
     cudaFree(t->d_gam);
     cudaFree(t->d_hh);
+    cudaFree(t->d_stamp);
     cudaFree(t->d_edit_rgb);
     cudaFree(t->d_edit_t);
     cudaFree(t->d_a);
@@ -633,6 +640,74 @@ int vv_render_rays_visits(const vv_tree *t, int32_t frame, const vv_slice *cache
                             nullptr, visit_start, visit_leaf, stream);
 }
 
+// Deferred-colour camera render (vv_deferred.cuh): one pooled block for the
+// per-call buffers, the tree's stamp array, then the launch sequence.
+constexpr int kDeferCap = 32;  // shaded samples recorded per ray (cfg2 max: 28)
+
+static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned grid, cudaStream_t st) {
+    const int64_t nl = t->n_leaves, npix = (int64_t)p.cam.width * p.cam.height;
+    int cap = kDeferCap;  // VV_DEFER_CAP: tests force the overflow path with a small record
+    if (const char *e = getenv("VV_DEFER_CAP")) cap = std::max(1, atoi(e));
+    const int rec4 = slice_rec4(t->S);
+    if (!t->d_stamp) {
+        if (cudaMalloc(&t->d_stamp, (size_t)std::max<int64_t>(nl, 1) * 4) != cudaSuccess) {
+            cudaGetLastError();
+            t->d_stamp = nullptr;
+            return set_error(VV_E_NOMEM, "stamp allocation failed");
+        }
+        cudaMemsetAsync(t->d_stamp, 0, (size_t)std::max<int64_t>(nl, 1) * 4, st);
+        t->epoch = 0;
+    }
+    if (++t->epoch == 0) {  // wrapped: clear the stamps
+        cudaMemsetAsync(t->d_stamp, 0, (size_t)std::max<int64_t>(nl, 1) * 4, st);
+        t->epoch = 1;
+    }
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_sig = al(nl * 8), b_rec = al((size_t)nl * rec4 * 16), b_list = al(nl * 4), b_cnt = 256,
+                 b_aacc = al(npix * 8), b_count = al(npix * 4), b_sl = al((size_t)npix * cap * 4),
+                 b_sw = al((size_t)npix * cap * 8), b_ovf = al(npix * 4);
+    const size_t total = b_sig + b_rec + b_list + b_cnt + b_aacc + b_count + b_sl + b_sw + b_ovf;
+    pool_setup(t->device);
+    Transient tr;
+    if (cudaMallocAsync(&tr.mem, total, st) != cudaSuccess) {
+        cudaGetLastError();
+        tr.mem = nullptr;
+        return set_error(VV_E_NOMEM, "deferred render buffers (%zu bytes) failed", total);
+    }
+    tr.st = st;
+    char *m = static_cast<char *>(tr.mem);
+    auto take = [&](size_t b) {
+        char *r = m;
+        m += b;
+        return r;
+    };
+    DeferBuffers B;
+    memset(&B, 0, sizeof(B));
+    B.sig8 = reinterpret_cast<double *>(take(b_sig));
+    B.rec = reinterpret_cast<float4 *>(take(b_rec));
+    B.list = reinterpret_cast<uint32_t *>(take(b_list));
+    B.counters = reinterpret_cast<uint32_t *>(take(b_cnt));
+    B.D.aacc = reinterpret_cast<double *>(take(b_aacc));
+    B.D.count = reinterpret_cast<int32_t *>(take(b_count));
+    B.D.sleaf = reinterpret_cast<uint32_t *>(take(b_sl));
+    B.D.sw = reinterpret_cast<double *>(take(b_sw));
+    B.ovf = reinterpret_cast<uint32_t *>(take(b_ovf));
+    B.D.sig8 = B.sig8;
+    B.D.stamp = t->d_stamp;
+    B.D.epoch = t->epoch;
+    B.D.cap = cap;
+    B.D.npix = npix;
+    B.n_leaves = nl;
+    B.rec4 = rec4;
+    B.mS = B.mG = 0;
+    B.mS = host_nz_chunks(t, p.frame, 0);
+    B.mG = host_nz_chunks(t, p.frame, 1);
+    if (cudaMemsetAsync(B.counters, 0, 8, st) != cudaSuccess) return set_error(VV_E_CUDA, "memset failed");
+    p.S.rec = B.rec;
+    p.S.rec4 = rec4;
+    return launch_deferred(t->n_max, wide, p, B, grid, st);
+}
+
 static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *o,
                               const vv_camera *cam, float *rgb, float *alpha, float *depth, float *packed,
                               int tile, int shard, int n_shards, int peer, void *stream) {
@@ -686,8 +761,12 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     cudaStream_t st = (cudaStream_t)stream;
     Transient tr;
     const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
-    const int mode =
+    int mode =
         cache ? 1 : decode_mode(t, share * cube_footprint(*cam, lo, t->view.side, nullptr), opts.frame_slice);
+    if (mode == 2) {
+        if (!tile && !t->has_edits) return render_deferred(t, p, wide, grid_blocks, st);
+        mode = 1;  // tiles and edited trees: the one-pass sliced kernel
+    }
     if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;

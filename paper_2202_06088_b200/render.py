@@ -151,7 +151,7 @@ class LayerImages:
         return LayerImages(c(self.rgb), c(self.alpha), c(self.depth))
 
 
-_SLICE_MODES = {"auto": 0, "per_sample": 1, "per_frame": 2}
+_SLICE_MODES = {"auto": 0, "per_sample": 1, "per_frame": 2, "deferred": 3}
 
 
 @dataclass(frozen=True)
