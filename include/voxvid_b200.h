@@ -230,7 +230,7 @@ int vv_ipc_free(int32_t device, void *ptr);
 
 /* The leaf-decode mode VV_SLICE_AUTO picks for a camera render of this tree
  * (1 = per-frame slice pass, 0 = decode per sample): slice when the leaves
- * number <= 3 x the rays that can reach the tree (its projected footprint). */
+ * number <= 4 x the rays that can reach the tree (its projected footprint). */
 int vv_camera_decode_mode(const vv_tree *tree, const vv_camera *cam, const vv_render_opts *opts, int32_t *mode);
 /* Playback: n_frames (2..4) frames of ONE camera in one walk -- the rays and
  * therefore the traversal are frame-independent, so one walk serves every

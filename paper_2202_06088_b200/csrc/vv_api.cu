@@ -201,16 +201,17 @@ void pool_setup(int device) {
 // the render kernel), 1 = per-frame slice pre-pass.  VV_SLICE_AUTO takes the
 // pre-pass when the rays that can reach the tree are numerous enough that
 // every leaf is likely decoded several times per frame anyway: n_leaves <=
-// 3 x rays (measured: a full-screen 1080p tree at leaves/rays 1.7 renders
-// 2.4x faster sliced; the cfg4 performers, each seen by ~280 k of the 2 M
-// rays, 2x faster per sample).  (Decoding lazily on first visit inside the
+// 4 x rays (measured on tile shares of cfg2 / cfg3 at leaves/rays 3.4: the
+// slice pass wins, 0.64 vs 0.66 ms and 1.27 vs 1.41 ms; at 5.1 the shell
+// tree decodes faster per sample; the cfg4 performers at 12.7, 2x faster
+// per sample).  (Decoding lazily on first visit inside the
 // render kernel was measured slower: the claim atomics, release fences and
 // sub-warp decode bursts cost more than the skipped decodes.)
 int decode_mode(const vv_tree *t, double n_rays, int policy) {
     if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return 0;
     if (policy == VV_SLICE_PER_FRAME) return 1;
     if (policy == VV_SLICE_DEFERRED) return 2;
-    return (double)t->n_leaves <= 3.0 * n_rays ? 1 : 0;
+    return (double)t->n_leaves <= 4.0 * n_rays ? 1 : 0;
 }
 
 // Rays of `cam` that can reach a tree: the screen rectangle bounding its

@@ -10,7 +10,9 @@ import paper_2202_06088_b200 as vv  # noqa: E402
 from paper_2202_06088_b200 import synthetic  # noqa: E402
 from paper_2202_06088_b200.distributed import TileRenderer  # noqa: E402
 
-tree = synthetic.shell_tree()
+import os  # noqa: E402
+
+tree = synthetic.motion_tree() if os.environ.get("VV_PROBE_TREE") == "motion" else synthetic.shell_tree()
 cam = synthetic.bench_camera()
 
 
@@ -27,10 +29,10 @@ def timed(fn, n=10):
     return s.elapsed_time(e) / n
 
 
-for world in (1, 2, 4, 8):
+for world in (1, 2, 3, 4, 6, 8):
     tr = TileRenderer(cam.width, cam.height, 64, rank=0, world=world)
     row = []
     for mode in ("auto", "per_frame", "per_sample"):
         o = vv.RenderOptions(frame_slice=mode)
-        row.append(f"{mode} {timed(lambda f: tr.render_slab(tree, cam, f % 30, o)):.3f} ms")
+        row.append(f"{mode} {timed(lambda f: tr.render_slab(tree, cam, f % tree.frames, o)):.3f} ms")
     print(f"world {world}: " + " | ".join(row))
