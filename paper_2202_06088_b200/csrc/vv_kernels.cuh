@@ -421,8 +421,15 @@ static_assert(kSliceChunk % 32 == 0, "slice chunk must be whole warps of leaves"
 __host__ __device__ inline size_t slice_stage_floats4(int need, int hh4) {
     return (size_t)kSliceChunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
 }
-__host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4) {
-    return 2 * slice_stage_floats4(need, hh4) * 16 + 32;  // 2 stages + 4 mbarriers
+#ifndef VV_SLICE_STAGE_OUT
+#define VV_SLICE_STAGE_OUT 1  // records staged in shared memory, written out coalesced (0: direct per-lane stores)
+#endif
+// float4 per warp for the staged output records (row stride R4 + 1: no bank conflicts)
+__host__ __device__ inline size_t slice_out_floats4(int kf, int r4) {
+    return VV_SLICE_STAGE_OUT ? (size_t)kf * kSliceChunk * (r4 + 1) : 0;
+}
+__host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4, size_t out4 = 0) {
+    return 2 * slice_stage_floats4(need, hh4) * 16 + 32 + out4 * 16;  // 2 stages + 4 mbarriers + records
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
@@ -442,7 +449,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     const uint32_t mS = p.mS, mG = p.mG;  // chunk masks (host: nz_chunks of the group's rows)
     const int nS = __popc(mS), nG = __popc(mG);
     const size_t stage4 = slice_stage_floats4(nS + nG, hh4);
-    float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 2);
+    const size_t out4 = slice_out_floats4(KF, R4);
+    float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 2 + out4);
+    float4 *obuf = wbase + 2 * stage4 + 2;  // (KF, kSliceChunk, R4 + 1) when VV_SLICE_STAGE_OUT
     // bar[0..1]: a stage's staged copies; bar[2..3]: its colour rows fetched late
     uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
     if (lane == 0) {
@@ -598,12 +607,22 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
                 q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
                 q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
-                float4 *o = p.rec[f] + (base + r) * p.rec4;
+                float4 *o = VV_SLICE_STAGE_OUT ? obuf + ((size_t)f * kSliceChunk + r) * (R4 + 1)
+                                               : p.rec[f] + (base + r) * p.rec4;
 #pragma unroll
                 for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
             }
         }
         __syncwarp();
+        if (VV_SLICE_STAGE_OUT && bright) {  // the chunk's records are contiguous: coalesced float4 stores
+#pragma unroll
+            for (int f = 0; f < KF; ++f) {
+                float4 *dst = p.rec[f] + base * R4;
+                const float4 *src = obuf + (size_t)f * kSliceChunk * (R4 + 1);
+                for (int k = lane; k < rows * R4; k += 32) dst[k] = src[(k / R4) * (R4 + 1) + k % R4];
+            }
+            __syncwarp();
+        }
         // stage consumed: refill it with the chunk two ahead, predicting its
         // colour rows are needed iff this chunk's were
         colour_in = (colour_in & ~(1u << stg)) | ((uint32_t)bright << stg);

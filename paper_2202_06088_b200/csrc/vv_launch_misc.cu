@@ -58,7 +58,8 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
-    const size_t per_warp = slice_warp_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4);
+    const size_t per_warp = slice_warp_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4,
+                                                  slice_out_floats4(KF, slice_rec4(Basis<NM>::S)));
     const size_t limit = 227 * 1024 - 4096;  // opt-in maximum less the static arrays
     const int nw = (int)std::min<size_t>(kSliceWarps, limit / per_warp);
     if (nw < 1)
