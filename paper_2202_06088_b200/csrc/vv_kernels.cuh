@@ -344,8 +344,12 @@ struct CamMultiParams {
     int blocks_x;
 };
 
+#ifndef VV_MULTI_MINB_HI
+#define VV_MULTI_MINB_HI kCamMinBlocks  // resident blocks for 3- and 4-frame walks
+#endif
 template <int NMAX, int KF, bool EDITS, class Entry>
-__global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
+__global__ void __launch_bounds__(kTileRays, KF >= 3 ? VV_MULTI_MINB_HI : kCamMinBlocks)
+    k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int bx = blockIdx.x % p.blocks_x, by = blockIdx.x / p.blocks_x;
     const int x0 = bx * kTW, y0 = by * kTH;
