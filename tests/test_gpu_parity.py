@@ -645,3 +645,36 @@ def test_deferred_colour_bitwise(cuda, cap, monkeypatch):
             _exact(out.rgb, ref.rgb, f"deferred rgb n_max {tree.n_max} frame {f}")
             _exact(out.alpha, ref.alpha, f"deferred alpha n_max {tree.n_max} frame {f}")
             _exact(out.depth, ref.depth, f"deferred depth n_max {tree.n_max} frame {f}")
+
+
+def test_slice_largest_stages_dense_c64_nmax3(cuda):
+    """The widest slice stages: C = 64 dense A / B rows (16 chunks each) and
+    n_max 3 (w_hh 30 x 3 floats) -- the launcher fits one warp per block.
+    Sigma bit-exact and q within 1e-5 vs the oracle; 1..4-frame passes equal
+    the single-frame pass bitwise; render-only slices render bitwise."""
+    rng = np.random.default_rng(21)
+    depth, c, k = 4, 64, 30
+    res = 1 << depth
+    coords = np.argwhere(rng.random((res, res, res)) < 0.5)
+    data = rng.normal(scale=0.3, size=(len(coords), 2 * c + 3 * k)).astype(np.float32)
+    a = rng.normal(scale=0.2, size=(6, c)).astype(np.float32)
+    a[:, 0] = 1.0
+    bases = vv.TemporalBases(a, rng.normal(scale=0.2, size=(6, c)).astype(np.float32))
+    tree = vv.VOctree.from_cells(coords, data, bases, 3, depth=depth)
+    for f in (0, 5):
+        sig, q = oracle.build_slice(tree, f)
+        one = vv.build_frame_cache(tree, f)
+        _exact(one.sigma.cpu().numpy(), sig, f"sigma {f}")
+        assert np.abs(one.q.cpu().numpy() - q).max() < 1e-5
+    for group in ([1], [0, 3], [1, 2, 4], [0, 2, 3, 5]):
+        multi = vv.build_frame_caches(tree, group)
+        for f, m in zip(group, multi):
+            one = vv.build_frame_cache(tree, f)
+            _exact(m.sigma.cpu().numpy(), one.sigma.cpu().numpy(), f"group {group} sigma {f}")
+            _exact(m.q.cpu().numpy(), one.q.cpu().numpy(), f"group {group} q {f}")
+    cam = synthetic.bench_camera(72, 48)
+    for f in (0, 4):
+        ref = vv.render(tree, cam, f, cache=vv.build_frame_cache(tree, f))
+        img = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="per_frame"))
+        _exact(img.rgb, ref.rgb, f"render-only rgb {f}")
+        _exact(img.alpha, ref.alpha, f"render-only alpha {f}")
