@@ -420,17 +420,22 @@ constexpr int kSliceWarps = VV_SLICE_WARPS;
 #define VV_SLICE_CHUNK 64  // leaves per staged chunk (a multiple of 32; lanes loop over their leaves)
 #endif
 constexpr int kSliceChunk = VV_SLICE_CHUNK;
-static_assert(kSliceChunk % 32 == 0, "slice chunk must be whole warps of leaves");
+#ifndef VV_SLICE_CHUNK_MULTI
+#define VV_SLICE_CHUNK_MULTI 32  // leaves per staged chunk for 3- and 4-frame passes (measured 6% faster than 64)
+#endif
+// a KF-frame pass stages KF frames' records per warp: more frames, smaller chunks (more warps)
+__host__ __device__ constexpr int slice_chunk(int kf) { return kf >= 3 ? VV_SLICE_CHUNK_MULTI : kSliceChunk; }
+static_assert(kSliceChunk % 32 == 0 && VV_SLICE_CHUNK_MULTI % 32 == 0, "slice chunk must be whole warps of leaves");
 
-__host__ __device__ inline size_t slice_stage_floats4(int need, int hh4) {
-    return (size_t)kSliceChunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
+__host__ __device__ inline size_t slice_stage_floats4(int need, int hh4, int chunk = kSliceChunk) {
+    return (size_t)chunk * (need + hh4);  // need = staged w_sigma + w_gamma chunks
 }
 #ifndef VV_SLICE_STAGE_OUT
 #define VV_SLICE_STAGE_OUT 1  // records staged in shared memory, written out coalesced (0: direct per-lane stores)
 #endif
 // float4 per warp for the staged output records (row stride R4 + 1: no bank conflicts)
 __host__ __device__ inline size_t slice_out_floats4(int kf, int r4) {
-    return VV_SLICE_STAGE_OUT ? (size_t)kf * kSliceChunk * (r4 + 1) : 0;
+    return VV_SLICE_STAGE_OUT ? (size_t)kf * slice_chunk(kf) * (r4 + 1) : 0;
 }
 __host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4, size_t out4 = 0) {
     return 2 * slice_stage_floats4(need, hh4) * 16 + 32 + out4 * 16;  // 2 stages + 4 mbarriers + records
@@ -446,16 +451,17 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
     __shared__ double dA[KF][kMaxC];  // A rows widened once (the values sigma_pre multiplies)
-    constexpr int kPer = kSliceChunk / 32;  // leaves per lane per chunk
+    constexpr int kChunk = slice_chunk(KF);
+    constexpr int kPer = kChunk / 32;  // leaves per lane per chunk
     constexpr int R4 = slice_rec4(Basis<NMAX>::S);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hh4 = p.T.hh4;
     const uint32_t mS = p.mS, mG = p.mG;  // chunk masks (host: nz_chunks of the group's rows)
     const int nS = __popc(mS), nG = __popc(mG);
-    const size_t stage4 = slice_stage_floats4(nS + nG, hh4);
+    const size_t stage4 = slice_stage_floats4(nS + nG, hh4, kChunk);
     const size_t out4 = slice_out_floats4(KF, R4);
     float4 *wbase = reinterpret_cast<float4 *>(smem_raw) + (size_t)warp * (2 * stage4 + 2 + out4);
-    float4 *obuf = wbase + 2 * stage4 + 2;  // (KF, kSliceChunk, R4 + 1) when VV_SLICE_STAGE_OUT
+    float4 *obuf = wbase + 2 * stage4 + 2;  // (KF, kChunk, R4 + 1) when VV_SLICE_STAGE_OUT
     // bar[0..1]: a stage's staged copies; bar[2..3]: its colour rows fetched late
     uint64_t *bar = reinterpret_cast<uint64_t *>(wbase + 2 * stage4);
     if (lane == 0) {
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     __syncthreads();
     const int C = p.T.C;
     const int64_t ls = p.T.lstride;
-    const int64_t n_chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
+    const int64_t n_chunks = (p.n_leaves + kChunk - 1) / kChunk;
     const int nw = blockDim.x >> 5;  // <= kSliceWarps: the launcher fits the stages in shared memory
     const int64_t n_warps = (int64_t)gridDim.x * nw, wid = (int64_t)blockIdx.x * nw + warp;
 #if VV_SLICE_RUNS
@@ -481,25 +487,25 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // neighbours in HBM
     const int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
 #endif
-    // stage: [needed w_sigma chunks][kSliceChunk leaves] | [needed w_gamma chunks][kSliceChunk] | [leaves][hh4]
-    auto rows_of = [&](int64_t c) { return (int)min((int64_t)kSliceChunk, p.n_leaves - c * kSliceChunk); };
+    // stage: [needed w_sigma chunks][kChunk leaves] | [needed w_gamma chunks][kChunk] | [leaves][hh4]
+    auto rows_of = [&](int64_t c) { return (int)min((int64_t)kChunk, p.n_leaves - c * kChunk); };
     auto issue_colour = [&](int64_t c, int stg, uint64_t *b, bool arrive) {
-        const int64_t base = c * kSliceChunk;
+        const int64_t base = c * kChunk;
         const int rows = rows_of(c);
-        float4 *dst = wbase + stg * stage4 + (size_t)nS * kSliceChunk;
+        float4 *dst = wbase + stg * stage4 + (size_t)nS * kChunk;
         const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
         if (arrive) mbar_expect_tx(b, (uint32_t)nG * cb + hb);
-        for (uint32_t m = mG; m; m &= m - 1, dst += kSliceChunk)
+        for (uint32_t m = mG; m; m &= m - 1, dst += kChunk)
             bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, b);
         bulk_g2s(dst, p.T.hh + base * hh4, hb, b);
     };
     auto issue = [&](int64_t c, int stg, bool colour) {  // lane 0
-        const int64_t base = c * kSliceChunk;
+        const int64_t base = c * kChunk;
         const int rows = rows_of(c);
         float4 *dst = wbase + stg * stage4;
         const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
         mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
-        for (uint32_t m = mS; m; m &= m - 1, dst += kSliceChunk)
+        for (uint32_t m = mS; m; m &= m - 1, dst += kChunk)
             bulk_g2s(dst, p.T.sig + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
         if (colour) issue_colour(c, stg, &bar[stg], false);
     };
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     for (int64_t c = c_begin; c < c_end; c += c_step, ++k) {
         const int stg = k & 1;
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
-        const int64_t base = c * kSliceChunk;
+        const int64_t base = c * kChunk;
         const int rows = rows_of(c);
         const float4 *st4 = wbase + stg * stage4;
         // sigma_pre (kernels.py:374-381, f64, sequential), every frame, over
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
             for (int f = 0; f < KF; ++f) sp[u][f] = 0.0;
             if (r < rows) {
                 const float4 *sv = st4 + r;
-                for (uint32_t m = mS; m; m &= m - 1, sv += kSliceChunk) {
+                for (uint32_t m = mS; m; m &= m - 1, sv += kChunk) {
                     const float4 v = ld4<false>(sv);
                     const double w[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
                     const int cc = 4 * (__ffs(m) - 1);
@@ -577,8 +583,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
             float gp[KF];
 #pragma unroll
             for (int f = 0; f < KF; ++f) gp[f] = 0.0f;
-            const float4 *sv = st4 + (size_t)nS * kSliceChunk + r;
-            for (uint32_t m = mG; m; m &= m - 1, sv += kSliceChunk) {
+            const float4 *sv = st4 + (size_t)nS * kChunk + r;
+            for (uint32_t m = mG; m; m &= m - 1, sv += kChunk) {
                 const float4 g = ld4<false>(sv);
                 const float gw[4] = {g.x, g.y, g.z, g.w};
                 const int cc = 4 * (__ffs(m) - 1);
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                     }
                 }
             }
-            const float4 *shh = st4 + (size_t)(nS + nG) * kSliceChunk + (size_t)r * hh4;
+            const float4 *shh = st4 + (size_t)(nS + nG) * kChunk + (size_t)r * hh4;
             float wh[4 * Basis<NMAX>::HH4];
             load_hh<NMAX, false>(shh, wh);
 #pragma unroll
@@ -611,7 +617,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
                 q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
                 q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
-                float4 *o = VV_SLICE_STAGE_OUT ? obuf + ((size_t)f * kSliceChunk + r) * (R4 + 1)
+                float4 *o = VV_SLICE_STAGE_OUT ? obuf + ((size_t)f * kChunk + r) * (R4 + 1)
                                                : p.rec[f] + (base + r) * p.rec4;
 #pragma unroll
                 for (int i = 0; i < R4; ++i) o[i] = make_float4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
 #pragma unroll
             for (int f = 0; f < KF; ++f) {
                 float4 *dst = p.rec[f] + base * R4;
-                const float4 *src = obuf + (size_t)f * kSliceChunk * (R4 + 1);
+                const float4 *src = obuf + (size_t)f * kChunk * (R4 + 1);
                 for (int k = lane; k < rows * R4; k += 32) dst[k] = src[(k / R4) * (R4 + 1) + k % R4];
             }
             __syncwarp();

@@ -58,8 +58,10 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
-    const size_t per_warp = slice_warp_smem_bytes(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4,
-                                                  slice_out_floats4(KF, slice_rec4(Basis<NM>::S)));
+    constexpr int kChunk = slice_chunk(KF);
+    const size_t per_warp =
+        2 * slice_stage_floats4(__builtin_popcount(p.mS) + __builtin_popcount(p.mG), p.T.hh4, kChunk) * 16 + 32 +
+        slice_out_floats4(KF, slice_rec4(Basis<NM>::S)) * 16;
     const size_t limit = 227 * 1024 - 4096;  // opt-in maximum less the static arrays
     const int nw = (int)std::min<size_t>(kSliceWarps, limit / per_warp);
     if (nw < 1)
@@ -68,7 +70,7 @@ static int go_slice(const SliceParams &p, cudaStream_t st) {
     auto kern = k_build_slice<NM, KF>;
     int r = prep_smem(kern, smem);
     if (r) return r;
-    const int64_t chunks = (p.n_leaves + kSliceChunk - 1) / kSliceChunk;
+    const int64_t chunks = (p.n_leaves + kChunk - 1) / kChunk;
     const unsigned want = (unsigned)((chunks + nw - 1) / nw);
     unsigned grid = persistent_grid(kern, nw * 32, smem, want);
     if (VV_SLICE_BPS > 0) {
