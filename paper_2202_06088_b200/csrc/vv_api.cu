@@ -39,10 +39,6 @@ struct vv_tree {
     int2 *d_edit_t;
     float *d_a, *d_b;
     std::vector<float> h_a, h_b;  // host copies of the basis rows (slice-pass chunk masks)
-    // deferred renders: per-leaf stamp (== epoch: shaded in the current
-    // render), allocated on first use
-    mutable uint32_t *d_stamp = nullptr;
-    mutable uint32_t epoch = 0;
 };
 
 // float4 chunks of the frame's fp32 A (which = 0) or B (1) row holding a
@@ -439,7 +435,6 @@ int vv_tree_free(vv_tree *t) {
     cudaFree(t->d_sig);
     cudaFree(t->d_gam);
     cudaFree(t->d_hh);
-    cudaFree(t->d_stamp);
     cudaFree(t->d_edit_rgb);
     cudaFree(t->d_edit_t);
     cudaFree(t->d_a);
@@ -650,24 +645,13 @@ static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned g
     int cap = kDeferCap;  // VV_DEFER_CAP: tests force the overflow path with a small record
     if (const char *e = getenv("VV_DEFER_CAP")) cap = std::max(1, atoi(e));
     const int rec4 = slice_rec4(t->S);
-    if (!t->d_stamp) {
-        if (cudaMalloc(&t->d_stamp, (size_t)std::max<int64_t>(nl, 1) * 4) != cudaSuccess) {
-            cudaGetLastError();
-            t->d_stamp = nullptr;
-            return set_error(VV_E_NOMEM, "stamp allocation failed");
-        }
-        cudaMemsetAsync(t->d_stamp, 0, (size_t)std::max<int64_t>(nl, 1) * 4, st);
-        t->epoch = 0;
-    }
-    if (++t->epoch == 0) {  // wrapped: clear the stamps
-        cudaMemsetAsync(t->d_stamp, 0, (size_t)std::max<int64_t>(nl, 1) * 4, st);
-        t->epoch = 1;
-    }
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    // per-call stamps (concurrent renders of one tree must not share them)
+    const size_t b_stamp = al(nl * 4);
     const size_t b_sig = al(nl * 8), b_rec = al((size_t)nl * rec4 * 16), b_list = al(nl * 4), b_cnt = 256,
                  b_aacc = al(npix * 8), b_count = al(npix * 4), b_sl = al((size_t)npix * cap * 4),
                  b_sw = al((size_t)npix * cap * 8), b_ovf = al(npix * 4);
-    const size_t total = b_sig + b_rec + b_list + b_cnt + b_aacc + b_count + b_sl + b_sw + b_ovf;
+    const size_t total = b_stamp + b_sig + b_rec + b_list + b_cnt + b_aacc + b_count + b_sl + b_sw + b_ovf;
     pool_setup(t->device);
     Transient tr;
     if (cudaMallocAsync(&tr.mem, total, st) != cudaSuccess) {
@@ -684,6 +668,7 @@ static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned g
     };
     DeferBuffers B;
     memset(&B, 0, sizeof(B));
+    uint32_t *stamp = reinterpret_cast<uint32_t *>(take(b_stamp));
     B.sig8 = reinterpret_cast<double *>(take(b_sig));
     B.rec = reinterpret_cast<float4 *>(take(b_rec));
     B.list = reinterpret_cast<uint32_t *>(take(b_list));
@@ -694,8 +679,8 @@ static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned g
     B.D.sw = reinterpret_cast<double *>(take(b_sw));
     B.ovf = reinterpret_cast<uint32_t *>(take(b_ovf));
     B.D.sig8 = B.sig8;
-    B.D.stamp = t->d_stamp;
-    B.D.epoch = t->epoch;
+    B.D.stamp = stamp;
+    B.D.epoch = 1;
     B.D.cap = cap;
     B.D.npix = npix;
     B.n_leaves = nl;
@@ -703,7 +688,8 @@ static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned g
     B.mS = B.mG = 0;
     B.mS = host_nz_chunks(t, p.frame, 0);
     B.mG = host_nz_chunks(t, p.frame, 1);
-    if (cudaMemsetAsync(B.counters, 0, 8, st) != cudaSuccess) return set_error(VV_E_CUDA, "memset failed");
+    if (cudaMemsetAsync(B.counters, 0, 8, st) != cudaSuccess || cudaMemsetAsync(stamp, 0, b_stamp, st) != cudaSuccess)
+        return set_error(VV_E_CUDA, "deferred render: memset failed");
     p.S.rec = B.rec;
     p.S.rec4 = rec4;
     return launch_deferred(t->n_max, wide, p, B, grid, st);

@@ -23,7 +23,7 @@ using namespace vv;
 
 struct DeferView {
     const double *sig8;  // (n_leaves) max(0, sigma_pre) of the frame
-    uint32_t *stamp;     // (n_leaves) == epoch: some ray shades the leaf this render
+    uint32_t *stamp;     // (n_leaves) == epoch: some ray shades the leaf (per-call, zeroed)
     uint32_t epoch;
     uint32_t *sleaf;     // (cap, n_pix) shaded leaves per ray, in order (sample-major: coalesced)
     double *sw;          // (cap, n_pix) their compositing weights
