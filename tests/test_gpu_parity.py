@@ -678,3 +678,31 @@ def test_slice_largest_stages_dense_c64_nmax3(cuda):
         img = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="per_frame"))
         _exact(img.rgb, ref.rgb, f"render-only rgb {f}")
         _exact(img.alpha, ref.alpha, f"render-only alpha {f}")
+
+
+def test_no_device_memory_growth(cuda):
+    """Repeated renders in every decode mode, slice caches and playback
+    release their transient device memory (stream-ordered pool frees)."""
+    import torch
+
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=5)
+    cam = synthetic.bench_camera(96, 64)
+    modes = ("auto", "per_sample", "per_frame", "deferred")
+
+    def work():
+        for f in range(8):
+            for m in modes:
+                vv.render(tree, cam, f, vv.RenderOptions(frame_slice=m))
+            c = vv.build_frame_cache(tree, f)
+            vv.render(tree, cam, f, cache=c)
+            del c
+        for _ in vv.render_sequence(tree, cam, range(8)):
+            pass
+        torch.cuda.synchronize()
+
+    work()  # pools and caches reach their steady size
+    free0 = torch.cuda.mem_get_info(cuda)[0]
+    for _ in range(5):
+        work()
+    free1 = torch.cuda.mem_get_info(cuda)[0]
+    assert free0 - free1 < (64 << 20), f"device memory fell by {(free0 - free1) >> 20} MB"
