@@ -975,7 +975,10 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
             if (r) return r;
         }
     }
-    return launch_scene(t0->n_max, wide, p, grid, smem, st);
+    bool lean = true;  // every instance decoded per sample, no edits: the lean instantiation
+    for (int i = 0; i < n_inst; ++i)
+        if (p.inst[i].S.rec || inst[i].tree->has_edits) lean = false;
+    return launch_scene(t0->n_max, wide, lean, p, grid, smem, st);
 }
 
 static int segments_impl(const vv_tree *t, const double *origins, const double *dirs, int64_t n, double tmin,

@@ -224,8 +224,11 @@ struct SceneParams {
     float *image, *alpha, *depth;
 };
 
-template <int NMAX, class Entry>
-__global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__ SceneParams p) {
+// CACHED 2: per-instance decode decided at run time (some instances sliced);
+// CACHED 0 with EDITS false: every instance decoded per sample and no
+// edits (the common scene case, k_render_scene_lean).
+template <int NMAX, class Entry, int CACHED, bool EDITS>
+__device__ __forceinline__ void scene_body(const SceneParams &p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
     __shared__ uint32_t sM[kMaxInst][2];
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
             scaled = true;
         }
         FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight, sM[i][0], sM[i][1]};
-        Shader<NMAX, 2, true, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
+        Shader<NMAX, CACHED, EDITS, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
         Ray ray;
         if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
             traverse<Entry>(v.T.child, v.T.depth, ray, smem_raw, sh);
@@ -327,6 +330,21 @@ __global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__
     }
     if (p.alpha) p.alpha[pix] = (float)A;
     if (p.depth) p.depth[pix] = (float)D;
+}
+
+template <int NMAX, class Entry>
+__global__ void __launch_bounds__(kBlock) k_render_scene(const __grid_constant__ SceneParams p) {
+    scene_body<NMAX, Entry, 2, true>(p);
+}
+
+#ifdef VV_SCENE_LEAN_MINB
+#define VV_SCENE_LEAN_BOUNDS __launch_bounds__(kBlock, VV_SCENE_LEAN_MINB)
+#else
+#define VV_SCENE_LEAN_BOUNDS __launch_bounds__(kBlock)
+#endif
+template <int NMAX, class Entry>
+__global__ void VV_SCENE_LEAN_BOUNDS k_render_scene_lean(const __grid_constant__ SceneParams p) {
+    scene_body<NMAX, Entry, 0, false>(p);
 }
 
 // ------------------------------------------------------------------ playback, several frames
@@ -799,7 +817,7 @@ int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p,
                   cudaStream_t st);
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
                         cudaStream_t st);
-int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
+int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);

@@ -3,19 +3,20 @@
 
 namespace vvk {
 
-template <int NM, class Entry>
+template <int NM, class Entry, bool LEAN>
 static int go(const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st) {
-    auto kern = k_render_scene<NM, Entry>;
+    auto kern = LEAN ? k_render_scene_lean<NM, Entry> : k_render_scene<NM, Entry>;
     int r = prep_smem(kern, smem);
     if (r) return r;
     kern<<<grid, kBlock, smem, st>>>(p);
     return check_launch("render_scene");
 }
 
-int launch_scene(int nmax, bool wide, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st) {
+int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st) {
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
-        return wide ? go<NM, EntryW>(p, grid, smem, st) : go<NM, EntryN>(p, grid, smem, st);
+        if (lean) return wide ? go<NM, EntryW, true>(p, grid, smem, st) : go<NM, EntryN, true>(p, grid, smem, st);
+        return wide ? go<NM, EntryW, false>(p, grid, smem, st) : go<NM, EntryN, false>(p, grid, smem, st);
     });
 }
 
