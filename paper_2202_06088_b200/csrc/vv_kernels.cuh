@@ -414,16 +414,21 @@ struct SliceParams {
     int skip_dark;              // render-internal slice: dark chunks get sigma only (no colour)
 };
 
-// build_slice_kernel (kernels.py:397-407).  Persistent warps, each owning a
-// double-buffered shared-memory stage: one lane issues TMA bulk copies
-// (cp.async.bulk, completed on an mbarrier) for a chunk of 32 consecutive
-// leaves -- one per w_sigma / w_gamma float4 chunk the group's A / B rows do
-// not zero out (chunk-major planes: 512 contiguous bytes each) and one for
-// their w_hh rows -- while the warp slices the previous chunk, one leaf per
-// lane, from shared memory.  Chunks whose basis entries are all zero are
-// never read: their products are +-0 and the sums skip them bit-exactly
-// (nz_chunks).  Rows reach shared memory without touching registers; the
-// next chunk streams in during the fp64 sigma chains.
+// build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
+// consecutive leaves (64; 32 for 3- and 4-frame passes), strided over the
+// grid so the chunks in flight are neighbours in HBM.  Each warp owns a
+// double-buffered shared-memory stage.  One lane issues the chunk's TMA
+// bulk copies, completed on an mbarrier: one per w_sigma / w_gamma float4
+// chunk the group's A / B rows do not zero out (chunk-major planes, 1 KB
+// contiguous each) and one for the w_hh rows.  Meanwhile the warp slices
+// the previous chunk, each lane taking leaves lane and lane + 32, from
+// shared memory.
+//   * Basis chunks that are all zero are never read; their products are
+//     +-0 and the sums skip them bit-exactly (nz_chunks).
+//   * The records are staged in shared memory and leave as the chunk's
+//     contiguous bytes (coalesced stores).
+//   * Render-only passes also skip the colour of chunks dark in every frame
+//     (see below).
 #ifndef VV_SLICE_WARPS
 #define VV_SLICE_WARPS 4  // max warps per block (fewer when a warp's stages are large)
 #endif
@@ -454,9 +459,6 @@ __host__ __device__ inline size_t slice_stage_floats4(int need, int hh4, int chu
 // float4 per warp for the staged output records (row stride R4 + 1: no bank conflicts)
 __host__ __device__ inline size_t slice_out_floats4(int kf, int r4) {
     return VV_SLICE_STAGE_OUT ? (size_t)kf * slice_chunk(kf) * (r4 + 1) : 0;
-}
-__host__ __device__ inline size_t slice_warp_smem_bytes(int need, int hh4, size_t out4 = 0) {
-    return 2 * slice_stage_floats4(need, hh4) * 16 + 32 + out4 * 16;  // 2 stages + 4 mbarriers + records
 }
 
 // KF frames (playback groups) are sliced from ONE read of the payload: a
