@@ -39,6 +39,7 @@ struct vv_tree {
     int2 *d_edit_t;
     float *d_a, *d_b;
     std::vector<float> h_a, h_b;  // host copies of the basis rows (slice-pass chunk masks)
+    float dark_frac = 0.0f;       // share of leaves with sigma 0, over a few frames (queue threshold)
 };
 
 // float4 chunks of the frame's fp32 A (which = 0) or B (1) row holding a
@@ -402,6 +403,29 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     v.hh4 = hh4;
     v.frames = d->frames;
     v.nmax = d->n_max;
+    // dark fraction over frames 0, T/2, T-1 (picks the camera kernel's
+    // queue threshold; the images are bitwise the same either way)
+    if (nl > 0) {
+        unsigned long long *cnt = nullptr;
+        if (cudaMalloc(&cnt, sizeof(unsigned long long)) == cudaSuccess) {
+            const int fr[3] = {0, d->frames / 2, d->frames - 1};
+            unsigned long long total = 0;
+            int used = 0;
+            for (int k = 0; k < 3; ++k) {
+                if (k && fr[k] == fr[k - 1]) continue;
+                unsigned long long v = 0;
+                if (cudaMemset(cnt, 0, sizeof(v)) != cudaSuccess ||
+                    launch_count_dark(t->view, fr[k], host_nz_chunks(t, fr[k], 0), nl, cnt, nullptr) != VV_OK ||
+                    cudaMemcpy(&v, cnt, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+                    break;
+                total += v;
+                ++used;
+            }
+            if (used) t->dark_frac = (float)((double)total / ((double)nl * used));
+            cudaFree(cnt);
+        }
+        cudaGetLastError();
+    }
     *out = t;
     return VV_OK;
 }
@@ -758,7 +782,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
-    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st);
+    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, t->dark_frac > 0.5f);
 }
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,

@@ -35,6 +35,7 @@ struct DeferView {
 
 // The weight half of Shader::leaf (same fp64 operations, same order).
 struct DeferShader {
+    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     const DeferView &D;
     double early_stop;

@@ -282,18 +282,23 @@ struct Trav {
 constexpr int kSegMin = VV_SEG_MIN;
 constexpr int kSegSlots = VV_SEG_SLOTS;
 static_assert(kSegSlots >= kSegMin + 3, "a last-level node queues up to 4 segments");
+// every visitor declares the queue geometry it walks with (kSegMin,
+// kSegSlots); Shader takes it as a parameter: long, mostly dark walks prefer
+// a longer queue
 // (the visit counts only for visitors that report them, kPops)
-__host__ __device__ constexpr uint32_t seg_bytes_per_thread(bool pops) { return kSegSlots * (pops ? 24u : 20u); }
+__host__ __device__ constexpr uint32_t seg_bytes_per_thread(bool pops, int slots = kSegSlots) {
+    return (uint32_t)slots * (pops ? 24u : 20u);
+}
 struct SegBuf {
     uint32_t t0, t1, leaf, pops;  // shared addresses of this thread's slot 0
     uint32_t sl, sd;              // slot strides (bytes) of the int and double arrays
-    __device__ __forceinline__ void init(uint32_t base, int nthreads, int tid) {
+    __device__ __forceinline__ void init(uint32_t base, int nthreads, int tid, int slots) {
         sl = 4u * nthreads;
         sd = 8u * nthreads;
         t0 = base + 8u * tid;
-        t1 = t0 + kSegSlots * sd;
-        leaf = base + 2 * kSegSlots * sd + 4u * tid;
-        pops = leaf + kSegSlots * sl;
+        t1 = t0 + slots * sd;
+        leaf = base + 2 * slots * sd + 4u * tid;
+        pops = leaf + slots * sl;
     }
     template <bool POPS>
     __device__ __forceinline__ void put(int s, int32_t L, double a, double b, int np) const {
@@ -399,7 +404,7 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
                 seg.put<Visitor::kPops>(n, cp[s], st[s], st[s + 1], vis.pop_count());
                 n += (keep >> s) & 1;
             }
-            if (n >= kSegMin) return n;
+            if (n >= Visitor::kSegMin) return n;
             continue;
         }
         if (!keep) {
@@ -461,8 +466,9 @@ __device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int 
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     const int nt = blockDim.x, tid = threadIdx.x;
     SegBuf seg;
-    seg.init(sbase, nt, tid);
-    const uint32_t base = sbase + seg_bytes_per_thread(Visitor::kPops) * nt + (uint32_t)tid * Entry::kBytes;
+    seg.init(sbase, nt, tid, Visitor::kSegSlots);
+    const uint32_t base =
+        sbase + seg_bytes_per_thread(Visitor::kPops, Visitor::kSegSlots) * nt + (uint32_t)tid * Entry::kBytes;
     const uint32_t stride = (uint32_t)nt * Entry::kBytes;
     Trav<Entry> t;
     t.init(r, base);
@@ -472,7 +478,7 @@ __device__ __forceinline__ void traverse(const int32_t *__restrict__ child, int 
         int n = 0;
         if (alive) {
             n = trav_next(t, child, depth, r, base, stride, vis, seg);
-            alive = n >= kSegMin;  // fewer: the walk is exhausted
+            alive = n >= Visitor::kSegMin;  // fewer: the walk is exhausted
         }
         __syncwarp(mask);
         if (n && vis.batch(seg, n)) alive = false;
@@ -662,9 +668,10 @@ struct FrameCtx {
 
 // CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
 // run time by S.rec != nullptr (scene kernel, per-instance slices).
-template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false>
+template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false, int SEG = VV_SEG_MIN>
 struct Shader {
     static constexpr bool kPops = POPS;  // exact node-pop counts (stats)
+    static constexpr int kSegMin = SEG, kSegSlots = SEG + 3;
     const TreeView &T;
     const SliceView &S;
     const FrameCtx &F;
@@ -830,6 +837,7 @@ struct Shader {
 constexpr int kMaxMulti = 4;
 template <int NMAX, int KF, bool EDITS>
 struct ShaderMulti {
+    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     const TreeView &T;
     const SliceView *S;  // KF frame slices
@@ -942,6 +950,7 @@ struct ShaderMulti {
 
 // Traversal-only visitors (count / collect, kernels.py:313-367)
 struct CountVisitor {
+    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     int64_t count = 0;
     __device__ __forceinline__ void pop() {}
@@ -952,6 +961,7 @@ struct CountVisitor {
     }
 };
 struct CollectVisitor {
+    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     int64_t *leaf_out;
     double *t0_out, *t1_out;

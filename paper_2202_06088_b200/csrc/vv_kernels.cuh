@@ -169,7 +169,7 @@ __device__ __forceinline__ void cam_write(const CamParams &p, int ix, int iy, lo
 // (each warp an 8x4-pixel chunk), so the block's warps stay on neighbouring
 // pixels (L1 reuse of node rows and slice rows).  Refill-on-finish
 // (persistent) variants were measured slower: see DESIGN.md.
-template <int NMAX, int CACHED, bool EDITS, class Entry>
+template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(const __grid_constant__ CamParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxC], sB[kMaxC];
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         if (ix < p.cam.width && iy < p.cam.height) {
             double dx, dy, dz;
             camera_ray(p.cam, ix, iy, dx, dy, dz);
-            Shader<NMAX, CACHED, EDITS, false> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+            Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
             Ray ray;
             if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
                 traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
@@ -711,6 +711,7 @@ struct TermParams {
 };
 
 struct TerminateVisitor {
+    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     const TreeView &T;
     const float *sA;
@@ -771,9 +772,9 @@ inline int with_nmax(int nmax, F &&f) {
 
 // traversal shared memory per block: segment queues + stacks (traverse());
 // pops: the visitor queues node-visit counts (k_render_rays)
-inline size_t stack_bytes(int depth, bool wide, bool pops = false, int threads = kBlock) {
-    return (size_t)threads *
-           (seg_bytes_per_thread(pops) + (size_t)stack_cap(depth) * (wide ? EntryW::kBytes : EntryN::kBytes));
+inline size_t stack_bytes(int depth, bool wide, bool pops = false, int threads = kBlock, int slots = kSegSlots) {
+    return (size_t)threads * (seg_bytes_per_thread(pops, slots) +
+                              (size_t)stack_cap(depth) * (wide ? EntryW::kBytes : EntryN::kBytes));
 }
 
 template <class Kern>
@@ -815,8 +816,10 @@ inline unsigned persistent_grid(Kern k, int block, size_t smem, unsigned max_blo
 int launch_rays(int nmax, int mode, bool edits, bool wide, bool visits, const RaysParams &p, unsigned grid,
                 size_t smem, cudaStream_t st);
 // one block per 32x16 tile (max_blocks = tile count)
+int launch_count_dark(const TreeView &T, int frame, uint32_t mS, int64_t n, unsigned long long *count,
+                      cudaStream_t st);
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
-                  cudaStream_t st);
+                  cudaStream_t st, bool long_queue = false);
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
                         cudaStream_t st);
 int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);

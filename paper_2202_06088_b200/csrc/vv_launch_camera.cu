@@ -3,9 +3,13 @@
 
 namespace vvk {
 
-template <int NM, int CACHED, bool EDITS, class Entry>
+// queue threshold for trees whose frames are mostly dark (long walks, few
+// shaded leaves: the cfg3 motion tree renders 6% faster with 8 than with 6)
+constexpr int kSegLong = 8;
+
+template <int NM, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t st) {
-    auto kern = k_render_camera<NM, CACHED, EDITS, Entry>;
+    auto kern = k_render_camera<NM, CACHED, EDITS, Entry, SEG>;
     int r = prep_smem(kern, smem);
     if (r) return r;
     kern<<<max_blocks, kTileRays, smem, st>>>(p);
@@ -24,7 +28,15 @@ static int pick(int mode, bool edits, const CamParams &p, unsigned grid, size_t 
 }
 
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned grid, size_t smem,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool long_queue) {
+    if (long_queue && mode == 1 && !edits) {
+        smem = stack_bytes(p.T.depth, wide, false, kTileRays, kSegLong + 3);
+        return with_nmax(nmax, [&](auto N) {
+            constexpr int NM = decltype(N)::value;
+            return wide ? go<NM, 1, false, EntryW, kSegLong>(p, grid, smem, st)
+                        : go<NM, 1, false, EntryN, kSegLong>(p, grid, smem, st);
+        });
+    }
     smem = stack_bytes(p.T.depth, wide, false, kTileRays);  // this TU's queue geometry (A/B builds vary it)
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;

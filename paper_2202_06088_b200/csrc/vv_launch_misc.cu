@@ -56,6 +56,28 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
 }
 
 
+// leaves whose sigma is 0 at `frame` (the tree's dark fraction, estimated at
+// upload from a few frames, picks the camera kernel's queue threshold)
+__global__ void k_count_dark(const __grid_constant__ TreeView T, int frame, uint32_t mS, int64_t n,
+                             unsigned long long *count) {
+    __shared__ float sA[kMaxC];
+    for (int c = threadIdx.x; c < kMaxC; c += blockDim.x)
+        sA[c] = c < T.C ? T.basis_a[(size_t)frame * T.C + c] : 0.0f;
+    __syncthreads();
+    unsigned long long dark = 0;
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n; L += (int64_t)gridDim.x * blockDim.x)
+        dark += sigma_pre(T.sig + L, T.lstride, sA, T.C, mS) > 0.0 ? 0 : 1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dark += __shfl_down_sync(0xffffffffu, dark, o);
+    if ((threadIdx.x & 31) == 0 && dark) atomicAdd(count, dark);
+}
+
+int launch_count_dark(const TreeView &T, int frame, uint32_t mS, int64_t n, unsigned long long *count,
+                      cudaStream_t st) {
+    k_count_dark<<<592, 256, 0, st>>>(T, frame, mS, n, count);
+    return check_launch("count_dark");
+}
+
 template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
     constexpr int kChunk = slice_chunk(KF);
