@@ -834,7 +834,7 @@ int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *fr
     const unsigned grid = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
     if (grid == 0) return VV_OK;
     return launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid,
-                               (cudaStream_t)stream);
+                               (cudaStream_t)stream, t->dark_frac > 0.5f);
 }
 
 int vv_render_camera_tiles(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,

@@ -835,9 +835,9 @@ struct Shader {
 // same segments in the same order as a single-frame render -- identical
 // results.  The walk ends when every frame has terminated.
 constexpr int kMaxMulti = 4;
-template <int NMAX, int KF, bool EDITS>
+template <int NMAX, int KF, bool EDITS, int SEG = VV_SEG_MIN>
 struct ShaderMulti {
-    static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
+    static constexpr int kSegMin = SEG, kSegSlots = SEG + 3;
     static constexpr bool kPops = false;
     const TreeView &T;
     const SliceView *S;  // KF frame slices

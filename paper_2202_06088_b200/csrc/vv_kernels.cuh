@@ -365,7 +365,7 @@ struct CamMultiParams {
 #ifndef VV_MULTI_MINB_HI
 #define VV_MULTI_MINB_HI kCamMinBlocks  // resident blocks for 3- and 4-frame walks
 #endif
-template <int NMAX, int KF, bool EDITS, class Entry>
+template <int NMAX, int KF, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 __global__ void __launch_bounds__(kTileRays, KF >= 3 ? VV_MULTI_MINB_HI : kCamMinBlocks)
     k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kTileRays, KF >= 3 ? VV_MULTI_MINB_HI : kCamMi
         if (ix >= p.cam.width || iy >= p.cam.height) return;
         double dx, dy, dz;
         camera_ray(p.cam, ix, iy, dx, dy, dz);
-        ShaderMulti<NMAX, KF, EDITS> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
+        ShaderMulti<NMAX, KF, EDITS, SEG> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
                                         (float)dz);
         Ray ray;
         if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
@@ -821,7 +821,7 @@ int launch_count_dark(const TreeView &T, int frame, uint32_t mS, int64_t n, unsi
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
                   cudaStream_t st, bool long_queue = false);
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
-                        cudaStream_t st);
+                        cudaStream_t st, bool long_queue = false);
 int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);

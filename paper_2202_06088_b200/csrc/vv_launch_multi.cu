@@ -4,10 +4,13 @@
 
 namespace vvk {
 
-template <int NM, int KF, bool EDITS, class Entry>
+// queue threshold for mostly dark trees (as vv_launch_camera.cu)
+constexpr int kSegLong = 8;
+
+template <int NM, int KF, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 static int go(const CamMultiParams &p, unsigned grid, cudaStream_t st) {
-    auto kern = k_render_camera_multi<NM, KF, EDITS, Entry>;
-    const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes, false, kTileRays);
+    auto kern = k_render_camera_multi<NM, KF, EDITS, Entry, SEG>;
+    const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes, false, kTileRays, SEG + 3);
     int r = prep_smem(kern, smem);
     if (r) return r;
     kern<<<grid, kTileRays, smem, st>>>(p);
@@ -24,8 +27,23 @@ static int pick(int kf, bool edits, const CamMultiParams &p, unsigned grid, cuda
     }
 }
 
+template <int NM, class Entry>
+static int pick_long(int kf, const CamMultiParams &p, unsigned grid, cudaStream_t st) {
+    switch (kf) {
+        case 2: return go<NM, 2, false, Entry, kSegLong>(p, grid, st);
+        case 3: return go<NM, 3, false, Entry, kSegLong>(p, grid, st);
+        case 4: return go<NM, 4, false, Entry, kSegLong>(p, grid, st);
+        default: return set_error(VV_E_UNSUPPORTED, "%d frames per walk (2..%d)", kf, kMaxMulti);
+    }
+}
+
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool long_queue) {
+    if (long_queue && !edits)
+        return with_nmax(nmax, [&](auto N) {
+            constexpr int NM = decltype(N)::value;
+            return wide ? pick_long<NM, EntryW>(kf, p, grid, st) : pick_long<NM, EntryN>(kf, p, grid, st);
+        });
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
         return wide ? pick<NM, EntryW>(kf, edits, p, grid, st) : pick<NM, EntryN>(kf, edits, p, grid, st);
