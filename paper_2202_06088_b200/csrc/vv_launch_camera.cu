@@ -5,7 +5,10 @@ namespace vvk {
 
 // queue threshold for trees whose frames are mostly dark (long walks, few
 // shaded leaves: the cfg3 motion tree renders 6% faster with 8 than with 6)
-constexpr int kSegLong = 8;
+#ifndef VV_SEG_LONG
+#define VV_SEG_LONG 8
+#endif
+constexpr int kSegLong = VV_SEG_LONG;
 
 template <int NM, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t st) {

@@ -5,7 +5,10 @@
 namespace vvk {
 
 // queue threshold for mostly dark trees (as vv_launch_camera.cu)
-constexpr int kSegLong = 8;
+#ifndef VV_SEG_LONG
+#define VV_SEG_LONG 8
+#endif
+constexpr int kSegLong = VV_SEG_LONG;
 
 template <int NM, int KF, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 static int go(const CamMultiParams &p, unsigned grid, cudaStream_t st) {
