@@ -100,6 +100,14 @@ __device__ __forceinline__ double pmin(double a, double b) { return (b < a) ? b 
 __device__ __forceinline__ void prefetch_l1(const void *p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
+// ---- programmatic dependent launch: a kernel launched with the
+// programmatic-serialization attribute may start while the previous kernel
+// on the stream finishes; it does its read-only prologue, then pdl_wait()s
+// (the previous grid complete and its memory visible) before touching
+// anything that grid or an earlier one produces or may still use.  Both are
+// no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 // ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {

@@ -187,13 +187,19 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         const long long slot = p.packed ? my_tile * p.tile * p.tile + (long long)(ly0 + dy_) * p.tile + (lx0 + dx_)
                                         : (long long)iy * p.cam.width + ix;
         float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
-        if (ix < p.cam.width && iy < p.cam.height) {
-            double dx, dy, dz;
+        const bool inside = ix < p.cam.width && iy < p.cam.height;
+        double dx = 0.0, dy = 0.0, dz = 1.0;
+        Ray ray;
+        bool hit = false;
+        if (inside) {  // pure arithmetic: overlaps the previous kernel's tail
             camera_ray(p.cam, ix, iy, dx, dy, dz);
+            hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
+        }
+        pdl_trigger();
+        pdl_wait();  // the frame slice is complete; earlier writers of the outputs are done
+        if (inside) {
             Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
-            Ray ray;
-            if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
-                traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+            if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
         }
@@ -535,10 +541,12 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // written, and while chunks stay dark the colour rows are not fetched
     // (render-internal slices of trees without edits: p.skip_dark)
     uint32_t colour_in = 3u;  // bit s: stage s was issued with its colour rows
-    if (lane == 0) {
+    if (lane == 0) {  // payload reads only: may overlap the previous kernel
         if (c_begin < c_end) issue(c_begin, 0, true);
         if (c_begin + c_step < c_end) issue(c_begin + c_step, 1, true);
     }
+    pdl_trigger();
+    pdl_wait();  // no record is written before the previous kernel is complete
     uint32_t late_par = 0;  // phase parity of bar[2], bar[3]
     int k = 0;
     for (int64_t c = c_begin; c < c_end; c += c_step, ++k) {
@@ -789,6 +797,27 @@ inline int prep_smem(Kern k, size_t smem) {
         if (e != cudaSuccess) return set_error(VV_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     }
     return VV_OK;
+}
+
+#ifndef VV_PDL
+#define VV_PDL 1  // launch the slice pass and the camera kernel with programmatic serialization
+#endif
+// kernel<<<grid, block, smem, st>>>(args...), with programmatic stream
+// serialization when VV_PDL (the kernel must pdl_wait() before dependent
+// accesses)
+template <class Kern, class... Args>
+inline void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = VV_PDL ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 inline int check_launch(const char *what) {

@@ -15,7 +15,7 @@ static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t
     auto kern = k_render_camera<NM, CACHED, EDITS, Entry, SEG>;
     int r = prep_smem(kern, smem);
     if (r) return r;
-    kern<<<max_blocks, kTileRays, smem, st>>>(p);
+    launch_pdl(kern, dim3(max_blocks), dim3(kTileRays), smem, st, p);
     return check_launch("render_camera");
 }
 

@@ -101,7 +101,7 @@ static int go_slice(const SliceParams &p, cudaStream_t st) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = std::min(grid, (unsigned)(VV_SLICE_BPS * sms));
     }
-    kern<<<grid, nw * 32, smem, st>>>(p);
+    launch_pdl(kern, dim3(grid), dim3(nw * 32), smem, st, p);
     return check_launch("build_slice");
 }
 
