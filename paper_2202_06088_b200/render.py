@@ -159,8 +159,9 @@ class RenderOptions:
     """render.py:148-153, plus ``frame_slice``: how leaves are decoded when no
     FrameSlice is passed -- "per_sample" (inside the render kernel, like the
     reference's uncached branch), "per_frame" (one coalesced pass over all
-    leaves into a transient device slice, then render from it) or "auto".
-    All three are bitwise identical."""
+    leaves into a transient device slice, then render from it), "auto", or
+    "deferred" (opt-in: colour only for the leaves some ray shades, see
+    DESIGN.md).  All are bitwise identical."""
 
     early_stop: float = 1e-4
     far_plane: float = 1e9

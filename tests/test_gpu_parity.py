@@ -706,3 +706,29 @@ def test_no_device_memory_growth(cuda):
         work()
     free1 = torch.cuda.mem_get_info(cuda)[0]
     assert free0 - free1 < (64 << 20), f"device memory fell by {(free0 - free1) >> 20} MB"
+
+
+def test_render_options_through_camera_kernel(cuda):
+    """Non-default RenderOptions (alpha floor, far plane, early stop)
+    through the fused camera kernel: within tolerance of the oracle's rays +
+    the host finalize_layer, every decode mode bitwise alike."""
+    tree = synthetic.shell_tree(depth=7, n_max=2, frames=6, seed=8)
+    cam = synthetic.bench_camera(96, 64)
+    opts = dict(alpha_floor=0.3, far_plane=7.5, early_stop=1e-3)
+    o, d = cam.rays()
+    for f in (1, 4):
+        ref = oracle.render_rays(tree, o, d, f, early_stop=opts["early_stop"])
+        host = vv.finalize_layer(ref["premult"], ref["alpha"], ref["tbar"], (cam.height, cam.width),
+                                 vv.RenderOptions(**opts))
+        imgs = [vv.render(tree, cam, f, vv.RenderOptions(frame_slice=m, **opts))
+                for m in ("per_frame", "per_sample", "auto", "deferred")]
+        a0 = np.asarray(imgs[0].alpha)
+        assert np.abs(np.asarray(imgs[0].rgb) - host.rgb).max() <= TOL
+        assert np.abs(a0 - host.alpha).max() <= TOL
+        hit = a0 >= opts["alpha_floor"]
+        assert np.all(np.asarray(imgs[0].depth)[~hit] == np.float32(opts["far_plane"]))
+        assert np.abs(np.asarray(imgs[0].depth)[hit] - np.asarray(host.depth)[hit]).max() <= TOL
+        for other in imgs[1:]:
+            _exact(other.rgb, imgs[0].rgb, f"frame {f} rgb across modes")
+            _exact(other.alpha, imgs[0].alpha, f"frame {f} alpha across modes")
+            _exact(other.depth, imgs[0].depth, f"frame {f} depth across modes")
