@@ -181,3 +181,32 @@ def test_back_to_back_renders_same_outputs_ordered(cuda):
     ref = vv.render(tree, cam, (3 * 5) % tree.frames)
     _eq(rgb, ref.rgb, "rgb after tile rounds")
     _eq(alpha, ref.alpha, "alpha after tile rounds")
+
+
+@pytest.mark.parametrize("tile,world", [(16, 2), (32, 5), (128, 2)])
+def test_direct_tiles_sizes_and_worlds(cuda, tile, world):
+    """Direct tile rendering for other tile sizes and shard counts (ragged
+    image): the shards' union is render() bitwise."""
+    import ctypes
+
+    import torch
+
+    from paper_2202_06088_b200 import _native
+    from paper_2202_06088_b200.device import replica, stream_ptr
+
+    w, h = 200, 136
+    tree, cam = _tree(), synthetic.bench_camera(w, h)
+    ref = vv.render(tree, cam, 3)
+    rep = replica(tree, cuda)
+    rgb = torch.full((h, w, 3), float("nan"), device=cuda)
+    alpha = torch.full((h, w), float("nan"), device=cuda)
+    depth = torch.full((h, w), float("nan"), device=cuda)
+    oc, cd = vv.RenderOptions().c_struct(), cam.desc()
+    for s in range(world):
+        _native.check(_native.lib().vv_render_camera_tiles_direct(
+            rep.handle, 3, None, ctypes.byref(oc), ctypes.byref(cd), tile, s, world, rgb.data_ptr(),
+            alpha.data_ptr(), depth.data_ptr(), 0, stream_ptr(cuda)))
+    torch.cuda.synchronize()
+    _eq(rgb, ref.rgb, "rgb")
+    _eq(alpha, ref.alpha, "alpha")
+    _eq(depth, ref.depth, "depth")
