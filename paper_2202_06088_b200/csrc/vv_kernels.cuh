@@ -111,7 +111,7 @@ __device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
 // Block work unit: a kTW x kTH pixel tile (one ray per thread); warps take
 // VV_CHUNK_W-wide chunks of it.
 #ifndef VV_CHUNK_W
-#define VV_CHUNK_W 8  // warp chunk = VV_CHUNK_W x (32 / VV_CHUNK_W) pixels
+#define VV_CHUNK_W 4  // warp chunk = VV_CHUNK_W x (32 / VV_CHUNK_W) pixels (4 x 8 measured best)
 #endif
 #ifndef VV_CAM_TH
 #define VV_CAM_TH 8  // camera block = 16 x VV_CAM_TH pixels, one thread each
