@@ -116,9 +116,13 @@ __device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
 #ifndef VV_CAM_TH
 #define VV_CAM_TH 8  // camera block = 16 x VV_CAM_TH pixels, one thread each
 #endif
-constexpr int kTW = 16, kTH = VV_CAM_TH, kTileRays = kTW * kTH;
+#ifndef VV_CAM_TW
+#define VV_CAM_TW 16  // camera block width in pixels
+#endif
+constexpr int kTW = VV_CAM_TW, kTH = VV_CAM_TH, kTileRays = kTW * kTH;
 constexpr int kCamMinBlocks = VV_CAM_MINB * kBlock / kTileRays;  // same warps per SM for any tile height
-static_assert(kTileRays % 32 == 0 && kTH % (32 / VV_CHUNK_W) == 0, "camera tile must hold whole warp chunks");
+static_assert(kTileRays % 32 == 0 && kTH % (32 / VV_CHUNK_W) == 0 && kTW % VV_CHUNK_W == 0,
+              "camera tile must hold whole warp chunks");
 
 // block -> tile origin (image mode: row-major tiles; tile mode: sub-tiles of
 // this shard's tiles); local ray id -> pixel and output slot
