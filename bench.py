@@ -41,6 +41,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "Mrays/s and FPS at 1080p (VOctree HH render) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "Mrays/s"
 WIDTH, HEIGHT, FRAMES = 1920, 1080, 30
+WORKLOAD = ("cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached render "
+            "(ray gen + traversal + HH shading + compositing + finalize), frame sweep")
 C_COEF, K_HH = 31, 14
 L2_BYTES = 126 * 2**20
 
@@ -190,8 +192,10 @@ def _nz_chunks(row, c):
 
 
 # --------------------------------------------------------------------------- CPU baselines
-def cpu_reference_render(tree, cam, frames):
-    """Time the reference's own render() (voxvid numba) if installed in baseline/_ref."""
+def cpu_reference_render(tree, cam, frames, warm=()):
+    """Time the reference's own render() (voxvid numba) if installed in baseline/_ref.
+
+    ``warm`` frames are rendered untimed first (the W warm-up steps)."""
     ref_dir = ROOT / "baseline" / "_ref"
     if not (ref_dir / "voxvid").exists():
         return None
@@ -210,6 +214,8 @@ def cpu_reference_render(tree, cam, frames):
     t0 = time.time()
     rr.render(rtree, small, frames[0])  # JIT warm-up
     log(f"[bench] reference JIT warm-up {time.time() - t0:.1f}s, numba threads {numba.get_num_threads()}")
+    for f in warm:
+        rr.render(rtree, rcam, f)
     times = []
     for f in frames:
         t0 = time.perf_counter()
@@ -219,11 +225,17 @@ def cpu_reference_render(tree, cam, frames):
                 impl="voxvid.render.render (numba, baseline/_ref), uncached")
 
 
-def cpu_port_render(tree, cam, frames):
-    """Time the C oracle port (OpenMP, all host threads): ray gen + render_kernel + finalize."""
+def cpu_port_render(tree, cam, frames, warm=()):
+    """Time the C oracle port (OpenMP, all host threads): ray gen + render_kernel + finalize.
+
+    ``warm`` frames are rendered untimed first (the W warm-up steps)."""
     from oracle import oracle
 
     nt = oracle.num_procs()
+    for f in warm:
+        o, d = cam.rays()
+        out = oracle.render_rays(tree, o, d, f, nthreads=nt)
+        oracle.finalize(out["premult"], out["alpha"], out["tbar"])
     times = []
     for f in frames:
         t0 = time.perf_counter()
@@ -240,10 +252,11 @@ def run_reference_arm(args, rank, world):
     cam_mod = __import__("paper_2202_06088_b200.synthetic", fromlist=["bench_camera"])
     tree = make_tree(args.config)
     cam = cam_mod.bench_camera(WIDTH, HEIGHT)
+    warm = [i % FRAMES for i in range(args.warmup)]
     frames = [i % FRAMES for i in range(args.warmup, args.warmup + args.steps)]
-    res = cpu_reference_render(tree, cam, frames) if not args.port else None
+    res = cpu_reference_render(tree, cam, frames, warm) if not args.port else None
     if res is None:
-        res = cpu_port_render(tree, cam, frames)
+        res = cpu_port_render(tree, cam, frames, warm)
     n_rays = WIDTH * HEIGHT
     ms = 1e3 * sum(res["times"]) / len(res["times"])
     value = n_rays * len(res["times"]) / sum(res["times"]) / 1e6
@@ -252,8 +265,8 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "fps": round(1e3 / ms, 4),
-        "config": {"workload": "cfg2: depth-9 shell VOctree, n_max 2, T 30, 1920x1080, uncached render, frame sweep",
-                   "frames": frames, "rays_per_step": n_rays},
+        "config": {"workload": WORKLOAD, "rays_per_step": n_rays, "frames": frames,
+                   "warmup_frames": warm},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
                          "sample": f"{len(frames)} full 1080p frames {frames}", "impl": res["impl"]},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -505,8 +518,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "fps": round(world * 1e3 / ms, 2),
         "config": {
-            "workload": "cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached "
-                        "render (ray gen + traversal + HH shading + compositing + finalize), frame sweep",
+            "workload": WORKLOAD,
             "rays_per_step": n_rays * world, "frames_rank0": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
             "l2": "inputs larger than L2 (1.54 GB tree) and L2 flushed between steps (252 MiB memset outside "
                   "the per-step CUDA events)",
