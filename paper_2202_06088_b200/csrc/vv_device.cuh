@@ -224,7 +224,12 @@ struct EntryW {
     }
 };
 
-__host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 : 3 * (depth - 1) + 1; }
+// slots per thread: a level-L node (L <= depth-2; last-level nodes queue
+// segments, they do not push) holds <= 3L entries and writes slots up to
+// 3L+2, so 3(depth-1) slots suffice.  One slot (8 B/thread) less than the
+// looser 3(depth-1)+1 lets four 128-thread camera blocks fit the 196 KB
+// shared-memory carveout at depth 9, leaving 60 KB of L1 instead of 28 KB.
+__host__ __device__ constexpr int stack_cap(int depth) { return depth <= 1 ? 1 : 3 * (depth - 1); }
 
 // ------------------------------------------------------------ traversal
 // Visitor interface:
@@ -428,7 +433,7 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
             // branch-free: the entry always goes to the top slot and the top
             // moves only for a real push (a slot above the top is scratch;
             // at a level-L node the stack holds <= 3L entries, so the slot
-            // is <= 3(depth-2)+2 < stack_cap)
+            // is <= 3(depth-2)+2 < stack_cap = 3(depth-1))
             const bool push = ((keep >> s) & 1) && (keep & ((1 << s) - 1));
             Entry::store(t.sp, (uint32_t)cp[s], t.L + 1, pc2 | Entry::spread(cb[s]));
             t.sp += push ? stride : 0u;

@@ -272,6 +272,43 @@ def test_camera_rays_vs_host(cuda):
     assert np.abs(layer.depth.reshape(-1)[hit] - depth[hit]).max() < TOL
 
 
+@pytest.mark.parametrize("depth", [2, 3, 6])
+def test_dense_tree_full_stack(cuda, depth):
+    """Every cell occupied and no early stop: oblique rays cross four children
+    at every internal node, so the traversal stack reaches its bound
+    (3 entries per level above the current node, stack_cap in vv_device.cuh).
+    Visit lists and segments bit-exact, camera image within tolerance."""
+    rng = np.random.default_rng(40 + depth)
+    res = 1 << depth
+    coords = np.argwhere(np.ones((res, res, res), bool))
+    k = vv.hh.basis_count(1)
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * 3 + 3 * k)).astype(np.float32)
+    data[:, 0] = rng.uniform(0.01, 0.05, len(coords)).astype(np.float32)
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(4, 3), 1, depth=depth)
+    n = 4000
+    o = rng.uniform(-1.0, 2.0, (n, 3))
+    o[:, rng.integers(0, 3)] = -0.75  # start outside the box
+    d = rng.uniform(0.2, 0.8, 3) + rng.uniform(-0.1, 0.1, (n, 3))
+    d *= np.where(o > 0.5, -1.0, 1.0)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ref = oracle.render_rays(tree, o, d, 1, early_stop=0.0, visits=True)
+    used, start, leaf = vv.render_ray_visits(tree, o, d, 1, vv.RenderOptions(early_stop=0.0))
+    assert ref["used"].max() >= 3 * (depth - 1)
+    _exact(used, ref["used"], "visit counts")
+    _exact(leaf, ref["visit_leaf"], "visited leaves")
+    start_g, leaf_g, t0_g, t1_g = vv.collect_segments(tree, o, d)
+    start_r, leaf_r, t0_r, t1_r = oracle.collect_segments(tree, o, d)
+    _exact(leaf_g, leaf_r)
+    _exact(t0_g, t0_r)
+    cam = vv.Camera.look_at([1.9, 1.6, -0.7], [0.5, 0.5, 0.5], width=96, height=64)
+    co, cd = cam.rays()
+    ref = oracle.render_rays(tree, co, cd, 2)
+    rgb, alpha, _ = oracle.finalize(ref["premult"], ref["alpha"], ref["tbar"])
+    layer = vv.render(tree, cam, 2)
+    assert np.abs(layer.rgb.reshape(-1, 3) - rgb).max() < TOL
+    assert np.abs(layer.alpha.reshape(-1) - alpha).max() < TOL
+
+
 @pytest.mark.parametrize("name", ["cache_d3", "edits_d3"])
 def test_decode_modes_bitwise_equal(cuda, name):
     """per_sample / per_frame / lazy leaf decoding give bitwise-identical
