@@ -75,15 +75,12 @@ typedef struct {
      * VV_SLICE_AUTO picks per call, VV_SLICE_PER_SAMPLE decodes each visited
      * leaf inside the render kernel (render_kernel's uncached branch),
      * VV_SLICE_PER_FRAME first decodes every leaf once into a transient
-     * stream-ordered slice, then renders from it.  VV_SLICE_DEFERRED
-     * (vv_render_camera only; others treat it as PER_FRAME): sigma per leaf,
-     * the walk with the compositing weights, the colour of the leaves some
-     * ray shades, then colour per ray -- see DESIGN.md. */
+     * stream-ordered slice, then renders from it. */
     int32_t frame_slice;
     int32_t reserved;
 } vv_render_opts;
 
-enum { VV_SLICE_AUTO = 0, VV_SLICE_PER_SAMPLE = 1, VV_SLICE_PER_FRAME = 2, VV_SLICE_DEFERRED = 3 };
+enum { VV_SLICE_AUTO = 0, VV_SLICE_PER_SAMPLE = 1, VV_SLICE_PER_FRAME = 2 };
 
 /* Pinhole camera (render.py:42-125): intrinsics in pixels, row-major c2w. */
 typedef struct {
@@ -126,6 +123,10 @@ int vv_tree_bind(const vv_tree_desc *dev, int device, vv_tree **out);
 int vv_tree_free(vv_tree *tree);
 int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, int32_t *depth,
                  int32_t *frames, int64_t *device_bytes);
+/* Share of leaves with sigma 0, measured at upload over frames 0, T/2 and
+ * T-1.  Above 0.5 the sliced camera and playback kernels walk with the long
+ * segment queue (a kernel choice only: images are bitwise the same). */
+int vv_tree_dark_fraction(const vv_tree *tree, float *dark_frac);
 
 /* ---- per-frame slice cache -----------------------------------------------
  * Replaces build_frame_cache (render.py:170-179) -> build_slice_kernel
@@ -189,6 +190,13 @@ int vv_render_rays_visits(const vv_tree *tree, int32_t frame, const vv_slice *ca
 int vv_render_camera(const vv_tree *tree, int32_t frame, const vv_slice *cache,
                      const vv_render_opts *opts, const vv_camera *cam, float *rgb,
                      float *alpha, float *depth, void *stream);
+/* vv_render_camera plus, per pixel, the leaf samples the ray consumed
+ * (int32, device, (H, W)): the reference's per-ray `used` count
+ * (shade_forward_kernel, kernels.py:700-738; Trainer._forward, train.py:
+ * 269-296), written by the same kernel instantiation vv_render_camera runs. */
+int vv_render_camera_counts(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                            const vv_render_opts *opts, const vv_camera *cam, float *rgb,
+                            float *alpha, float *depth, int32_t *sample_count, void *stream);
 
 /* Tile-sharded variant for multi-GPU: renders only the square tiles of
  * size `tile` whose linear index i (row-major over the tile grid) has
@@ -255,6 +263,11 @@ int vv_render_camera_multi(const vv_tree *tree, int32_t n_frames, const int32_t 
 int vv_render_scene(const vv_instance *instances, int32_t n_instances,
                     const vv_render_opts *opts, const vv_camera *cam, const double *background,
                     float *image, float *alpha, float *depth, void *stream);
+/* Leaf-decode mode vv_render_scene picks for each instance (0: per sample
+ * inside the scene kernel -- every instance 0 and no edits runs the lean
+ * instantiation --, 1: a per-frame slice pass first). */
+int vv_scene_decode_modes(const vv_instance *inst, int32_t n_inst, const vv_render_opts *opts,
+                          const vv_camera *cam, int32_t *modes);
 
 /* ---- traversal only --------------------------------------------------------
  * Replace count_segments_kernel / collect_segments_kernel

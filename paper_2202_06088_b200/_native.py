@@ -54,6 +54,7 @@ EXPORTED_SYMBOLS = (
     "vv_tree_bind",
     "vv_tree_free",
     "vv_tree_info",
+    "vv_tree_dark_fraction",
     "vv_slice_build",
     "vv_slice_free",
     "vv_slice_export",
@@ -61,6 +62,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_rays",
     "vv_render_rays_visits",
     "vv_render_camera",
+    "vv_render_camera_counts",
     "vv_render_camera_tiles",
     "vv_unpack_tiles",
     "vv_render_camera_tiles_direct",
@@ -69,6 +71,7 @@ EXPORTED_SYMBOLS = (
     "vv_ipc_close",
     "vv_ipc_free",
     "vv_render_scene",
+    "vv_scene_decode_modes",
     "vv_render_camera_multi",
     "vv_slice_build_multi",
     "vv_slice_build_frames",
@@ -204,6 +207,7 @@ _SIGNATURES = {
     "vv_tree_bind": (ctypes.c_int, [ctypes.POINTER(TreeDesc), ctypes.c_int, ctypes.POINTER(_P)]),
     "vv_tree_free": (ctypes.c_int, [_P]),
     "vv_tree_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "vv_tree_dark_fraction": (ctypes.c_int, [_P, _P]),
     "vv_slice_build": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_P)]),
     "vv_slice_free": (ctypes.c_int, [_P]),
     "vv_slice_export": (ctypes.c_int, [_P, _P, _P, _P]),
@@ -219,6 +223,10 @@ _SIGNATURES = {
     "vv_render_camera": (
         ctypes.c_int,
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P],
+    ),
+    "vv_render_camera_counts": (
+        ctypes.c_int,
+        [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P, _P],
     ),
     "vv_render_camera_tiles": (
         ctypes.c_int,
@@ -245,6 +253,8 @@ _SIGNATURES = {
         [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),
          _P, _P, _P, _P, _P],
     ),
+    "vv_scene_decode_modes": (
+        ctypes.c_int, [ctypes.POINTER(InstanceDesc), _I32, _P, ctypes.POINTER(CameraDesc), _P]),
     "vv_count_segments": (ctypes.c_int, [_P, _P, _P, _I64, _D, _D, _P, _P]),
     "vv_collect_segments": (ctypes.c_int, [_P, _P, _P, _I64, _D, _D, _P, _P, _P, _P, _P]),
     "vv_termination_leaves": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _I64, _D, _P, _P]),

@@ -16,12 +16,12 @@
 #include <string.h>
 
 #include <algorithm>
+#include <memory>
 #include <mutex>
 #include <vector>
 
 #include "../../include/voxvid_b200.h"
 #include "vv_kernels.cuh"
-#include "vv_deferred.cuh"
 
 using namespace vv;
 using namespace vvk;
@@ -40,6 +40,27 @@ struct vv_tree {
     float *d_a, *d_b;
     std::vector<float> h_a, h_b;  // host copies of the basis rows (slice-pass chunk masks)
     float dark_frac = 0.0f;       // share of leaves with sigma 0, over a few frames (queue threshold)
+    // node-mask tables (vv_launch_mask.cu), set when the table is a tree
+    // (one parent per node, every leaf row at the last level)
+    int32_t *d_parent, *d_last, *d_upper;
+    int64_t n_last, n_upper;
+    bool mask_ok;
+};
+
+// Per-frame (or per frame group) node mask: the slice pass's lit bits, the
+// marker scratch and the masked child table, in one stream-ordered block
+// shared by the slices of a group.
+struct NodeMask {
+    void *mem = nullptr;
+    cudaStream_t st = nullptr;
+    uint8_t *lit = nullptr;
+    uint32_t *flag = nullptr;
+    int32_t *mask = nullptr;
+    NodeMask() = default;
+    NodeMask(const NodeMask &) = delete;
+    ~NodeMask() {
+        if (mem) cudaFreeAsync(mem, st);
+    }
 };
 
 // float4 chunks of the frame's fp32 A (which = 0) or B (1) row holding a
@@ -69,6 +90,7 @@ struct vv_slice {
     bool render_only;  // colour omitted where sigma is 0 (VV_SLICE_RENDER_ONLY): not exportable
     int64_t n_leaves;
     cudaStream_t stream;  // stream-ordered allocation: freed on this stream
+    std::shared_ptr<NodeMask> nmask;  // dark subtrees cut (image renders), or null
 };
 
 #define VV_CUDA(call)                                                                          \
@@ -155,7 +177,8 @@ SliceView slice_view(const vv_slice *c) {
     return s;
 }
 
-int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only) {
+int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only,
+                       uint8_t *lit = nullptr) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
     memset(&p, 0, sizeof(p));
@@ -167,6 +190,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
     p.rec[0] = rec;
     p.rec4 = rec4;
     p.skip_dark = render_only && !t->has_edits;
+    p.lit = lit;
     set_slice_masks(t, p);
     return launch_slice(t->n_max, p, st);
 }
@@ -176,6 +200,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
 struct Transient {
     void *mem = nullptr;
     cudaStream_t st = nullptr;
+    std::shared_ptr<NodeMask> nmask;
     Transient() = default;
     Transient(const Transient &) = delete;
     ~Transient() {
@@ -194,6 +219,100 @@ void pool_setup(int device) {
     });
 }
 
+// Node masks pay off when a frame leaves large subtrees dark (cfg3: ~90% of
+// leaves); they are skipped for trees with edits (an edit can give a dark
+// leaf density).  VV_NODE_MASK=0 / 1 forces them off / on (A/B and tests).
+bool mask_wanted(const vv_tree *t) {
+    if (!t->mask_ok || t->has_edits || t->n_leaves == 0) return false;
+    if (const char *e = getenv("VV_NODE_MASK")) {
+        if (e[0] == '0') return false;
+        if (e[0] == '1') return true;
+    }
+    return t->dark_frac >= 0.25f;
+}
+
+int alloc_mask(const vv_tree *t, cudaStream_t st, std::shared_ptr<NodeMask> &out) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_lit = al((size_t)t->n_leaves), b_flag = al((size_t)t->n_internal * 4);
+    const size_t total = b_lit + b_flag + (size_t)t->n_internal * 8 * sizeof(int32_t);
+    auto m = std::make_shared<NodeMask>();
+    if (cudaMallocAsync(&m->mem, total, st) != cudaSuccess) {
+        cudaGetLastError();
+        m->mem = nullptr;
+        return set_error(VV_E_NOMEM, "node mask allocation (%zu bytes) failed", total);
+    }
+    m->st = st;
+    char *b = static_cast<char *>(m->mem);
+    m->lit = reinterpret_cast<uint8_t *>(b);
+    m->flag = reinterpret_cast<uint32_t *>(b + b_lit);
+    m->mask = reinterpret_cast<int32_t *>(b + b_lit + b_flag);
+    out = std::move(m);
+    return VV_OK;
+}
+
+int build_mask(const vv_tree *t, const NodeMask &m, cudaStream_t st) {
+    MaskParams p;
+    p.child = t->d_child;
+    p.parent = t->d_parent;
+    p.last = t->d_last;
+    p.upper = t->d_upper;
+    p.n_last = t->n_last;
+    p.n_upper = t->n_upper;
+    p.n_internal = t->n_internal;
+    p.lit = m.lit;
+    p.flag = m.flag;
+    p.mask = m.mask;
+    return launch_node_mask(p, st);
+}
+
+// Node tables of the mask kernels from the host copy of the child table:
+// levels by breadth-first search from the root; mask_ok only for a proper
+// tree (no node reached twice, leaf rows exactly at the last level).
+int setup_mask_tables(vv_tree *t, const int32_t *child) {
+    t->mask_ok = false;
+    const int64_t ni = t->n_internal;
+    std::vector<int32_t> parent((size_t)ni, -2), last, upper;
+    std::vector<int32_t> cur{0}, next;
+    parent[0] = -1;
+    for (int L = 0; L < t->depth && !cur.empty(); ++L) {
+        const bool at_last = L + 1 == t->depth;
+        next.clear();
+        for (int32_t n : cur) {
+            (at_last ? last : upper).push_back(n);
+            if (at_last) continue;
+            for (int b = 0; b < 8; ++b) {
+                const int32_t c = child[(size_t)n * 8 + b];
+                if (c < 0) continue;
+                if (c >= ni || parent[c] != -2) return VV_OK;  // not a tree: no masks
+                parent[c] = n;
+                next.push_back(c);
+            }
+        }
+        cur.swap(next);
+    }
+    for (int32_t n : last)
+        for (int b = 0; b < 8; ++b)
+            if (child[(size_t)n * 8 + b] >= t->n_leaves) return VV_OK;
+    for (auto &v : parent) v = v == -2 ? -1 : v;
+    auto up = [&](int32_t **d, const std::vector<int32_t> &h) -> int {
+        if (h.empty()) return VV_OK;
+        if (cudaMalloc(d, h.size() * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(VV_E_NOMEM, "node mask table allocation failed");
+        }
+        t->bytes += (int64_t)h.size() * 4;
+        if (cudaMemcpy(*d, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            return set_error(VV_E_CUDA, "node mask table copy failed");
+        return VV_OK;
+    };
+    int rc;
+    if ((rc = up(&t->d_parent, parent)) || (rc = up(&t->d_last, last)) || (rc = up(&t->d_upper, upper))) return rc;
+    t->n_last = (int64_t)last.size();
+    t->n_upper = (int64_t)upper.size();
+    t->mask_ok = true;
+    return VV_OK;
+}
+
 // Leaf-decode mode for a call without a user cache: 0 = per sample (inside
 // the render kernel), 1 = per-frame slice pre-pass.  VV_SLICE_AUTO takes the
 // pre-pass when the rays that can reach the tree are numerous enough that
@@ -207,7 +326,6 @@ void pool_setup(int device) {
 int decode_mode(const vv_tree *t, double n_rays, int policy) {
     if (t->n_leaves == 0 || policy == VV_SLICE_PER_SAMPLE) return 0;
     if (policy == VV_SLICE_PER_FRAME) return 1;
-    if (policy == VV_SLICE_DEFERRED) return 2;
     return (double)t->n_leaves <= 4.0 * n_rays ? 1 : 0;
 }
 
@@ -273,8 +391,25 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     tr.st = st;
     sv.rec = reinterpret_cast<float4 *>(tr.mem);
     sv.rec4 = rec4;
-    return launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st, true);
+    int rc;
+    if (mask_wanted(t) && (rc = alloc_mask(t, st, tr.nmask))) return rc;
+    rc = launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st, true,
+                            tr.nmask ? tr.nmask->lit : nullptr);
+    if (rc || !tr.nmask) return rc;
+    return build_mask(t, *tr.nmask, st);
 }
+
+// Long segment queue for mostly dark trees (the cfg3 motion tree).  Measured
+// at cfg3 with node masks: 0.493 vs 0.502 ms per frame (without masks 2.02
+// vs 2.18); VV_LONG_QUEUE=0 / 1 forces the choice (A/B runs).
+bool long_queue(const vv_tree *t, const NodeMask *) {
+    if (const char *e = getenv("VV_LONG_QUEUE")) return e[0] == '1';
+    return t->dark_frac > 0.5f;
+}
+
+// The child table an image render walks: the frame's node mask when one was
+// built (dark subtrees cut; bitwise the same pixels), else the tree's own.
+const int32_t *image_child(const vv_tree *t, const NodeMask *m) { return m ? m->mask : t->d_child; }
 
 // src_stride: floats per source payload row (0: 2C + 3K; .voct rows with
 // edit channels carry 5 more, vv_voct_upload)
@@ -293,8 +428,7 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     if ((d->edit_rgb == nullptr) != (d->edit_t == nullptr))
         return set_error(VV_E_INVALID, "edit_rgb and edit_t must both be set or both be NULL");
     DeviceGuard g(device);
-    vv_tree *t = new vv_tree();
-    memset(t, 0, sizeof(*t));
+    vv_tree *t = new vv_tree();  // value-initialised: every pointer and count zero
     t->device = device;
     t->n_leaves = d->n_leaves;
     t->n_internal = d->n_internal;
@@ -379,9 +513,22 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
                 return fail(lrc);
             }
         }
+        // PDL invariant (launch_pdl, vv_kernels.cuh): the planes are complete
+        // before any render or slice kernel can be launched on this tree
         e = cudaDeviceSynchronize();
         if (stage) cudaFree(stage);
         if (e != cudaSuccess) return fail(set_error(VV_E_CUDA, "repack failed: %s", cudaGetErrorString(e)));
+    }
+    {  // node-mask tables need the child table on the host
+        std::vector<int32_t> hc;
+        const int32_t *hchild = d->node_child;
+        if (!host_src) {
+            hc.resize((size_t)d->n_internal * 8);
+            if ((e = cudaMemcpy(hc.data(), d->node_child, child_b, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return fail(set_error(VV_E_CUDA, "node table copy failed: %s", cudaGetErrorString(e)));
+            hchild = hc.data();
+        }
+        if ((rc = setup_mask_tables(t, hchild))) return fail(rc);
     }
     TreeView &v = t->view;
     v.child = t->d_child;
@@ -463,6 +610,9 @@ int vv_tree_free(vv_tree *t) {
     cudaFree(t->d_edit_t);
     cudaFree(t->d_a);
     cudaFree(t->d_b);
+    cudaFree(t->d_parent);
+    cudaFree(t->d_last);
+    cudaFree(t->d_upper);
     delete t;
     return VV_OK;
 }
@@ -475,6 +625,12 @@ int vv_tree_info(const vv_tree *t, int64_t *n_leaves, int64_t *n_internal, int32
     if (depth) *depth = t->depth;
     if (frames) *frames = t->frames;
     if (device_bytes) *device_bytes = t->bytes;
+    return VV_OK;
+}
+
+int vv_tree_dark_fraction(const vv_tree *t, float *dark_frac) {
+    if (!t || !dark_frac) return set_error(VV_E_INVALID, "null argument");
+    *dark_frac = t->dark_frac;
     return VV_OK;
 }
 
@@ -498,7 +654,13 @@ int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out
         vv_slice_free(s);
         return set_error(VV_E_NOMEM, "slice allocation failed");
     }
-    rc = launch_build_slice(t, frame, s->d_rec, s->rec4, (cudaStream_t)stream, false);
+    if (mask_wanted(t) && (rc = alloc_mask(t, s->stream, s->nmask))) {
+        vv_slice_free(s);
+        return rc;
+    }
+    rc = launch_build_slice(t, frame, s->d_rec, s->rec4, (cudaStream_t)stream, false,
+                            s->nmask ? s->nmask->lit : nullptr);
+    if (!rc && s->nmask) rc = build_mask(t, *s->nmask, s->stream);
     if (rc) {
         vv_slice_free(s);
         return rc;
@@ -560,8 +722,17 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
     if (t->n_leaves == 0) return VV_OK;
     p.skip_dark = (flags & VV_SLICE_RENDER_ONLY) && !t->has_edits;
     set_slice_masks(t, p);
-    const int rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
-    return rc ? fail(rc) : VV_OK;
+    // one node mask for the group: a subtree is kept if lit in any of its
+    // frames (each frame's dark leaves still read sigma 0 from its record)
+    std::shared_ptr<NodeMask> nm;
+    int rc;
+    if (mask_wanted(t) && (rc = alloc_mask(t, (cudaStream_t)stream, nm))) return fail(rc);
+    p.lit = nm ? nm->lit : nullptr;
+    rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
+    if (!rc && nm) rc = build_mask(t, *nm, (cudaStream_t)stream);
+    if (rc) return fail(rc);
+    for (int f = 0; f < n_frames; ++f) out[f]->nmask = nm;
+    return VV_OK;
 }
 
 int vv_slice_free(vv_slice *s) {
@@ -642,6 +813,9 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
+    // plain image accumulators may walk the frame's node mask; counts and
+    // visit lists need the reference's full walk
+    if (!visits && !used && !pops && !shaded) p.T.child = image_child(t, cache ? cache->nmask.get() : tr.nmask.get());
     return launch_rays(t->n_max, mode, t->has_edits, wide, visits, p, grid, smem, st);
 }
 
@@ -660,68 +834,9 @@ int vv_render_rays_visits(const vv_tree *t, int32_t frame, const vv_slice *cache
                             nullptr, visit_start, visit_leaf, stream);
 }
 
-// Deferred-colour camera render (vv_deferred.cuh): one pooled block for the
-// per-call buffers, the tree's stamp array, then the launch sequence.
-constexpr int kDeferCap = 32;  // shaded samples recorded per ray (cfg2 max: 28)
-
-static int render_deferred(const vv_tree *t, CamParams &p, bool wide, unsigned grid, cudaStream_t st) {
-    const int64_t nl = t->n_leaves, npix = (int64_t)p.cam.width * p.cam.height;
-    int cap = kDeferCap;  // VV_DEFER_CAP: tests force the overflow path with a small record
-    if (const char *e = getenv("VV_DEFER_CAP")) cap = std::max(1, atoi(e));
-    const int rec4 = slice_rec4(t->S);
-    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    // per-call stamps (concurrent renders of one tree must not share them)
-    const size_t b_stamp = al(nl * 4);
-    const size_t b_sig = al(nl * 8), b_rec = al((size_t)nl * rec4 * 16), b_list = al(nl * 4), b_cnt = 256,
-                 b_aacc = al(npix * 8), b_count = al(npix * 4), b_sl = al((size_t)npix * cap * 4),
-                 b_sw = al((size_t)npix * cap * 8), b_ovf = al(npix * 4);
-    const size_t total = b_stamp + b_sig + b_rec + b_list + b_cnt + b_aacc + b_count + b_sl + b_sw + b_ovf;
-    pool_setup(t->device);
-    Transient tr;
-    if (cudaMallocAsync(&tr.mem, total, st) != cudaSuccess) {
-        cudaGetLastError();
-        tr.mem = nullptr;
-        return set_error(VV_E_NOMEM, "deferred render buffers (%zu bytes) failed", total);
-    }
-    tr.st = st;
-    char *m = static_cast<char *>(tr.mem);
-    auto take = [&](size_t b) {
-        char *r = m;
-        m += b;
-        return r;
-    };
-    DeferBuffers B;
-    memset(&B, 0, sizeof(B));
-    uint32_t *stamp = reinterpret_cast<uint32_t *>(take(b_stamp));
-    B.sig8 = reinterpret_cast<double *>(take(b_sig));
-    B.rec = reinterpret_cast<float4 *>(take(b_rec));
-    B.list = reinterpret_cast<uint32_t *>(take(b_list));
-    B.counters = reinterpret_cast<uint32_t *>(take(b_cnt));
-    B.D.aacc = reinterpret_cast<double *>(take(b_aacc));
-    B.D.count = reinterpret_cast<int32_t *>(take(b_count));
-    B.D.sleaf = reinterpret_cast<uint32_t *>(take(b_sl));
-    B.D.sw = reinterpret_cast<double *>(take(b_sw));
-    B.ovf = reinterpret_cast<uint32_t *>(take(b_ovf));
-    B.D.sig8 = B.sig8;
-    B.D.stamp = stamp;
-    B.D.epoch = 1;
-    B.D.cap = cap;
-    B.D.npix = npix;
-    B.n_leaves = nl;
-    B.rec4 = rec4;
-    B.mS = B.mG = 0;
-    B.mS = host_nz_chunks(t, p.frame, 0);
-    B.mG = host_nz_chunks(t, p.frame, 1);
-    if (cudaMemsetAsync(B.counters, 0, 8, st) != cudaSuccess || cudaMemsetAsync(stamp, 0, b_stamp, st) != cudaSuccess)
-        return set_error(VV_E_CUDA, "deferred render: memset failed");
-    p.S.rec = B.rec;
-    p.S.rec4 = rec4;
-    return launch_deferred(t->n_max, wide, p, B, grid, st);
-}
-
 static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *o,
                               const vv_camera *cam, float *rgb, float *alpha, float *depth, float *packed,
-                              int tile, int shard, int n_shards, int peer, void *stream) {
+                              int tile, int shard, int n_shards, int peer, void *stream, int32_t *used = nullptr) {
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
@@ -747,6 +862,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.rgb = rgb;
     p.alpha = alpha;
     p.depth = depth;
+    p.used = used;
     unsigned grid_blocks = 0;
     double share = 1.0;  // fraction of the frame's pixels this call renders
     p.peer = peer;
@@ -774,20 +890,27 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
     int mode =
         cache ? 1 : decode_mode(t, share * cube_footprint(*cam, lo, t->view.side, nullptr), opts.frame_slice);
-    if (mode == 2) {
-        if (!tile && !t->has_edits) return render_deferred(t, p, wide, grid_blocks, st);
-        mode = 1;  // tiles and edited trees: the one-pass sliced kernel
-    }
     if (!cache && mode != 0) {
         int r = build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
-    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, t->dark_frac > 0.5f);
+    // sample counts report the reference's full walk: the tree's own table
+    const NodeMask *nm = used ? nullptr : (cache ? cache->nmask.get() : tr.nmask.get());
+    p.T.child = image_child(t, nm);
+    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
 }
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
                      const vv_camera *cam, float *rgb, float *alpha, float *depth, void *stream) {
     return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream);
+}
+
+int vv_render_camera_counts(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
+                            const vv_camera *cam, float *rgb, float *alpha, float *depth, int32_t *sample_count,
+                            void *stream) {
+    if (!sample_count) return set_error(VV_E_INVALID, "null sample_count");
+    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream,
+                              sample_count);
 }
 
 int vv_camera_decode_mode(const vv_tree *t, const vv_camera *cam, const vv_render_opts *o, int32_t *mode) {
@@ -833,8 +956,15 @@ int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *fr
     p.blocks_x = (cam->width + kTW - 1) / kTW;
     const unsigned grid = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
     if (grid == 0) return VV_OK;
+    // a node mask built for a group holding every frame of this walk (slices
+    // of one vv_slice_build_frames call share it) keeps every subtree lit
+    // in any of them
+    const NodeMask *nm = caches[0]->nmask.get();
+    for (int k = 1; k < n_frames && nm; ++k)
+        if (caches[k]->nmask.get() != nm) nm = nullptr;
+    p.T.child = image_child(t, nm);
     return launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid,
-                               (cudaStream_t)stream, t->dark_frac > 0.5f);
+                               (cudaStream_t)stream, long_queue(t, nm));
 }
 
 int vv_render_camera_tiles(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -915,6 +1045,39 @@ int vv_unpack_tiles(const float *packed_all, int32_t width, int32_t height, int3
                          (cudaStream_t)stream);
 }
 
+// Decode mode of scene instance i: the rays that can reach its tree at its
+// frame, summed over every instance sharing both, against the leaf count.
+static int scene_decode_mode(const vv_instance *inst, int n_inst, int i, const vv_camera &cam, int policy) {
+    double reach = 0.0;
+    for (int j = 0; j < n_inst; ++j) {
+        if (inst[j].tree != inst[i].tree || inst[j].frame != inst[i].frame) continue;
+        const vv_tree *tj = inst[j].tree;
+        const double lo[3] = {tj->view.lo0, tj->view.lo1, tj->view.lo2};
+        if (inst[j].mode == 0) {  // rigid: the pulled-back camera in the tree's frame
+            vv_camera c2 = cam;
+            memcpy(c2.c2w, inst[j].pose, sizeof(c2.c2w));
+            reach += cube_footprint(c2, lo, tj->view.side, nullptr);
+        } else {
+            double A[12];
+            affine_from_inverse(inst[j].inv, A);
+            reach += cube_footprint(cam, lo, tj->view.side, A);
+        }
+    }
+    reach = std::min(reach, (double)cam.width * cam.height);
+    return decode_mode(inst[i].tree, reach, policy);
+}
+
+int vv_scene_decode_modes(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
+                          int32_t *modes) {
+    if (!inst || !cam || !modes || n_inst < 1) return set_error(VV_E_INVALID, "bad argument");
+    const vv_render_opts opts = o ? *o : default_opts();
+    for (int i = 0; i < n_inst; ++i) {
+        if (!inst[i].tree) return set_error(VV_E_INVALID, "null tree in instance %d", i);
+        modes[i] = scene_decode_mode(inst, n_inst, i, *cam, opts.frame_slice);
+    }
+    return VV_OK;
+}
+
 int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
                     const double *background, float *image, float *alpha, float *depth, void *stream) {
     if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
@@ -974,29 +1137,14 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
         int same = -1;
         for (int j = 0; j < i; ++j)
             if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.rec) same = j;
-        // rays that can reach this tree at this frame, over every instance sharing it
-        double reach = 0.0;
-        for (int j = 0; j < n_inst; ++j) {
-            if (inst[j].tree != inst[i].tree || inst[j].frame != inst[i].frame) continue;
-            const vv_tree *tj = inst[j].tree;
-            const double lo[3] = {tj->view.lo0, tj->view.lo1, tj->view.lo2};
-            if (inst[j].mode == 0) {  // rigid: the pulled-back camera in the tree's frame
-                vv_camera c2 = *cam;
-                memcpy(c2.c2w, inst[j].pose, sizeof(c2.c2w));
-                reach += cube_footprint(c2, lo, tj->view.side, nullptr);
-            } else {
-                double A[12];
-                affine_from_inverse(inst[j].inv, A);
-                reach += cube_footprint(*cam, lo, tj->view.side, A);
-            }
-        }
-        reach = std::min(reach, (double)cam->width * cam->height);
-        const int mode = decode_mode(inst[i].tree, reach, opts.frame_slice);
+        const int mode = scene_decode_mode(inst, n_inst, i, *cam, opts.frame_slice);
         if (same >= 0) {
             p.inst[i].S = p.inst[same].S;
+            p.inst[i].T.child = p.inst[same].T.child;
         } else if (mode != 0) {
             int r = build_transient(inst[i].tree, inst[i].frame, st, p.inst[i].S, tr[i]);
             if (r) return r;
+            p.inst[i].T.child = image_child(inst[i].tree, tr[i].nmask.get());
         }
     }
     bool lean = true;  // every instance decoded per sample, no edits: the lean instantiation
@@ -1147,7 +1295,10 @@ int vv_tree_set_edits(vv_tree *t, const float *edit_rgb, const int32_t *edit_t) 
         }
         t->bytes += nl * (int64_t)(sizeof(float4) + sizeof(int2));
     }
-    cudaDeviceSynchronize();  // stream-ordered renders may still read the old values
+    // stream-ordered renders may still read the old values; the sync also
+    // keeps the PDL invariant (launch_pdl, vv_kernels.cuh): no kernel is in
+    // flight while tree state changes
+    cudaDeviceSynchronize();
     VV_CUDA(cudaMemcpy(t->d_edit_rgb, edit_rgb, (size_t)nl * sizeof(float4), cudaMemcpyHostToDevice));
     VV_CUDA(cudaMemcpy(t->d_edit_t, edit_t, (size_t)nl * sizeof(int2), cudaMemcpyHostToDevice));
     t->has_edits = true;

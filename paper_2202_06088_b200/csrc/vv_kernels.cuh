@@ -99,6 +99,11 @@ struct CamParams {
     int tile, shard, n_shards, tiles_x;
     int peer;                     // image planes live on another GPU: fence at exit
     int blocks_x;                 // tiles per row (image mode)
+    // optional per-pixel leaf-sample counts (render_kernel's consumed
+    // segments, up to and including the early-stop one; image mode): written
+    // by the production instantiation itself, so its walk is checked
+    // bit-exactly against the oracle
+    int32_t *used;
 };
 
 // block = 16x8 pixels; warp = 16x2 pixels (spatially coherent rays)
@@ -177,6 +182,9 @@ template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(const __grid_constant__ CamParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxC], sB[kMaxC];
+    // basis rows before griddepcontrol.wait: immutable tree state (the PDL
+    // invariant at launch_pdl); after the wait it costs 1.8% (0.7435 vs
+    // 0.730 ms at cfg2)
     load_rows(p.T, p.frame, sA, sB);
     __syncthreads();
     int x0, y0, lx0, ly0;
@@ -200,12 +208,13 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
         }
         pdl_trigger();
-        pdl_wait();  // the frame slice is complete; earlier writers of the outputs are done
+        pdl_wait();  // the frame slice (and node mask) is complete; earlier writers of the outputs are done
         if (inside) {
             Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
             if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
+            if (p.used) p.used[slot] = sh.used;
         }
         cam_write(p, ix, iy, slot, r, g, b, a, d);
     }
@@ -422,6 +431,7 @@ struct SliceParams {
     int rec4;
     uint32_t mS, mG;            // w_sigma / w_gamma chunks the frames need (union of nz_chunks)
     int skip_dark;              // render-internal slice: dark chunks get sigma only (no colour)
+    uint8_t *lit;               // optional (n_leaves): bit f set iff frame f's sigma > 0 (node masks)
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -599,6 +609,12 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         for (int u = 0; u < kPer; ++u) {
             const int r = lane + 32 * u;
             if (r >= rows) continue;
+            if (p.lit) {  // coalesced byte per leaf: which frames see it lit
+                uint32_t bits = 0;
+#pragma unroll
+                for (int f = 0; f < KF; ++f) bits |= (sp[u][f] > 0.0 ? 1u : 0u) << f;
+                p.lit[base + r] = (uint8_t)bits;
+            }
             if (!bright) {  // sigma only: the record's last float4 pair (one sector at even R4)
 #pragma unroll
                 for (int f = 0; f < KF; ++f) {
@@ -808,7 +824,16 @@ inline int prep_smem(Kern k, size_t smem) {
 #endif
 // kernel<<<grid, block, smem, st>>>(args...), with programmatic stream
 // serialization when VV_PDL (the kernel must pdl_wait() before dependent
-// accesses)
+// accesses).
+// Invariant the PDL prologues rely on: a tree's node table, payload planes
+// and basis rows are immutable once vv_tree_upload/bind/voct_upload has
+// returned, and every in-place writer of tree state (the repack at upload,
+// vv_tree_set_edits) ends with cudaDeviceSynchronize -- so the only tree
+// reads issued before griddepcontrol.wait (k_build_slice's TMA loads of the
+// payload and basis rows, k_render_camera's basis rows) can never race a
+// stream-ordered write.  A future stream-ordered tree update must move those
+// reads after the wait.  (Per-frame data -- slices, node masks -- is read
+// only after it.)
 template <class Kern, class... Args>
 inline void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -857,6 +882,19 @@ int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiP
                         cudaStream_t st, bool long_queue = false);
 int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
+// per-frame node mask (vv_launch_mask.cu): child table with every child whose
+// subtree holds no lit leaf replaced by -1
+struct MaskParams {
+    const int32_t *child;       // (n_internal, 8) the tree's table
+    const int32_t *parent;      // (n_internal) parent node id, -1 at the root
+    const int32_t *last;        // last-level internal nodes (children are leaf rows)
+    const int32_t *upper;       // the other internal nodes
+    int64_t n_last, n_upper, n_internal;
+    const uint8_t *lit;         // (n_leaves) from the slice pass
+    uint32_t *flag;             // (n_internal) scratch: subtree holds a lit leaf
+    int32_t *mask;              // (n_internal, 8) out
+};
+int launch_node_mask(const MaskParams &p, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_shadow_blur(const float *alpha, int res, const double *weights, int radius, double *tmp, double *out,

@@ -166,6 +166,14 @@ class DeviceTree:
         self.device_bytes = int(nb.value)
         return self
 
+    @property
+    def dark_fraction(self) -> float:
+        """Share of leaves with sigma 0 over frames 0, T/2, T-1 (measured at
+        upload; above 0.5 the sliced kernels walk with the long segment queue)."""
+        v = ctypes.c_float()
+        _native.check(_native.lib().vv_tree_dark_fraction(self.handle, ctypes.byref(v)))
+        return float(v.value)
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:

@@ -151,7 +151,7 @@ class LayerImages:
         return LayerImages(c(self.rgb), c(self.alpha), c(self.depth))
 
 
-_SLICE_MODES = {"auto": 0, "per_sample": 1, "per_frame": 2, "deferred": 3}
+_SLICE_MODES = {"auto": 0, "per_sample": 1, "per_frame": 2}
 
 
 @dataclass(frozen=True)
@@ -159,9 +159,8 @@ class RenderOptions:
     """render.py:148-153, plus ``frame_slice``: how leaves are decoded when no
     FrameSlice is passed -- "per_sample" (inside the render kernel, like the
     reference's uncached branch), "per_frame" (one coalesced pass over all
-    leaves into a transient device slice, then render from it), "auto", or
-    "deferred" (opt-in: colour only for the leaves some ray shades, see
-    DESIGN.md).  All are bitwise identical."""
+    leaves into a transient device slice, then render from it) or "auto".
+    All are bitwise identical."""
 
     early_stop: float = 1e-4
     far_plane: float = 1e9
@@ -265,9 +264,17 @@ class _PinnedPool:
 _PINNED = _PinnedPool()
 
 
-def _frame_index(frame) -> int:
+def _frame_index(frame, tree=None) -> int:
+    """Frame index of ``frame``.  A non-integer float is a continuous time:
+    clamped to [0, T-1] and rounded to the nearest frame, as the reference's
+    track_value does (temporal.py:229-235); integers keep the
+    reference's range check (ValueError in _check_frame)."""
     if isinstance(frame, (float, np.floating)) and not float(frame).is_integer():
-        return int(round(float(frame)))  # continuous t -> nearest frame
+        t = float(frame)
+        if tree is not None:
+            frames = tree.bases.frames if hasattr(tree, "bases") else tree.frames
+            t = min(max(t, 0.0), frames - 1.0)
+        return int(round(t))
     return int(frame)
 
 
@@ -290,7 +297,7 @@ def _check_cache(cache, frame, rep):
 
 
 def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
-    frame = _frame_index(frame)
+    frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
     dev = torch_device(device)
     rep = replica(tree, dev)
@@ -306,7 +313,7 @@ def build_frame_caches(tree, frames, device=None, *, render_only: bool = False) 
     colour of leaves dark (sigma 0) in every frame is omitted
     (VV_SLICE_RENDER_ONLY) -- rendering is bitwise the same, ``q`` cannot be
     read."""
-    frames = [_frame_index(f) for f in frames]
+    frames = [_frame_index(f, tree) for f in frames]
     for f in frames:
         _check_frame(tree, f)
     if not 1 <= len(frames) <= 4:
@@ -339,7 +346,7 @@ def render_rays(tree, origins, dirs, frame: int, opts: RenderOptions = RenderOpt
     early-stop one), ``node_pops`` and ``shaded``.
     """
     torch = require_cuda()
-    frame = _frame_index(frame)
+    frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
     if cache is not None and getattr(cache, "frame", frame) != frame:
         raise ValueError(f"cache built for frame {cache.frame}, not {frame}")
@@ -383,7 +390,7 @@ def render_ray_visits(tree, origins, dirs, frame: int, opts: RenderOptions = Ren
     train.py:269-296).
     """
     torch = require_cuda()
-    frame = _frame_index(frame)
+    frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
     dev = torch_device(device)
     rep = replica(tree, dev)
@@ -423,13 +430,15 @@ def finalize_layer(premult, alpha, tbar, shape, opts: RenderOptions, depth_scale
 
 
 def render_into(tree, cam: Camera, frame: int, rgb, alpha, depth, opts: RenderOptions = RenderOptions(),
-                cache=None, *, stream=None):
+                cache=None, *, stream=None, sample_count=None):
     """Render into caller-owned CUDA float32 tensors (rgb (H,W,3), alpha/depth (H,W); any may be None).
 
     The allocation-free device path used by the benchmark; asynchronous on
-    the current (or given) stream.
+    the current (or given) stream.  ``sample_count``: optional CUDA int32
+    (H, W) tensor receiving each pixel's consumed leaf samples (the
+    reference's per-ray ``used`` count), from the same kernel.
     """
-    frame = _frame_index(frame)
+    frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
     ref = next(x for x in (rgb, alpha, depth) if x is not None)
     dev = ref.device
@@ -438,18 +447,21 @@ def render_into(tree, cam: Camera, frame: int, rgb, alpha, depth, opts: RenderOp
     oc = opts.c_struct()
     cd = cam.desc()
     s = int(stream.cuda_stream) if stream is not None else stream_ptr(dev)
-    _native.check(_native.lib().vv_render_camera(
-        rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd),
-        rgb.data_ptr() if rgb is not None else None,
-        alpha.data_ptr() if alpha is not None else None,
-        depth.data_ptr() if depth is not None else None, s))
+    planes = (rgb.data_ptr() if rgb is not None else None, alpha.data_ptr() if alpha is not None else None,
+              depth.data_ptr() if depth is not None else None)
+    if sample_count is not None:
+        _native.check(_native.lib().vv_render_camera_counts(
+            rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd), *planes, sample_count.data_ptr(), s))
+        return
+    _native.check(_native.lib().vv_render_camera(rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd),
+                                                 *planes, s))
 
 
 def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(), cache=None, *,
            out: str = "numpy", device=None) -> LayerImages:
     """Render one VOctree (render.py:236-240): rays + render + finalize in one kernel."""
     torch = require_cuda()
-    frame = _frame_index(frame)
+    frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
     if cache is not None and getattr(cache, "frame", frame) != frame:
         raise ValueError(f"cache built for frame {cache.frame}, not {frame}")
@@ -482,7 +494,7 @@ def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = Re
     by one instead.  Asynchronous on the current (or given) stream.
     """
     torch = require_cuda()
-    frames = [_frame_index(f) for f in frames]
+    frames = [_frame_index(f, tree) for f in frames]
     if len(frames) != len(outs):
         raise ValueError(f"{len(frames)} frames but {len(outs)} outputs")
     if not 1 <= len(frames) <= 4:
@@ -608,6 +620,20 @@ def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
 
     frames = list(frames)
     G = min(SEQUENCE_GROUP, playback_group(tree))
+    try:
+        yield from _playback_groups(torch, tree, cam, frames, opts, comp, copy, bufs, n, G, copied, pending, views,
+                                    split)
+    finally:
+        # a consumer that stops early (generator closed) drops the pinned
+        # arrays of the groups still in flight: wait for their copies first,
+        # or the pool could hand a buffer to another call while the DMA into
+        # it is still running
+        for ev, _ in pending:
+            ev.synchronize()
+        pending.clear()
+
+
+def _playback_groups(torch, tree, cam, frames, opts, comp, copy, bufs, n, G, copied, pending, views, split):
     for gi, g0 in enumerate(range(0, len(frames), G)):
         group = frames[g0:g0 + G]
         b = gi % 2

@@ -170,8 +170,90 @@ def sha(*arrays):
     return h.hexdigest()
 
 
+def cfg4_scene_case():
+    """BASELINE configs[3] shape at reduced size: the SURVEY 8(d) cfg4 scene
+    (4 shell performers, affines T(1.1(i-1.5),0,0) T(c) Rz(0.5 i) S_i T(-c)
+    with S_3 = 0.8 I -- the non-rigid per-ray pull-back --, timemaps
+    shift(3i)|loop(30)) through the reference's compose.render_scene, with
+    depth-8 trees (seeds 0-3) at 320x180, global frames 7 and 22."""
+    from paper_2202_06088_b200 import synthetic
+
+    trees = []
+    for i in range(4):
+        t = synthetic.shell_tree(depth=8, n_max=2, frames=30, seed=i)
+        rt_ = VOctree.from_cells(t.leaf_coords, t.leaf_data, rt.TemporalBases(t.bases.a, t.bases.b), 2, depth=8)
+        assert np.array_equal(rt_.node_child, t.node_child)
+        trees.append(rt_)
+    scene_ours, cam_ours = synthetic.scene_config4(trees, 320, 180)
+    insts = [SceneInstance(name=i.name, tree=i.tree, affine=i.affine, timemap=TimeMap.parse(str(i.timemap)))
+             for i in scene_ours.instances]
+    scene = Scene(instances=insts)
+    cam = Camera(cam_ours.width, cam_ours.height, cam_ours.fx, cam_ours.fy, cam_ours.cx, cam_ours.cy, cam_ours.c2w)
+    c = dict(cam_c2w=cam.c2w, cam_wh=np.array([cam.width, cam.height]),
+             cam_f=np.array([cam.fx, cam.fy, cam.cx, cam.cy]))
+    for g in (7, 22):
+        img, blended, layers = render_scene(scene, cam, g, want_layers=True)
+        c[f"g{g}_image"] = img.astype(np.float32)
+        c[f"g{g}_alpha"] = blended.alpha.astype(np.float32)
+        c[f"g{g}_depth"] = blended.depth.astype(np.float32)
+        c[f"g{g}_local_frames"] = np.array([i.local_frame(g) for i in insts])
+        c[f"g{g}_layer_alpha_max"] = np.array([float(l.alpha.max()) for l in layers])
+    return c
+
+
+def joint_case():
+    """Per-sample depth-ordered joint composition: the reference's own
+    joint_segments_oracle (pkg/tests/util.py:205-245) -- every instance's
+    leaf segments merged by world depth and composited once, no early stop
+    -- on depth-separated instances (where SPEC.md:555 makes Alg. 1 equal to
+    it) and on interleaved ones (where only the joint oracle is the truth)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from util import joint_segments_oracle
+
+    rng = np.random.default_rng(91)
+    ta = random_payload_tree(rng, depth=3, fill=0.5, frames=6, sigma_scale=6.0)
+    tb = random_payload_tree(rng, depth=4, fill=0.3, frames=6, sigma_scale=9.0)
+
+    def tr(x, y, z):
+        m = np.eye(4)
+        m[:3, 3] = [x, y, z]
+        return m
+
+    scl = np.diag([0.7, 0.7, 0.7, 1.0]) @ tr(0.2, 0.3, 0.1)
+    bg = np.array([0.1, 0.12, 0.2])
+    c = dict(tree_arrays(ta, "ta_"), **tree_arrays(tb, "tb_"), bg=bg)
+    layouts = {
+        # separated along the view direction: b entirely behind a for every ray
+        "sep": [SceneInstance(name="a", tree=ta, affine=tr(0.0, 0.0, 0.0)),
+                SceneInstance(name="b", tree=tb, affine=tr(0.0, 2.5, 0.0), timemap=TimeMap.parse("shift(2)"))],
+        # interleaved: overlapping volumes, a scaled (non-rigid) one and a yaw
+        "mix": [SceneInstance(name="a", tree=ta, affine=tr(0.0, 0.0, 0.0)),
+                SceneInstance(name="b", tree=tb, affine=tr(0.25, 0.1, 0.05), timemap=TimeMap.parse("reverse")),
+                SceneInstance(name="c", tree=ta, affine=scl, yaw_rate=20.0)],
+    }
+    cam = Camera.look_at([0.5, -2.2, 0.9], [0.5, 0.8, 0.5], width=24, height=20)
+    c.update(cam_c2w=cam.c2w, cam_wh=np.array([cam.width, cam.height]),
+             cam_f=np.array([cam.fx, cam.fy, cam.cx, cam.cy]))
+    for name, insts in layouts.items():
+        for g in (0, 3):
+            c[f"{name}_g{g}_joint"] = joint_segments_oracle(insts, cam, g, bg)
+            c[f"{name}_g{g}_alg1"] = render_scene(Scene(instances=insts, background=bg), cam, g,
+                                                  RenderOptions(early_stop=0.0))
+    return c
+
+
+EXTRA = {"cfg4_scene": cfg4_scene_case, "joint": joint_case}
+
+
 def main():
+    want = set(sys.argv[1:])
     cases = {}
+    if want and want <= set(EXTRA):
+        for name in sorted(want):
+            path = HERE / f"{name}.npz"
+            np.savez_compressed(path, **EXTRA[name]())
+            print(f"{path.name}: {path.stat().st_size / 1024:.0f} KiB")
+        return
 
     # A. scalar-reference case (test_render.py:103-113 shape)
     rng = np.random.default_rng(23)
@@ -393,7 +475,9 @@ def main():
         c[f"g{g}_falloff1"] = falloff_pass(blended, cam, lights[1])
     cases["lights"] = c
 
-    want = set(sys.argv[1:])
+    for name, fn in EXTRA.items():
+        if not want or name in want:
+            cases[name] = fn()
     for name, arrays in cases.items():
         if want and name not in want:
             continue

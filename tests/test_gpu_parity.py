@@ -664,26 +664,6 @@ def test_render_only_slices_dark_chunks_bitwise(cuda):
         _exact(d.cpu().numpy(), ref.depth, f"playback depth {f}")
 
 
-@pytest.mark.parametrize("cap", [None, "2"])
-def test_deferred_colour_bitwise(cuda, cap, monkeypatch):
-    """frame_slice="deferred" (sigma slice, walk with the weights, colour of
-    the shaded leaves only, colour per ray) renders bitwise like the
-    one-pass kernel -- also when rays overflow the per-ray sample record
-    (cap 2 sends most hit rays through the per-sample fallback)."""
-    if cap:
-        monkeypatch.setenv("VV_DEFER_CAP", cap)
-    cases = [(synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=2), synthetic.bench_camera(120, 80)),
-             (synthetic.motion_tree(depth=7, frames=12), synthetic.bench_camera(160, 96)),
-             (synthetic.shell_tree(depth=6, n_max=3, frames=5, seed=4), synthetic.bench_camera(64, 48))]
-    for tree, cam in cases:
-        for f in (0, tree.frames - 1):
-            ref = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="per_frame"))
-            out = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="deferred"))
-            _exact(out.rgb, ref.rgb, f"deferred rgb n_max {tree.n_max} frame {f}")
-            _exact(out.alpha, ref.alpha, f"deferred alpha n_max {tree.n_max} frame {f}")
-            _exact(out.depth, ref.depth, f"deferred depth n_max {tree.n_max} frame {f}")
-
-
 def test_slice_largest_stages_dense_c64_nmax3(cuda):
     """The widest slice stages: C = 64 dense A / B rows (16 chunks each) and
     n_max 3 (w_hh 30 x 3 floats) -- the launcher fits one warp per block.
@@ -724,7 +704,7 @@ def test_no_device_memory_growth(cuda):
 
     tree = synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=5)
     cam = synthetic.bench_camera(96, 64)
-    modes = ("auto", "per_sample", "per_frame", "deferred")
+    modes = ("auto", "per_sample", "per_frame")
 
     def work():
         for f in range(8):
@@ -758,7 +738,7 @@ def test_render_options_through_camera_kernel(cuda):
         host = vv.finalize_layer(ref["premult"], ref["alpha"], ref["tbar"], (cam.height, cam.width),
                                  vv.RenderOptions(**opts))
         imgs = [vv.render(tree, cam, f, vv.RenderOptions(frame_slice=m, **opts))
-                for m in ("per_frame", "per_sample", "auto", "deferred")]
+                for m in ("per_frame", "per_sample", "auto")]
         a0 = np.asarray(imgs[0].alpha)
         assert np.abs(np.asarray(imgs[0].rgb) - host.rgb).max() <= TOL
         assert np.abs(a0 - host.alpha).max() <= TOL
