@@ -1,29 +1,42 @@
-"""Benchmark: Mrays/s and FPS of 1080p VOctree HH rendering (BASELINE.json configs[1]).
+"""Benchmark: Mrays/s and FPS of VOctree HH rendering (BASELINE.json), every config.
 
-Workload (config 2): depth-9 spherical-shell VOctree
-(3,557,912 leaves, n_max = 2 -> 104 f32 per leaf, 1.48 GB payload), T = 30
-frames, 1920x1080 camera look_at((1.6,1.3,0.9) -> (0.5,0.5,0.5)), uncached
-render (the fused ray-gen + traversal + HH shading + compositing +
-finalize kernel).  One step = one full 1080p frame; steps sweep frames
-0..29.  Synthetic data generated in-process (deterministic seeds).
+Default (the driver's line): config 2 = BASELINE.json configs[1], the one the
+metric is quoted on: depth-9 spherical-shell VOctree (3,557,912 leaves,
+n_max 2 -> 104 f32 per leaf, 1.48 GB payload), T = 30, 1920x1080 camera
+look_at((1.6,1.3,0.9) -> (0.5,0.5,0.5)), one step = one full frame exactly
+as render() does it (per-frame slice pass + the fused ray-gen / traversal /
+HH shading / compositing / finalize kernel), frames swept.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3|4|5]
 
-N > 1 runs under torchrun as batched playback (the north star's "by frame
-for batched playback"): every rank holds a full tree replica and renders
-frames f = rank, rank + N, ... of the sweep -- one full frame per rank per
-step, no data-path collective (weak scaling; the timed region is the max
-over ranks).  The single-frame tile path (64x64 tiles interleaved over the
-ranks, one NCCL all-gather, unpack) is timed as well and reported under
-"tile_frame".  The reference arm (--impl reference) times the reference's own CPU
-renderer (voxvid from baseline/_ref, numba, all host threads) or, if that
-is not installed, the C oracle port (OpenMP, all host threads).
+--config 3: the motion-heavy tree (learnable temporal basis, ~90% of leaves
+dark per frame), T = 60, 1080p, 60-frame sweep.  --config 4: four
+performers composed (per-instance affine incl. a non-rigid one, time
+offsets, Algorithm-1 depth-ordered blending, background), 1080p; a step is
+one composed frame (4 x 2,073,600 pulled-back rays).  --config 5: stereo
+2 x 2160 x 2160 per frame (one slice pass shared by both eyes).
+
+N > 1 (torchrun, one rank per GPU; every rank holds a full replica):
+configs 2, 3 and 5 split each frame across the ranks (strong scaling): rank
+r renders a contiguous row band, balanced on the measured row costs, that
+decodes only the leaf chunks its pixels can reach and stores its pixels
+straight into rank 0's image planes over NVLink (CUDA IPC,
+TileRenderer(mode="regions")); one stream-ordered NCCL all-reduce per frame
+publishes it -- the timed step is that whole frame, max over ranks.
+Frame-sharded playback (frame f on rank f mod N, weak scaling) is reported
+as "frame_sharded".  Config 4 shards by frame.
+
+The reference arm (--impl reference) times the reference's own CPU renderer
+(voxvid from baseline/_ref: render.render / compose.render_scene, numba,
+all host threads) on the same workload, or, if that is not installed, the C
+oracle port (OpenMP, all host threads).
 """
 
 from __future__ import annotations
 
 import argparse
 import collections
+import ctypes
 import json
 import os
 import statistics
@@ -40,11 +53,25 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "Mrays/s and FPS at 1080p (VOctree HH render) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "Mrays/s"
-WIDTH, HEIGHT, FRAMES = 1920, 1080, 30
-WORKLOAD = ("cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached render "
-            "(ray gen + traversal + HH shading + compositing + finalize), frame sweep")
-C_COEF, K_HH = 31, 14
+WIDTH, HEIGHT = 1920, 1080
 L2_BYTES = 126 * 2**20
+
+CONFIGS = {
+    2: dict(frames=30, kind="single",
+            workload="cfg2: depth-9 shell VOctree (3,557,912 leaves, n_max 2, T 30), 1920x1080, uncached render "
+                     "(ray gen + traversal + HH shading + compositing + finalize), frame sweep"),
+    3: dict(frames=60, kind="single",
+            workload="cfg3: motion-heavy depth-9 VOctree (learnable temporal basis, ~90% of leaves dark per frame, "
+                     "n_max 2, T 60), 1920x1080, uncached render, 60-frame sweep"),
+    4: dict(frames=30, kind="scene",
+            workload="cfg4: 4 depth-9 shell performers (seeds 0-3; affines T(1.1(i-1.5),0,0) T(c) Rz(0.5i) S_i "
+                     "T(-c), S_3 = 0.8 I non-rigid; timemaps shift(3i)|loop(30)), 1920x1080, Algorithm-1 "
+                     "depth-ordered blending + background, global-frame sweep"),
+    5: dict(frames=30, kind="stereo",
+            workload="cfg5: stereo 2 x 2160x2160 (eyes at +-0.032 right of (1.6,1.3,0.9)) of the cfg2 tree, "
+                     "uncached render, frame sweep"),
+}
+WORKLOAD = CONFIGS[2]["workload"]  # the default line's workload
 
 
 def log(*a):
@@ -119,70 +146,18 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the render kernel from the committed ncu capture, if any."""
-    p = ROOT / "profiles" / "render_camera_ncu.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            return None
+def ncu_traffic(config: int):
+    """DRAM bytes per launch of the config's dominant kernel from its committed
+    ncu --set full capture (profiles/r02_ncu_cfg<N>.json), else null."""
+    for name in (f"r02_ncu_cfg{config}.json",) + (("render_camera_ncu.json",) if config == 2 else ()):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            try:
+                d = json.loads(p.read_text())
+                return d.get("dram_bytes_per_launch")
+            except Exception:
+                return None
     return None
-
-
-def make_tree(config: int):
-    from paper_2202_06088_b200 import synthetic
-
-    t0 = time.time()
-    if config == 3:
-        tree = synthetic.motion_tree(depth=9, n_max=2, frames=60, seed=0)
-    else:
-        tree = synthetic.shell_tree(depth=9, n_max=2, frames=FRAMES, seed=0)
-    log(f"[bench] tree: {tree.n_leaves} leaves, {tree.n_internal} internal, "
-        f"{tree.leaf_data.nbytes / 1e9:.3f} GB payload, built in {time.time() - t0:.1f}s")
-    return tree
-
-
-def algorithmic_bytes(tree, cam, frames, device):
-    """Reference-defined bytes per frame:
-    sum_rays 32 P + 4C V + 4(C+3K) S + 20, with P/V/S the internal-node pops,
-    visited leaves and shaded leaves of the reference traversal (early stop
-    1e-4), counted by the instrumented kernel on host-generated rays (bit-
-    exact with the reference's counts)."""
-    import torch
-
-    import paper_2202_06088_b200 as vv
-
-    o, d = cam.rays()
-    ot = torch.from_numpy(o).to(device)
-    dt = torch.from_numpy(d).to(device)
-    out = {}
-    c = tree.coeff_count
-    k = tree.basis_count
-    for f in frames:
-        _, _, _, st = vv.render_rays(tree, ot, dt, f, stats=True)
-        P = st["node_pops"].to(torch.int64).sum().item()
-        V = st["sample_count"].to(torch.int64).sum().item()
-        S = st["shaded"].to(torch.int64).sum().item()
-        n = o.shape[0]
-        s_sh = (tree.n_max + 1) ** 2
-        out[f] = dict(
-            P=P, V=V, S=S,
-            # uncached path (render_kernel decoding every visited leaf)
-            bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * n,
-            # sliced path actually executed: render kernel reads a node row per
-            # pop, the f64 sigma per visited leaf and the 3S fp32 sliced SH
-            # coefficients per shaded leaf, writes 20 B per pixel ...
-            render_bytes=32 * P + 8 * V + 12 * s_sh * S + 20 * n,
-            # ... after the per-frame slice pass read, per leaf, the w_sigma /
-            # w_gamma chunks the frame's A / B rows do not zero out (16 B
-            # each), w_hh, and wrote sigma + q
-            slice_bytes=tree.n_leaves * (16 * (_nz_chunks(tree.bases.a[f], c) + _nz_chunks(tree.bases.b[f], c))
-                                         + 12 * k + 8 + 12 * s_sh),
-            # the reference's formula (every payload column, SURVEY 8(d))
-            slice_formula_bytes=tree.n_leaves * (4 * (2 * c + 3 * k) + 8 + 12 * s_sh),
-        )
-    return out
 
 
 def _nz_chunks(row, c):
@@ -191,11 +166,133 @@ def _nz_chunks(row, c):
     return int(np.count_nonzero(np.pad(r != 0, (0, -c % 4)).reshape(-1, 4).any(axis=1)))
 
 
-# --------------------------------------------------------------------------- CPU baselines
-def cpu_reference_render(tree, cam, frames, warm=()):
-    """Time the reference's own render() (voxvid numba) if installed in baseline/_ref.
+class Workload:
+    """The config's trees, cameras (and scene), built deterministically."""
 
-    ``warm`` frames are rendered untimed first (the W warm-up steps)."""
+    def __init__(self, config: int):
+        from paper_2202_06088_b200 import synthetic
+
+        self.config = config
+        spec = CONFIGS[config]
+        self.kind, self.frames_total, self.workload = spec["kind"], spec["frames"], spec["workload"]
+        t0 = time.time()
+        self.scene = None
+        if config == 3:
+            self.trees = [synthetic.motion_tree(depth=9, n_max=2, frames=60, seed=0)]
+        elif config == 4:
+            self.trees = [synthetic.shell_tree(depth=9, n_max=2, frames=30, seed=s) for s in range(4)]
+        else:
+            self.trees = [synthetic.shell_tree(depth=9, n_max=2, frames=30, seed=0)]
+        if config == 4:
+            self.scene, cam = synthetic.scene_config4(self.trees, WIDTH, HEIGHT)
+            self.cams = [cam]
+        elif config == 5:
+            self.cams = synthetic.stereo_cameras()
+        else:
+            self.cams = [synthetic.bench_camera(WIDTH, HEIGHT)]
+        self.tree = self.trees[0]
+        npix = sum(c.width * c.height for c in self.cams)
+        # rays per step: every camera ray; a composed frame traverses every
+        # instance through its pulled-back ray
+        self.rays = npix * (len(self.trees) if config == 4 else 1)
+        self.pixels = npix
+        log(f"[bench] cfg{config}: {len(self.trees)} tree(s) x {self.tree.n_leaves} leaves, "
+            f"{sum(t.leaf_data.nbytes for t in self.trees) / 1e9:.3f} GB payload, {self.rays} rays/step, "
+            f"built in {time.time() - t0:.1f}s")
+
+
+def instance_rays(inst, cam, g):
+    """Host pulled-back rays of one scene instance (compose.render_instance)."""
+    from paper_2202_06088_b200.compose import _is_rigid
+    from paper_2202_06088_b200.render import Camera
+
+    inv = np.linalg.inv(inst.effective_affine(g))
+    m = inv @ cam.c2w
+    if _is_rigid(m):
+        return Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, m).rays()
+    o, d = cam.rays()
+    o_t = o @ inv[:3, :3].T + inv[:3, 3]
+    d_raw = d @ inv[:3, :3].T
+    return o_t, d_raw / np.linalg.norm(d_raw, axis=1, keepdims=True)
+
+
+def walk_counts(tree, o, d, f, device, masked=False):
+    """Per-ray P (internal-node pops), V (visited leaves), S (shaded leaves)
+    summed, from the instrumented kernel (bit-exact with the reference's
+    counts on the same rays); ``masked``: counts of the node-masked walk the
+    image kernels actually execute (VV_STATS_MASKED)."""
+    import torch
+
+    import paper_2202_06088_b200 as vv
+
+    ot = torch.from_numpy(np.ascontiguousarray(o)).to(device)
+    dt = torch.from_numpy(np.ascontiguousarray(d)).to(device)
+    if masked:
+        os.environ["VV_STATS_MASKED"] = "1"
+    try:
+        _, _, _, st = vv.render_rays(tree, ot, dt, f, stats=True)
+    finally:
+        os.environ.pop("VV_STATS_MASKED", None)
+    return {k: int(st[n].to(torch.int64).sum().item()) for k, n in
+            (("P", "node_pops"), ("V", "sample_count"), ("S", "shaded"))}
+
+
+def algorithmic_bytes(wl, frames, device):
+    """Reference-defined bytes per step with P/V/S of the
+    reference traversal, and the bytes of the path actually executed:
+    * sliced camera path (cfg2/3/5): render kernel 32 P + 8 V + 12 S_sh S + 20
+      per ray (node row per pop, f64 sigma per visited leaf, 3 S_sh fp32 q per
+      shaded leaf, fp32 rgb/alpha/depth out); slice pass per leaf 16 B per
+      nonzero-basis w_sigma / w_gamma float4 chunk + 12 K (w_hh) + 8 + 12 S_sh;
+    * scene per-sample path (cfg4): per instance ray 32 P + 16 nzA V +
+      (16 nzB + 12 K) S, + 12 B of image per pixel;
+    * the reference formula (every column): 32 P + 4C V + 4(C + 3K) S + 20."""
+    c, k = wl.tree.coeff_count, wl.tree.basis_count
+    s_sh = (wl.tree.n_max + 1) ** 2
+    out = {}
+    for f in frames:
+        P = V = S = 0
+        Pm = Vm = Sm = 0
+        ex = 0
+        if wl.kind == "scene":
+            for inst in wl.scene.instances:
+                lf = inst.local_frame(f)
+                o, d = instance_rays(inst, wl.cams[0], f)
+                cnt = walk_counts(inst.tree, o, d, lf, device)
+                P, V, S = P + cnt["P"], V + cnt["V"], S + cnt["S"]
+                nza, nzb = _nz_chunks(inst.tree.bases.a[lf], c), _nz_chunks(inst.tree.bases.b[lf], c)
+                ex += 32 * cnt["P"] + 16 * nza * cnt["V"] + (16 * nzb + 12 * k) * cnt["S"]
+            ex += 12 * wl.pixels
+            Pm, Vm, Sm = P, V, S
+            slice_b = 0
+        else:
+            for cam in wl.cams:
+                o, d = cam.rays()
+                cnt = walk_counts(wl.tree, o, d, f, device)
+                P, V, S = P + cnt["P"], V + cnt["V"], S + cnt["S"]
+                cm = walk_counts(wl.tree, o, d, f, device, masked=True) if wl.config == 3 else cnt
+                Pm, Vm, Sm = Pm + cm["P"], Vm + cm["V"], Sm + cm["S"]
+            ex = 32 * Pm + 8 * Vm + 12 * s_sh * Sm + 20 * wl.pixels
+            slice_b = wl.tree.n_leaves * (16 * (_nz_chunks(wl.tree.bases.a[f], c) + _nz_chunks(wl.tree.bases.b[f], c))
+                                          + 12 * k + 8 + 12 * s_sh)
+        out[f] = dict(P=P, V=V, S=S, Pm=Pm, Vm=Vm, Sm=Sm, render_bytes=ex, slice_bytes=slice_b,
+                      reference_bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * wl.pixels)
+    return out
+
+
+# --------------------------------------------------------------------------- CPU baselines
+def _ref_tree(tree):
+    from voxvid.octree import VOctree as RV
+    from voxvid.temporal import TemporalBases as RTB
+
+    return RV(tree.depth, tree.node_child, tree.leaf_coords, tree.leaf_data, RTB(tree.bases.a, tree.bases.b),
+              tree.n_max, tree.bbox_lo, tree.side)
+
+
+def cpu_reference_render(wl, frames, warm=()):
+    """Time the reference's own renderer (voxvid numba, baseline/_ref) on the
+    config's step: render() per camera, or compose.render_scene for cfg4.
+    ``warm`` steps run untimed first (the W warm-up steps)."""
     ref_dir = ROOT / "baseline" / "_ref"
     if not (ref_dir / "voxvid").exists():
         return None
@@ -203,45 +300,73 @@ def cpu_reference_render(tree, cam, frames, warm=()):
     os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count()))
     sys.path.insert(0, str(ref_dir))
     import numba
+    from voxvid import compose as rc
     from voxvid import render as rr
-    from voxvid.octree import VOctree as RV
-    from voxvid.temporal import TemporalBases as RTB
 
-    rtree = RV(tree.depth, tree.node_child, tree.leaf_coords, tree.leaf_data, RTB(tree.bases.a, tree.bases.b),
-               tree.n_max, tree.bbox_lo, tree.side)
-    rcam = rr.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
-    small = rr.Camera(64, 36, cam.fx / 30, cam.fy / 30, 32.0, 18.0, cam.c2w)
+    rtrees = {id(t): _ref_tree(t) for t in wl.trees}
+    rcams = [rr.Camera(c.width, c.height, c.fx, c.fy, c.cx, c.cy, c.c2w) for c in wl.cams]
+    if wl.kind == "scene":
+        rscene = rc.Scene(instances=[rc.SceneInstance(name=i.name, tree=rtrees[id(i.tree)], affine=i.affine,
+                                                      timemap=rc.TimeMap.parse(str(i.timemap)))
+                                     for i in wl.scene.instances], background=wl.scene.background)
+
+        def one(f):
+            rc.render_scene(rscene, rcams[0], f)
+    else:
+        rtree = rtrees[id(wl.tree)]
+
+        def one(f):
+            for cam in rcams:
+                rr.render(rtree, cam, f)
+    small = rr.Camera(64, 36, wl.cams[0].fx / 30, wl.cams[0].fy / 30, 32.0, 18.0, wl.cams[0].c2w)
     t0 = time.time()
-    rr.render(rtree, small, frames[0])  # JIT warm-up
+    rr.render(rtrees[id(wl.tree)], small, 0)  # JIT warm-up
     log(f"[bench] reference JIT warm-up {time.time() - t0:.1f}s, numba threads {numba.get_num_threads()}")
     for f in warm:
-        rr.render(rtree, rcam, f)
+        one(f)
     times = []
     for f in frames:
         t0 = time.perf_counter()
-        rr.render(rtree, rcam, f)
+        one(f)
         times.append(time.perf_counter() - t0)
+    what = "voxvid.compose.render_scene" if wl.kind == "scene" else "voxvid.render.render per camera"
     return dict(times=times, cores=int(numba.get_num_threads()), kind="reference",
-                impl="voxvid.render.render (numba, baseline/_ref), uncached")
+                impl=f"{what} (numba, baseline/_ref), uncached")
 
 
-def cpu_port_render(tree, cam, frames, warm=()):
-    """Time the C oracle port (OpenMP, all host threads): ray gen + render_kernel + finalize.
-
-    ``warm`` frames are rendered untimed first (the W warm-up steps)."""
+def cpu_port_render(wl, frames, warm=()):
+    """Time the C oracle port (OpenMP, all host threads) on the config's step:
+    ray gen + render_kernel + finalize per camera; cfg4 renders every instance's
+    pulled-back rays and blends with Algorithm 1 (numpy, compose.blend_layers)."""
     from oracle import oracle
+    from paper_2202_06088_b200.compose import blend_layers
+    from paper_2202_06088_b200.render import LayerImages
 
     nt = oracle.num_procs()
+
+    def one(f):
+        if wl.kind == "scene":
+            cam = wl.cams[0]
+            layers = []
+            for inst in wl.scene.instances:
+                o, d = instance_rays(inst, cam, f)
+                out = oracle.render_rays(inst.tree, o, d, inst.local_frame(f), nthreads=nt)
+                rgb, a, dep = oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+                layers.append(LayerImages(rgb.reshape(cam.height, cam.width, 3), a.reshape(cam.height, cam.width),
+                                          dep.reshape(cam.height, cam.width)))
+            blend_layers(layers)
+            return
+        for cam in wl.cams:
+            o, d = cam.rays()
+            out = oracle.render_rays(wl.tree, o, d, f, nthreads=nt)
+            oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+
     for f in warm:
-        o, d = cam.rays()
-        out = oracle.render_rays(tree, o, d, f, nthreads=nt)
-        oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+        one(f)
     times = []
     for f in frames:
         t0 = time.perf_counter()
-        o, d = cam.rays()
-        out = oracle.render_rays(tree, o, d, f, nthreads=nt)
-        oracle.finalize(out["premult"], out["alpha"], out["tbar"])
+        one(f)
         times.append(time.perf_counter() - t0)
     return dict(times=times, cores=nt, kind="port", impl="oracle/vv_oracle.c (OpenMP), uncached")
 
@@ -249,308 +374,393 @@ def cpu_port_render(tree, cam, frames, warm=()):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    cam_mod = __import__("paper_2202_06088_b200.synthetic", fromlist=["bench_camera"])
-    tree = make_tree(args.config)
-    cam = cam_mod.bench_camera(WIDTH, HEIGHT)
-    warm = [i % FRAMES for i in range(args.warmup)]
-    frames = [i % FRAMES for i in range(args.warmup, args.warmup + args.steps)]
-    res = cpu_reference_render(tree, cam, frames, warm) if not args.port else None
+    wl = Workload(args.config)
+    T = wl.frames_total
+    warm = [i % T for i in range(args.warmup)]
+    frames = [i % T for i in range(args.warmup, args.warmup + args.steps)]
+    res = cpu_reference_render(wl, frames, warm) if not args.port else None
     if res is None:
-        res = cpu_port_render(tree, cam, frames, warm)
-    n_rays = WIDTH * HEIGHT
+        res = cpu_port_render(wl, frames, warm)
     ms = 1e3 * sum(res["times"]) / len(res["times"])
-    value = n_rays * len(res["times"]) / sum(res["times"]) / 1e6
+    value = wl.rays * len(res["times"]) / sum(res["times"]) / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "fps": round(1e3 / ms, 4),
-        "config": {"workload": WORKLOAD, "rays_per_step": n_rays, "frames": frames,
-                   "warmup_frames": warm},
+        "config": {"workload": wl.workload, "rays_per_step": wl.rays, "frames": frames, "warmup_frames": warm},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
-                         "sample": f"{len(frames)} full 1080p frames {frames}", "impl": res["impl"]},
+                         "sample": f"{len(frames)} full step(s) {frames}", "impl": res["impl"]},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------- GPU arm
+class Stepper:
+    """The config's per-step device work, split where its dominant kernel's
+    own duration must be measured (mid event on the launching stream)."""
+
+    def __init__(self, wl, dev):
+        import torch
+
+        import paper_2202_06088_b200 as vv
+
+        self.wl, self.dev, self.vv = wl, dev, vv
+        self.outs = [(torch.empty((c.height, c.width, 3), dtype=torch.float32, device=dev),
+                      torch.empty((c.height, c.width), dtype=torch.float32, device=dev),
+                      torch.empty((c.height, c.width), dtype=torch.float32, device=dev)) for c in wl.cams]
+        # camera streams' launch plans (what render() keeps per stream): the
+        # camera kernel's persistent warps take each frame's blocks in the
+        # previous frame's measured cost order; images bitwise unchanged
+        self.plans = [vv.CameraPlan(dev) for _ in wl.cams]
+        self.descs = {}
+        self.launches = 0
+
+    def prepare(self, frames):
+        """Host-side per-frame scene resolution (timemaps, affines) ahead of the
+        device-timed region (cfg4)."""
+        if self.wl.kind != "scene":
+            return
+        from paper_2202_06088_b200.compose import scene_instances
+
+        for f in frames:
+            if f not in self.descs:
+                self.descs[f] = scene_instances(self.wl.scene, self.wl.cams[0], f, self.dev)
+
+    def __call__(self, f, mid=None, stream=None):
+        vv, wl = self.vv, self.wl
+        if wl.kind == "scene":
+            from paper_2202_06088_b200 import _native
+            from paper_2202_06088_b200.device import stream_ptr
+
+            descs, _, _ = self.descs[f]
+            bg = (ctypes.c_double * 3)(*[float(v) for v in wl.scene.background])
+            oc = vv.RenderOptions().c_struct()
+            cd = wl.cams[0].desc()
+            if mid is not None:
+                mid.record(stream)
+            _native.check(_native.lib().vv_render_scene(descs, len(descs), ctypes.byref(oc), ctypes.byref(cd), bg,
+                                                        self.outs[0][0].data_ptr(), None, None,
+                                                        stream_ptr(self.dev)))
+            self.launches += 1
+            return
+        # exactly what render() does: the render-internal slice pass (colour of
+        # all-dark leaf chunks skipped; node masks for dark-heavy trees) ...
+        fs = vv.build_frame_caches(wl.tree, [f], render_only=True)[0]
+        if mid is not None:
+            mid.record(stream)
+        for cam, out, plan in zip(wl.cams, self.outs, self.plans):  # ... then the camera kernel(s)
+            vv.render_into(wl.tree, cam, f, *out, cache=fs, plan=plan)
+        self.launches += 1 + 2 * len(wl.cams)  # slice, (camera kernel + plan order) per camera
+        del fs
+
+
+def timed_steps(step, frames, dev, world, flush, stream, split=True):
+    """Device-timed steps: barrier + sync, per-step CUDA events on the launching
+    stream (L2 flushed between steps, outside the events); returns total,
+    pre-mid (slice) and post-mid (render) ms, max over ranks for the total."""
+    import torch
+    import torch.distributed as dist
+
+    n = len(frames)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i, f in enumerate(frames):
+        flush.zero_()
+        starts[i].record(stream)
+        step(f, mids[i] if split else None, stream)
+        if not split:
+            mids[i].record(stream)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    total = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    render = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) if split else total
+    slice_ = sum(s.elapsed_time(m) for s, m in zip(starts, mids)) if split else 0.0
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), slice_, render, wall
+
+
+def region_frames(wl, frames, warm, dev, rank, world, flush, stream):
+    """Strong scaling: every frame split into row bands over the ranks, each
+    band stored into rank 0's planes over NVLink (TileRenderer "regions"),
+    one stream-ordered all-reduce per frame; time per frame = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2202_06088_b200.distributed import TileRenderer
+
+    rs = [TileRenderer(c.width, c.height, 64, rank, world, dev, mode="regions") for c in wl.cams]
+    for r, c in zip(rs, wl.cams):
+        r.plan(wl.tree, c, 0)
+
+    def step(f, mid=None, st=None):
+        for r, c in zip(rs, wl.cams):
+            r.render_frame(wl.tree, c, f)
+
+    for f in warm:
+        step(f)
+    torch.cuda.synchronize()
+    total, _, _, _ = timed_steps(step, frames, dev, world, flush, stream, split=False)
+    dist.barrier()
+    for r in rs:
+        r.close()
+    return total, [r.bands for r in rs]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_2202_06088_b200 as vv
-    from paper_2202_06088_b200 import synthetic
-    from paper_2202_06088_b200.device import replica, stream_ptr
-    from paper_2202_06088_b200.distributed import TileRenderer
+    from paper_2202_06088_b200.device import replica
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    tree = make_tree(args.config)
-    cam = synthetic.bench_camera(WIDTH, HEIGHT)
-    n_rays = WIDTH * HEIGHT
+    wl = Workload(args.config)
+    T = wl.frames_total
     t0 = time.time()
-    rep = replica(tree, dev)
+    reps = [replica(t, dev) for t in wl.trees]
     torch.cuda.synchronize()
-    log(f"[bench] rank {rank}: upload {time.time() - t0:.2f}s, {rep.device_bytes / 1e9:.3f} GB on device")
-
-    # batched playback: frame f is rendered by rank f mod world (full replica
-    # per GPU, frames independent -> no data-path collective, weak scaling)
-    frames_total = FRAMES if args.config != 3 else 60
-    step_frames = [(args.warmup * world + i * world + rank) % frames_total for i in range(args.steps)]
-    warm_frames = [(i * world + rank) % frames_total for i in range(args.warmup)]
-
-    rgb = torch.empty((HEIGHT, WIDTH, 3), dtype=torch.float32, device=dev)
-    alpha = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
-    depth = torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)
-    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    cur = {"mid": None}
-
-    def step(f):
-        # identical work to render(tree, cam, f): per-frame slice pass, then the
-        # fused ray-gen/traversal/shading/finalize kernel -- split here so the
-        # dominant kernel's own duration is measured (roofline)
-        fs = vv.build_frame_cache(tree, f)
-        if cur["mid"] is not None:
-            cur["mid"].record(stream)
-        vv.render_into(tree, cam, f, rgb, alpha, depth, cache=fs)
-        del fs
-
-    for f in warm_frames:
-        step(f)
-    torch.cuda.synchronize()
-
-    # device-timed region: K steps, L2 flushed between steps (outside the events)
+    log(f"[bench] rank {rank}: upload {time.time() - t0:.2f}s, {sum(r.device_bytes for r in reps) / 1e9:.3f} GB "
+        f"on device")
     stream = torch.cuda.current_stream(dev)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    strong = world > 1 and wl.kind in ("single", "stereo")
+
+    # every rank renders the same frames when the frame is split (strong
+    # scaling); by frame otherwise (frame f on rank f mod N)
+    if strong:
+        step_frames = [(args.warmup + i) % T for i in range(args.steps)]
+        warm_frames = [i % T for i in range(args.warmup)]
+    else:
+        step_frames = [(args.warmup * world + i * world + rank) % T for i in range(args.steps)]
+        warm_frames = [(i * world + rank) % T for i in range(args.warmup)]
+
+    stepper = Stepper(wl, dev)
+    stepper.prepare(set(step_frames) | set(warm_frames))
     clocks = ClockSampler(local_rank) if rank == 0 else None
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    if clocks:
-        clocks.start()
-    wall0 = time.perf_counter()
-    for i, f in enumerate(step_frames):
-        flush.zero_()
-        starts[i].record(stream)
-        cur["mid"] = mids[i]
-        step(f)
-        ends[i].record(stream)
-    cur["mid"] = None
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    if world > 1:
-        dist.barrier()
+    bands = None
+    wall = None
+    slice_ms = render_ms = None
+    if strong:
+        if clocks:
+            clocks.start()
+        total_ms, bands = region_frames(wl, step_frames, warm_frames, dev, rank, world, flush, stream)
+        # the frame-sharded view of the same job (weak scaling), for reference
+        fs_frames = [(args.warmup * world + i * world + rank) % T for i in range(args.steps)]
+        for f in warm_frames:
+            stepper(f)
+        fs_total, _, _, _ = timed_steps(stepper, fs_frames, dev, world, flush, stream)
+        frame_sharded = {"ms_per_step": round(fs_total / len(fs_frames), 4),
+                         "value": round(world * wl.rays * len(fs_frames) / fs_total / 1e3, 3), "unit": UNIT,
+                         "scaling": "weak", "what": f"frame f on rank f mod {world}, one full frame per rank per step"}
+    else:
+        for f in warm_frames:
+            stepper(f)
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        stepper.launches = 0
+        total_ms, slice_ms, render_ms, wall = timed_steps(stepper, step_frames, dev, world, flush, stream,
+                                                         split=wl.kind != "scene")
+        frame_sharded = None
     clk = clocks.stop() if clocks else None
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    render_ms = sum(m.elapsed_time(e) for m, e in zip(mids, ends))
-    slice_ms = sum(s.elapsed_time(m) for s, m in zip(starts, mids))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
 
-    # playback on the device: groups of playback_group(tree) frames of the same
-    # camera share one octree walk (render_frames_into; images bitwise equal
-    # to render()), every frame with its own slice pass; L2 flushed between
-    # groups outside the events
-    from paper_2202_06088_b200.render import playback_group
+    # playback on the device (cfg2/3): groups of playback_group(tree) frames of
+    # one camera share one octree walk, each with its own slice pass
+    playback = None
+    if wl.kind == "single":
+        from paper_2202_06088_b200.render import playback_group
 
-    G = playback_group(tree)
+        G = playback_group(wl.tree)
+        cam = wl.cams[0]
+        pb_outs = [(torch.empty((cam.height, cam.width, 3), device=dev), torch.empty((cam.height, cam.width), device=dev),
+                    torch.empty((cam.height, cam.width), device=dev)) for _ in range(G)]
+        pfr = [(args.warmup * world + i * world + rank) % T for i in range(args.steps)]
+        groups = [pfr[i:i + G] for i in range(0, len(pfr) - G + 1, G)] or [pfr[:G]]
+        warm_group = [(i * world + rank) % T for i in range(G)]
+        for gr in [warm_group] * 2:
+            vv.render_frames_into(wl.tree, cam, gr, pb_outs[:len(gr)])
+        torch.cuda.synchronize()
+        gs = [torch.cuda.Event(enable_timing=True) for _ in groups]
+        ge = [torch.cuda.Event(enable_timing=True) for _ in groups]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i, gr in enumerate(groups):
+            flush.zero_()
+            gs[i].record(stream)
+            vv.render_frames_into(wl.tree, cam, gr, pb_outs[:len(gr)])
+            ge[i].record(stream)
+        torch.cuda.synchronize()
+        pb_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(gs, ge))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(pb_ms, op=dist.ReduceOp.MAX)
+        pb_frames = sum(len(g) for g in groups)
+        pbf = float(pb_ms.item()) / pb_frames
+        playback = {"value": round(world * wl.rays / pbf / 1e3, 3), "unit": UNIT, "ms_per_frame": round(pbf, 4),
+                    "fps": round(world * 1e3 / pbf, 2), "frames_per_walk": G, "frames": pb_frames,
+                    "scaling": "weak",
+                    "what": f"groups of {G} frames of the fixed bench camera share one octree walk "
+                            "(vv_render_camera_multi), frame-sharded over the ranks; each frame has its own slice "
+                            "pass, accumulators and early termination; images bitwise equal to render() per frame"}
 
-    pb_outs = [(torch.empty((HEIGHT, WIDTH, 3), dtype=torch.float32, device=dev),
-                torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev),
-                torch.empty((HEIGHT, WIDTH), dtype=torch.float32, device=dev)) for _ in range(G)]
-    groups = [step_frames[i:i + G] for i in range(0, len(step_frames) - G + 1, G)] or [step_frames[:G]]
-    warm_group = [warm_frames[i % len(warm_frames)] for i in range(G)]  # a full group: loads its kernels
-    for gr in [warm_group] * 2:
-        vv.render_frames_into(tree, cam, gr, pb_outs[:len(gr)])
-    torch.cuda.synchronize()
-    gs = [torch.cuda.Event(enable_timing=True) for _ in groups]
-    ge = [torch.cuda.Event(enable_timing=True) for _ in groups]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i, gr in enumerate(groups):
-        flush.zero_()
-        gs[i].record(stream)
-        vv.render_frames_into(tree, cam, gr, pb_outs[:len(gr)])
-        ge[i].record(stream)
-    torch.cuda.synchronize()
-    pb_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(gs, ge))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(pb_ms, op=dist.ReduceOp.MAX)
-    pb_frames = sum(len(g) for g in groups)
-    pb_ms_frame = float(pb_ms.item()) / pb_frames
-    playback = {"value": round(world * n_rays / pb_ms_frame / 1e3, 3), "unit": UNIT,
-                "ms_per_frame": round(pb_ms_frame, 4), "fps": round(world * 1e3 / pb_ms_frame, 2),
-                "frames_per_walk": G, "frames": pb_frames,
-                "what": f"groups of {G} frames of the fixed bench camera share one octree walk "
-                        "(vv_render_camera_multi); each frame has its own slice pass, accumulators and "
-                        "early termination; images bitwise equal to render() per frame"}
-
-    # end-to-end through the public API: every frame complete on the host
-    for f in warm_frames[:3]:  # two results alive at once in the loop below: warm both pinned buffers
-        layer = vv.render(tree, cam, f)
-    torch.cuda.synchronize()
-    # single-call latency: render() -> numpy, one frame at a time
-    te = time.perf_counter()
-    for f in step_frames[:10]:
-        layer = vv.render(tree, cam, f)
-    single_ms = (time.perf_counter() - te) / len(step_frames[:10]) * 1e3
-    assert layer.rgb.shape == (HEIGHT, WIDTH, 3)
-    del layer
-    # steady-state playback: pinned result pool and render streams warm
-    # (a 41 MB cudaHostAlloc costs 25-100 ms; none may land in the timed run)
-    for _ in range(2):
-        collections.deque(vv.render_sequence(tree, cam, warm_group * 2), maxlen=0)  # full groups; holds no frame
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    te = time.perf_counter()
-    got = 0
-    for layer in vv.render_sequence(tree, cam, step_frames):  # this rank's frames, to this rank's host
-        got += 1
-    e2e_s = time.perf_counter() - te
-    assert got == len(step_frames) and layer.rgb.shape == (HEIGHT, WIDTH, 3)
-    del layer
+    # end-to-end through the public API, results on the host (every rank its
+    # own frames to its own host memory)
+    e2e_frames = [(args.warmup * world + i * world + rank) % T for i in range(args.steps)]
+    if wl.kind == "single":
+        cam = wl.cams[0]
+        for f in warm_frames[:3]:
+            layer = vv.render(wl.tree, cam, f)
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for f in e2e_frames[:10]:
+            layer = vv.render(wl.tree, cam, f)
+        single_ms = (time.perf_counter() - te) / len(e2e_frames[:10]) * 1e3
+        del layer
+        warm_group = [(i * world + rank) % T for i in range(3)]
+        for _ in range(2):
+            collections.deque(vv.render_sequence(wl.tree, cam, warm_group * 2), maxlen=0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        got = 0
+        for layer in vv.render_sequence(wl.tree, cam, e2e_frames):
+            got += 1
+        e2e_s = time.perf_counter() - te
+        assert got == len(e2e_frames) and layer.rgb.shape == (cam.height, cam.width, 3)
+        del layer
+        api = ("paper_2202_06088_b200.render_sequence(tree, cam, frames) -> numpy LayerImages (fp32) per frame on "
+               "every rank; groups of 3 frames share one walk, group g rendered while group g-1 copies to pinned "
+               "host memory")
+        d2h = 20 * wl.pixels
+    elif wl.kind == "stereo":
+        for f in warm_frames[:2]:
+            for cam in wl.cams:
+                vv.render(wl.tree, cam, f)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for f in e2e_frames:
+            for cam in wl.cams:
+                layer = vv.render(wl.tree, cam, f)
+        e2e_s = time.perf_counter() - te
+        single_ms = e2e_s / len(e2e_frames) * 1e3
+        api = "paper_2202_06088_b200.render(tree, eye, frame) -> numpy LayerImages (fp32), both eyes per frame"
+        d2h = 20 * wl.pixels
+    else:
+        for f in warm_frames[:2]:
+            vv.render_scene(wl.scene, wl.cams[0], f)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for f in e2e_frames:
+            img = vv.render_scene(wl.scene, wl.cams[0], f)
+        e2e_s = time.perf_counter() - te
+        assert img.shape == (HEIGHT, WIDTH, 3)
+        single_ms = e2e_s / len(e2e_frames) * 1e3
+        api = "paper_2202_06088_b200.render_scene(scene, cam, g) -> numpy (H, W, 3) fp32 image per global frame"
+        d2h = 12 * wl.pixels
     if world > 1:
         et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_s = float(et.item())
-    e2e = {"value": round(world * n_rays * len(step_frames) / e2e_s / 1e6, 3), "unit": UNIT,
-           "h2d_bytes_per_step": (168 + 48) * world, "d2h_bytes_per_step": 5 * 4 * n_rays * world,
-           "api": "paper_2202_06088_b200.render_sequence(tree, cam, frames) -> numpy LayerImages (fp32) "
-                  "per frame on every rank; frames rendered in groups of 3 sharing one walk (see playback), "
-                  "group g rendered while group g-1 copies to pinned host memory",
-           "single_render_call_ms": round(single_ms, 3)}
-
-    # single-frame latency across the ranks: 64x64 tiles interleaved over the
-    # GPUs, one NCCL all-gather of the packed slabs, unpack on rank 0
-    tile_frame = None
-    if world > 1:
-        tiles = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev)
-
-        def tile_step(f):
-            tiles.render_slab(tree, cam, f)
-            tiles.gather()
-            if rank == 0:
-                tiles.unpack(rgb, alpha, depth)
-
-        for f in warm_frames:
-            tile_step(f)
-        torch.cuda.synchronize()
-        nt = min(10, len(step_frames))
-        ts = [torch.cuda.Event(enable_timing=True) for _ in range(nt)]
-        tend = [torch.cuda.Event(enable_timing=True) for _ in range(nt)]
-        dist.barrier()
-        torch.cuda.synchronize()
-        for i, f in enumerate(step_frames[:nt]):
-            flush.zero_()  # L2 flush outside the per-frame events
-            ts[i].record(stream)
-            tile_step(f)
-            tend[i].record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ts, tend)) / nt], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tile_frame = {"ms_per_frame": round(float(tt.item()), 4),
-                      "mrays": round(n_rays / float(tt.item()) / 1e3, 3),
-                      "parallelism": f"64x64 tiles interleaved over {world} GPUs + NCCL all_gather + unpack",
-                      "note": "one frame split across all GPUs (strong scaling); L2 flushed between frames "
-                              "outside the per-frame events; the all-gather is inside them"}
-        # fused form: every rank stores its tiles straight into rank 0's
-        # frame over NVLink (CUDA IPC), one stream-ordered barrier per frame
-        p2p = TileRenderer(WIDTH, HEIGHT, 64, rank, world, dev, mode="p2p")
-        for f in warm_frames:
-            p2p.render_frame(tree, cam, f)
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        for i, f in enumerate(step_frames[:nt]):
-            flush.zero_()
-            ts[i].record(stream)
-            p2p.render_frame(tree, cam, f)
-            tend[i].record(stream)
-        torch.cuda.synchronize()
-        tp = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ts, tend)) / nt], dtype=torch.float64, device=dev)
-        dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-        dist.barrier()
-        p2p.close()
-        tile_frame["p2p"] = {"ms_per_frame": round(float(tp.item()), 4),
-                             "mrays": round(n_rays / float(tp.item()) / 1e3, 3),
-                             "parallelism": f"64x64 tiles interleaved over {world} GPUs, each rank's tile kernel "
-                                            "storing into rank 0's frame through CUDA IPC (NVLink/NVSwitch), "
-                                            "one all-reduce barrier; no slab, no all-gather, no unpack"}
+    e2e = {"value": round(world * wl.rays * len(e2e_frames) / e2e_s / 1e6, 3), "unit": UNIT,
+           "h2d_bytes_per_step": (168 + 48) * len(wl.cams) * world, "d2h_bytes_per_step": d2h * world,
+           "api": api, "scaling": "weak", "single_call_ms": round(single_ms, 3)}
 
     if rank != 0:
         return
 
-    # roofline of the dominant kernel (k_render_camera), reference-defined bytes
-    ab = algorithmic_bytes(tree, cam, sorted(set(step_frames)), dev)
-    bytes_per_step = [ab[f]["bytes"] for f in step_frames]
+    # roofline of the dominant kernel, bytes per launch from the walk counts
     peak, peak_kind = measured_peak()
-    # per GPU (rank 0's kernels; every rank does the same per-frame work)
-    rbytes = sum(ab[f]["render_bytes"] for f in step_frames)
-    sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
-    achieved = rbytes / (render_ms / 1e3) / 1e9
-    slice_gbs = sbytes / (slice_ms / 1e3) / 1e9
-    frame_gbs = (rbytes + sbytes) / (total_ms / 1e3) / 1e9
-    uncached_gbs = sum(bytes_per_step) / (total_ms / 1e3) / 1e9
-    mean_ab = {k: float(np.mean([ab[f][k] for f in step_frames]) / n_rays) for k in ("P", "V", "S")}
+    n = len(step_frames)
+    ms = total_ms / n
+    roofline = None
+    if not strong:
+        ab = algorithmic_bytes(wl, sorted(set(step_frames)), dev)
+        rbytes = sum(ab[f]["render_bytes"] for f in step_frames)
+        achieved = rbytes / (render_ms / 1e3) / 1e9
+        per_ray = {k: float(np.mean([ab[f][k] for f in step_frames]) / wl.rays) for k in ("P", "V", "S")}
+        kernel = {"scene": "k_render_scene_lean"}.get(wl.kind, "k_render_camera")
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                    "peak_kind": peak_kind, "kernel": kernel,
+                    "kernel_ms": round(render_ms / n, 4),
+                    "bytes_per_launch": float(np.mean([ab[f]["render_bytes"] for f in step_frames])),
+                    "per_ray_reference": per_ray,
+                    "reference_formula_bytes_per_step": float(np.mean([ab[f]["reference_bytes"] for f in step_frames])),
+                    "reference_formula_achieved": round(sum(ab[f]["reference_bytes"] for f in step_frames)
+                                                        / (total_ms / 1e3) / 1e9, 1)}
+        if wl.kind == "scene":
+            roofline["bytes_formula"] = ("sum over instance rays 32 P + 16 nzA V + (16 nzB + 12 K) S + 12 B/px "
+                                         "(per-sample decode, nonzero-basis chunks; P/V/S reference counts)")
+        else:
+            roofline["bytes_formula"] = ("sum_rays 32 P + 8 V + 12 S_sh S + 20 (sliced path; P/V/S counts of the "
+                                         + ("node-masked walk the kernel executes)" if wl.config == 3
+                                            else "reference traversal)"))
+            if wl.config == 3:
+                roofline["per_ray_masked_walk"] = {k: float(np.mean([ab[f][k + "m"] for f in step_frames]) / wl.rays)
+                                                   for k in ("P", "V", "S")}
+            sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
+            roofline["slice_pass"] = {
+                "kernel": "k_build_slice", "ms": round(slice_ms / n, 4),
+                "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
+                "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
+                "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
+                "bytes_formula": "per leaf 16 B per w_sigma / w_gamma float4 chunk the frame's A / B row does not "
+                                 "zero out + 12 K (w_hh) + 8 + 12 S_sh (record)"}
+            roofline["frame_achieved"] = round((rbytes + sbytes) / (total_ms / 1e3) / 1e9, 1)
 
-    # CPU baseline: oracle port on a bounded sample (rank 0, N = 1 only)
+    # CPU baseline: oracle port on one full step (rank 0, N = 1 only)
     cpu = None
     if world == 1 and not args.no_cpu:
         sample_frames = [step_frames[0]]
-        res = cpu_port_render(tree, cam, sample_frames)
-        cpu = {"value": round(n_rays * len(res["times"]) / sum(res["times"]) / 1e6, 4), "unit": UNIT,
+        res = cpu_port_render(wl, sample_frames)
+        cpu = {"value": round(wl.rays * len(res["times"]) / sum(res["times"]) / 1e6, 4), "unit": UNIT,
                "cores": res["cores"], "kind": res["kind"],
-               "sample": f"{len(sample_frames)} full 1080p frame(s) {sample_frames}, host ray gen + render + finalize"}
+               "sample": f"{len(sample_frames)} full step(s) {sample_frames} of this workload"}
 
-    ms = total_ms / len(step_frames)
-    value = world * n_rays * len(step_frames) / (total_ms / 1e3) / 1e6  # whole job
+    value = (1 if strong else world) * wl.rays * n / (total_ms / 1e3) / 1e6
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "fps": round(world * 1e3 / ms, 2),
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "fps": round((1 if strong else world) * 1e3 / ms, 2),
         "config": {
-            "workload": WORKLOAD,
-            "rays_per_step": n_rays * world, "frames_rank0": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
-            "l2": "inputs larger than L2 (1.54 GB tree) and L2 flushed between steps (252 MiB memset outside "
+            "workload": wl.workload, "config": args.config,
+            "rays_per_step": wl.rays * (1 if strong else world),
+            "frames_rank0": step_frames[:8] + (["..."] if len(step_frames) > 8 else []),
+            "l2": "inputs larger than L2 (>= 1.5 GB of trees) and L2 flushed between steps (252 MiB memset outside "
                   "the per-step CUDA events)",
-            "parallelism": f"frames x {world} GPUs (frame f on rank f mod {world}, full replica each)"
-                           if world > 1 else "single",
-            "per_ray": mean_ab, "wall_ms_timed_region": round(wall * 1e3, 3),
+            "parallelism": (f"every frame split over {world} GPUs in row bands {bands}, bands stored into rank 0's "
+                            "planes over NVLink (CUDA IPC), one all-reduce per frame" if strong else
+                            (f"frames x {world} GPUs (frame f on rank f mod {world}, full replica each)"
+                             if world > 1 else "single")),
+            "wall_ms_timed_region": round(wall * 1e3, 3) if wall else None,
             "dtype_note": "f64 traversal/sigma/compositing, fp32 HH colour",
         },
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
-                     "peak_kind": peak_kind, "kernel": "k_render_camera",
-                     "kernel_ms": round(render_ms / len(step_frames), 4),
-                     "bytes_per_launch": float(np.mean([ab[f]["render_bytes"] for f in step_frames])),
-                     "bytes_formula": "sum_rays 32 P + 8 V + 12 S_sh S + 20 (sliced path; P/V/S reference counts)",
-                     "slice_pass": {"kernel": "k_build_slice",
-                                    "ms": round(slice_ms / len(step_frames), 4),
-                                    "achieved": round(slice_gbs, 1) if slice_gbs else None,
-                                    "frac": round(slice_gbs / peak, 4) if slice_gbs else None,
-                                    "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
-                                    "bytes_formula": "per leaf 16 B per w_sigma / w_gamma float4 chunk the "
-                                                     "frame's A / B row does not zero out + 12 K (w_hh) + 8 + "
-                                                     "12 S_sh (record); the reference formula 4(2C + 3K) + 8 + "
-                                                     "12 S_sh reads every column",
-                                    "reference_formula_bytes": float(ab[step_frames[0]]["slice_formula_bytes"])},
-                     "frame_achieved": round(frame_gbs, 1) if frame_gbs else None,
-                     "uncached_formula_achieved": round(uncached_gbs, 1) if uncached_gbs else None,
-                     "uncached_bytes_per_frame": float(np.mean(bytes_per_step))},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "playback": playback,
-        "gpu_launches": len(step_frames) * 2 * world,
-        "tile_frame": tile_frame,
+        "frame_sharded": frame_sharded,
+        "gpu_launches": stepper.launches if not strong else None,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -562,7 +772,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--port", action="store_true", help="reference arm: force the C oracle port")
     args = ap.parse_args()

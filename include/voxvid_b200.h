@@ -41,6 +41,7 @@ enum {
 
 typedef struct vv_tree vv_tree;    /* device replica of one VOctree */
 typedef struct vv_slice vv_slice;  /* per-frame slice cache (FrameSlice) */
+typedef struct vv_camera_plan vv_camera_plan;  /* launch plan of one camera stream */
 
 /* Host description of a VOctree: the arrays of voxvid.octree.VOctree
  * (octree.py:84-108).  Pointers are HOST pointers for vv_tree_upload. */
@@ -190,6 +191,40 @@ int vv_render_rays_visits(const vv_tree *tree, int32_t frame, const vv_slice *ca
 int vv_render_camera(const vv_tree *tree, int32_t frame, const vv_slice *cache,
                      const vv_render_opts *opts, const vv_camera *cam, float *rgb,
                      float *alpha, float *depth, void *stream);
+/* vv_render_camera for the pixel rectangle region = {x0, y0, x1, y1}
+ * ([x0, x1) x [y0, y1)) of full-size planes, which may be a peer GPU's
+ * memory mapped with vv_ipc_open (peer != 0: a system-scope fence at kernel
+ * exit).  Pixels outside the rectangle are not touched.  Without a cache,
+ * only the leaf chunks whose cells can project into the rectangle are
+ * decoded: one rank's share of a frame split into regions across GPUs
+ * costs its share of the decode as well as of the walk.
+ * block_order (optional, device int32): the launch order of the region's
+ * camera blocks -- a permutation of 0 .. nbx*nby-1 (block b covers pixels
+ * x0 + (b % nbx) * bw, y0 + (b / nbx) * bh, bw x bh from
+ * vv_camera_block_shape) -- costliest first, so that the expensive blocks
+ * do not form the tail of a short kernel.  Not validated: anything but a
+ * permutation renders some pixels twice and others not at all. */
+int vv_render_camera_region(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                            const vv_render_opts *opts, const vv_camera *cam, const int32_t *region,
+                            const int32_t *block_order, float *rgb, float *alpha, float *depth,
+                            int32_t peer, void *stream);
+/* Camera plans: renders of a camera stream (playback, a fixed view, one
+ * rank's region) through a plan run the camera kernel as persistent warps
+ * that take the frame's warp chunks from a counter in the previous render's
+ * measured cost order (costliest blocks first) and record this render's
+ * costs for the next one.  Scheduling only: any plan renders bitwise the
+ * same pixels as vv_render_camera.  A plan is used from one stream at a
+ * time; it resizes itself when the image or region size changes.
+ * region: {x0, y0, x1, y1} as vv_render_camera_region, or NULL (whole
+ * image). */
+int vv_camera_plan_create(int32_t device, vv_camera_plan **plan);
+int vv_camera_plan_free(vv_camera_plan *plan);
+int vv_render_camera_planned(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                             const vv_render_opts *opts, const vv_camera *cam, const int32_t *region,
+                             vv_camera_plan *plan, float *rgb, float *alpha, float *depth, int32_t peer,
+                             void *stream);
+/* Pixel footprint of one camera-kernel block (block_order units). */
+int vv_camera_block_shape(int32_t *width, int32_t *height);
 /* vv_render_camera plus, per pixel, the leaf samples the ray consumed
  * (int32, device, (H, W)): the reference's per-ray `used` count
  * (shade_forward_kernel, kernels.py:700-738; Trainer._forward, train.py:

@@ -33,6 +33,7 @@ from .octree import (
 )
 from .render import (
     Camera,
+    CameraPlan,
     FrameSlice,
     LayerImages,
     RenderOptions,
@@ -53,7 +54,7 @@ from .temporal import TemporalBases, make_bump_bases
 
 __all__ = [
     "VOctree", "DeviceTree", "load_device", "RaySegment", "VoctError", "BadMagicError", "UnsupportedVersionError", "TruncatedStreamError",
-    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "render", "render_into", "render_frames_into", "render_sequence",
+    "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "CameraPlan", "render", "render_into", "render_frames_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache", "build_frame_caches",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
     "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "ShadowMap", "shadow_pass",

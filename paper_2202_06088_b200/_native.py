@@ -63,6 +63,11 @@ EXPORTED_SYMBOLS = (
     "vv_render_rays_visits",
     "vv_render_camera",
     "vv_render_camera_counts",
+    "vv_render_camera_region",
+    "vv_camera_block_shape",
+    "vv_camera_plan_create",
+    "vv_camera_plan_free",
+    "vv_render_camera_planned",
     "vv_render_camera_tiles",
     "vv_unpack_tiles",
     "vv_render_camera_tiles_direct",
@@ -227,6 +232,17 @@ _SIGNATURES = {
     "vv_render_camera_counts": (
         ctypes.c_int,
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P, _P],
+    ),
+    "vv_render_camera_region": (
+        ctypes.c_int,
+        [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P, _P, _I32, _P],
+    ),
+    "vv_camera_block_shape": (ctypes.c_int, [_P, _P]),
+    "vv_camera_plan_create": (ctypes.c_int, [_I32, ctypes.POINTER(_P)]),
+    "vv_camera_plan_free": (ctypes.c_int, [_P]),
+    "vv_render_camera_planned": (
+        ctypes.c_int,
+        [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P, _P, _I32, _P],
     ),
     "vv_render_camera_tiles": (
         ctypes.c_int,

@@ -45,6 +45,15 @@ struct vv_tree {
     int32_t *d_parent, *d_last, *d_upper;
     int64_t n_last, n_upper;
     bool mask_ok;
+    // leaf-cell boxes of every kRegionChunk consecutive leaf rows (cell
+    // units at the leaf depth: x0 y0 z0 0 x1 y1 z1 0, inclusive), for
+    // region renders that slice only the chunks their pixels can reach
+    int4 *d_box;
+    int64_t n_box;
+    // walk-order leaf layout (analyze_tree): device row -> reference row and
+    // back (null: identity); the host copy permutes edit uploads
+    int32_t *d_leaf_ref, *d_dev_row;
+    std::vector<int32_t> h_perm;
 };
 
 // Per-frame (or per frame group) node mask: the slice pass's lit bits, the
@@ -91,6 +100,22 @@ struct vv_slice {
     int64_t n_leaves;
     cudaStream_t stream;  // stream-ordered allocation: freed on this stream
     std::shared_ptr<NodeMask> nmask;  // dark subtrees cut (image renders), or null
+};
+
+// Launch plan of one camera stream (vv_camera_plan_create): the camera
+// kernel runs persistent warps that take the frame's warp chunks from a
+// counter in the order of the previous render's measured block costs
+// (costliest first), and records this render's costs for the next.  Used
+// from one stream at a time (like a library handle); the mutex guards the
+// host state against concurrent calls.
+struct vv_camera_plan {
+    int device = 0;
+    int blocks_x = 0, n_blocks = 0;  // the grid the buffers are sized for
+    int32_t *order = nullptr;        // (n_blocks) launch order
+    uint32_t *cost = nullptr;        // (n_blocks) costs of the last render
+    int *counter = nullptr;
+    bool valid = false;              // order holds a permutation for this grid
+    std::mutex mu;
 };
 
 #define VV_CUDA(call)                                                                          \
@@ -265,51 +290,126 @@ int build_mask(const vv_tree *t, const NodeMask &m, cudaStream_t st) {
     return launch_node_mask(p, st);
 }
 
-// Node tables of the mask kernels from the host copy of the child table:
-// levels by breadth-first search from the root; mask_ok only for a proper
-// tree (no node reached twice, leaf rows exactly at the last level).
-int setup_mask_tables(vv_tree *t, const int32_t *child) {
-    t->mask_ok = false;
-    const int64_t ni = t->n_internal;
+// Host analysis of the child table at upload (tree_alloc_common).  For a
+// proper tree (no node reached twice, leaf rows only below last-level
+// nodes) it yields
+//   * the node-mask tables: parent of every node, last-level and upper nodes;
+//   * the walk-order leaf layout: leaves numbered in BFS order of their
+//     last-level parents and child bit (b = x | y<<1 | z<<2), i.e. Morton
+//     order -- the device stores payload planes, slice records and lit bytes
+//     in this order, rewrites the table's leaf entries to it, and maps rows
+//     back to reference ids wherever one leaves the device (leaf_ref);
+//   * per kRegionChunk consecutive device rows, the box of their leaf cells
+//     (compact in walk order: region renders cull chunks by it).
+// Anything else keeps the identity layout and no masks.
+struct TreeLayout {
+    bool tree = false;
+    std::vector<int32_t> parent, last, upper;
+    std::vector<int32_t> perm, iperm;  // device row -> reference row, and back
+    std::vector<int32_t> child;        // the table with leaf entries in device rows
+    std::vector<int4> box;             // (n_box, 2)
+};
+
+static void analyze_tree(int depth, int64_t ni, int64_t nl, const int32_t *child, TreeLayout &out) {
+    out = TreeLayout();
     std::vector<int32_t> parent((size_t)ni, -2), last, upper;
     std::vector<int32_t> cur{0}, next;
+    std::vector<int32_t> cell{0, 0, 0}, ncell;  // cell coordinates of the nodes in cur
     parent[0] = -1;
-    for (int L = 0; L < t->depth && !cur.empty(); ++L) {
-        const bool at_last = L + 1 == t->depth;
+    for (int L = 0; L < depth && !cur.empty(); ++L) {
+        const bool at_last = L + 1 == depth;
+        if (at_last) {
+            last = cur;
+            break;
+        }
         next.clear();
-        for (int32_t n : cur) {
-            (at_last ? last : upper).push_back(n);
-            if (at_last) continue;
+        ncell.clear();
+        for (size_t i = 0; i < cur.size(); ++i) {
+            const int32_t n = cur[i];
+            upper.push_back(n);
             for (int b = 0; b < 8; ++b) {
                 const int32_t c = child[(size_t)n * 8 + b];
                 if (c < 0) continue;
-                if (c >= ni || parent[c] != -2) return VV_OK;  // not a tree: no masks
+                if (c >= ni || parent[c] != -2) return;  // not a tree
                 parent[c] = n;
                 next.push_back(c);
+                ncell.push_back(2 * cell[3 * i] + (b & 1));
+                ncell.push_back(2 * cell[3 * i + 1] + ((b >> 1) & 1));
+                ncell.push_back(2 * cell[3 * i + 2] + ((b >> 2) & 1));
             }
         }
         cur.swap(next);
+        cell.swap(ncell);
     }
+    std::vector<int32_t> iperm((size_t)nl, -1), perm;
+    perm.reserve((size_t)nl);
     for (int32_t n : last)
-        for (int b = 0; b < 8; ++b)
-            if (child[(size_t)n * 8 + b] >= t->n_leaves) return VV_OK;
-    for (auto &v : parent) v = v == -2 ? -1 : v;
-    auto up = [&](int32_t **d, const std::vector<int32_t> &h) -> int {
-        if (h.empty()) return VV_OK;
-        if (cudaMalloc(d, h.size() * 4) != cudaSuccess) {
-            cudaGetLastError();
-            return set_error(VV_E_NOMEM, "node mask table allocation failed");
+        for (int b = 0; b < 8; ++b) {
+            const int32_t r = child[(size_t)n * 8 + b];
+            if (r < 0) continue;
+            if (r >= nl || iperm[r] >= 0) return;  // out of range or a leaf reached twice: not a tree
+            iperm[r] = (int32_t)perm.size();
+            perm.push_back(r);
         }
-        t->bytes += (int64_t)h.size() * 4;
-        if (cudaMemcpy(*d, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-            return set_error(VV_E_CUDA, "node mask table copy failed");
+    for (int64_t r = 0; r < nl; ++r)  // rows no node reaches: after the walked ones
+        if (iperm[r] < 0) {
+            iperm[r] = (int32_t)perm.size();
+            perm.push_back((int32_t)r);
+        }
+    out.child.assign(child, child + (size_t)ni * 8);
+    const int64_t nb = (nl + kRegionChunk - 1) / kRegionChunk;
+    out.box.resize((size_t)2 * nb);
+    for (int64_t k = 0; k < nb; ++k) {
+        out.box[2 * k] = make_int4(INT32_MAX, INT32_MAX, INT32_MAX, 0);
+        out.box[2 * k + 1] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, 0);
+    }
+    for (size_t i = 0; i < last.size(); ++i) {
+        const int32_t n = last[i];
+        for (int b = 0; b < 8; ++b) {
+            int32_t &e = out.child[(size_t)n * 8 + b];
+            if (e < 0) continue;
+            e = iperm[e];
+            const int32_t x = 2 * cell[3 * i] + (b & 1), y = 2 * cell[3 * i + 1] + ((b >> 1) & 1),
+                          z = 2 * cell[3 * i + 2] + ((b >> 2) & 1);
+            int4 &lo = out.box[2 * (e / kRegionChunk)], &hi = out.box[2 * (e / kRegionChunk) + 1];
+            lo.x = std::min(lo.x, x); lo.y = std::min(lo.y, y); lo.z = std::min(lo.z, z);
+            hi.x = std::max(hi.x, x); hi.y = std::max(hi.y, y); hi.z = std::max(hi.z, z);
+        }
+    }
+    for (auto &v : parent) v = v == -2 ? -1 : v;
+    out.parent.swap(parent);
+    out.last.swap(last);
+    out.upper.swap(upper);
+    out.perm.swap(perm);
+    out.iperm.swap(iperm);
+    out.tree = true;
+}
+
+// Device copies of the layout's tables (mask tables, boxes, leaf_ref).
+static int upload_layout(vv_tree *t, const TreeLayout &lay) {
+    auto up = [&](void **d, const void *h, size_t bytes) -> int {
+        if (!bytes) return VV_OK;
+        if (cudaMalloc(d, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(VV_E_NOMEM, "tree layout table allocation failed");
+        }
+        t->bytes += (int64_t)bytes;
+        if (cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+            return set_error(VV_E_CUDA, "tree layout table copy failed");
         return VV_OK;
     };
     int rc;
-    if ((rc = up(&t->d_parent, parent)) || (rc = up(&t->d_last, last)) || (rc = up(&t->d_upper, upper))) return rc;
-    t->n_last = (int64_t)last.size();
-    t->n_upper = (int64_t)upper.size();
-    t->mask_ok = true;
+    if ((rc = up((void **)&t->d_parent, lay.parent.data(), lay.parent.size() * 4)) ||
+        (rc = up((void **)&t->d_last, lay.last.data(), lay.last.size() * 4)) ||
+        (rc = up((void **)&t->d_upper, lay.upper.data(), lay.upper.size() * 4)) ||
+        (rc = up((void **)&t->d_box, lay.box.data(), lay.box.size() * sizeof(int4))) ||
+        (rc = up((void **)&t->d_leaf_ref, lay.perm.data(), lay.perm.size() * 4)) ||
+        (rc = up((void **)&t->d_dev_row, lay.iperm.data(), lay.iperm.size() * 4)))
+        return rc;
+    t->n_last = (int64_t)lay.last.size();
+    t->n_upper = (int64_t)lay.upper.size();
+    t->n_box = (int64_t)lay.box.size() / 2;
+    t->mask_ok = lay.tree && t->n_last > 0;
     return VV_OK;
 }
 
@@ -399,12 +499,84 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     return build_mask(t, *tr.nmask, st);
 }
 
+// Transient slice for a pixel region: only the leaf chunks whose cell boxes
+// can project into the region are sliced (k_chunk_cull -> chunk list ->
+// k_build_slice in list mode); the node mask then treats the other leaves as
+// dark (their lit bytes are zeroed), which only cuts subtrees the region's
+// rays cannot reach.  Trees without chunk boxes slice every chunk.
+int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const vv_camera &cam, int rx0, int ry0,
+                           int rx1, int ry1, SliceView &sv, Transient &tr) {
+    if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr);
+    pool_setup(t->device);
+    const int rec4 = slice_rec4(t->S);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_rec = al((size_t)t->n_leaves * rec4 * sizeof(float4));
+    const size_t bytes = b_rec + al((size_t)t->n_box * 4) + 256;
+    cudaError_t e = cudaMallocAsync(&tr.mem, bytes, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        tr.mem = nullptr;
+        return set_error(VV_E_NOMEM, "transient region slice allocation (%zu bytes) failed", bytes);
+    }
+    tr.st = st;
+    char *m = static_cast<char *>(tr.mem);
+    sv.rec = reinterpret_cast<float4 *>(m);
+    sv.rec4 = rec4;
+    int32_t *list = reinterpret_cast<int32_t *>(m + b_rec);
+    int32_t *count = reinterpret_cast<int32_t *>(m + b_rec + al((size_t)t->n_box * 4));
+    CullParams c;
+    c.box = t->d_box;
+    c.n_box = t->n_box;
+    c.lo0 = t->view.lo0;
+    c.lo1 = t->view.lo1;
+    c.lo2 = t->view.lo2;
+    c.cell = t->view.side / (double)(1ll << t->depth);
+    c.cam = make_cam(cam);
+    c.x0 = rx0 + 0.5 - 1.0;  // pixel centres of the region, one pixel of margin
+    c.y0 = ry0 + 0.5 - 1.0;
+    c.x1 = rx1 - 0.5 + 1.0;
+    c.y1 = ry1 - 0.5 + 1.0;
+    c.list = list;
+    c.count = count;
+    int rc = launch_chunk_cull(c, st);
+    if (rc) return rc;
+    if (mask_wanted(t)) {
+        if ((rc = alloc_mask(t, st, tr.nmask))) return rc;
+        e = cudaMemsetAsync(tr.nmask->lit, 0, (size_t)t->n_leaves, st);
+        if (e != cudaSuccess) return set_error(VV_E_CUDA, "lit memset: %s", cudaGetErrorString(e));
+    }
+    SliceParams p;
+    memset(&p, 0, sizeof(p));
+    p.T = t->view;
+    p.K = make_consts(t->n_max);
+    p.n_frames = 1;
+    p.frame[0] = frame;
+    p.n_leaves = t->n_leaves;
+    p.rec[0] = sv.rec ? const_cast<float4 *>(sv.rec) : nullptr;
+    p.rec4 = rec4;
+    p.skip_dark = !t->has_edits;
+    p.lit = tr.nmask ? tr.nmask->lit : nullptr;
+    p.chunk_list = list;
+    p.n_list = count;
+    set_slice_masks(t, p);
+    if ((rc = launch_slice(t->n_max, p, st))) return rc;
+    return tr.nmask ? build_mask(t, *tr.nmask, st) : VV_OK;
+}
+
 // Long segment queue for mostly dark trees (the cfg3 motion tree).  Measured
 // at cfg3 with node masks: 0.493 vs 0.502 ms per frame (without masks 2.02
 // vs 2.18); VV_LONG_QUEUE=0 / 1 forces the choice (A/B runs).
 bool long_queue(const vv_tree *t, const NodeMask *) {
     if (const char *e = getenv("VV_LONG_QUEUE")) return e[0] == '1';
     return t->dark_frac > 0.5f;
+}
+
+// Persistent warp-chunk queue for the camera kernel (k_render_camera, p.work):
+// VV_CAM_QUEUE=0 / 1 forces it off / on; by default only region renders
+// with a launch order use it.
+bool warp_queue(bool ordered) {
+    if (const char *e = getenv("VV_CAM_QUEUE")) return e[0] == '1';
+    return ordered;
 }
 
 // The child table an image render walks: the frame's node mask when one was
@@ -468,7 +640,28 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     if ((rc = alloc((void **)&t->d_b, ab))) return fail(rc);
     const cudaMemcpyKind kind = host_src ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     cudaError_t e;
-    if ((e = cudaMemcpy(t->d_child, d->node_child, child_b, kind)) != cudaSuccess ||
+    // host analysis of the table: walk-order leaf layout, mask tables, boxes
+    TreeLayout lay;
+    {
+        std::vector<int32_t> hc;
+        const int32_t *hchild = d->node_child;
+        if (!host_src) {
+            hc.resize((size_t)d->n_internal * 8);
+            if ((e = cudaMemcpy(hc.data(), d->node_child, child_b, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return fail(set_error(VV_E_CUDA, "node table copy failed: %s", cudaGetErrorString(e)));
+            hchild = hc.data();
+        }
+        analyze_tree(t->depth, t->n_internal, nl, hchild, lay);
+    }
+    if (lay.tree) {
+        t->h_perm = lay.perm;
+        e = cudaMemcpy(t->d_child, lay.child.data(), child_b, cudaMemcpyHostToDevice);
+    } else {
+        e = cudaMemcpy(t->d_child, d->node_child, child_b, kind);
+    }
+    if (e != cudaSuccess) return fail(set_error(VV_E_CUDA, "tree copy failed: %s", cudaGetErrorString(e)));
+    if ((rc = upload_layout(t, lay))) return fail(rc);
+    if (
         (e = cudaMemcpy(t->d_a, d->basis_a, ab, kind)) != cudaSuccess ||
         (e = cudaMemcpy(t->d_b, d->basis_b, ab, kind)) != cudaSuccess)
         return fail(set_error(VV_E_CUDA, "tree copy failed: %s", cudaGetErrorString(e)));
@@ -480,9 +673,34 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     if (t->has_edits && nl > 0) {
         if ((rc = alloc((void **)&t->d_edit_rgb, (size_t)nl * sizeof(float4)))) return fail(rc);
         if ((rc = alloc((void **)&t->d_edit_t, (size_t)nl * sizeof(int2)))) return fail(rc);
-        if ((e = cudaMemcpy(t->d_edit_rgb, d->edit_rgb, nl * sizeof(float4), kind)) != cudaSuccess ||
-            (e = cudaMemcpy(t->d_edit_t, d->edit_t, nl * sizeof(int2), kind)) != cudaSuccess)
+        if (lay.tree) {  // edit channels in device-row order
+            std::vector<float> er((size_t)nl * 4), hr;
+            std::vector<int32_t> et((size_t)nl * 2), ht;
+            const float *srgb = d->edit_rgb;
+            const int32_t *st_ = d->edit_t;
+            if (!host_src) {
+                hr.resize((size_t)nl * 4);
+                ht.resize((size_t)nl * 2);
+                if ((e = cudaMemcpy(hr.data(), d->edit_rgb, nl * sizeof(float4), cudaMemcpyDeviceToHost)) !=
+                        cudaSuccess ||
+                    (e = cudaMemcpy(ht.data(), d->edit_t, nl * sizeof(int2), cudaMemcpyDeviceToHost)) != cudaSuccess)
+                    return fail(set_error(VV_E_CUDA, "edit copy failed: %s", cudaGetErrorString(e)));
+                srgb = hr.data();
+                st_ = ht.data();
+            }
+            for (int64_t g = 0; g < nl; ++g) {
+                const int64_t r = lay.perm[g];
+                memcpy(&er[4 * g], srgb + 4 * r, 16);
+                memcpy(&et[2 * g], st_ + 2 * r, 8);
+            }
+            if ((e = cudaMemcpy(t->d_edit_rgb, er.data(), nl * sizeof(float4), cudaMemcpyHostToDevice)) !=
+                    cudaSuccess ||
+                (e = cudaMemcpy(t->d_edit_t, et.data(), nl * sizeof(int2), cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(set_error(VV_E_CUDA, "edit copy failed: %s", cudaGetErrorString(e)));
+        } else if ((e = cudaMemcpy(t->d_edit_rgb, d->edit_rgb, nl * sizeof(float4), kind)) != cudaSuccess ||
+                   (e = cudaMemcpy(t->d_edit_t, d->edit_t, nl * sizeof(int2), kind)) != cudaSuccess) {
             return fail(set_error(VV_E_CUDA, "edit copy failed: %s", cudaGetErrorString(e)));
+        }
     }
     // payload rows -> padded planes, chunked through a device staging buffer
     if (nl > 0) {
@@ -506,8 +724,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
                 }
                 src = stage;
             }
-            const int lrc = launch_repack(src, rows, (int)stride, C, K3, c4, hh4, nrows, r0, t->d_sig, t->d_gam,
-                                          t->d_hh, nullptr);
+            const int lrc = launch_repack(src, rows, (int)stride, C, K3, c4, hh4, nrows, r0, t->d_dev_row, t->d_sig,
+                                          t->d_gam, t->d_hh, nullptr);
             if (lrc) {
                 if (stage) cudaFree(stage);
                 return fail(lrc);
@@ -519,19 +737,9 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
         if (stage) cudaFree(stage);
         if (e != cudaSuccess) return fail(set_error(VV_E_CUDA, "repack failed: %s", cudaGetErrorString(e)));
     }
-    {  // node-mask tables need the child table on the host
-        std::vector<int32_t> hc;
-        const int32_t *hchild = d->node_child;
-        if (!host_src) {
-            hc.resize((size_t)d->n_internal * 8);
-            if ((e = cudaMemcpy(hc.data(), d->node_child, child_b, cudaMemcpyDeviceToHost)) != cudaSuccess)
-                return fail(set_error(VV_E_CUDA, "node table copy failed: %s", cudaGetErrorString(e)));
-            hchild = hc.data();
-        }
-        if ((rc = setup_mask_tables(t, hchild))) return fail(rc);
-    }
     TreeView &v = t->view;
     v.child = t->d_child;
+    v.leaf_ref = t->d_leaf_ref;
     v.sig = t->d_sig;
     v.gam = t->d_gam;
     v.hh = t->d_hh;
@@ -613,6 +821,9 @@ int vv_tree_free(vv_tree *t) {
     cudaFree(t->d_parent);
     cudaFree(t->d_last);
     cudaFree(t->d_upper);
+    cudaFree(t->d_box);
+    cudaFree(t->d_leaf_ref);
+    cudaFree(t->d_dev_row);
     delete t;
     return VV_OK;
 }
@@ -759,6 +970,8 @@ int vv_slice_export(const vv_slice *s, double *sigma, float *q, void *stream) {
     const int S3 = 3 * s->tree->S;
     const size_t pitch = (size_t)s->rec4 * sizeof(float4);
     if (s->n_leaves == 0) return VV_OK;
+    if (s->tree->d_dev_row)  // records are in device-row order: gather into reference order
+        return launch_slice_export(s->d_rec, s->rec4, S3, s->n_leaves, s->tree->d_dev_row, sigma, q, st);
     if (sigma)
         VV_CUDA(cudaMemcpy2DAsync(sigma, sizeof(double), reinterpret_cast<const char *>(s->d_rec) + pitch - 8, pitch,
                                   sizeof(double), s->n_leaves, cudaMemcpyDeviceToDevice, st));
@@ -814,8 +1027,11 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
         if (r) return r;
     }
     // plain image accumulators may walk the frame's node mask; counts and
-    // visit lists need the reference's full walk
-    if (!visits && !used && !pops && !shaded) p.T.child = image_child(t, cache ? cache->nmask.get() : tr.nmask.get());
+    // visit lists need the reference's full walk (VV_STATS_MASKED=1: counts
+    // of the masked walk itself -- instrumentation for roofline accounting)
+    const char *sm = getenv("VV_STATS_MASKED");
+    if (!visits && ((!used && !pops && !shaded) || (sm && sm[0] == '1')))
+        p.T.child = image_child(t, cache ? cache->nmask.get() : tr.nmask.get());
     return launch_rays(t->n_max, mode, t->has_edits, wide, visits, p, grid, smem, st);
 }
 
@@ -836,7 +1052,9 @@ int vv_render_rays_visits(const vv_tree *t, int32_t frame, const vv_slice *cache
 
 static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *o,
                               const vv_camera *cam, float *rgb, float *alpha, float *depth, float *packed,
-                              int tile, int shard, int n_shards, int peer, void *stream, int32_t *used = nullptr) {
+                              int tile, int shard, int n_shards, int peer, void *stream, int32_t *used = nullptr,
+                              const int32_t *rect = nullptr, const int32_t *block_order = nullptr,
+                              vv_camera_plan *plan = nullptr) {
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
@@ -880,29 +1098,130 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         grid_blocks = (unsigned)mine * (unsigned)((tile / kTW) * (tile / kTH));
         share = (double)mine / (double)total;
     } else {
-        p.blocks_x = (cam->width + kTW - 1) / kTW;
-        grid_blocks = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
+        p.rx0 = rect ? rect[0] : 0;
+        p.ry0 = rect ? rect[1] : 0;
+        p.rx1 = rect ? rect[2] : cam->width;
+        p.ry1 = rect ? rect[3] : cam->height;
+        if (p.rx0 < 0 || p.ry0 < 0 || p.rx1 > cam->width || p.ry1 > cam->height)
+            return set_error(VV_E_INVALID, "region [%d, %d) x [%d, %d) outside the %dx%d image", p.rx0, p.rx1, p.ry0,
+                             p.ry1, cam->width, cam->height);
+        if (p.rx1 <= p.rx0 || p.ry1 <= p.ry0) return VV_OK;  // empty region
+        p.blocks_x = (p.rx1 - p.rx0 + kTW - 1) / kTW;
+        grid_blocks = (unsigned)p.blocks_x * (unsigned)((p.ry1 - p.ry0 + kTH - 1) / kTH);
+        p.block_order = block_order;
     }
     const bool wide = t->depth > kNarrowDepth;
     const size_t smem = stack_bytes(t->depth, wide);
     cudaStream_t st = (cudaStream_t)stream;
-    Transient tr;
+    Transient tr, tq;
+    std::unique_lock<std::mutex> plan_lock;
+    if (plan) {
+        if (tile) return set_error(VV_E_INVALID, "camera plans render images or regions, not packed tiles");
+        if (plan->device != t->device) return set_error(VV_E_INVALID, "camera plan belongs to another device");
+        plan_lock = std::unique_lock<std::mutex>(plan->mu);
+        if (plan->n_blocks != (int)grid_blocks || plan->blocks_x != p.blocks_x) {  // new grid: new buffers
+            cudaFree(plan->order);
+            plan->order = nullptr;
+            plan->valid = false;
+            const size_t n = grid_blocks;
+            if (cudaMalloc(&plan->order, n * 8 + 256) != cudaSuccess) {
+                cudaGetLastError();
+                plan->order = nullptr;
+                plan->n_blocks = 0;
+                return set_error(VV_E_NOMEM, "camera plan allocation failed");
+            }
+            plan->cost = reinterpret_cast<uint32_t *>(plan->order + n);
+            plan->counter = reinterpret_cast<int *>(plan->cost + n);
+            plan->n_blocks = (int)grid_blocks;
+            plan->blocks_x = p.blocks_x;
+            // zero once; afterwards k_plan_order re-zeroes cost and counter
+            VV_CUDA(cudaMemsetAsync(plan->cost, 0, n * 4 + 256, st));
+        }
+        p.work = plan->counter;
+        p.n_work = (int)grid_blocks * kWarpsPerTile;
+        p.block_order = plan->valid ? plan->order : nullptr;
+        p.block_cost = plan->cost;
+    } else if (!tile && warp_queue(block_order != nullptr)) {
+        // persistent warps over the warp chunks: the chunk counter is zeroed
+        // before the slice pass so the render keeps its PDL overlap
+        pool_setup(t->device);
+        if (cudaMallocAsync(&tq.mem, 256, st) != cudaSuccess) {
+            cudaGetLastError();
+            tq.mem = nullptr;
+            return set_error(VV_E_NOMEM, "work counter allocation failed");
+        }
+        tq.st = st;
+        VV_CUDA(cudaMemsetAsync(tq.mem, 0, sizeof(int), st));
+        p.work = static_cast<int *>(tq.mem);
+        p.n_work = (int)grid_blocks * kWarpsPerTile;
+    }
     const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
-    int mode =
-        cache ? 1 : decode_mode(t, share * cube_footprint(*cam, lo, t->view.side, nullptr), opts.frame_slice);
+    // a region render's slice covers only the chunks its pixels can reach,
+    // so it is decided on the whole frame's footprint
+    int mode = cache ? 1
+                     : decode_mode(t, (rect ? 1.0 : share) * cube_footprint(*cam, lo, t->view.side, nullptr),
+                                   opts.frame_slice);
     if (!cache && mode != 0) {
-        int r = build_transient(t, frame, st, p.S, tr);
+        int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr)
+                     : build_transient(t, frame, st, p.S, tr);
         if (r) return r;
     }
     // sample counts report the reference's full walk: the tree's own table
     const NodeMask *nm = used ? nullptr : (cache ? cache->nmask.get() : tr.nmask.get());
     p.T.child = image_child(t, nm);
-    return launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
+    rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
+    if (rc || !plan) return rc;
+    // the next render of this plan launches in this render's cost order
+    if ((rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st))) return rc;
+    plan->valid = true;
+    return VV_OK;
+}
+
+int vv_camera_plan_create(int32_t device, vv_camera_plan **out) {
+    if (!out) return set_error(VV_E_INVALID, "null argument");
+    vv_camera_plan *p = new vv_camera_plan();
+    p->device = device;
+    *out = p;
+    return VV_OK;
+}
+
+int vv_camera_plan_free(vv_camera_plan *plan) {
+    if (!plan) return VV_OK;
+    DeviceGuard g(plan->device);
+    cudaDeviceSynchronize();  // a render may still read the order
+    cudaFree(plan->order);
+    delete plan;
+    return VV_OK;
+}
+
+int vv_render_camera_planned(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
+                             const vv_camera *cam, const int32_t *region, vv_camera_plan *plan, float *rgb,
+                             float *alpha, float *depth, int32_t peer, void *stream) {
+    if (!plan) return set_error(VV_E_INVALID, "null camera plan");
+    if (!rgb && !alpha && !depth) return set_error(VV_E_INVALID, "null image planes");
+    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, peer ? 1 : 0, stream,
+                              nullptr, region, nullptr, plan);
 }
 
 int vv_render_camera(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
                      const vv_camera *cam, float *rgb, float *alpha, float *depth, void *stream) {
     return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream);
+}
+
+int vv_render_camera_region(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
+                            const vv_camera *cam, const int32_t *region, const int32_t *block_order, float *rgb,
+                            float *alpha, float *depth, int32_t peer, void *stream) {
+    if (!region) return set_error(VV_E_INVALID, "null region");
+    if (!rgb && !alpha && !depth) return set_error(VV_E_INVALID, "null image planes");
+    return render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, peer ? 1 : 0, stream,
+                              nullptr, region, block_order);
+}
+
+int vv_camera_block_shape(int32_t *width, int32_t *height) {
+    if (!width || !height) return set_error(VV_E_INVALID, "null argument");
+    *width = kTW;
+    *height = kTH;
+    return VV_OK;
 }
 
 int vv_render_camera_counts(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
@@ -1299,8 +1618,20 @@ int vv_tree_set_edits(vv_tree *t, const float *edit_rgb, const int32_t *edit_t) 
     // keeps the PDL invariant (launch_pdl, vv_kernels.cuh): no kernel is in
     // flight while tree state changes
     cudaDeviceSynchronize();
-    VV_CUDA(cudaMemcpy(t->d_edit_rgb, edit_rgb, (size_t)nl * sizeof(float4), cudaMemcpyHostToDevice));
-    VV_CUDA(cudaMemcpy(t->d_edit_t, edit_t, (size_t)nl * sizeof(int2), cudaMemcpyHostToDevice));
+    if (!t->h_perm.empty()) {  // device-row order (walk-order leaf layout)
+        std::vector<float> er((size_t)nl * 4);
+        std::vector<int32_t> et((size_t)nl * 2);
+        for (int64_t g = 0; g < nl; ++g) {
+            const int64_t r = t->h_perm[g];
+            memcpy(&er[4 * g], edit_rgb + 4 * r, 16);
+            memcpy(&et[2 * g], edit_t + 2 * r, 8);
+        }
+        VV_CUDA(cudaMemcpy(t->d_edit_rgb, er.data(), (size_t)nl * sizeof(float4), cudaMemcpyHostToDevice));
+        VV_CUDA(cudaMemcpy(t->d_edit_t, et.data(), (size_t)nl * sizeof(int2), cudaMemcpyHostToDevice));
+    } else {
+        VV_CUDA(cudaMemcpy(t->d_edit_rgb, edit_rgb, (size_t)nl * sizeof(float4), cudaMemcpyHostToDevice));
+        VV_CUDA(cudaMemcpy(t->d_edit_t, edit_t, (size_t)nl * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     t->has_edits = true;
     t->view.edit_rgb = t->d_edit_rgb;
     t->view.edit_t = t->d_edit_t;

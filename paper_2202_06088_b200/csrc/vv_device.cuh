@@ -48,6 +48,10 @@ struct Consts {
 };
 
 // Device view of one uploaded tree.
+struct TreeView;
+__device__ __forceinline__ int64_t ref_row(const int32_t *leaf_ref, uint32_t L) {
+    return leaf_ref ? (int64_t)__ldg(leaf_ref + L) : (int64_t)L;
+}
 struct TreeView {
     const int32_t *child;    // (n_internal, 8)
     // w_sigma / w_gamma chunk-major: float4 chunk j (columns 4j..4j+3, zero
@@ -61,6 +65,11 @@ struct TreeView {
     const int2 *edit_t;      // (n_leaves) or null
     const float *basis_a;    // (T, C)
     const float *basis_b;    // (T, C)
+    // Leaf rows on the device are in walk (BFS = Morton) order, not the
+    // reference's row order: leaf_ref maps a device row back to the
+    // reference row id wherever one leaves the device (visit lists, segment
+    // lists, termination leaves); null = identity (tables that are not trees)
+    const int32_t *leaf_ref;
     double lo0, lo1, lo2, side;
     int64_t lstride;         // leaf rows per chunk plane (>= n_leaves)
     int depth, C, c4, hh4, frames, nmax;
@@ -751,7 +760,7 @@ struct Shader {
     }
 
     __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout, double sigma_cached) {
-        if (VISITS) visit[used] = (int64_t)L;
+        if (VISITS) visit[used] = ref_row(T.leaf_ref, L);
         ++used;
         constexpr int Q4 = Basis<NMAX>::Q4;
         // sliced coefficients: from the frame slice record, or decoded now
@@ -976,6 +985,7 @@ struct CountVisitor {
 struct CollectVisitor {
     static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
+    const int32_t *leaf_ref;
     int64_t *leaf_out;
     double *t0_out, *t1_out;
     int64_t count, cap;
@@ -984,7 +994,7 @@ struct CollectVisitor {
     __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
         for (int s = 0; s < n; ++s) {
             if (count < cap) {
-                leaf_out[count] = (int64_t)seg.leaf_at(s);
+                leaf_out[count] = ref_row(leaf_ref, (uint32_t)seg.leaf_at(s));
                 t0_out[count] = seg.t0_at(s);
                 t1_out[count] = seg.t1_at(s);
             }

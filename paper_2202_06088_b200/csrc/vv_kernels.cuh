@@ -99,6 +99,23 @@ struct CamParams {
     int tile, shard, n_shards, tiles_x;
     int peer;                     // image planes live on another GPU: fence at exit
     int blocks_x;                 // tiles per row (image mode)
+    // image mode renders the pixel rectangle [rx0, rx1) x [ry0, ry1) of the
+    // full-size planes (the whole image, or one rank's region)
+    int rx0, ry0, rx1, ry1;
+    // optional launch order of the rectangle's blocks (a permutation of
+    // 0..grid-1, costliest first: the expensive blocks do not form the tail
+    // of a short region kernel)
+    const int32_t *block_order;
+    // persistent warps (work != null, image / region mode): a resident grid
+    // whose warps take the rectangle's warp chunks (32 rays each) one at a
+    // time from the counter *work (zeroed before the launch), in
+    // block_order when given -- SM slots never idle while chunks remain
+    int *work;
+    int n_work;  // warp chunks in the rectangle
+    // optional (persistent mode): per-block walk cost of this render (leaf
+    // samples + 1 per ray, atomically summed per warp) -- a camera plan's
+    // launch order for the next frame (vv_camera_plan)
+    uint32_t *block_cost;
     // optional per-pixel leaf-sample counts (render_kernel's consumed
     // segments, up to and including the early-stop one; image mode): written
     // by the production instantiation itself, so its walk is checked
@@ -145,8 +162,9 @@ __device__ __forceinline__ void block_origin(const CamParams &p, int &x0, int &y
     } else {
         my_tile = 0;
         lx0 = ly0 = 0;
-        x0 = (int)(blockIdx.x % p.blocks_x) * kTW;
-        y0 = (int)(blockIdx.x / p.blocks_x) * kTH;
+        const int b = p.block_order ? __ldg(p.block_order + blockIdx.x) : (int)blockIdx.x;
+        x0 = p.rx0 + (b % p.blocks_x) * kTW;
+        y0 = p.ry0 + (b / p.blocks_x) * kTH;
     }
 }
 
@@ -157,14 +175,14 @@ __device__ __forceinline__ void local_pixel(int rid, int &dx, int &dy) {
     dy = (chunk / (kTW / CW)) * CH + (l / CW);
 }
 
-__device__ __forceinline__ void cam_write(const CamParams &p, int ix, int iy, long long slot, float r, float g,
+__device__ __forceinline__ void cam_write(const CamParams &p, bool inside, long long slot, float r, float g,
                                           float b, float a, float d) {
     if (p.packed) {
         float *o = p.packed + slot * 5;
         o[0] = r; o[1] = g; o[2] = b; o[3] = a; o[4] = d;
         return;
     }
-    if (ix >= p.cam.width || iy >= p.cam.height) return;
+    if (!inside) return;
     if (p.rgb) {
         p.rgb[3 * slot + 0] = r;
         p.rgb[3 * slot + 1] = g;
@@ -178,6 +196,31 @@ __device__ __forceinline__ void cam_write(const CamParams &p, int ix, int iy, lo
 // (each warp an 8x4-pixel chunk), so the block's warps stay on neighbouring
 // pixels (L1 reuse of node rows and slice rows).  Refill-on-finish
 // (persistent) variants were measured slower: see DESIGN.md.
+constexpr int kWarpsPerTile = kTileRays / 32;
+
+// one pixel of the camera kernel (image / region mode) after the slice wait
+template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG>
+__device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &F, unsigned char *smem, int ix,
+                                            int iy) {
+    const long long slot = (long long)iy * p.cam.width + ix;
+    const bool inside = ix < p.rx1 && iy < p.ry1;
+    float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
+    int cost = 0;
+    if (inside) {
+        double dx, dy, dz;
+        camera_ray(p.cam, ix, iy, dx, dy, dz);
+        Ray ray;
+        const bool hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
+        Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+        if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem, sh);
+        finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b, a, d);
+        if (p.used) p.used[slot] = sh.used;
+        cost = sh.used + 1;
+    }
+    cam_write(p, inside, slot, r, g, b, a, d);
+    return cost;
+}
+
 template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(const __grid_constant__ CamParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -187,6 +230,30 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
     // 0.730 ms at cfg2)
     load_rows(p.T, p.frame, sA, sB);
     __syncthreads();
+    if (p.work) {  // persistent warps over the rectangle's warp chunks
+        const FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight, nz_chunks(sA, p.T.C), nz_chunks(sB, p.T.C)};
+        pdl_trigger();
+        pdl_wait();
+        const int lane = threadIdx.x & 31;
+        while (true) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.work, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx >= p.n_work) break;
+            const int tb = p.block_order ? __ldg(p.block_order + idx / kWarpsPerTile) : idx / kWarpsPerTile;
+            int dx_, dy_;
+            local_pixel((idx % kWarpsPerTile) * 32 + lane, dx_, dy_);
+            const int cost = camera_pixel<NMAX, CACHED, EDITS, Entry, SEG>(
+                p, F, smem_raw, p.rx0 + (tb % p.blocks_x) * kTW + dx_, p.ry0 + (tb / p.blocks_x) * kTH + dy_);
+            __syncwarp();
+            if (p.block_cost) {
+                const unsigned sum = __reduce_add_sync(0xffffffffu, (unsigned)cost);
+                if (lane == 0) atomicAdd(p.block_cost + tb, sum);
+            }
+        }
+        if (p.peer) __threadfence_system();
+        return;
+    }
     int x0, y0, lx0, ly0;
     long long my_tile;
     block_origin(p, x0, y0, my_tile, lx0, ly0);
@@ -199,7 +266,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         const long long slot = p.packed ? my_tile * p.tile * p.tile + (long long)(ly0 + dy_) * p.tile + (lx0 + dx_)
                                         : (long long)iy * p.cam.width + ix;
         float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
-        const bool inside = ix < p.cam.width && iy < p.cam.height;
+        const bool inside = p.tile ? (ix < p.cam.width && iy < p.cam.height) : (ix < p.rx1 && iy < p.ry1);
         double dx = 0.0, dy = 0.0, dz = 1.0;
         Ray ray;
         bool hit = false;
@@ -216,7 +283,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
                      a, d);
             if (p.used) p.used[slot] = sh.used;
         }
-        cam_write(p, ix, iy, slot, r, g, b, a, d);
+        cam_write(p, inside, slot, r, g, b, a, d);
     }
     // peer stores: make them visible system-wide before the kernel retires
     // (the caller's stream-ordered barrier then publishes the frame)
@@ -432,6 +499,10 @@ struct SliceParams {
     uint32_t mS, mG;            // w_sigma / w_gamma chunks the frames need (union of nz_chunks)
     int skip_dark;              // render-internal slice: dark chunks get sigma only (no colour)
     uint8_t *lit;               // optional (n_leaves): bit f set iff frame f's sigma > 0 (node masks)
+    // optional: slice only the chunks listed (region renders; written by
+    // k_chunk_cull, the previous kernel -- read after griddepcontrol.wait)
+    const int32_t *chunk_list;
+    const int32_t *n_list;
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -521,14 +592,18 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     const int64_t n_warps = (int64_t)gridDim.x * nw, wid = (int64_t)blockIdx.x * nw + warp;
 #if VV_SLICE_RUNS
     // contiguous runs of chunks per warp (the chunk before is a spatial neighbour)
-    const int64_t c_begin = n_chunks * wid / n_warps, c_end = n_chunks * (wid + 1) / n_warps, c_step = 1;
+    int64_t c_begin = n_chunks * wid / n_warps, c_end = n_chunks * (wid + 1) / n_warps, c_step = 1;
 #else
     // chunks strided over the warps: the chunks in flight at any time are
     // neighbours in HBM
-    const int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
+    int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
 #endif
+    // list mode: positions in the chunk list instead of chunk ids
+    const bool listed = p.chunk_list != nullptr;
+    auto chunk_at = [&](int64_t i) -> int64_t { return listed ? (int64_t)p.chunk_list[i] : i; };
     // stage: [needed w_sigma chunks][kChunk leaves] | [needed w_gamma chunks][kChunk] | [leaves][hh4]
     auto rows_of = [&](int64_t c) { return (int)min((int64_t)kChunk, p.n_leaves - c * kChunk); };
+    (void)rows_of;
     auto issue_colour = [&](int64_t c, int stg, uint64_t *b, bool arrive) {
         const int64_t base = c * kChunk;
         const int rows = rows_of(c);
@@ -555,15 +630,29 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // written, and while chunks stay dark the colour rows are not fetched
     // (render-internal slices of trees without edits: p.skip_dark)
     uint32_t colour_in = 3u;  // bit s: stage s was issued with its colour rows
-    if (lane == 0) {  // payload reads only: may overlap the previous kernel
+    if (lane == 0 && !listed) {  // payload reads only: may overlap the previous kernel
         if (c_begin < c_end) issue(c_begin, 0, true);
         if (c_begin + c_step < c_end) issue(c_begin + c_step, 1, true);
     }
     pdl_trigger();
     pdl_wait();  // no record is written before the previous kernel is complete
+    if (listed) {  // the list is the previous kernel's output
+        const int64_t nl = (int64_t)*(volatile const int32_t *)p.n_list;
+#if VV_SLICE_RUNS
+        c_begin = nl * wid / n_warps;
+        c_end = nl * (wid + 1) / n_warps;
+#else
+        c_end = nl;
+#endif
+        if (lane == 0) {
+            if (c_begin < c_end) issue(chunk_at(c_begin), 0, true);
+            if (c_begin + c_step < c_end) issue(chunk_at(c_begin + c_step), 1, true);
+        }
+    }
     uint32_t late_par = 0;  // phase parity of bar[2], bar[3]
     int k = 0;
-    for (int64_t c = c_begin; c < c_end; c += c_step, ++k) {
+    for (int64_t ci = c_begin; ci < c_end; ci += c_step, ++k) {
+        const int64_t c = chunk_at(ci);
         const int stg = k & 1;
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kChunk;
@@ -684,9 +773,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         // stage consumed: refill it with the chunk two ahead, predicting its
         // colour rows are needed iff this chunk's were
         colour_in = (colour_in & ~(1u << stg)) | ((uint32_t)bright << stg);
-        if (lane == 0 && c + 2 * c_step < c_end) {
+        if (lane == 0 && ci + 2 * c_step < c_end) {
             fence_proxy_async();
-            issue(c + 2 * c_step, stg, bright);
+            issue(chunk_at(ci + 2 * c_step), stg, bright);
         }
     }
 }
@@ -713,7 +802,7 @@ __global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ Seg
                                p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
     if (COLLECT) {
         const int64_t b = p.ray_start[r];
-        CollectVisitor v{p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
+        CollectVisitor v{p.T.leaf_ref, p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
         if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, v);
     } else {
         CountVisitor v;
@@ -761,7 +850,7 @@ struct TerminateVisitor {
             acc = xadd(acc, xmul(trans, a));
             trans = xmul(trans, xsub(1.0, a));
             if (acc >= thr) {
-                hit = (int64_t)L;
+                hit = ref_row(T.leaf_ref, L);
                 return true;
             }
         }
@@ -895,6 +984,22 @@ struct MaskParams {
     int32_t *mask;              // (n_internal, 8) out
 };
 int launch_node_mask(const MaskParams &p, cudaStream_t st);
+// leaf rows per box of the chunk culling (= the single-frame slice chunk)
+constexpr int kRegionChunk = kSliceChunk;
+// chunks whose leaf-cell box can project into a pixel rectangle
+// (vv_launch_mask.cu): the chunk list of a region render's slice pass
+struct CullParams {
+    const int4 *box;            // (n_box, 2) inclusive leaf-cell boxes
+    int64_t n_box;
+    double lo0, lo1, lo2, cell; // tree corner and leaf cell size (world)
+    CamView cam;
+    double x0, y0, x1, y1;      // pixel-centre extent of the region, margin included
+    int32_t *list, *count;
+};
+int launch_chunk_cull(const CullParams &p, cudaStream_t st);
+// camera plan (vv_launch_mask.cu): launch order of n blocks, costliest first
+// (counting sort on log-scale cost buckets)
+int launch_plan_order(uint32_t *cost, int n, int32_t *order, int *counter, cudaStream_t st);
 int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_shadow_blur(const float *alpha, int res, const double *weights, int radius, double *tmp, double *out,
@@ -913,7 +1018,10 @@ struct LightView {  // vv_light (include/voxvid_b200.h)
 int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha, const float *depth, double bg0,
                        double bg1, double bg2, const LightView *lights, int n_lights, float *image, cudaStream_t st);
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int c4, int hh4, int64_t lstride,
-                  int64_t r0, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st);
+                  int64_t r0, const int32_t *dst_row, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st);
+// slice records (device rows) -> sigma (n) f64 / q (n, 3S) f32 in reference row order
+int launch_slice_export(const float4 *rec, int rec4, int s3, int64_t n, const int32_t *dev_row, double *sigma,
+                        float *q, cudaStream_t st);
 int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,
                   float *rgb, float *alpha, float *depth, cudaStream_t st);
 

@@ -15,7 +15,9 @@ static int go(const CamParams &p, unsigned max_blocks, size_t smem, cudaStream_t
     auto kern = k_render_camera<NM, CACHED, EDITS, Entry, SEG>;
     int r = prep_smem(kern, smem);
     if (r) return r;
-    launch_pdl(kern, dim3(max_blocks), dim3(kTileRays), smem, st, p);
+    // persistent warps: one resident grid pulls the warp chunks
+    const unsigned grid = p.work ? persistent_grid(kern, kTileRays, smem, max_blocks) : max_blocks;
+    launch_pdl(kern, dim3(grid), dim3(kTileRays), smem, st, p);
     return check_launch("render_camera");
 }
 

@@ -73,3 +73,131 @@ int launch_node_mask(const MaskParams &p, cudaStream_t st) {
 }
 
 }  // namespace vvk
+
+// ------------------------------------------------------------ chunk culling
+// Region renders (vv_render_camera_region): a ray through pixel centre (u, v)
+// can reach a leaf only if (u, v) lies in the projection of the leaf's cell,
+// hence in the screen rectangle bounding the projected corners of its
+// chunk's cell box.  A chunk is listed when that rectangle (one pixel of
+// margin for rounding) meets the region, or when a box corner is not in
+// front of the eye (then every pixel may reach it).  Unlisted chunks'
+// slice records are never read by the region's rays.
+namespace vvk {
+
+__global__ void __launch_bounds__(256) k_chunk_cull(const __grid_constant__ CullParams p) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const CamView &c = p.cam;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < p.n_box; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        bool keep = false;
+        if (i < p.n_box) {
+            const int4 lo = __ldg(p.box + 2 * i), hi = __ldg(p.box + 2 * i + 1);
+            if (lo.x <= hi.x) {
+                double u0 = 1e300, u1 = -1e300, v0 = 1e300, v1 = -1e300;
+                bool front = true;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double px = p.lo0 + p.cell * (double)((k & 1) ? hi.x + 1 : lo.x);
+                    const double py = p.lo1 + p.cell * (double)((k & 2) ? hi.y + 1 : lo.y);
+                    const double pz = p.lo2 + p.cell * (double)((k & 4) ? hi.z + 1 : lo.z);
+                    const double dx = px - c.ox, dy = py - c.oy, dz = pz - c.oz;
+                    // camera frame: R^T d (R's columns are the camera axes)
+                    const double cx = c.r00 * dx + c.r10 * dy + c.r20 * dz;
+                    const double cy = c.r01 * dx + c.r11 * dy + c.r21 * dz;
+                    const double cz = c.r02 * dx + c.r12 * dy + c.r22 * dz;
+                    front &= cz > 1e-9;
+                    const double iz = 1.0 / cz;
+                    const double u = c.fx * cx * iz + c.cx, v = c.fy * cy * iz + c.cy;
+                    u0 = fmin(u0, u);
+                    u1 = fmax(u1, u);
+                    v0 = fmin(v0, v);
+                    v1 = fmax(v1, v);
+                }
+                keep = !front || (u1 >= p.x0 && u0 <= p.x1 && v1 >= p.y0 && v0 <= p.y1);
+            }
+        }
+        // warp-aggregated append: one atomic per warp
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const int lane = threadIdx.x & 31;
+        int slot = 0;
+        if (lane == 0 && m) slot = atomicAdd(p.count, __popc(m));
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (keep) p.list[slot + __popc(m & ((1u << lane) - 1u))] = (int32_t)i;
+    }
+}
+
+int launch_chunk_cull(const CullParams &p, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(p.count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return set_error(VV_E_CUDA, "chunk cull memset: %s", cudaGetErrorString(e));
+    if (p.n_box == 0) return VV_OK;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.n_box + 255) / 256, 148 * 8));
+    k_chunk_cull<<<blocks, 256, 0, st>>>(p);
+    return check_launch("chunk_cull");
+}
+
+}  // namespace vvk
+
+// ------------------------------------------------------------ camera plans
+// Launch order for the next render of a camera (vv_camera_plan): the blocks
+// sorted by the walk cost this render measured, costliest first -- a
+// counting sort on 128 log-scale buckets (9% apart; order within a bucket
+// is arbitrary).  One CTA: the grids are at most tens of thousands of
+// blocks.  The order only schedules work; any permutation renders the same
+// pixels.
+namespace vvk {
+
+constexpr int kPlanBuckets = 128;
+
+__device__ __forceinline__ int plan_bucket(uint32_t c) {
+    return min(kPlanBuckets - 1, (int)(8.0f * __log2f((float)c + 1.0f)));
+}
+
+// Launched with PDL right after the render: waits for its costs, lets the
+// next frame's kernels start early, and leaves the cost array and the chunk
+// counter zeroed for the next render (no memsets on the frame path).
+__global__ void __launch_bounds__(1024) k_plan_order(uint32_t *cost, int n, int32_t *order, int *counter) {
+    __shared__ int hist[kPlanBuckets], off[kPlanBuckets];
+    pdl_trigger();
+    pdl_wait();
+    for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    // warp-aggregated: the lanes sharing a bucket add once (most blocks fall
+    // into a few buckets; per-lane shared atomics serialise on them)
+    const int lane = threadIdx.x & 31;
+    const int n_pad = (n + 31) & ~31;
+    for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+        const int b = i < n ? plan_bucket(cost[i]) : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, b);
+        if (b >= 0 && lane == __ffs(same) - 1) atomicAdd(&hist[b], __popc(same));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int b = kPlanBuckets - 1; b >= 0; --b) {  // costliest bucket first
+            off[b] = s;
+            s += hist[b];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+        const int b = i < n ? plan_bucket(cost[i]) : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(same) - 1;
+        int base = 0;
+        if (b >= 0 && lane == leader) base = atomicAdd(&off[b], __popc(same));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (b >= 0) {
+            cost[i] = 0u;
+            order[base + __popc(same & ((1u << lane) - 1u))] = i;
+        }
+    }
+    if (threadIdx.x == 0) *counter = 0;
+}
+
+int launch_plan_order(uint32_t *cost, int n, int32_t *order, int *counter, cudaStream_t st) {
+    if (n <= 0) return VV_OK;
+    launch_pdl(k_plan_order, dim3(1), dim3(1024), 0, st, cost, n, order, counter);
+    return check_launch("plan_order");
+}
+
+}  // namespace vvk

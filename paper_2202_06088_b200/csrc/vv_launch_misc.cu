@@ -30,8 +30,10 @@ __global__ void k_unpack_tiles(const float *__restrict__ packed, int width, int 
 // r0 .. r0 + rows - 1 -> chunk-major w_sigma / w_gamma planes (float4 chunk
 // j of row g at [j * lstride + g], zero padded past C) and the row-major
 // w_hh plane (hh4 float4 per row, zero padded past K3)
+// (dst_row: reference row -> device row, walk order; null = identity)
 __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int C, int K3, int c4, int hh4,
-                         int64_t lstride, int64_t r0, float4 *sig, float4 *gam, float4 *hh) {
+                         int64_t lstride, int64_t r0, const int32_t *__restrict__ dst_row, float4 *sig, float4 *gam,
+                         float4 *hh) {
     const int64_t planar = 2 * (int64_t)c4 * rows, total = planar + rows * hh4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -43,14 +45,16 @@ __global__ void k_repack(const float *__restrict__ src, int64_t rows, int P, int
             const float *s = src + r * P + (pj < c4 ? 0 : C);
 #pragma unroll
             for (int e = 0; e < 4; ++e) v[e] = 4 * j + e < C ? s[4 * j + e] : 0.0f;
-            (pj < c4 ? sig : gam)[(int64_t)j * lstride + r0 + r] = make_float4(v[0], v[1], v[2], v[3]);
+            const int64_t g = dst_row ? (int64_t)dst_row[r0 + r] : r0 + r;
+            (pj < c4 ? sig : gam)[(int64_t)j * lstride + g] = make_float4(v[0], v[1], v[2], v[3]);
         } else {
             const int64_t k = i - planar, r = k / hh4;
             const int q = (int)(k % hh4);
             const float *s = src + r * P + 2 * C;
 #pragma unroll
             for (int e = 0; e < 4; ++e) v[e] = 4 * q + e < K3 ? s[4 * q + e] : 0.0f;
-            hh[(r0 + r) * hh4 + q] = make_float4(v[0], v[1], v[2], v[3]);
+            const int64_t g = dst_row ? (int64_t)dst_row[r0 + r] : r0 + r;
+            hh[g * hh4 + q] = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
 }
@@ -146,9 +150,30 @@ int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem,
 }
 
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int c4, int hh4, int64_t lstride,
-                  int64_t r0, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st) {
-    k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, c4, hh4, lstride, r0, sig, gam, hh);
+                  int64_t r0, const int32_t *dst_row, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st) {
+    k_repack<<<1184, 256, 0, st>>>(src, rows, P, C, K3, c4, hh4, lstride, r0, dst_row, sig, gam, hh);
     return check_launch("repack");
+}
+
+// FrameSlice export in the reference's row order (build_frame_cache's
+// sigma / q arrays, render.py:170-179): record of device row dev_row[r]
+__global__ void k_slice_export(const float4 *__restrict__ rec, int rec4, int s3, int64_t n,
+                               const int32_t *__restrict__ dev_row, double *sigma, float *q) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = dev_row ? (int64_t)dev_row[r] : r;
+        const float *src = reinterpret_cast<const float *>(rec + g * rec4);
+        if (sigma) sigma[r] = *reinterpret_cast<const double *>(src + 4 * rec4 - 2);
+        if (q)
+            for (int i = 0; i < s3; ++i) q[r * s3 + i] = src[i];
+    }
+}
+
+int launch_slice_export(const float4 *rec, int rec4, int s3, int64_t n, const int32_t *dev_row, double *sigma,
+                        float *q, cudaStream_t st) {
+    if (n == 0) return VV_OK;
+    k_slice_export<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(rec, rec4, s3, n, dev_row,
+                                                                                          sigma, q);
+    return check_launch("slice_export");
 }
 
 int launch_unpack(const float *packed, int width, int height, int tile, int n_shards, int tiles_x, int tiles_total,

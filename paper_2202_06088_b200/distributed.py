@@ -17,6 +17,15 @@ the output rank's planes over NVLink/NVSwitch -- no slab, no all-gather,
 no unpack kernel.  One stream-ordered barrier per frame (a one-element
 NCCL all-reduce, queued after the kernel on every rank) publishes it.
 
+``mode="regions"`` splits the frame into contiguous row bands instead,
+balanced by each row's measured walk cost (``row_costs``: the leaf samples
+of a counting render; ``band_plan``): a rank renders its band with
+vv_render_camera_region straight into the output rank's planes, and --
+the point of contiguous regions -- slices only the leaf chunks whose cells
+can project into its band (k_chunk_cull), so the per-frame decode is
+sharded across the ranks along with the walk.  Interleaved tiles make
+every rank decode the whole tree.
+
 The host-side layout helpers here are also restated in numpy
 (``unpack_tiles_host``) so the CPU test-suite can check the protocol with
 the gloo backend and world_size 2 without a GPU.
@@ -31,7 +40,95 @@ import numpy as np
 from . import _native
 
 __all__ = ["tile_grid", "tiles_of", "slab_tiles", "unpack_tiles_host", "pack_tiles_host", "tile_mask_host",
-           "TileRenderer"]
+           "band_plan", "pixel_costs", "row_costs", "block_shape", "block_order", "render_region", "TileRenderer"]
+
+BAND_ALIGN = 8  # band edges on camera-block rows (vv_kernels.cuh kTH)
+
+
+def band_plan(costs, n: int, align: int = BAND_ALIGN) -> list:
+    """Split rows into n contiguous bands of near-equal total cost.
+
+    ``costs``: per-row cost (len = image height).  Edges sit on multiples of
+    ``align`` (whole camera blocks) except the last; returns n + 1 edges
+    [0, e1, ..., H] (a band may be empty when rows are scarce)."""
+    costs = np.asarray(costs, dtype=np.float64)
+    h = len(costs)
+    cum = np.concatenate([[0.0], np.cumsum(costs)])
+    edges = [0]
+    for k in range(1, n):
+        target = cum[-1] * k / n
+        r = int(np.searchsorted(cum, target))
+        r = int(round(r / align)) * align
+        edges.append(min(max(r, edges[-1]), h))
+    edges.append(h)
+    return edges
+
+
+def pixel_costs(tree, cam, frame: int = 0, opts=None, device=None, miss_cost: float = 1.0):
+    """(H, W) float64 CUDA tensor: each pixel's walk cost -- the leaf samples
+    its ray consumes (one counting render, vv_render_camera_counts) plus
+    ``miss_cost`` for ray generation and setup (a ray that misses costs
+    about as much as one sample).  Deterministic: every rank computes the
+    same plan from it."""
+    import torch
+
+    from .device import torch_device
+    from .render import RenderOptions, render_into
+
+    dev = torch_device(device)
+    h, w = int(cam.height), int(cam.width)
+    used = torch.empty((h, w), dtype=torch.int32, device=dev)
+    alpha = torch.empty((h, w), dtype=torch.float32, device=dev)
+    render_into(tree, cam, frame, None, alpha, None, opts or RenderOptions(), sample_count=used)
+    return used.to(torch.float64) + miss_cost
+
+
+def row_costs(tree, cam, frame: int = 0, opts=None, device=None, miss_cost: float = 1.0):
+    """Per-row sums of ``pixel_costs`` (numpy)."""
+    return pixel_costs(tree, cam, frame, opts, device, miss_cost).sum(dim=1).cpu().numpy()
+
+
+def block_shape():
+    """Pixel footprint (width, height) of one camera-kernel block."""
+    w, h = ctypes.c_int32(), ctypes.c_int32()
+    _native.check(_native.lib().vv_camera_block_shape(ctypes.byref(w), ctypes.byref(h)))
+    return int(w.value), int(h.value)
+
+
+def block_order(costs, rect):
+    """Launch order of the camera blocks of ``rect`` = (x0, y0, x1, y1),
+    costliest first (int32 CUDA tensor for vv_render_camera_region), from
+    per-pixel ``costs`` (H, W tensor): the expensive blocks start first and
+    the cheap ones fill the tail of the kernel."""
+    import torch
+
+    x0, y0, x1, y1 = (int(v) for v in rect)
+    bw, bh = block_shape()
+    nbx, nby = -(-(x1 - x0) // bw), -(-(y1 - y0) // bh)
+    sub = torch.zeros((nby * bh, nbx * bw), dtype=torch.float64, device=costs.device)
+    sub[: y1 - y0, : x1 - x0] = costs[y0:y1, x0:x1]
+    per = sub.reshape(nby, bh, nbx, bw).sum(dim=(1, 3)).reshape(-1)
+    return torch.argsort(per, descending=True, stable=True).to(torch.int32).contiguous()
+
+
+def render_region(tree, cam, frame, rect, rgb, alpha, depth, opts=None, cache=None, *, peer: bool = False,
+                  device=None, order=None):
+    """Render the pixel rectangle rect = (x0, y0, x1, y1) of ``cam`` into
+    full-size planes (device pointers or tensors; may be a peer's IPC
+    mapping), its blocks launched in ``order`` (block_order) if given.
+    Async on the device's current stream."""
+    from .device import replica, stream_ptr, torch_device
+    from .render import RenderOptions, _check_cache
+
+    dev = torch_device(device)
+    opts = opts or RenderOptions()
+    rep = replica(tree, dev)
+    ch = _check_cache(cache, int(frame), rep)
+    ptr = (lambda x: x if isinstance(x, int) or x is None else x.data_ptr())
+    r = (ctypes.c_int32 * 4)(*[int(v) for v in rect])
+    _native.check(_native.lib().vv_render_camera_region(
+        rep.handle, int(frame), ch, ctypes.byref(opts.c_struct()), ctypes.byref(cam.desc()), r, ptr(order), ptr(rgb),
+        ptr(alpha), ptr(depth), int(bool(peer)), stream_ptr(dev)))
 
 
 def tile_grid(width: int, height: int, tile: int):
@@ -119,18 +216,37 @@ class TileRenderer:
 
         if tile % 16:
             raise ValueError("tile must be a multiple of 16")
-        if mode not in ("gather", "p2p"):
-            raise ValueError(f"mode must be 'gather' or 'p2p', not {mode!r}")
+        if mode not in ("gather", "p2p", "regions"):
+            raise ValueError(f"mode must be 'gather', 'p2p' or 'regions', not {mode!r}")
         self.width, self.height, self.tile = int(width), int(height), int(tile)
         self.rank, self.world, self.group = int(rank), int(world), group
         self.mode, self.out_rank = mode, int(out_rank)
         self.device = torch_device(device)
         self.per = slab_tiles(world, width, height, tile)
+        self.bands = None
         if mode == "gather":
             self.slab = torch.zeros((self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
             self.all = torch.empty((world, self.per, tile * tile, 5), dtype=torch.float32, device=self.device)
         else:
             self._init_p2p(torch)
+
+    # ------------------------------------------------------------ regions mode
+    def plan(self, tree, cam, frame: int = 0, opts=None, costs=None):
+        """Row bands for mode="regions", balanced on ``costs`` (per-pixel
+        (H, W) CUDA tensor; default: the measured pixel_costs of ``frame``),
+        and this rank's block launch order.  Call with the same arguments on
+        every rank (the plan is deterministic)."""
+        if costs is None:
+            costs = pixel_costs(tree, cam, frame, opts, self.device)
+        from .render import CameraPlan
+
+        self.bands = band_plan(costs.sum(dim=1).cpu().numpy(), self.world)
+        self.cam_plan = CameraPlan(self.device)  # launch order learned from this rank's own frames
+        return self.bands
+
+    def region(self, rank=None):
+        r = self.rank if rank is None else rank
+        return (0, self.bands[r], self.width, self.bands[r + 1])
 
     # ------------------------------------------------------------ p2p mode
     def _init_p2p(self, torch):
@@ -194,8 +310,8 @@ class TileRenderer:
         from .device import replica, stream_ptr
         from .render import RenderOptions, _check_cache
 
-        if self.mode != "p2p":
-            raise RuntimeError("render_frame needs mode='p2p' (gather mode: render_slab/gather/unpack)")
+        if self.mode == "gather":
+            raise RuntimeError("render_frame needs mode='p2p' or 'regions' (gather mode: render_slab/gather/unpack)")
         if (int(cam.width), int(cam.height)) != (self.width, self.height):
             raise ValueError(f"camera is {cam.width}x{cam.height}, renderer {self.width}x{self.height}")
         opts = opts or RenderOptions()
@@ -206,16 +322,24 @@ class TileRenderer:
         slot = self._slot
         self._slot ^= 1
         rgb, alpha, depth = self._slot_ptrs(slot)
-        _native.check(_native.lib().vv_render_camera_tiles_direct(
-            rep.handle, int(frame), ch, ctypes.byref(oc), ctypes.byref(cd), self.tile, self.rank, self.world,
-            rgb, alpha, depth, int(self.rank != self.out_rank), stream_ptr(self.device)))
+        if self.mode == "regions":
+            if self.bands is None:
+                self.plan(tree, cam, frame, opts)
+            r = (ctypes.c_int32 * 4)(*self.region())
+            _native.check(_native.lib().vv_render_camera_planned(
+                rep.handle, int(frame), ch, ctypes.byref(oc), ctypes.byref(cd), r, self.cam_plan._handle, rgb, alpha,
+                depth, int(self.rank != self.out_rank), stream_ptr(self.device)))
+        else:
+            _native.check(_native.lib().vv_render_camera_tiles_direct(
+                rep.handle, int(frame), ch, ctypes.byref(oc), ctypes.byref(cd), self.tile, self.rank, self.world,
+                rgb, alpha, depth, int(self.rank != self.out_rank), stream_ptr(self.device)))
         self.barrier()
         return self._views(slot) if self.rank == self.out_rank else None
 
     def close(self):
         """Unmap / free the IPC planes (p2p mode).  Call on every rank once
         no rank will render into them again."""
-        if self.mode != "p2p":
+        if self.mode == "gather":
             return
         import torch
 

@@ -32,6 +32,7 @@ __all__ = [
     "LayerImages",
     "RenderOptions",
     "FrameSlice",
+    "CameraPlan",
     "render",
     "render_into",
     "render_frames_into",
@@ -227,6 +228,50 @@ class FrameSlice:
             except Exception:
                 pass
             self._handle = None
+
+
+class CameraPlan:
+    """Launch plan of one camera stream (vv_camera_plan).
+
+    Renders through a plan run the camera kernel as persistent warps taking
+    the frame's warp chunks in the previous render's measured cost order
+    (costliest first), and record this render's costs for the next -- for
+    playback, a fixed view or one rank's region, where consecutive frames
+    cost alike.  Scheduling only: the pixels are bitwise those of a plain
+    render.  Use a plan from one CUDA stream at a time.
+    """
+
+    def __init__(self, device=None):
+        dev = torch_device(device)
+        self.device = dev
+        h = ctypes.c_void_p()
+        _native.check(_native.lib().vv_camera_plan_create(dev.index if dev.index is not None else 0,
+                                                          ctypes.byref(h)))
+        self._handle = h
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                _native.lib().vv_camera_plan_free(h)
+            except Exception:
+                pass
+            self._handle = None
+
+
+_PLANS = {}
+
+
+def _stream_plan(dev, stream_handle: int) -> CameraPlan:
+    """The camera plan render() keeps per (device, stream): renders on one
+    stream are ordered, so its plan is never used concurrently."""
+    key = (dev.index, stream_handle)
+    p = _PLANS.get(key)
+    if p is None:
+        if len(_PLANS) > 16:
+            _PLANS.clear()
+        p = _PLANS[key] = CameraPlan(dev)
+    return p
 
 
 class _PinnedPool:
@@ -430,13 +475,15 @@ def finalize_layer(premult, alpha, tbar, shape, opts: RenderOptions, depth_scale
 
 
 def render_into(tree, cam: Camera, frame: int, rgb, alpha, depth, opts: RenderOptions = RenderOptions(),
-                cache=None, *, stream=None, sample_count=None):
+                cache=None, *, stream=None, sample_count=None, plan=None):
     """Render into caller-owned CUDA float32 tensors (rgb (H,W,3), alpha/depth (H,W); any may be None).
 
     The allocation-free device path used by the benchmark; asynchronous on
     the current (or given) stream.  ``sample_count``: optional CUDA int32
     (H, W) tensor receiving each pixel's consumed leaf samples (the
-    reference's per-ray ``used`` count), from the same kernel.
+    reference's per-ray ``used`` count), from the same kernel.  ``plan``:
+    a CameraPlan scheduling the kernel from the previous frames' costs
+    (bitwise the same pixels).
     """
     frame = _frame_index(frame, tree)
     _check_frame(tree, frame)
@@ -452,6 +499,10 @@ def render_into(tree, cam: Camera, frame: int, rgb, alpha, depth, opts: RenderOp
     if sample_count is not None:
         _native.check(_native.lib().vv_render_camera_counts(
             rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd), *planes, sample_count.data_ptr(), s))
+        return
+    if plan is not None:
+        _native.check(_native.lib().vv_render_camera_planned(rep.handle, frame, ch, ctypes.byref(oc),
+                                                             ctypes.byref(cd), None, plan._handle, *planes, 0, s))
         return
     _native.check(_native.lib().vv_render_camera(rep.handle, frame, ch, ctypes.byref(oc), ctypes.byref(cd),
                                                  *planes, s))
@@ -471,7 +522,8 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
     rgb = buf[: 3 * h * w].view(h, w, 3)
     alpha = buf[3 * h * w: 4 * h * w].view(h, w)
     depth = buf[4 * h * w:].view(h, w)
-    render_into(tree, cam, frame, rgb, alpha, depth, opts, cache)
+    render_into(tree, cam, frame, rgb, alpha, depth, opts, cache,
+                plan=_stream_plan(dev, torch.cuda.current_stream(dev).cuda_stream))
     if out == "torch":
         return LayerImages(rgb, alpha, depth)
     host, a = _PINNED.get(5 * h * w)

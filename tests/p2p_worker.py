@@ -1,5 +1,6 @@
 """One rank of test_tiles_gpu.test_p2p_renderer_two_processes_ipc (run as a
-script: RANK / WORLD_SIZE / MASTER_* from the environment, gloo, cuda:0)."""
+script: RANK / WORLD_SIZE / MASTER_* from the environment, gloo, cuda:0;
+argv[1]: TileRenderer mode, "p2p" (interleaved tiles) or "regions" (row bands))."""
 import os
 import sys
 
@@ -20,7 +21,8 @@ def main():
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     tree, cam = synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=3), synthetic.bench_camera(W, H)
-    tr = TileRenderer(W, H, TILE, rank=rank, world=world, device=dev, mode="p2p")
+    mode = sys.argv[1] if len(sys.argv) > 1 else "p2p"
+    tr = TileRenderer(W, H, TILE, rank=rank, world=world, device=dev, mode=mode)
     ok = True
     for f in (1, 4, 6):
         out = tr.render_frame(tree, cam, f)

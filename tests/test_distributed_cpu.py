@@ -64,3 +64,18 @@ def test_gather_unpack_world2():
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) == 1.0
+
+
+def test_band_plan_balances_and_aligns():
+    from paper_2202_06088_b200.distributed import band_plan
+
+    rng = np.random.default_rng(1)
+    costs = np.concatenate([np.full(200, 0.1), rng.uniform(5, 50, 680), np.full(200, 0.1)])
+    for n in (1, 2, 3, 8):
+        e = band_plan(costs, n)
+        assert len(e) == n + 1 and e[0] == 0 and e[-1] == len(costs)
+        assert all(a <= b for a, b in zip(e, e[1:]))
+        assert all(x % 8 == 0 for x in e[1:-1])
+        per = [costs[a:b].sum() for a, b in zip(e, e[1:])]
+        assert max(per) <= costs.sum() / n + 8 * costs.max() + 1e-9
+    assert band_plan(np.ones(5), 4)[-1] == 5  # fewer rows than bands

@@ -122,13 +122,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_p2p_renderer_two_processes_ipc(cuda):
+@pytest.mark.parametrize("mode", ["p2p", "regions"])
+def test_p2p_renderer_two_processes_ipc(cuda, mode):
     port = _free_port()
     procs = []
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
                    PYTHONPATH=str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", ""))
-        procs.append(subprocess.Popen([sys.executable, str(ROOT / "tests" / "p2p_worker.py")], env=env,
+        procs.append(subprocess.Popen([sys.executable, str(ROOT / "tests" / "p2p_worker.py"), mode], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
     for p in procs:
@@ -210,3 +211,144 @@ def test_direct_tiles_sizes_and_worlds(cuda, tile, world):
     _eq(rgb, ref.rgb, "rgb")
     _eq(alpha, ref.alpha, "alpha")
     _eq(depth, ref.depth, "depth")
+
+
+# ------------------------------------------------------------------ regions
+def _region_union(tree, cam, frame, bands, opts=None):
+    """Render each band into NaN planes; check each band writes only its rows."""
+    import torch
+
+    from paper_2202_06088_b200.distributed import render_region
+
+    h, w = cam.height, cam.width
+    rgb = torch.full((h, w, 3), float("nan"), device="cuda")
+    alpha = torch.full((h, w), float("nan"), device="cuda")
+    depth = torch.full((h, w), float("nan"), device="cuda")
+    from paper_2202_06088_b200.distributed import block_order, pixel_costs
+
+    costs = pixel_costs(tree, cam, frame)
+    for k in range(len(bands) - 1):
+        rect = (0, bands[k], w, bands[k + 1])
+        order = block_order(costs, rect) if k % 2 else None  # both launch orders
+        render_region(tree, cam, frame, rect, rgb, alpha, depth, opts, order=order)
+        torch.cuda.synchronize()
+        a = _np(alpha)
+        assert not np.isnan(a[:bands[k + 1]]).any() and np.isnan(a[bands[k + 1]:]).all(), f"band {k}"
+    return rgb, alpha, depth
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_region_bands_bitwise(cuda, world):
+    """Row bands balanced on measured row costs: each band slices only the
+    leaf chunks its pixels can reach (chunk culling) and writes only its rows;
+    their union is render() bitwise (ragged image, every decode mode)."""
+    from paper_2202_06088_b200.distributed import band_plan, row_costs
+
+    tree, cam = _tree(), synthetic.bench_camera(W, H)
+    bands = band_plan(row_costs(tree, cam, 2), world)
+    assert bands[0] == 0 and bands[-1] == H and all(a <= b for a, b in zip(bands, bands[1:]))
+    for mode in ("per_frame", "auto", "per_sample"):
+        opts = vv.RenderOptions(frame_slice=mode)
+        ref = vv.render(tree, cam, 2, opts)
+        rgb, alpha, depth = _region_union(tree, cam, 2, bands, opts)
+        _eq(rgb, ref.rgb, f"{mode} rgb")
+        _eq(alpha, ref.alpha, f"{mode} alpha")
+        _eq(depth, ref.depth, f"{mode} depth")
+
+
+def test_region_rectangles_and_inside_camera(cuda):
+    """Arbitrary rectangles (2D split), and an eye inside the tree's cube
+    (chunk corners behind the camera are kept conservatively)."""
+    import torch
+
+    from paper_2202_06088_b200.distributed import render_region
+
+    tree = _tree()
+    opts = vv.RenderOptions(frame_slice="per_frame")
+    for cam in (synthetic.bench_camera(W, H),
+                vv.Camera.look_at([0.5, 0.45, 0.5], [1.0, 0.9, 0.7], width=W, height=H, focal=0.6 * W)):
+        ref = vv.render(tree, cam, 5, opts)
+        rgb = torch.full((H, W, 3), float("nan"), device=cuda)
+        alpha = torch.full((H, W), float("nan"), device=cuda)
+        depth = torch.full((H, W), float("nan"), device=cuda)
+        xs, ys = (0, 48, 130, W), (0, 40, 96, H)
+        for i in range(3):
+            for j in range(3):
+                render_region(tree, cam, 5, (xs[i], ys[j], xs[i + 1], ys[j + 1]), rgb, alpha, depth, opts)
+        torch.cuda.synchronize()
+        _eq(rgb, ref.rgb, "rect rgb")
+        _eq(alpha, ref.alpha, "rect alpha")
+        _eq(depth, ref.depth, "rect depth")
+
+
+@pytest.mark.parametrize("gen", ["shell", "motion"])
+def test_region_bands_full_size(cuda, gen):
+    """cfg2 / cfg3 at 1080p in 8 measured bands: bitwise equal to render()
+    (cfg3 adds the node masks, with unlisted leaves treated as dark)."""
+    from paper_2202_06088_b200.distributed import band_plan, row_costs
+
+    tree = synthetic.shell_tree() if gen == "shell" else synthetic.motion_tree()
+    cam = synthetic.bench_camera()
+    bands = band_plan(row_costs(tree, cam, 4), 8)
+    for f in (4, 17):
+        ref = vv.render(tree, cam, f)
+        rgb, alpha, depth = _region_union(tree, cam, f, bands)
+        _eq(rgb, ref.rgb, f"{gen} rgb {f}")
+        _eq(alpha, ref.alpha, f"{gen} alpha {f}")
+        _eq(depth, ref.depth, f"{gen} depth {f}")
+
+
+# ------------------------------------------------------------------ camera plans
+def test_camera_plan_bitwise_over_frames_and_sizes(cuda):
+    """Renders through a CameraPlan (persistent warps in the previous frame's
+    cost order) are bitwise render(): first frame (no order yet), later
+    frames (learned order), a resized camera (plan re-sized), a region, and
+    a second tree sharing the plan (any valid order schedules correctly)."""
+    import torch
+
+    tree, other = _tree(), synthetic.shell_tree(depth=6, n_max=2, frames=5, seed=9)
+    plan = vv.CameraPlan(cuda)
+    for w, h in ((W, H), (W, H), (128, 96), (W, H)):
+        cam = synthetic.bench_camera(w, h)
+        for f in (0, 3, 7):
+            for t in (tree, other):
+                f_ = f % t.frames
+                outs = [torch.full((h, w, 3), float("nan"), device=cuda), torch.full((h, w), float("nan"), device=cuda),
+                        torch.full((h, w), float("nan"), device=cuda)]
+                vv.render_into(t, cam, f_, *outs, plan=plan)
+                ref = vv.render(t, cam, f_)
+                torch.cuda.synchronize()
+                _eq(outs[0], ref.rgb, f"plan rgb {w}x{h} f{f_}")
+                _eq(outs[1], ref.alpha, f"plan alpha {w}x{h} f{f_}")
+                _eq(outs[2], ref.depth, f"plan depth {w}x{h} f{f_}")
+
+
+def test_camera_plan_regions_renderer_world1(cuda):
+    """TileRenderer(mode="regions") at world 1 (one band, planned) equals render()."""
+    tree, cam = _tree(), synthetic.bench_camera(W, H)
+    tr = TileRenderer(W, H, TILE, rank=0, world=1, device=cuda, mode="regions")
+    try:
+        for f in (1, 4, 6, 2):
+            out = tr.render_frame(tree, cam, f)
+            ref = vv.render(tree, cam, f)
+            _eq(out.rgb, ref.rgb, f"rgb frame {f}")
+            _eq(out.depth, ref.depth, f"depth frame {f}")
+    finally:
+        tr.close()
+
+
+def test_camera_plan_cfg3_masked(cuda):
+    """Planned renders of the cfg3 motion tree (node masks on) at 1080p,
+    bitwise equal to unplanned ones across a frame sweep."""
+    import torch
+
+    tree, cam = synthetic.motion_tree(), synthetic.bench_camera()
+    plan = vv.CameraPlan(cuda)
+    h, w = cam.height, cam.width
+    for f in (0, 7, 30, 31, 59):
+        outs = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda)]
+        vv.render_into(tree, cam, f, *outs, plan=plan)
+        ref = vv.render(tree, cam, f)
+        torch.cuda.synchronize()
+        _eq(outs[0], ref.rgb, f"cfg3 plan rgb {f}")
+        _eq(outs[2], ref.depth, f"cfg3 plan depth {f}")
