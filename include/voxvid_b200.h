@@ -298,6 +298,20 @@ int vv_render_camera_multi(const vv_tree *tree, int32_t n_frames, const int32_t 
 int vv_render_scene(const vv_instance *instances, int32_t n_instances,
                     const vv_render_opts *opts, const vv_camera *cam, const double *background,
                     float *image, float *alpha, float *depth, void *stream);
+/* Per-sample depth-ordered joint composition (north-star kernel 4; an
+ * extension: the reference composes by Algorithm 1 and checks it against
+ * this joint rendering in its tests, pkg/tests/util.py:205-245).  Same
+ * arguments as vv_render_scene (<= 8 instances): every instance walks its
+ * tree along its pulled-back ray, the leaf segments of all walks are merged
+ * by world depth (ties to the earlier instance) and composited once,
+ * tau = sigma (t1 - t0) in tree units, front to back, early termination at
+ * opts->early_stop (0: none).  image = C + (1 - A) background (premultiplied
+ * joint colour C), or C / A without a background; alpha A; depth = expected
+ * world t (far_plane below alpha_floor).  Equal to vv_render_scene where the
+ * instances do not interleave along any ray. */
+int vv_render_scene_joint(const vv_instance *inst, int32_t n_inst, const vv_render_opts *opts,
+                          const vv_camera *cam, const double *background, float *image, float *alpha,
+                          float *depth, void *stream);
 /* Leaf-decode mode vv_render_scene picks for each instance (0: per sample
  * inside the scene kernel -- every instance 0 and no edits runs the lean
  * instantiation --, 1: a per-frame slice pass first). */
@@ -341,10 +355,17 @@ int vv_shadow_blur(const float *alpha, int32_t res, const double *weights, int32
                    double *out, void *stream);
 /* Lights applied in order to the blended layer (vv_render_scene with
  * background NULL), then composite_background over `background`
- * (render_scene, compose.py:462-471).  Device fp32 images; at most 16 lights. */
+ * (render_scene, compose.py:462-471).  Device fp32 images; any number of
+ * lights (0: the plain background composite). */
 int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
                       const double *background, const vv_light *lights, int32_t n_lights, float *image,
                       void *stream);
+/* vv_scene_lighting that also writes lit_rgb (H, W, 3): the blended rgb
+ * after every light's falloff -- the `blended` layer render_scene returns
+ * with want_layers (compose.py:462-466). */
+int vv_scene_lighting_ex(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
+                         const double *background, const vv_light *lights, int32_t n_lights, float *image,
+                         float *lit_rgb, void *stream);
 
 /* ---- paint / termination voxel ---------------------------------------------
  * Replaces the per-pixel loop of compose.paint (compose.py:482-532): for

@@ -77,12 +77,14 @@ EXPORTED_SYMBOLS = (
     "vv_ipc_free",
     "vv_render_scene",
     "vv_scene_decode_modes",
+    "vv_render_scene_joint",
     "vv_render_camera_multi",
     "vv_slice_build_multi",
     "vv_slice_build_frames",
     "vv_camera_decode_mode",
     "vv_shadow_blur",
     "vv_scene_lighting",
+    "vv_scene_lighting_ex",
     "vv_count_segments",
     "vv_collect_segments",
     "vv_termination_leaves",
@@ -264,7 +266,13 @@ _SIGNATURES = {
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),
+    "vv_scene_lighting_ex": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_render_scene": (
+        ctypes.c_int,
+        [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),
+         _P, _P, _P, _P, _P],
+    ),
+    "vv_render_scene_joint": (
         ctypes.c_int,
         [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),
          _P, _P, _P, _P, _P],

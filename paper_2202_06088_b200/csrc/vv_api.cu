@@ -1397,34 +1397,26 @@ int vv_scene_decode_modes(const vv_instance *inst, int32_t n_inst, const vv_rend
     return VV_OK;
 }
 
-int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
-                    const double *background, float *image, float *alpha, float *depth, void *stream) {
-    if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
-    if (!image && !alpha && !depth) return set_error(VV_E_INVALID, "no output");
-    if (background && !image) return set_error(VV_E_INVALID, "background given without an image output");
-    if (n_inst < 1) return set_error(VV_E_INVALID, "scene has no visible instances");
-    if (n_inst > kMaxInst) return set_error(VV_E_UNSUPPORTED, "at most %d instances per fused scene", kMaxInst);
-    const vv_tree *t0 = inst[0].tree;
-    if (!t0) return set_error(VV_E_INVALID, "null tree");
+// One fused scene launch over instances [b, e) of the visible list (<= 16,
+// one n_max), continuing Algorithm 1 from state_in and handing it on through
+// state_out when the scene needs several launches (more than 16 instances or
+// mixed n_max); decode modes consider every instance sharing a tree.
+static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_render_opts &opts,
+                     const vv_camera *cam, const double *background, float *image, float *alpha, float *depth,
+                     cudaStream_t st, bool joint, double *state_in, double *state_out) {
+    const vv_tree *t0 = inst[b].tree;
     int max_depth = 0;
-    for (int i = 0; i < n_inst; ++i) {
-        const vv_tree *t = inst[i].tree;
-        if (!t) return set_error(VV_E_INVALID, "null tree in instance %d", i);
-        if (t->device != t0->device) return set_error(VV_E_INVALID, "instances on different devices");
-        if (t->n_max != t0->n_max) return set_error(VV_E_UNSUPPORTED, "mixed n_max in one fused scene");
-        int rc = check_frame(t, inst[i].frame);
-        if (rc) return rc;
-        max_depth = std::max(max_depth, t->depth);
-    }
-    DeviceGuard g(t0->device);
-    const vv_render_opts opts = o ? *o : default_opts();
+    for (int i = b; i < e; ++i) max_depth = std::max(max_depth, inst[i].tree->depth);
     SceneParams p;
     memset(&p, 0, sizeof(p));
     p.K = make_consts(t0->n_max);
     p.cam = make_cam(*cam);
-    p.n_inst = n_inst;
-    for (int i = 0; i < n_inst; ++i) {
-        InstView &v = p.inst[i];
+    p.n_inst = e - b;
+    p.total_inst = n_all;
+    p.state_in = state_in;
+    p.state_out = state_out;
+    for (int i = b; i < e; ++i) {
+        InstView &v = p.inst[i - b];
         v.T = inst[i].tree->view;
         v.frame = inst[i].frame;
         v.mode = inst[i].mode;
@@ -1446,30 +1438,101 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
     p.image = image;
     p.alpha = alpha;
     p.depth = depth;
+    p.max_depth = max_depth;
     const bool wide = max_depth > kNarrowDepth;
     const size_t smem = stack_bytes(max_depth, wide);
     dim3 grid((unsigned)((cam->width + 15) / 16), (unsigned)((cam->height + 7) / 8));
-    cudaStream_t st = (cudaStream_t)stream;
     Transient tr[kMaxInst];
-    for (int i = 0; i < n_inst; ++i) {
-        p.inst[i].S = SliceView{nullptr, 0};
+    for (int i = b; i < e; ++i) {
+        InstView &v = p.inst[i - b];
+        v.S = SliceView{nullptr, 0};
         int same = -1;
-        for (int j = 0; j < i; ++j)
-            if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j].S.rec) same = j;
-        const int mode = scene_decode_mode(inst, n_inst, i, *cam, opts.frame_slice);
+        for (int j = b; j < i; ++j)
+            if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j - b].S.rec) same = j - b;
+        const int mode = scene_decode_mode(inst, n_all, i, *cam, opts.frame_slice);
         if (same >= 0) {
-            p.inst[i].S = p.inst[same].S;
-            p.inst[i].T.child = p.inst[same].T.child;
+            v.S = p.inst[same].S;
+            v.T.child = p.inst[same].T.child;
         } else if (mode != 0) {
-            int r = build_transient(inst[i].tree, inst[i].frame, st, p.inst[i].S, tr[i]);
+            int r = build_transient(inst[i].tree, inst[i].frame, st, v.S, tr[i - b]);
             if (r) return r;
-            p.inst[i].T.child = image_child(inst[i].tree, tr[i].nmask.get());
+            v.T.child = image_child(inst[i].tree, tr[i - b].nmask.get());
         }
     }
+    if (joint) return launch_scene_joint(t0->n_max, wide, p, st);
     bool lean = true;  // every instance decoded per sample, no edits: the lean instantiation
-    for (int i = 0; i < n_inst; ++i)
-        if (p.inst[i].S.rec || inst[i].tree->has_edits) lean = false;
+    for (int i = b; i < e; ++i)
+        if (p.inst[i - b].S.rec || inst[i].tree->has_edits) lean = false;
     return launch_scene(t0->n_max, wide, lean, p, grid, smem, st);
+}
+
+static int render_scene_impl(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
+                             const double *background, float *image, float *alpha, float *depth, void *stream,
+                             bool joint) {
+    if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
+    if (!image && !alpha && !depth) return set_error(VV_E_INVALID, "no output");
+    if (background && !image) return set_error(VV_E_INVALID, "background given without an image output");
+    if (n_inst < 1) return set_error(VV_E_INVALID, "scene has no visible instances");
+    const vv_tree *t0 = inst[0].tree;
+    if (!t0) return set_error(VV_E_INVALID, "null tree");
+    bool mixed = false;
+    for (int i = 0; i < n_inst; ++i) {
+        const vv_tree *t = inst[i].tree;
+        if (!t) return set_error(VV_E_INVALID, "null tree in instance %d", i);
+        if (t->device != t0->device) return set_error(VV_E_INVALID, "instances on different devices");
+        mixed |= t->n_max != t0->n_max;
+        int rc = check_frame(t, inst[i].frame);
+        if (rc) return rc;
+    }
+    DeviceGuard g(t0->device);
+    const vv_render_opts opts = o ? *o : default_opts();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (joint) {
+        if (mixed) return set_error(VV_E_UNSUPPORTED, "mixed n_max in one joint render");
+        return scene_run(inst, n_inst, 0, n_inst, opts, cam, background, image, alpha, depth, st, true, nullptr,
+                         nullptr);
+    }
+    // runs of consecutive instances with one n_max, at most kMaxInst each
+    std::vector<std::pair<int, int>> runs;
+    for (int b = 0; b < n_inst;) {
+        int e = b + 1;
+        while (e < n_inst && e - b < kMaxInst && inst[e].tree->n_max == inst[b].tree->n_max) ++e;
+        runs.emplace_back(b, e);
+        b = e;
+    }
+    if (runs.size() == 1)
+        return scene_run(inst, n_inst, 0, n_inst, opts, cam, background, image, alpha, depth, st, false, nullptr,
+                         nullptr);
+    // several launches: the per-pixel Algorithm-1 state (I rgb, D, A; f64)
+    // carried between them in a stream-ordered buffer
+    Transient state;
+    pool_setup(t0->device);
+    const size_t bytes = (size_t)cam->width * cam->height * 5 * sizeof(double);
+    if (cudaMallocAsync(&state.mem, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        state.mem = nullptr;
+        return set_error(VV_E_NOMEM, "scene state allocation (%zu bytes) failed", bytes);
+    }
+    state.st = st;
+    double *sb = static_cast<double *>(state.mem);
+    for (size_t r = 0; r < runs.size(); ++r) {
+        const bool last = r + 1 == runs.size();
+        int rc = scene_run(inst, n_inst, runs[r].first, runs[r].second, opts, cam, last ? background : nullptr,
+                           last ? image : nullptr, last ? alpha : nullptr, last ? depth : nullptr, st, false,
+                           r ? sb : nullptr, last ? nullptr : sb);
+        if (rc) return rc;
+    }
+    return VV_OK;
+}
+
+int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
+                    const double *background, float *image, float *alpha, float *depth, void *stream) {
+    return render_scene_impl(inst, n_inst, o, cam, background, image, alpha, depth, stream, false);
+}
+
+int vv_render_scene_joint(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
+                          const double *background, float *image, float *alpha, float *depth, void *stream) {
+    return render_scene_impl(inst, n_inst, o, cam, background, image, alpha, depth, stream, true);
 }
 
 static int segments_impl(const vv_tree *t, const double *origins, const double *dirs, int64_t n, double tmin,
@@ -1526,14 +1589,13 @@ int vv_shadow_blur(const float *alpha, int32_t res, const double *weights, int32
     return rc;
 }
 
-int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
-                      const double *background, const vv_light *lights, int32_t n_lights, float *image,
-                      void *stream) {
+int vv_scene_lighting_ex(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
+                         const double *background, const vv_light *lights, int32_t n_lights, float *image,
+                         float *lit_rgb, void *stream) {
     if (!cam || !rgb || !alpha || !depth || !background || !image || (n_lights > 0 && !lights))
         return set_error(VV_E_INVALID, "null argument");
-    if (n_lights < 0 || n_lights > kMaxLights)
-        return set_error(VV_E_UNSUPPORTED, "%d lights (at most %d per pass)", n_lights, kMaxLights);
-    LightView L[kMaxLights];
+    if (n_lights < 0) return set_error(VV_E_INVALID, "negative light count");
+    std::vector<LightView> L((size_t)std::max(n_lights, 1));
     for (int i = 0; i < n_lights; ++i) {
         const vv_light &s = lights[i];
         if (s.cast_shadows && (!s.shadow_map || s.shadow_res < 1))
@@ -1558,8 +1620,23 @@ int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha
         L[i].cx = s.cx;
         L[i].cy = s.cy;
     }
-    return launch_scene_light(make_cam(*cam), rgb, alpha, depth, background[0], background[1], background[2], L,
-                              n_lights, image, (cudaStream_t)stream);
+    // the lights ride along stream-ordered in device memory (any number)
+    cudaStream_t st = (cudaStream_t)stream;
+    LightView *dl = nullptr;
+    if (n_lights > 0) {
+        VV_CUDA(cudaMallocAsync(&dl, (size_t)n_lights * sizeof(LightView), st));
+        VV_CUDA(cudaMemcpyAsync(dl, L.data(), (size_t)n_lights * sizeof(LightView), cudaMemcpyHostToDevice, st));
+    }
+    const int rc = launch_scene_light(make_cam(*cam), rgb, alpha, depth, background[0], background[1], background[2],
+                                      dl, n_lights, image, lit_rgb, st);
+    if (dl) cudaFreeAsync(dl, st);
+    return rc;
+}
+
+int vv_scene_lighting(const vv_camera *cam, const float *rgb, const float *alpha, const float *depth,
+                      const double *background, const vv_light *lights, int32_t n_lights, float *image,
+                      void *stream) {
+    return vv_scene_lighting_ex(cam, rgb, alpha, depth, background, lights, n_lights, image, nullptr, stream);
 }
 
 int vv_termination_leaves(const vv_tree *t, int32_t frame, const double *origins, const double *dirs,

@@ -308,6 +308,14 @@ struct SceneParams {
     double bg0, bg1, bg2;
     int composite;  // 1: image = composite over bg; 0: image = blended (unpremultiplied) rgb
     float *image, *alpha, *depth;
+    int max_depth;  // deepest instance tree (stack sizing)
+    // a scene in several launches (> kMaxInst instances, mixed n_max): the
+    // per-pixel Algorithm-1 state (I0, I1, I2, D, A; f64) continues from
+    // state_in and, except in the last launch, goes to state_out instead of
+    // the outputs; total_inst counts every launch's instances
+    const double *state_in;
+    double *state_out;
+    int total_inst;
 };
 
 // CACHED 2: per-instance decode decided at run time (some instances sliced);
@@ -331,7 +339,14 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
     double cdx, cdy, cdz;
     camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
     // blended state (compose.py:386-405): I (3), D, A
+    const int64_t pix = (int64_t)iy * p.cam.width + ix;
     double I0 = 0, I1 = 0, I2 = 0, D = 0, A = 0;
+    bool have = false;
+    if (p.state_in) {  // an earlier launch's instances
+        const double *s = p.state_in + 5 * pix;
+        I0 = s[0]; I1 = s[1]; I2 = s[2]; D = s[3]; A = s[4];
+        have = true;
+    }
     for (int i = 0; i < p.n_inst; ++i) {
         const InstView &v = p.inst[i];
         double ox, oy, oz, dx, dy, dz, scale = 1.0;
@@ -374,8 +389,9 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
         double t = xdiv(sh.tacc, safe);
         if (scaled) t = xmul(t, scale);
         const double ld = al >= p.alpha_floor ? t : p.far_plane;
-        if (i == 0) {
+        if (!have) {
             I0 = li0; I1 = li1; I2 = li2; D = ld; A = al;
+            have = true;
         } else {
             // Algorithm 1 (compose.py:393-404); ties go to the incoming layer
             const double om_ai = xsub(1.0, al), om_a = xsub(1.0, A);
@@ -392,7 +408,12 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
             A = xadd(A, xmul(al, om_a));
         }
     }
-    if (p.n_inst > 1) {  // unpremultiply the blend (compose.py:457-460)
+    if (p.state_out) {  // a later launch continues the blend
+        double *s = p.state_out + 5 * pix;
+        s[0] = I0; s[1] = I1; s[2] = I2; s[3] = D; s[4] = A;
+        return;
+    }
+    if (p.total_inst > 1) {  // unpremultiply the blend (compose.py:457-460)
         const double safe = A > 1e-300 ? A : 1e-300;
         if (A > 0.0) {
             I0 = xdiv(I0, safe);
@@ -402,7 +423,6 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
             I0 = I1 = I2 = 0.0;
         }
     }
-    const int64_t pix = (int64_t)iy * p.cam.width + ix;
     if (p.image && p.composite) {
         // composite_background: a * rgb + (1 - a) * bg (render.py:243-251)
         const double om = xsub(1.0, A);
@@ -970,6 +990,8 @@ int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p,
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
                         cudaStream_t st, bool long_queue = false);
 int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
+// per-sample depth-ordered joint composition (vv_launch_joint.cu)
+int launch_scene_joint(int nmax, bool wide, const SceneParams &p, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
 // per-frame node mask (vv_launch_mask.cu): child table with every child whose
 // subtree holds no lit leaf replaced by -1
@@ -1004,7 +1026,6 @@ int launch_segments(bool wide, bool collect, const SegParams &p, unsigned grid, 
 int launch_terminate(bool wide, const TermParams &p, unsigned grid, size_t smem, cudaStream_t st);
 int launch_shadow_blur(const float *alpha, int res, const double *weights, int radius, double *tmp, double *out,
                        cudaStream_t st);
-constexpr int kMaxLights = 16;
 struct LightView {  // vv_light (include/voxvid_b200.h)
     double px, py, pz;
     double ga, gb, gc, gd;
@@ -1016,7 +1037,8 @@ struct LightView {  // vv_light (include/voxvid_b200.h)
     double fx, fy, cx, cy;
 };
 int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha, const float *depth, double bg0,
-                       double bg1, double bg2, const LightView *lights, int n_lights, float *image, cudaStream_t st);
+                       double bg1, double bg2, const LightView *lights, int n_lights, float *image, float *lit_rgb,
+                       cudaStream_t st);
 int launch_repack(const float *src, int64_t rows, int P, int C, int K3, int c4, int hh4, int64_t lstride,
                   int64_t r0, const int32_t *dst_row, float4 *sig, float4 *gam, float4 *hh, cudaStream_t st);
 // slice records (device rows) -> sigma (n) f64 / q (n, 3S) f32 in reference row order

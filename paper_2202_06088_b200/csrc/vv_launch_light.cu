@@ -49,9 +49,10 @@ struct LightParams {
     CamView cam;
     const float *rgb, *alpha, *depth;
     double bg0, bg1, bg2;
-    LightView L[kMaxLights];
+    const LightView *L;  // (n_lights) device array
     int n_lights;
     float *image;
+    float *lit_rgb;  // optional: the blended rgb after the falloffs (render_scene's returned `blended`)
 };
 
 // map_coordinates(order=1, mode="constant", cval=0): bilinear inside
@@ -81,7 +82,7 @@ __global__ void k_scene_light(const __grid_constant__ LightParams p) {
     double r = p.rgb[3 * pix + 0], g = p.rgb[3 * pix + 1], b = p.rgb[3 * pix + 2];
     double bg0 = p.bg0, bg1 = p.bg1, bg2 = p.bg2;  // bg *= factor per light
     for (int li = 0; li < p.n_lights; ++li) {
-        const LightView &L = p.L[li];
+        const LightView L = p.L[li];
         if (L.falloff_enabled && a > 0.0) {  // falloff_pass (compose.py:606-619)
             const double qx = xsub(xadd(ox, xmul(dep, dx)), L.px);
             const double qy = xsub(xadd(oy, xmul(dep, dy)), L.py);
@@ -117,6 +118,11 @@ __global__ void k_scene_light(const __grid_constant__ LightParams p) {
             }
         }
     }
+    if (p.lit_rgb) {
+        p.lit_rgb[3 * pix + 0] = (float)r;
+        p.lit_rgb[3 * pix + 1] = (float)g;
+        p.lit_rgb[3 * pix + 2] = (float)b;
+    }
     // composite_background (render.py:243-251) over the darkened background
     const double om = xsub(1.0, a);
     p.image[3 * pix + 0] = (float)xadd(xmul(a, r), xmul(om, bg0));
@@ -125,7 +131,8 @@ __global__ void k_scene_light(const __grid_constant__ LightParams p) {
 }
 
 int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha, const float *depth, double bg0,
-                       double bg1, double bg2, const LightView *lights, int n_lights, float *image, cudaStream_t st) {
+                       double bg1, double bg2, const LightView *lights, int n_lights, float *image, float *lit_rgb,
+                       cudaStream_t st) {
     LightParams p;
     p.cam = cam;
     p.rgb = rgb;
@@ -135,8 +142,9 @@ int launch_scene_light(const CamView &cam, const float *rgb, const float *alpha,
     p.bg1 = bg1;
     p.bg2 = bg2;
     p.n_lights = n_lights;
-    for (int i = 0; i < n_lights; ++i) p.L[i] = lights[i];
+    p.L = lights;
     p.image = image;
+    p.lit_rgb = lit_rgb;
     const int64_t npix = (int64_t)cam.width * cam.height;
     if (npix == 0) return VV_OK;
     k_scene_light<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(p);
