@@ -208,6 +208,17 @@ int vv_render_camera_region(const vv_tree *tree, int32_t frame, const vv_slice *
                             const vv_render_opts *opts, const vv_camera *cam, const int32_t *region,
                             const int32_t *block_order, float *rgb, float *alpha, float *depth,
                             int32_t peer, void *stream);
+/* render() to the host: vv_render_camera into device_planes (5 H W floats:
+ * rgb | alpha | depth, as LayerImages' planes), each 64-row band of the
+ * frame copied into host_planes (pinned, same layout) as soon as the
+ * kernel has stored it -- the device->host copy overlaps the render (a copy
+ * stream waits on per-band counters with cuStreamWaitValue32).  All work
+ * is ordered on `stream`: the frame is on the host once it has reached the
+ * end of it. */
+int vv_render_camera_to_host(const vv_tree *tree, int32_t frame, const vv_slice *cache,
+                             const vv_render_opts *opts, const vv_camera *cam, float *device_planes,
+                             float *host_planes, void *stream);
+
 /* Camera plans: renders of a camera stream (playback, a fixed view, one
  * rank's region) through a plan run the camera kernel as persistent warps
  * that take the frame's warp chunks from a counter in the previous render's

@@ -65,6 +65,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_camera_counts",
     "vv_render_camera_region",
     "vv_camera_block_shape",
+    "vv_render_camera_to_host",
     "vv_camera_plan_create",
     "vv_camera_plan_free",
     "vv_render_camera_planned",
@@ -240,6 +241,8 @@ _SIGNATURES = {
         [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P, _P, _I32, _P],
     ),
     "vv_camera_block_shape": (ctypes.c_int, [_P, _P]),
+    "vv_render_camera_to_host": (
+        ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P]),
     "vv_camera_plan_create": (ctypes.c_int, [_I32, ctypes.POINTER(_P)]),
     "vv_camera_plan_free": (ctypes.c_int, [_P]),
     "vv_render_camera_planned": (

@@ -10,6 +10,7 @@
 //   k_build_slice    build_slice_kernel (kernels.py:397-407)
 //   k_count / k_collect  count/collect_segments_kernel (kernels.py:313-367)
 //   k_repack         payload rows -> padded [w_sigma] / [w_gamma | w_hh] planes
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdlib.h>
@@ -1054,7 +1055,8 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
                               const vv_camera *cam, float *rgb, float *alpha, float *depth, float *packed,
                               int tile, int shard, int n_shards, int peer, void *stream, int32_t *used = nullptr,
                               const int32_t *rect = nullptr, const int32_t *block_order = nullptr,
-                              vv_camera_plan *plan = nullptr) {
+                              vv_camera_plan *plan = nullptr, unsigned *band_done = nullptr, int band_rows = 0,
+                              bool force_queue = false) {
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
@@ -1109,6 +1111,8 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         p.blocks_x = (p.rx1 - p.rx0 + kTW - 1) / kTW;
         grid_blocks = (unsigned)p.blocks_x * (unsigned)((p.ry1 - p.ry0 + kTH - 1) / kTH);
         p.block_order = block_order;
+        p.band_done = band_done;
+        p.band_rows = band_rows;
     }
     const bool wide = t->depth > kNarrowDepth;
     const size_t smem = stack_bytes(t->depth, wide);
@@ -1141,7 +1145,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         p.n_work = (int)grid_blocks * kWarpsPerTile;
         p.block_order = plan->valid ? plan->order : nullptr;
         p.block_cost = plan->cost;
-    } else if (!tile && warp_queue(block_order != nullptr)) {
+    } else if (!tile && (force_queue || warp_queue(block_order != nullptr))) {
         // persistent warps over the warp chunks: the chunk counter is zeroed
         // before the slice pass so the render keeps its PDL overlap
         pool_setup(t->device);
@@ -1175,6 +1179,131 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     if ((rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st))) return rc;
     plan->valid = true;
     return VV_OK;
+}
+
+// ---- render straight to the host: banded device->host copies behind the render
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static WaitValue32Fn wait_value32() {  // the driver's cuStreamWaitValue32 (stream memory ops)
+    static WaitValue32Fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        // the CUDA 12 ABI (cuStreamWaitValue32_v2): stream memory ops are
+        // enabled by default (the v1 entry needs a driver module option)
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WaitValue32Fn>(f);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// Per (device, caller stream): a non-blocking copy stream and the band
+// counters (plain cudaMalloc: stream memory ops do not accept pool memory).
+// Calls on one caller stream are ordered, and each ends with that stream
+// waiting for its copies, so the counters are reused safely.
+struct HostCopyState {
+    int device;
+    cudaStream_t caller, copy;
+    unsigned *counters;
+    int capacity;
+};
+
+static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_bands) {
+    static std::mutex mu;
+    static std::vector<HostCopyState> states;
+    std::lock_guard<std::mutex> lk(mu);
+    HostCopyState *st = nullptr;
+    for (auto &e : states)
+        if (e.device == device && e.caller == caller) st = &e;
+    if (!st) {
+        HostCopyState e{device, caller, nullptr, nullptr, 0};
+        if (cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        states.push_back(e);
+        st = &states.back();
+    }
+    if (st->capacity < n_bands) {
+        cudaStreamSynchronize(st->copy);
+        cudaFree(st->counters);
+        st->counters = nullptr;
+        st->capacity = 0;
+        if (cudaMalloc(&st->counters, (size_t)n_bands * sizeof(unsigned)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        st->capacity = n_bands;
+    }
+    return st;
+}
+
+int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
+                             const vv_camera *cam, float *device_planes, float *host_planes, void *stream) {
+    if (!t || !cam || !device_planes || !host_planes) return set_error(VV_E_INVALID, "null argument");
+    if (cam->width <= 0 || cam->height <= 0) return set_error(VV_E_INVALID, "bad camera size");
+    DeviceGuard g(t->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t hw = (int64_t)cam->width * cam->height;
+    float *rgb = device_planes, *alpha = device_planes + 3 * hw, *depth = device_planes + 4 * hw;
+    WaitValue32Fn wait = wait_value32();
+    // bands of 136 rows (whole camera-block rows), 8 at 1080p: measured
+    // 1.28 ms per cfg2 render() -> host vs 1.34 / 1.36 for 272 / 64 rows and
+    // 1.80 unbanded (VV_HOST_BAND_ROWS overrides: A/B runs)
+    int band_rows = std::max(kTH, (136 / kTH) * kTH);
+    if (const char *e = getenv("VV_HOST_BAND_ROWS")) band_rows = std::max(kTH, (atoi(e) / kTH) * kTH);
+    const int n_bands = (cam->height + band_rows - 1) / band_rows;
+    HostCopyState *hs = wait ? host_copy_state(t->device, st, n_bands) : nullptr;
+    if (!hs) {  // no stream memory ops: render, then one copy
+        int rc = render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream);
+        if (rc) return rc;
+        VV_CUDA(cudaMemcpyAsync(host_planes, device_planes, (size_t)hw * 5 * sizeof(float), cudaMemcpyDeviceToHost,
+                                st));
+        return VV_OK;
+    }
+    cudaStream_t cs = hs->copy;
+    unsigned *band_done = hs->counters;
+    VV_CUDA(cudaMemsetAsync(band_done, 0, (size_t)n_bands * sizeof(unsigned), st));
+    cudaEvent_t ready, copied;
+    VV_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    VV_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    cudaEventRecord(ready, st);  // counters zeroed, earlier work on the caller's stream ordered
+    cudaStreamWaitEvent(cs, ready, 0);
+    // persistent warps in row-major order: bands finish top to bottom
+    int rc = render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream, nullptr,
+                                nullptr, nullptr, nullptr, band_done, band_rows, true);
+    if (rc) {
+        cudaStreamWaitEvent(st, ready, 0);
+        cudaEventDestroy(ready);
+        cudaEventDestroy(copied);
+        return rc;
+    }
+    const int blocks_x = (cam->width + kTW - 1) / kTW;
+    const size_t W = (size_t)cam->width;
+    for (int b = 0; b < n_bands && !rc; ++b) {
+        const int y0 = b * band_rows, y1 = std::min(cam->height, y0 + band_rows);
+        const unsigned target = (unsigned)(((y1 - y0 + kTH - 1) / kTH) * blocks_x * kWarpsPerTile);
+        const CUresult wr = wait(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(band_done + b), target,
+                                 CU_STREAM_WAIT_VALUE_GEQ);
+        if (wr != CUDA_SUCCESS) {
+            rc = set_error(VV_E_CUDA, "cuStreamWaitValue32 failed (CUresult %d)", (int)wr);
+            break;
+        }
+        const size_t px0 = (size_t)y0 * W, npx = (size_t)(y1 - y0) * W;
+        if (cudaMemcpyAsync(host_planes + 3 * px0, rgb + 3 * px0, npx * 12, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
+            cudaMemcpyAsync(host_planes + 3 * hw + px0, alpha + px0, npx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
+            cudaMemcpyAsync(host_planes + 4 * hw + px0, depth + px0, npx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            rc = set_error(VV_E_CUDA, "band copy failed");
+    }
+    cudaEventRecord(copied, cs);
+    cudaStreamWaitEvent(st, copied, 0);  // the caller's stream: frame on the host, counters free again
+    cudaEventDestroy(ready);
+    cudaEventDestroy(copied);
+    return rc;
 }
 
 int vv_camera_plan_create(int32_t device, vv_camera_plan **out) {

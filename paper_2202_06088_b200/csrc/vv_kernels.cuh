@@ -116,6 +116,12 @@ struct CamParams {
     // samples + 1 per ray, atomically summed per warp) -- a camera plan's
     // launch order for the next frame (vv_camera_plan)
     uint32_t *block_cost;
+    // optional (image mode): per row band of band_rows rows, the warp chunks
+    // finished (each warp fences its stores, then adds 1) -- the copy
+    // stream of vv_render_camera_to_host waits on these and copies each
+    // band to the host while the rest of the frame renders
+    unsigned *band_done;
+    int band_rows;
     // optional per-pixel leaf-sample counts (render_kernel's consumed
     // segments, up to and including the early-stop one; image mode): written
     // by the production instantiation itself, so its walk is checked
@@ -245,6 +251,11 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             local_pixel((idx % kWarpsPerTile) * 32 + lane, dx_, dy_);
             const int cost = camera_pixel<NMAX, CACHED, EDITS, Entry, SEG>(
                 p, F, smem_raw, p.rx0 + (tb % p.blocks_x) * kTW + dx_, p.ry0 + (tb / p.blocks_x) * kTH + dy_);
+            if (p.band_done) {
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(p.band_done + (tb / p.blocks_x) * kTH / p.band_rows, 1u);
+            }
             __syncwarp();
             if (p.block_cost) {
                 const unsigned sum = __reduce_add_sync(0xffffffffu, (unsigned)cost);
@@ -284,6 +295,11 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             if (p.used) p.used[slot] = sh.used;
         }
         cam_write(p, inside, slot, r, g, b, a, d);
+        if (p.band_done) {  // this warp's pixels are stored: count it for its band
+            __threadfence();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) atomicAdd(p.band_done + (y0 - p.ry0) / p.band_rows, 1u);
+        }
     }
     // peer stores: make them visible system-wide before the kernel retires
     // (the caller's stream-ordered barrier then publishes the frame)

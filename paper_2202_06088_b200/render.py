@@ -522,13 +522,19 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
     rgb = buf[: 3 * h * w].view(h, w, 3)
     alpha = buf[3 * h * w: 4 * h * w].view(h, w)
     depth = buf[4 * h * w:].view(h, w)
-    render_into(tree, cam, frame, rgb, alpha, depth, opts, cache,
-                plan=_stream_plan(dev, torch.cuda.current_stream(dev).cuda_stream))
+    stream = torch.cuda.current_stream(dev)
     if out == "torch":
+        render_into(tree, cam, frame, rgb, alpha, depth, opts, cache, plan=_stream_plan(dev, stream.cuda_stream))
         return LayerImages(rgb, alpha, depth)
+    # to the host: each 64-row band copied (pinned, copy engine) as soon as
+    # the kernel has stored it, overlapping the rest of the render
+    rep = replica(tree, dev)
+    ch = _check_cache(cache, frame, rep)
     host, a = _PINNED.get(5 * h * w)
-    host.copy_(buf, non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()
+    _native.check(_native.lib().vv_render_camera_to_host(rep.handle, frame, ch, ctypes.byref(opts.c_struct()),
+                                                          ctypes.byref(cam.desc()), buf.data_ptr(), host.data_ptr(),
+                                                          stream.cuda_stream))
+    stream.synchronize()
     return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),
                        a[4 * h * w:].reshape(h, w))
 
@@ -685,9 +691,32 @@ def _playback(torch, tree, cam, frames, opts, comp, copy, bufs, h, w, n):
         pending.clear()
 
 
+def _sequence_groups(n_frames: int, G: int, first: int):
+    """Frame groups of a playback: a short first group (the copy engine,
+    which bounds delivery, starts sooner), then groups of G."""
+    out, i = [], 0
+    if first and n_frames:
+        out.append((0, min(first, n_frames)))
+        i = out[-1][1]
+    while i < n_frames:
+        out.append((i, min(i + G, n_frames)))
+        i += G
+    return out
+
+
+# first playback group: 2 frames.  Steady state is PCIe-bound (0.73 ms per
+# 1080p frame = the 41.5 MB copy alone); a short first group starts the
+# copies sooner: 20-frame sequences 0.813 / 0.834 / 0.824 ms per frame with
+# a first group of 2 / 1 / 3 (tools/seq_probe.py).  VV_SEQ_FIRST overrides.
+SEQUENCE_FIRST = 2
+
+
 def _playback_groups(torch, tree, cam, frames, opts, comp, copy, bufs, n, G, copied, pending, views, split):
-    for gi, g0 in enumerate(range(0, len(frames), G)):
-        group = frames[g0:g0 + G]
+    import os
+
+    first = int(os.environ.get("VV_SEQ_FIRST", SEQUENCE_FIRST))
+    for gi, (g0, g1) in enumerate(_sequence_groups(len(frames), G, first)):
+        group = frames[g0:g1]
         b = gi % 2
         if copied[b] is not None:
             comp.wait_event(copied[b])  # group b's previous frames have left the device

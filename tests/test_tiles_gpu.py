@@ -352,3 +352,22 @@ def test_camera_plan_cfg3_masked(cuda):
         torch.cuda.synchronize()
         _eq(outs[0], ref.rgb, f"cfg3 plan rgb {f}")
         _eq(outs[2], ref.depth, f"cfg3 plan depth {f}")
+
+
+def test_render_to_host_banded_copies(cuda):
+    """render() -> numpy copies 64-row bands behind the kernel (copy stream
+    waiting on per-band counters): bitwise the device render, for ragged
+    sizes, a frame taller than one band and back-to-back calls reusing
+    pinned buffers."""
+    import torch
+
+    tree = _tree()
+    for w, h in ((W, H), (97, 203), (1920, 1080)):
+        cam = synthetic.bench_camera(w, h)
+        for f in (2, 5):
+            dev = vv.render(tree, cam, f, out="torch")
+            host = vv.render(tree, cam, f)
+            torch.cuda.synchronize()
+            _eq(host.rgb, dev.rgb, f"rgb {w}x{h} f{f}")
+            _eq(host.alpha, dev.alpha, f"alpha {w}x{h} f{f}")
+            _eq(host.depth, dev.depth, f"depth {w}x{h} f{f}")
