@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "vv_abi_version",
     "vv_last_error",
     "vv_device_count",
+    "vv_debug_checks",
     "vv_basis_tables",
     "vv_tree_upload",
     "vv_tree_bind",
@@ -210,6 +211,7 @@ _SIGNATURES = {
     "vv_abi_version": (ctypes.c_int, []),
     "vv_last_error": (ctypes.c_char_p, []),
     "vv_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "vv_debug_checks": (ctypes.c_int, [_I32, _P, _P, _P, _I32]),
     "vv_basis_tables": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P]),
     "vv_tree_upload": (ctypes.c_int, [ctypes.POINTER(TreeDesc), ctypes.c_int, ctypes.POINTER(_P)]),
     "vv_tree_bind": (ctypes.c_int, [ctypes.POINTER(TreeDesc), ctypes.c_int, ctypes.POINTER(_P)]),

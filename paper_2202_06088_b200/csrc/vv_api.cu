@@ -21,8 +21,20 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/voxvid_b200.h"
 #include "vv_kernels.cuh"
+
+// NVTX ranges around the host-side phases of every entry point (slice pass,
+// node mask, chunk culling, render, band copies, scene, gather): they group
+// the launches in an Nsight Systems / ncu timeline.  Header-only NVTX v3;
+// no-ops unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+};
 
 using namespace vv;
 using namespace vvk;
@@ -277,6 +289,7 @@ int alloc_mask(const vv_tree *t, cudaStream_t st, std::shared_ptr<NodeMask> &out
 }
 
 int build_mask(const vv_tree *t, const NodeMask &m, cudaStream_t st) {
+    NvtxRange nv("vv:node_mask");
     MaskParams p;
     p.child = t->d_child;
     p.parent = t->d_parent;
@@ -479,6 +492,7 @@ void affine_from_inverse(const double *inv, double *A) {
 // Transient per-call slice from the stream-ordered pool (freed, stream
 // ordered, when the call returns).
 int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr) {
+    NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
     const size_t bytes = (size_t)t->n_leaves * rec4 * sizeof(float4);
@@ -507,6 +521,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
 // rays cannot reach.  Trees without chunk boxes slice every chunk.
 int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const vv_camera &cam, int rx0, int ry0,
                            int rx1, int ry1, SliceView &sv, Transient &tr) {
+    NvtxRange nv("vv:slice(region, culled)");
     if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr);
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
@@ -583,6 +598,19 @@ bool warp_queue(bool ordered) {
 // The child table an image render walks: the frame's node mask when one was
 // built (dark subtrees cut; bitwise the same pixels), else the tree's own.
 const int32_t *image_child(const vv_tree *t, const NodeMask *m) { return m ? m->mask : t->d_child; }
+
+// Bounds-check counter of the debug build (VV_DEBUG_CHECKS), one per device:
+// [violations, first violation code]; null in release builds.
+static unsigned *debug_counter(int device) {
+    if (!kDebugChecks) return nullptr;
+    static std::mutex mu;
+    static unsigned *ctr[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    unsigned *&c = ctr[device & 63];
+    if (!c && cudaMalloc(&c, 2 * sizeof(unsigned)) == cudaSuccess) cudaMemset(c, 0, 2 * sizeof(unsigned));
+    cudaGetLastError();
+    return c;
+}
 
 // src_stride: floats per source payload row (0: 2C + 3K; .voct rows with
 // edit channels carry 5 more, vv_voct_upload)
@@ -741,6 +769,9 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     TreeView &v = t->view;
     v.child = t->d_child;
     v.leaf_ref = t->d_leaf_ref;
+    v.n_leaves = nl;
+    v.n_internal = t->n_internal;
+    v.dbg = debug_counter(device);
     v.sig = t->d_sig;
     v.gam = t->d_gam;
     v.hh = t->d_hh;
@@ -791,6 +822,23 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
 // ====================================================================== C ABI
 extern "C" {
 
+int vv_debug_checks(int32_t device, int32_t *enabled, uint32_t *violations, uint32_t *first_code, int32_t reset) {
+    if (enabled) *enabled = kDebugChecks ? 1 : 0;
+    if (violations) *violations = 0;
+    if (first_code) *first_code = 0;
+    if (!kDebugChecks) return VV_OK;
+    DeviceGuard g(device);
+    unsigned *c = debug_counter(device);
+    if (!c) return set_error(VV_E_CUDA, "debug counter unavailable");
+    unsigned h[2] = {0, 0};
+    VV_CUDA(cudaDeviceSynchronize());
+    VV_CUDA(cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost));
+    if (violations) *violations = h[0];
+    if (first_code) *first_code = h[1];
+    if (reset) VV_CUDA(cudaMemset(c, 0, sizeof(h)));
+    return VV_OK;
+}
+
 int vv_device_count(int *count) {
     cudaError_t e = cudaGetDeviceCount(count);
     if (e != cudaSuccess) {
@@ -801,6 +849,7 @@ int vv_device_count(int *count) {
 }
 
 int vv_tree_upload(const vv_tree_desc *host, int device, vv_tree **out) {
+    NvtxRange nv("vv:tree_upload");
     return tree_alloc_common(host, device, out, true);
 }
 
@@ -847,6 +896,7 @@ int vv_tree_dark_fraction(const vv_tree *t, float *dark_frac) {
 }
 
 int vv_slice_build(const vv_tree *t, int32_t frame, void *stream, vv_slice **out) {
+    NvtxRange nv("vv:slice_build");
     if (!t || !out) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
@@ -887,6 +937,7 @@ int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *fram
 
 int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *frames, int32_t flags, void *stream,
                           vv_slice **out) {
+    NvtxRange nv("vv:slice_build_frames");
     if (!t || !frames || !out) return set_error(VV_E_INVALID, "null argument");
     if (flags & ~VV_SLICE_RENDER_ONLY) return set_error(VV_E_INVALID, "unknown slice flags 0x%x", flags);
     if (n_frames < 1 || n_frames > kMaxMulti)
@@ -1057,6 +1108,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
                               const int32_t *rect = nullptr, const int32_t *block_order = nullptr,
                               vv_camera_plan *plan = nullptr, unsigned *band_done = nullptr, int band_rows = 0,
                               bool force_queue = false) {
+    NvtxRange nv("vv:render_camera");
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
     if (rc) return rc;
@@ -1244,6 +1296,7 @@ static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_ban
 
 int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
                              const vv_camera *cam, float *device_planes, float *host_planes, void *stream) {
+    NvtxRange nv("vv:render_camera_to_host");
     if (!t || !cam || !device_planes || !host_planes) return set_error(VV_E_INVALID, "null argument");
     if (cam->width <= 0 || cam->height <= 0) return set_error(VV_E_INVALID, "bad camera size");
     DeviceGuard g(t->device);
@@ -1372,6 +1425,7 @@ int vv_camera_decode_mode(const vv_tree *t, const vv_camera *cam, const vv_rende
 int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
                            const vv_render_opts *o, const vv_camera *cam, float *const *rgb, float *const *alpha,
                            float *const *depth, void *stream) {
+    NvtxRange nv("vv:render_camera_multi");
     if (!t || !frames || !caches || !cam || !rgb || !alpha || !depth) return set_error(VV_E_INVALID, "null argument");
     if (n_frames < 2 || n_frames > kMaxMulti)
         return set_error(VV_E_UNSUPPORTED, "%d frames per walk (2..%d)", n_frames, kMaxMulti);
@@ -1598,6 +1652,7 @@ static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_
 static int render_scene_impl(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
                              const double *background, float *image, float *alpha, float *depth, void *stream,
                              bool joint) {
+    NvtxRange nv(joint ? "vv:render_scene_joint" : "vv:render_scene");
     if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
     if (!image && !alpha && !depth) return set_error(VV_E_INVALID, "no output");
     if (background && !image) return set_error(VV_E_INVALID, "background given without an image output");

@@ -47,6 +47,21 @@ struct Consts {
     float sh_pref[16];
 };
 
+// Device-side bounds checks of the debug build (the pool forbids
+// compute-sanitizer): a failed check counts a violation instead of trapping.
+#ifdef VV_DEBUG_CHECKS
+constexpr bool kDebugChecks = true;
+#else
+constexpr bool kDebugChecks = false;
+#endif
+enum : unsigned { VV_DBG_NODE = 1, VV_DBG_STACK = 2, VV_DBG_LEAF = 3, VV_DBG_QUEUE = 4, VV_DBG_CHUNK = 5 };
+__device__ __forceinline__ void debug_violation(unsigned *dbg, unsigned code) {
+    if (dbg) {
+        atomicAdd(dbg, 1u);
+        atomicCAS(dbg + 1, 0u, code);
+    }
+}
+
 // Device view of one uploaded tree.
 struct TreeView;
 __device__ __forceinline__ int64_t ref_row(const int32_t *leaf_ref, uint32_t L) {
@@ -70,6 +85,10 @@ struct TreeView {
     // reference row id wherever one leaves the device (visit lists, segment
     // lists, termination leaves); null = identity (tables that are not trees)
     const int32_t *leaf_ref;
+    int64_t n_leaves, n_internal;
+    // bounds-checked builds (VV_DEBUG_CHECKS, `make debug`): violations
+    // counted at dbg[0], first violation's code at dbg[1]; null otherwise
+    unsigned *dbg;
     double lo0, lo1, lo2, side;
     int64_t lstride;         // leaf rows per chunk plane (>= n_leaves)
     int depth, C, c4, hh4, frames, nmax;
@@ -380,6 +399,7 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
             t.need_pop = false;
         }
         vis.pop();
+        if (kDebugChecks) vis.check_node(t.ptr, (t.sp - stack_base) / stride);
         const double tin = t.tin, tout = t.tout;
         const double hh = xmul(t.h, 0.5);
         const double txm = xmul(xsub(xadd(t.xl, hh), o0), i0);
@@ -426,6 +446,7 @@ __device__ __forceinline__ int trav_next(Trav<Entry> &t, const int32_t *__restri
                 seg.put<Visitor::kPops>(n, cp[s], st[s], st[s + 1], vis.pop_count());
                 n += (keep >> s) & 1;
             }
+            if (kDebugChecks) vis.check_queue(n, Visitor::kSegSlots);
             if (n >= Visitor::kSegMin) return n;
             continue;
         }
@@ -712,6 +733,14 @@ struct Shader {
 
     __device__ __forceinline__ void pop() { ++pops; }
     __device__ __forceinline__ int pop_count() const { return pops; }
+    // bounds checks (debug build): node row, stack slots in use, queue fill
+    __device__ __forceinline__ void check_node(uint32_t ptr, uint32_t slots) const {
+        if (ptr >= (uint64_t)T.n_internal) debug_violation(T.dbg, VV_DBG_NODE);
+        if (slots > (uint32_t)stack_cap(T.depth)) debug_violation(T.dbg, VV_DBG_STACK);
+    }
+    __device__ __forceinline__ void check_queue(int n, int slots) const {
+        if (n > slots) debug_violation(T.dbg, VV_DBG_QUEUE);
+    }
 
     __device__ __forceinline__ void reset(float dx_, float dy_, float dz_) {
         dx = dx_;
@@ -760,6 +789,7 @@ struct Shader {
     }
 
     __device__ __forceinline__ bool leaf(uint32_t L, double tin, double tout, double sigma_cached) {
+        if (kDebugChecks && L >= (uint64_t)T.n_leaves) debug_violation(T.dbg, VV_DBG_LEAF);
         if (VISITS) visit[used] = ref_row(T.leaf_ref, L);
         ++used;
         constexpr int Q4 = Basis<NMAX>::Q4;
@@ -884,6 +914,13 @@ struct ShaderMulti {
     }
     __device__ __forceinline__ void pop() {}
     __device__ __forceinline__ int pop_count() const { return 0; }
+    __device__ __forceinline__ void check_node(uint32_t ptr, uint32_t slots) const {
+        if (ptr >= (uint64_t)T.n_internal) debug_violation(T.dbg, VV_DBG_NODE);
+        if (slots > (uint32_t)stack_cap(T.depth)) debug_violation(T.dbg, VV_DBG_STACK);
+    }
+    __device__ __forceinline__ void check_queue(int n, int slots) const {
+        if (n > slots) debug_violation(T.dbg, VV_DBG_QUEUE);
+    }
 
     __device__ __forceinline__ bool batch(const SegBuf &seg, int n) {
 #pragma unroll 1
@@ -912,6 +949,7 @@ struct ShaderMulti {
     // unrolling: the per-frame arrays stay in registers), sliced path
     __device__ __forceinline__ bool leaf(int k, uint32_t L, double tin, double tout, double sigma) {
         constexpr int Q4 = Basis<NMAX>::Q4;
+        if (kDebugChecks && L >= (uint64_t)T.n_leaves) debug_violation(T.dbg, VV_DBG_LEAF);
         bool edited = false;
         float4 erg = make_float4(0.f, 0.f, 0.f, 0.f);
         if (EDITS && T.edit_t != nullptr) {
@@ -971,7 +1009,11 @@ struct ShaderMulti {
 };
 
 // Traversal-only visitors (count / collect, kernels.py:313-367)
-struct CountVisitor {
+struct NoChecks {  // visitors without a tree view: no bounds checks
+    __device__ __forceinline__ void check_node(uint32_t, uint32_t) const {}
+    __device__ __forceinline__ void check_queue(int, int) const {}
+};
+struct CountVisitor : NoChecks {
     static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     int64_t count = 0;
@@ -982,7 +1024,7 @@ struct CountVisitor {
         return false;
     }
 };
-struct CollectVisitor {
+struct CollectVisitor : NoChecks {
     static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     const int32_t *leaf_ref;

@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     int k = 0;
     for (int64_t ci = c_begin; ci < c_end; ci += c_step, ++k) {
         const int64_t c = chunk_at(ci);
+        if (kDebugChecks && (c < 0 || c >= n_chunks)) debug_violation(p.T.dbg, VV_DBG_CHUNK);
         const int stg = k & 1;
         mbar_wait(&bar[stg], (uint32_t)((k >> 1) & 1));
         const int64_t base = c * kChunk;
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(kBlock) k_segments(const __grid_constant__ Seg
                                p.dirs[3 * r], p.dirs[3 * r + 1], p.dirs[3 * r + 2], p.tmin, p.tmax, ray);
     if (COLLECT) {
         const int64_t b = p.ray_start[r];
-        CollectVisitor v{p.T.leaf_ref, p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
+        CollectVisitor v{{}, p.T.leaf_ref, p.seg_leaf + b, p.seg_t0 + b, p.seg_t1 + b, 0, p.ray_start[r + 1] - b};
         if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, v);
     } else {
         CountVisitor v;
@@ -863,7 +864,7 @@ struct TermParams {
     int64_t *out_leaf;
 };
 
-struct TerminateVisitor {
+struct TerminateVisitor : NoChecks {
     static constexpr int kSegMin = VV_SEG_MIN, kSegSlots = VV_SEG_SLOTS;
     static constexpr bool kPops = false;
     const TreeView &T;

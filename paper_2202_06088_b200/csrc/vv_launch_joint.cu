@@ -30,7 +30,7 @@ constexpr int kMaxJoint = 8;  // instances per joint render
 
 // Visitor of one instance's walk: stop after every last-level node (the
 // merge needs only each walk's next segments), no counters.
-struct JointVisitor {
+struct JointVisitor : NoChecks {
     static constexpr int kSegMin = 1, kSegSlots = 4;
     static constexpr bool kPops = false;
     __device__ __forceinline__ void pop() {}

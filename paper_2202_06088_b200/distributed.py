@@ -296,6 +296,13 @@ class TileRenderer:
 
         if self.world == 1:
             return
+        torch.cuda.nvtx.range_push("vv:gather_barrier")
+        try:
+            self._barrier(torch, dist)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _barrier(self, torch, dist):
         if dist.get_backend(self.group) == "nccl":
             dist.all_reduce(self._flag, group=self.group)
         else:
@@ -374,6 +381,16 @@ class TileRenderer:
         """All-gather every rank's slab (one collective per frame)."""
         import torch.distributed as dist
 
+        import torch
+
+        torch.cuda.nvtx.range_push("vv:gather")
+        try:
+            self._gather(dist)
+        finally:
+            torch.cuda.nvtx.range_pop()
+        return self.all
+
+    def _gather(self, dist):
         if self.world == 1:
             self.all[0].copy_(self.slab)
         elif dist.get_backend(self.group) == "nccl":

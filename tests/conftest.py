@@ -27,3 +27,23 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.fail("gpu test selected but no CUDA device is visible")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(autouse=True)
+def _debug_checks_clean(request):
+    """Under the bounds-checked library (VV_LIB_PATH=.../_lib/debug/..., run by
+    tests/test_debug_checks.py with VV_DEBUG_EXPECT_CLEAN=1): every GPU test
+    must leave zero device-side bounds violations."""
+    yield
+    import os
+
+    if not os.environ.get("VV_DEBUG_EXPECT_CLEAN") or request.node.get_closest_marker("gpu") is None:
+        return
+    import ctypes
+
+    from paper_2202_06088_b200 import _native
+
+    en, n, code = ctypes.c_int32(), ctypes.c_uint32(), ctypes.c_uint32()
+    _native.check(_native.lib().vv_debug_checks(0, ctypes.byref(en), ctypes.byref(n), ctypes.byref(code), 1))
+    assert en.value == 1, "VV_DEBUG_EXPECT_CLEAN set but the loaded library has no bounds checks"
+    assert n.value == 0, f"{n.value} device-side bounds violations (first code {code.value})"
