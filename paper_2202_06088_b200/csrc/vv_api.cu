@@ -128,6 +128,7 @@ struct vv_camera_plan {
     uint32_t *cost = nullptr;        // (n_blocks) costs of the last render
     int *counter = nullptr;
     bool valid = false;              // order holds a permutation for this grid
+    int renders = 0;                 // renders since the last re-sort
     std::mutex mu;
 };
 
@@ -784,6 +785,12 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     v.lo1 = d->bbox_lo[1];
     v.lo2 = d->bbox_lo[2];
     v.side = d->side;
+    {
+        int ex = 0;
+        const double m = frexp(d->side, &ex);  // side = m 2^ex, m in [0.5, 1)
+        v.inv_side = 1.0 / d->side;
+        v.side_pow2 = (m == 0.5 && std::isnormal(v.inv_side) && std::isnormal(d->side)) ? 1 : 0;
+    }
     v.depth = d->depth;
     v.C = C;
     v.c4 = c4;
@@ -1190,7 +1197,9 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
             plan->counter = reinterpret_cast<int *>(plan->cost + n);
             plan->n_blocks = (int)grid_blocks;
             plan->blocks_x = p.blocks_x;
-            // zero once; afterwards k_plan_order re-zeroes cost and counter
+            plan->renders = 0;
+            // zero once; afterwards the kernel's last warp re-zeroes the
+            // counters and k_plan_order the costs it consumes
             VV_CUDA(cudaMemsetAsync(plan->cost, 0, n * 4 + 256, st));
         }
         p.work = plan->counter;
@@ -1207,7 +1216,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
             return set_error(VV_E_NOMEM, "work counter allocation failed");
         }
         tq.st = st;
-        VV_CUDA(cudaMemsetAsync(tq.mem, 0, sizeof(int), st));
+        VV_CUDA(cudaMemsetAsync(tq.mem, 0, 2 * sizeof(int), st));
         p.work = static_cast<int *>(tq.mem);
         p.n_work = (int)grid_blocks * kWarpsPerTile;
     }
@@ -1227,9 +1236,16 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.T.child = image_child(t, nm);
     rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
     if (rc || !plan) return rc;
-    // the next render of this plan launches in this render's cost order
-    if ((rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st))) return rc;
-    plan->valid = true;
+    // the launch order is re-sorted from the costs accumulated over the
+    // last kPlanResort renders (the first render sorts at once): a camera's
+    // block costs change slowly, and the sort (one CTA, ~15 us) is then
+    // amortised
+    constexpr int kPlanResort = 4;
+    if (!plan->valid || ++plan->renders >= kPlanResort) {
+        if ((rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st))) return rc;
+        plan->valid = true;
+        plan->renders = 0;
+    }
     return VV_OK;
 }
 

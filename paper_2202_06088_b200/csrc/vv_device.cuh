@@ -90,6 +90,11 @@ struct TreeView {
     // counted at dbg[0], first violation's code at dbg[1]; null otherwise
     unsigned *dbg;
     double lo0, lo1, lo2, side;
+    // side a power of two: v / side == v * (1 / side) exactly (both are the
+    // correctly rounded v * 2^-k), so ray setup multiplies instead of
+    // dividing -- 6 of the ray's 14 fp64 divisions
+    double inv_side;
+    int side_pow2;
     int64_t lstride;         // leaf rows per chunk plane (>= n_leaves)
     int depth, C, c4, hh4, frames, nmax;
 };
@@ -182,12 +187,13 @@ struct Ray {
 __device__ __forceinline__ bool ray_setup(const TreeView &T, double ox, double oy, double oz,
                                           double dx, double dy, double dz, double tmin,
                                           double tmax, Ray &r) {
-    double o0 = xdiv(xsub(ox, T.lo0), T.side);
-    double o1 = xdiv(xsub(oy, T.lo1), T.side);
-    double o2 = xdiv(xsub(oz, T.lo2), T.side);
-    double d0 = xdiv(dx, T.side);
-    double d1 = xdiv(dy, T.side);
-    double d2 = xdiv(dz, T.side);
+    auto scale = [&](double v) { return T.side_pow2 ? xmul(v, T.inv_side) : xdiv(v, T.side); };
+    double o0 = scale(xsub(ox, T.lo0));
+    double o1 = scale(xsub(oy, T.lo1));
+    double o2 = scale(xsub(oz, T.lo2));
+    double d0 = scale(dx);
+    double d1 = scale(dy);
+    double d2 = scale(dz);
     int mirror = 0;
     if (d0 < 0.0) { o0 = xsub(1.0, o0); d0 = -d0; mirror |= 1; }
     if (d1 < 0.0) { o1 = xsub(1.0, o1); d1 = -d1; mirror |= 2; }

@@ -110,7 +110,7 @@ struct CamParams {
     // whose warps take the rectangle's warp chunks (32 rays each) one at a
     // time from the counter *work (zeroed before the launch), in
     // block_order when given -- SM slots never idle while chunks remain
-    int *work;
+    int *work;   // [next chunk, warps finished]: the last warp out resets both
     int n_work;  // warp chunks in the rectangle
     // optional (persistent mode): per-block walk cost of this render (leaf
     // samples + 1 per ray, atomically summed per warp) -- a camera plan's
@@ -263,6 +263,12 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             }
         }
         if (p.peer) __threadfence_system();
+        // the last warp out leaves the counters zeroed for the next launch
+        // (camera plans reuse them without a memset between the kernels)
+        if (lane == 0 && atomicAdd(p.work + 1, 1) == (int)(gridDim.x * kWarpsPerTile) - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+        }
         return;
     }
     int x0, y0, lx0, ly0;

@@ -749,3 +749,30 @@ def test_render_options_through_camera_kernel(cuda):
             _exact(other.rgb, imgs[0].rgb, f"frame {f} rgb across modes")
             _exact(other.alpha, imgs[0].alpha, f"frame {f} alpha across modes")
             _exact(other.depth, imgs[0].depth, f"frame {f} depth across modes")
+
+
+@pytest.mark.parametrize("lo,side", [((-0.3, 0.2, 0.1), 1.7), ((0.5, -1.0, 0.25), 0.25), ((0.0, 0.0, 0.0), 4.0),
+                                     ((0.1, 0.1, 0.1), 3.0e-3)])
+def test_bbox_placement_vs_oracle(cuda, lo, side):
+    """Trees placed off the unit cube: ray setup divides by a general side and
+    multiplies by 1/side for a power-of-two side (exact either way) -- visit
+    lists, counts and images against the oracle."""
+    rng = np.random.default_rng(17)
+    depth, c, k = 5, 6, 14
+    res = 1 << depth
+    coords = np.argwhere(rng.random((res, res, res)) < 0.2)
+    data = rng.normal(scale=0.5, size=(len(coords), 2 * c + 3 * k)).astype(np.float32)
+    data[:, 0] = rng.uniform(0.5, 30.0, len(coords)) / side
+    tree = vv.VOctree.from_cells(coords, data, vv.make_bump_bases(4, c), 2, bbox_lo=lo, side=side, depth=depth)
+    lo_ = np.asarray(lo)
+    n = 3000
+    o = lo_ + side * rng.uniform(-1.0, 2.0, (n, 3))
+    d = lo_ + side * rng.uniform(0.2, 0.8, (n, 3)) - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ref = oracle.render_rays(tree, o, d, 2, visits=True)
+    used, start, leaf = vv.render_ray_visits(tree, o, d, 2)
+    _exact(used, ref["used"], "counts")
+    _exact(leaf, ref["visit_leaf"], "visits")
+    p, a, t = vv.render_rays(tree, o, d, 2)
+    assert np.abs(a - ref["alpha"]).max() <= 1e-12
+    assert np.abs(p - ref["premult"]).max() <= TOL

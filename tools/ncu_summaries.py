@@ -1,76 +1,65 @@
-"""Summaries for profiles/ from raw ncu outputs.
+"""Summarise ncu --set full reports into the JSON files bench.py and the
+profiles/ directory carry (dram bytes per launch = the roofline `traffic`).
 
-    python tools/ncu_summaries.py launches <launches.csv> <title>   > profiles/rNN_bench_launches_summary.txt
-    python tools/ncu_summaries.py full <report.ncu-rep>             > profiles/rNN_ncu_full_summary.json
-
-`launches`: a `--metrics gpu__time_duration.sum --csv` launch list -> per-kernel
-launches / mean / total / share.  `full`: key metrics per kernel of a
-`--set full` capture (time, DRAM bytes, hit rates, occupancy, issue, SIMT).
+    python tools/ncu_summaries.py gpurun_out/r02_ncu_cfg2.ncu-rep profiles/r02_ncu_cfg2.json [...]
 """
 import csv
 import io
 import json
-import re
 import subprocess
 import sys
-from collections import defaultdict
 
-FULL_METRICS = [
-    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
-    "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
-    "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-    "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__occupancy_limit_registers",
-    "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
-]
-
-
-def _short(name):
-    name = re.sub(r"\(.*\)$", "", name) if name.count("(") > 1 else name
-    return name[:60]
-
-
-def launches(path, title):
-    rows = list(csv.reader(open(path)))
-    hdr = None
-    for i, r in enumerate(rows):
-        if "Kernel Name" in r and "Metric Value" in r:
-            hdr = r
-            body = rows[i + 1:]
-            break
-    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = defaultdict(list)
-    for r in body:
-        if len(r) <= iv:
-            continue
-        v = float(r[iv].replace(",", ""))
-        unit = r[iu]
-        us = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
-        agg[r[ik]].append(us)
-    tot = sum(sum(v) for v in agg.values())
-    print(f"# ncu launch list of `{title}` (gpu__time_duration.sum, --clock-control none)")
-    print("# cold-cache, serialised per-launch times: compare SHARES, not absolutes\n")
-    print(f"{'kernel':60s} {'launches':>9s} {'mean_us':>10s} {'total_us':>10s} {'share':>7s}")
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{_short(k):60s} {len(v):9d} {sum(v) / len(v):10.1f} {sum(v):10.1f} {sum(v) / tot:7.3f}")
+METRICS = {
+    "gpu__time_duration.sum": "duration_us",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "smsp__inst_executed.sum": "warp_instructions",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "smsp__thread_inst_executed_per_inst_executed.ratio": "simt_threads_per_inst",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__cycles_active.avg": "sm_cycles_active_avg",
+    "gpc__cycles_elapsed.max": "cycles_elapsed",
+    "launch__registers_per_thread": "registers",
+    "launch__grid_size": "grid",
+    "launch__block_size": "block",
+    "launch__occupancy_limit_registers": "occupancy_limit_registers",
+    "sm__maximum_warps_per_active_cycle_pct": "theoretical_occupancy_pct",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "nsecond": 1e-3}
 
 
-def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics", ",".join(FULL_METRICS)],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    out = {}
-    for r in rows[2:]:
-        d = dict(zip(hdr, r))
-        key = d.get("Kernel Name", "?")
-        out[key] = {m: f"{d[m]} {units[hdr.index(m)]}".strip() for m in FULL_METRICS if m in d}
-    json.dump(out, sys.stdout, indent=1)
-    print()
+def summarise(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    res = []
+    for d in data:
+        r = {"kernel": d[hdr.index("Kernel Name")][:120]}
+        for m, k in METRICS.items():
+            if m not in hdr:
+                continue
+            i = hdr.index(m)
+            v = d[i].replace(",", "")
+            try:
+                v = float(v) * UNIT.get(units[i], 1.0)
+            except ValueError:
+                pass
+            r[k] = v
+        if "dram_read" in r and "dram_write" in r:
+            r["dram_bytes_per_launch"] = r["dram_read"] + r["dram_write"]
+        res.append(r)
+    return res[0] if len(res) == 1 else res
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
-        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else sys.argv[2])
-    else:
-        full(sys.argv[2])
+    args = sys.argv[1:]
+    for rep, dst in zip(args[::2], args[1::2]):
+        s = summarise(rep)
+        s["source"] = rep.split("/")[-1]
+        with open(dst, "w") as f:
+            json.dump(s, f, indent=1)
+        print(dst, json.dumps({k: s[k] for k in ("kernel", "duration_us", "dram_bytes_per_launch", "issue_active_pct",
+                                                 "warps_active_pct", "warp_instructions") if k in s}))
