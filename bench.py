@@ -237,6 +237,35 @@ def walk_counts(tree, o, d, f, device, masked=False):
             (("P", "node_pops"), ("V", "sample_count"), ("S", "shaded"))}
 
 
+def slice_pass_bytes(tree, f, device, chunk=64):
+    """Bytes the render-internal slice pass of frame f needs (render() runs it):
+    per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero
+    out; a 64-leaf chunk with a lit leaf also reads its w_gamma chunks (16 B
+    per nonzero B chunk) and w_hh (12 K) and writes the record (8 + 12 S_sh),
+    an all-dark chunk writes only each record's sigma pair (32 B); with node
+    masks (dark-heavy trees) 1 B of lit flags per leaf and the mask build
+    (child table read + masked table written, 2 x 32 B per internal node)."""
+    from paper_2202_06088_b200.device import replica
+
+    c, k = tree.coeff_count, tree.basis_count
+    s_sh = (tree.n_max + 1) ** 2
+    nza, nzb = _nz_chunks(tree.bases.a[f], c), _nz_chunks(tree.bases.b[f], c)
+    rep = replica(tree, device)
+    sig = tree.leaf_data[:, :c].astype(np.float64) @ tree.bases.a[f].astype(np.float64)
+    lit = (sig > 0.0)[rep.leaf_order]  # device (walk) order: the pass's chunks
+    n = len(lit)
+    pad = np.zeros(-n % chunk, dtype=bool)
+    bright = np.concatenate([lit, pad]).reshape(-1, chunk).any(axis=1)
+    rows = np.full(len(bright), chunk)
+    if len(rows):
+        rows[-1] = n - chunk * (len(rows) - 1)
+    nb, nd = int(rows[bright].sum()), int(rows[~bright].sum())
+    b = n * 16 * nza + nb * (16 * nzb + 12 * k + 8 + 12 * s_sh) + nd * 32
+    if rep.dark_fraction >= 0.25 and not getattr(tree, "has_edits", False):
+        b += n + 2 * 32 * tree.n_internal
+    return b
+
+
 def algorithmic_bytes(wl, frames, device):
     """Reference-defined bytes per step with P/V/S of the
     reference traversal, and the bytes of the path actually executed:
@@ -273,8 +302,7 @@ def algorithmic_bytes(wl, frames, device):
                 cm = walk_counts(wl.tree, o, d, f, device, masked=True) if wl.config == 3 else cnt
                 Pm, Vm, Sm = Pm + cm["P"], Vm + cm["V"], Sm + cm["S"]
             ex = 32 * Pm + 8 * Vm + 12 * s_sh * Sm + 20 * wl.pixels
-            slice_b = wl.tree.n_leaves * (16 * (_nz_chunks(wl.tree.bases.a[f], c) + _nz_chunks(wl.tree.bases.b[f], c))
-                                          + 12 * k + 8 + 12 * s_sh)
+            slice_b = slice_pass_bytes(wl.tree, f, device)
         out[f] = dict(P=P, V=V, S=S, Pm=Pm, Vm=Vm, Sm=Sm, render_bytes=ex, slice_bytes=slice_b,
                       reference_bytes=32 * P + 4 * c * V + 4 * (c + 3 * k) * S + 20 * wl.pixels)
     return out
@@ -722,8 +750,10 @@ def run_ours(args, rank, world, local_rank):
                 "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
                 "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
-                "bytes_formula": "per leaf 16 B per w_sigma / w_gamma float4 chunk the frame's A / B row does not "
-                                 "zero out + 12 K (w_hh) + 8 + 12 S_sh (record)"}
+                "bytes_formula": "per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
+                                 "per leaf of a 64-leaf chunk with a lit leaf + 16 B per nonzero w_gamma chunk + "
+                                 "12 K (w_hh) + 8 + 12 S_sh (record); of an all-dark chunk + 32 B (sigma); node "
+                                 "masks (dark-heavy trees): + 1 B/leaf + 64 B per internal node"}
             roofline["frame_achieved"] = round((rbytes + sbytes) / (total_ms / 1e3) / 1e9, 1)
 
     # CPU baseline: oracle port on one full step (rank 0, N = 1 only)

@@ -136,6 +136,10 @@ int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, in
  * T-1.  Above 0.5 the sliced camera and playback kernels walk with the long
  * segment queue (a kernel choice only: images are bitwise the same). */
 int vv_tree_dark_fraction(const vv_tree *tree, float *dark_frac);
+/* The device's leaf layout: ref_rows[g] = reference row id of device row g
+ * (n_leaves int32, host).  Leaves are stored in walk (BFS = Morton) order
+ * when the node table is a tree, else in reference order. */
+int vv_tree_leaf_order(const vv_tree *tree, int32_t *ref_rows);
 
 /* ---- per-frame slice cache -----------------------------------------------
  * Replaces build_frame_cache (render.py:170-179) -> build_slice_kernel

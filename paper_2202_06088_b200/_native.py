@@ -56,6 +56,7 @@ EXPORTED_SYMBOLS = (
     "vv_tree_free",
     "vv_tree_info",
     "vv_tree_dark_fraction",
+    "vv_tree_leaf_order",
     "vv_slice_build",
     "vv_slice_free",
     "vv_slice_export",
@@ -218,6 +219,7 @@ _SIGNATURES = {
     "vv_tree_free": (ctypes.c_int, [_P]),
     "vv_tree_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "vv_tree_dark_fraction": (ctypes.c_int, [_P, _P]),
+    "vv_tree_leaf_order": (ctypes.c_int, [_P, _P]),
     "vv_slice_build": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_P)]),
     "vv_slice_free": (ctypes.c_int, [_P]),
     "vv_slice_export": (ctypes.c_int, [_P, _P, _P, _P]),

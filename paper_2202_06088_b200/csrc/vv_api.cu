@@ -896,6 +896,16 @@ int vv_tree_info(const vv_tree *t, int64_t *n_leaves, int64_t *n_internal, int32
     return VV_OK;
 }
 
+int vv_tree_leaf_order(const vv_tree *t, int32_t *ref_rows) {
+    if (!t || !ref_rows) return set_error(VV_E_INVALID, "null argument");
+    if (t->h_perm.empty()) {
+        for (int64_t g = 0; g < t->n_leaves; ++g) ref_rows[g] = (int32_t)g;
+    } else {
+        memcpy(ref_rows, t->h_perm.data(), (size_t)t->n_leaves * sizeof(int32_t));
+    }
+    return VV_OK;
+}
+
 int vv_tree_dark_fraction(const vv_tree *t, float *dark_frac) {
     if (!t || !dark_frac) return set_error(VV_E_INVALID, "null argument");
     *dark_frac = t->dark_frac;

@@ -167,6 +167,13 @@ class DeviceTree:
         return self
 
     @property
+    def leaf_order(self) -> np.ndarray:
+        """Reference row id of every device leaf row (the walk-order layout)."""
+        out = np.empty(self.n_leaves, dtype=np.int32)
+        _native.check(_native.lib().vv_tree_leaf_order(self.handle, out.ctypes.data))
+        return out
+
+    @property
     def dark_fraction(self) -> float:
         """Share of leaves with sigma 0 over frames 0, T/2, T-1 (measured at
         upload; above 0.5 the sliced kernels walk with the long segment queue)."""
