@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -67,6 +68,7 @@ struct vv_tree {
     // back (null: identity); the host copy permutes edit uploads
     int32_t *d_leaf_ref, *d_dev_row;
     std::vector<int32_t> h_perm;
+    uint64_t serial;  // unique per upload (caches keyed on a tree never see a reused address)
 };
 
 // Per-frame (or per frame group) node mask: the slice pass's lit bits, the
@@ -129,6 +131,14 @@ struct vv_camera_plan {
     int *counter = nullptr;
     bool valid = false;              // order holds a permutation for this grid
     int renders = 0;                 // renders since the last re-sort
+    // coverage of the last (tree, camera) rendered through the plan: built
+    // once per view, reused by every frame of it
+    void *cov_mem = nullptr;
+    size_t cov_cap = 0;
+    uint64_t cov_tree = 0;  // serial of the tree the coverage belongs to
+    vv_camera cov_cam;
+    bool cov_valid = false;
+    CoverView cov{};
     std::mutex mu;
 };
 
@@ -580,6 +590,71 @@ int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const v
     return tr.nmask ? build_mask(t, *tr.nmask, st) : VV_OK;
 }
 
+// Coverage of the tree's leaf chunks for one camera (k_coverage): pixels
+// outside it skip their walk (exactly the empty pixel).  VV_COVERAGE=0
+// turns it off (A/B runs).  A = instance affine (3x4 rows) or null.
+bool coverage_wanted(const vv_tree *t) {
+    if (!t->d_box || t->n_box == 0) return false;
+    const char *e = getenv("VV_COVERAGE");
+    return !(e && e[0] == '0');
+}
+
+static size_t coverage_bytes(int width, int height) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int words = (width + 31) / 32, cw = (width + 15) / 16, ch = (height + 15) / 16;
+    return 256 + al((size_t)cw * ch) + (size_t)height * words * 4;
+}
+
+// mem: coverage_bytes(width, height) of device memory
+int build_coverage_into(const vv_tree *t, const CamView &cam, int width, int height, const double *A,
+                        cudaStream_t st, char *m, CoverView &cv) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int words = (width + 31) / 32, cw = (width + 15) / 16, ch = (height + 15) / 16;
+    const size_t b_hdr = 256, b_coarse = al((size_t)cw * ch), b_fine = (size_t)height * words * 4;
+    VV_CUDA(cudaMemsetAsync(m, 0, b_hdr + b_coarse + b_fine, st));
+    CoverParams p;
+    memset(&p, 0, sizeof(p));
+    p.box = t->d_box;
+    p.n_box = t->n_box;
+    p.lo0 = t->view.lo0;
+    p.lo1 = t->view.lo1;
+    p.lo2 = t->view.lo2;
+    p.cell = t->view.side / (double)(1ll << t->depth);
+    p.cam = cam;
+    if (A) {
+        memcpy(p.A, A, sizeof(p.A));
+        p.use_A = 1;
+    }
+    p.width = width;
+    p.height = height;
+    p.words = words;
+    p.cw = cw;
+    p.all = reinterpret_cast<int *>(m);
+    p.coarse = reinterpret_cast<uint8_t *>(m + b_hdr);
+    p.fine = reinterpret_cast<uint32_t *>(m + b_hdr + b_coarse);
+    int rc = launch_coverage(p, st);
+    if (rc) return rc;
+    cv.fine = p.fine;
+    cv.coarse = p.coarse;
+    cv.all = p.all;
+    cv.words = words;
+    cv.cw = cw;
+    return VV_OK;
+}
+
+int build_coverage(const vv_tree *t, const CamView &cam, int width, int height, const double *A, cudaStream_t st,
+                   Transient &tr, CoverView &cv) {
+    const size_t bytes = coverage_bytes(width, height);
+    pool_setup(t->device);
+    if (cudaMallocAsync(&tr.mem, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        tr.mem = nullptr;
+        return set_error(VV_E_NOMEM, "coverage allocation failed");
+    }
+    tr.st = st;
+    return build_coverage_into(t, cam, width, height, A, st, static_cast<char *>(tr.mem), cv);
+}
+
 // Long segment queue for mostly dark trees (the cfg3 motion tree).  Measured
 // at cfg3 with node masks: 0.493 vs 0.502 ms per frame (without masks 2.02
 // vs 2.18); VV_LONG_QUEUE=0 / 1 forces the choice (A/B runs).
@@ -631,6 +706,8 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
         return set_error(VV_E_INVALID, "edit_rgb and edit_t must both be set or both be NULL");
     DeviceGuard g(device);
     vv_tree *t = new vv_tree();  // value-initialised: every pointer and count zero
+    static std::atomic<uint64_t> next_serial{1};
+    t->serial = next_serial++;
     t->device = device;
     t->n_leaves = d->n_leaves;
     t->n_internal = d->n_internal;
@@ -1230,6 +1307,35 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         p.work = static_cast<int *>(tq.mem);
         p.n_work = (int)grid_blocks * kWarpsPerTile;
     }
+    // coverage (planned renders: built once per tree and camera, ~30 us,
+    // then reused by every frame of that view -- per call it costs about
+    // what it saves, measured on cfg2 / cfg3)
+    if (plan && coverage_wanted(t)) {
+        const bool same =
+            plan->cov_valid && plan->cov_tree == t->serial && memcmp(&plan->cov_cam, cam, sizeof(*cam)) == 0;
+        if (!same) {
+            const size_t bytes = coverage_bytes(cam->width, cam->height);
+            if (plan->cov_cap < bytes) {
+                cudaFree(plan->cov_mem);
+                plan->cov_mem = nullptr;
+                plan->cov_cap = 0;
+                if (cudaMalloc(&plan->cov_mem, bytes) != cudaSuccess) {
+                    cudaGetLastError();
+                    plan->cov_mem = nullptr;
+                    return set_error(VV_E_NOMEM, "coverage allocation failed");
+                }
+                plan->cov_cap = bytes;
+            }
+            plan->cov_valid = false;
+            int r = build_coverage_into(t, p.cam, cam->width, cam->height, nullptr, st,
+                                        static_cast<char *>(plan->cov_mem), plan->cov);
+            if (r) return r;
+            plan->cov_tree = t->serial;
+            plan->cov_cam = *cam;
+            plan->cov_valid = true;
+        }
+        p.cov = plan->cov;
+    }
     const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
     // a region render's slice covers only the chunks its pixels can reach,
     // so it is decided on the whole frame's footprint
@@ -1398,6 +1504,7 @@ int vv_camera_plan_free(vv_camera_plan *plan) {
     DeviceGuard g(plan->device);
     cudaDeviceSynchronize();  // a render may still read the order
     cudaFree(plan->order);
+    cudaFree(plan->cov_mem);
     delete plan;
     return VV_OK;
 }

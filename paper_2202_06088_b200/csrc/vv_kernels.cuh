@@ -83,6 +83,26 @@ __global__ void __launch_bounds__(kBlock, VV_CAM_MINB) k_render_rays(const __gri
     if (p.shaded) p.shaded[r] = sh.shaded;
 }
 
+// ------------------------------------------------------------------ coverage
+// Pixels whose ray can reach a leaf of a tree: the union of the projected
+// rectangles of its 64-leaf chunk boxes (k_coverage, vv_launch_mask.cu; one
+// pixel of margin; a box reaching behind the eye covers everything).  A ray
+// outside it meets no leaf cell, so its result is exactly the empty pixel
+// (premult 0, alpha 0, tbar 0 -> rgb 0, alpha 0, depth far_plane) and the
+// kernels skip its setup and walk; a layer of such a ray enters Algorithm 1
+// with exactly those values.
+struct CoverView {
+    const uint32_t *fine;   // (height, words): bit per pixel, small boxes; null: everything covered
+    const uint8_t *coarse;  // (ceil(h/16), cw): 16x16-pixel tiles of large boxes
+    const int *all;         // a box reached behind the eye: everything covered
+    int words, cw;
+};
+__device__ __forceinline__ bool covered(const CoverView &c, int ix, int iy) {
+    if (!c.fine) return true;
+    if ((__ldg(c.fine + (size_t)iy * c.words + (ix >> 5)) >> (ix & 31)) & 1u) return true;
+    return __ldg(c.coarse + (size_t)(iy >> 4) * c.cw + (ix >> 4)) != 0 || __ldg(c.all) != 0;
+}
+
 // ------------------------------------------------------------------ camera
 struct CamParams {
     TreeView T;
@@ -122,6 +142,7 @@ struct CamParams {
     // band to the host while the rest of the frame renders
     unsigned *band_done;
     int band_rows;
+    CoverView cov;  // image / region mode: pixels that can reach the tree
     // optional per-pixel leaf-sample counts (render_kernel's consumed
     // segments, up to and including the early-stop one; image mode): written
     // by the production instantiation itself, so its walk is checked
@@ -212,7 +233,9 @@ __device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &
     const bool inside = ix < p.rx1 && iy < p.ry1;
     float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
     int cost = 0;
-    if (inside) {
+    if (inside && !covered(p.cov, ix, iy)) {  // meets no leaf cell: the empty pixel
+        if (p.used) p.used[slot] = 0;
+    } else if (inside) {
         double dx, dy, dz;
         camera_ray(p.cam, ix, iy, dx, dy, dz);
         Ray ray;
@@ -292,10 +315,10 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
         }
         pdl_trigger();
-        pdl_wait();  // the frame slice (and node mask) is complete; earlier writers of the outputs are done
+        pdl_wait();  // the frame slice (and node mask, coverage) is complete; earlier writers of the outputs are done
         if (inside) {
             Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
-            if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+            if (hit && (p.tile || covered(p.cov, ix, iy))) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
             if (p.used) p.used[slot] = sh.used;
@@ -1042,6 +1065,21 @@ struct CullParams {
     int32_t *list, *count;
 };
 int launch_chunk_cull(const CullParams &p, cudaStream_t st);
+// coverage of one tree's leaf-chunk boxes as seen by a camera (optionally
+// through an instance affine A, 3x4 rows): the CoverView bitmaps
+struct CoverParams {
+    const int4 *box;
+    int64_t n_box;
+    double lo0, lo1, lo2, cell;
+    CamView cam;
+    double A[12];
+    int use_A;
+    int width, height, words, cw;
+    uint32_t *fine;
+    uint8_t *coarse;
+    int *all;
+};
+int launch_coverage(const CoverParams &p, cudaStream_t st);
 // camera plan (vv_launch_mask.cu): launch order of n blocks, costliest first
 // (counting sort on log-scale cost buckets)
 int launch_plan_order(uint32_t *cost, int n, int32_t *order, int *counter, cudaStream_t st);

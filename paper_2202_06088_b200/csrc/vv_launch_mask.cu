@@ -223,3 +223,82 @@ int launch_plan_order(uint32_t *cost, int n, int32_t *order, int *counter, cudaS
 }
 
 }  // namespace vvk
+
+// ------------------------------------------------------------ coverage
+// k_coverage: each 64-leaf chunk box -> its 8 corners (through the instance
+// affine A when given) -> the camera frame -> the pixel rectangle of their
+// projection, widened by one pixel; small rectangles set their pixels'
+// bits, large ones (> 1024 pixels) their 16x16 tiles; a corner not in front
+// of the eye sets `all`.  A ray through a pixel centre outside every
+// rectangle meets no leaf cell (the cells lie in the boxes, a box's
+// projection in its corners' rectangle).
+namespace vvk {
+
+__global__ void __launch_bounds__(256) k_coverage(const __grid_constant__ CoverParams p) {
+    pdl_trigger();
+    pdl_wait();  // the bitmaps were zeroed, earlier readers are done
+    const CamView &c = p.cam;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n_box; i += stride) {
+        const int4 lo = __ldg(p.box + 2 * i), hi = __ldg(p.box + 2 * i + 1);
+        if (lo.x > hi.x) continue;
+        double u0 = 1e300, u1 = -1e300, v0 = 1e300, v1 = -1e300;
+        bool front = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            double px = p.lo0 + p.cell * (double)((k & 1) ? hi.x + 1 : lo.x);
+            double py = p.lo1 + p.cell * (double)((k & 2) ? hi.y + 1 : lo.y);
+            double pz = p.lo2 + p.cell * (double)((k & 4) ? hi.z + 1 : lo.z);
+            if (p.use_A) {
+                const double *A = p.A;
+                const double qx = A[0] * px + A[1] * py + A[2] * pz + A[3];
+                const double qy = A[4] * px + A[5] * py + A[6] * pz + A[7];
+                const double qz = A[8] * px + A[9] * py + A[10] * pz + A[11];
+                px = qx;
+                py = qy;
+                pz = qz;
+            }
+            const double dx = px - c.ox, dy = py - c.oy, dz = pz - c.oz;
+            const double cx = c.r00 * dx + c.r10 * dy + c.r20 * dz;
+            const double cy = c.r01 * dx + c.r11 * dy + c.r21 * dz;
+            const double cz = c.r02 * dx + c.r12 * dy + c.r22 * dz;
+            front &= cz > 1e-9;
+            const double iz = 1.0 / cz;
+            const double u = c.fx * cx * iz + c.cx, v = c.fy * cy * iz + c.cy;
+            u0 = fmin(u0, u);
+            u1 = fmax(u1, u);
+            v0 = fmin(v0, v);
+            v1 = fmax(v1, v);
+        }
+        if (!front) {
+            *p.all = 1;
+            continue;
+        }
+        // pixel centres ix + 0.5 in [u0 - 1, u1 + 1]
+        const int x0 = (int)fmax(0.0, ceil(fmax(u0, -1e9) - 1.5));
+        const int x1 = (int)fmin((double)(p.width - 1), floor(fmin(u1, 1e9) + 0.5));
+        const int y0 = (int)fmax(0.0, ceil(fmax(v0, -1e9) - 1.5));
+        const int y1 = (int)fmin((double)(p.height - 1), floor(fmin(v1, 1e9) + 0.5));
+        if (x0 > x1 || y0 > y1) continue;
+        if ((int64_t)(x1 - x0 + 1) * (y1 - y0 + 1) > 1024) {
+            for (int ty = y0 >> 4; ty <= (y1 >> 4); ++ty)
+                for (int tx = x0 >> 4; tx <= (x1 >> 4); ++tx) p.coarse[(size_t)ty * p.cw + tx] = 1;
+            continue;
+        }
+        for (int y = y0; y <= y1; ++y)
+            for (int w = x0 >> 5; w <= (x1 >> 5); ++w) {
+                const int a = max(x0, 32 * w) - 32 * w, b = min(x1, 32 * w + 31) - 32 * w;  // bits a..b
+                const uint32_t m = (b == 31 ? 0xffffffffu : ((1u << (b + 1)) - 1u)) & ~((1u << a) - 1u);
+                atomicOr(p.fine + (size_t)y * p.words + w, m);
+            }
+    }
+}
+
+int launch_coverage(const CoverParams &p, cudaStream_t st) {
+    if (p.n_box == 0) return VV_OK;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.n_box + 255) / 256, 148 * 8));
+    launch_pdl(k_coverage, dim3(blocks), dim3(256), 0, st, p);
+    return check_launch("coverage");
+}
+
+}  // namespace vvk

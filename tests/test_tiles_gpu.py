@@ -371,3 +371,27 @@ def test_render_to_host_banded_copies(cuda):
             _eq(host.rgb, dev.rgb, f"rgb {w}x{h} f{f}")
             _eq(host.alpha, dev.alpha, f"alpha {w}x{h} f{f}")
             _eq(host.depth, dev.depth, f"depth {w}x{h} f{f}")
+
+
+def test_camera_plan_coverage_reuse_and_invalidation(cuda):
+    """A plan caches the chunk-box coverage of its (tree, camera): renders of
+    the same view reuse it, a new camera or a new tree (even one allocated
+    where a freed tree lived) rebuilds it -- bitwise render() every time."""
+    import torch
+
+    plan = vv.CameraPlan(cuda)
+    cams = [synthetic.bench_camera(W, H),
+            vv.Camera.look_at([-0.9, 1.6, 1.2], [0.5, 0.5, 0.5], width=W, height=H, focal=1.1 * W)]
+    for it in range(3):
+        tree = synthetic.shell_tree(depth=6, n_max=1, frames=6, seed=it)  # replaces the previous tree
+        for cam in cams + cams[:1]:
+            for f in (0, 4):
+                out = [torch.empty((H, W, 3), device=cuda), torch.empty((H, W), device=cuda),
+                       torch.empty((H, W), device=cuda)]
+                vv.render_into(tree, cam, f, *out, plan=plan)
+                ref = vv.render(tree, cam, f, out="torch")
+                torch.cuda.synchronize()
+                _eq(out[0], ref.rgb, f"rgb it{it} f{f}")
+                _eq(out[1], ref.alpha, f"alpha it{it} f{f}")
+                _eq(out[2], ref.depth, f"depth it{it} f{f}")
+        del tree
