@@ -69,6 +69,7 @@ struct vv_tree {
     int32_t *d_leaf_ref, *d_dev_row;
     std::vector<int32_t> h_perm;
     uint64_t serial;  // unique per upload (caches keyed on a tree never see a reused address)
+    double occ_lo[3], occ_hi[3];  // world box of the occupied leaf cells (empty: lo > hi)
 };
 
 // Per-frame (or per frame group) node mask: the slice pass's lit bits, the
@@ -688,6 +689,68 @@ static unsigned *debug_counter(int device) {
     return c;
 }
 
+// The occupied cells' world box (union of the chunk boxes); the whole cube
+// when the table has no walk-order layout.
+static void set_occupied_box(vv_tree *t, const TreeLayout &lay) {
+    int64_t mn[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, mx[3] = {INT64_MIN, INT64_MIN, INT64_MIN};
+    for (size_t k = 0; k + 1 < lay.box.size(); k += 2) {
+        const int4 lo = lay.box[k], hi = lay.box[k + 1];
+        if (lo.x > hi.x) continue;
+        mn[0] = std::min<int64_t>(mn[0], lo.x); mn[1] = std::min<int64_t>(mn[1], lo.y); mn[2] = std::min<int64_t>(mn[2], lo.z);
+        mx[0] = std::max<int64_t>(mx[0], hi.x); mx[1] = std::max<int64_t>(mx[1], hi.y); mx[2] = std::max<int64_t>(mx[2], hi.z);
+    }
+    const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
+    if (!lay.tree) {
+        for (int a = 0; a < 3; ++a) {
+            t->occ_lo[a] = lo[a];
+            t->occ_hi[a] = lo[a] + t->view.side;
+        }
+        return;
+    }
+    t->occ_lo[0] = 1.0;  // no occupied cell: empty box
+    t->occ_hi[0] = 0.0;
+    if (mn[0] > mx[0]) return;
+    const double cell = t->view.side / (double)(1ll << t->depth);
+    for (int a = 0; a < 3; ++a) {
+        t->occ_lo[a] = lo[a] + cell * (double)mn[a];
+        t->occ_hi[a] = lo[a] + cell * (double)(mx[a] + 1);
+    }
+}
+
+// Inclusive pixel rectangle {x0, y0, x1, y1} of the pixels whose ray (from
+// `cam`, or from the scene camera through the instance affine A) can reach
+// the tree's occupied box: its 8 corners projected, one pixel of margin; the
+// whole image when a corner is not in front of the eye; x0 > x1 when empty.
+static void occupied_rect(const vv_tree *t, const CamView &c, const double *A, int w, int h, int r[4]) {
+    r[0] = 0; r[1] = 0; r[2] = w - 1; r[3] = h - 1;
+    if (t->occ_lo[0] > t->occ_hi[0]) {
+        r[0] = 1; r[2] = 0;  // nothing to reach
+        return;
+    }
+    double u0 = 1e300, u1 = -1e300, v0 = 1e300, v1 = -1e300;
+    for (int k = 0; k < 8; ++k) {
+        double p[3] = {(k & 1) ? t->occ_hi[0] : t->occ_lo[0], (k & 2) ? t->occ_hi[1] : t->occ_lo[1],
+                       (k & 4) ? t->occ_hi[2] : t->occ_lo[2]};
+        if (A) {
+            double q[3];
+            for (int i = 0; i < 3; ++i) q[i] = A[4 * i] * p[0] + A[4 * i + 1] * p[1] + A[4 * i + 2] * p[2] + A[4 * i + 3];
+            p[0] = q[0]; p[1] = q[1]; p[2] = q[2];
+        }
+        const double dx = p[0] - c.ox, dy = p[1] - c.oy, dz = p[2] - c.oz;
+        const double cx = c.r00 * dx + c.r10 * dy + c.r20 * dz;
+        const double cy = c.r01 * dx + c.r11 * dy + c.r21 * dz;
+        const double cz = c.r02 * dx + c.r12 * dy + c.r22 * dz;
+        if (!(cz > 1e-9)) return;  // whole image
+        const double u = c.fx * cx / cz + c.cx, v = c.fy * cy / cz + c.cy;
+        u0 = std::min(u0, u); u1 = std::max(u1, u); v0 = std::min(v0, v); v1 = std::max(v1, v);
+    }
+    auto clampd = [](double x) { return std::max(-1e9, std::min(1e9, x)); };
+    r[0] = (int)std::max(0.0, std::ceil(clampd(u0) - 1.5));
+    r[2] = (int)std::min((double)(w - 1), std::floor(clampd(u1) + 0.5));
+    r[1] = (int)std::max(0.0, std::ceil(clampd(v0) - 1.5));
+    r[3] = (int)std::min((double)(h - 1), std::floor(clampd(v1) + 0.5));
+}
+
 // src_stride: floats per source payload row (0: 2C + 3K; .voct rows with
 // edit channels carry 5 more, vv_voct_upload)
 int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool host_src, int64_t src_stride = 0) {
@@ -850,6 +913,7 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     v.n_leaves = nl;
     v.n_internal = t->n_internal;
     v.dbg = debug_counter(device);
+
     v.sig = t->d_sig;
     v.gam = t->d_gam;
     v.hh = t->d_hh;
@@ -874,6 +938,7 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
     v.hh4 = hh4;
     v.frames = d->frames;
     v.nmax = d->n_max;
+    set_occupied_box(t, lay);
     // dark fraction over frames 0, T/2, T-1 (picks the camera kernel's
     // queue threshold; the images are bitwise the same either way)
     if (nl > 0) {
@@ -1257,6 +1322,9 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         p.blocks_x = (p.rx1 - p.rx0 + kTW - 1) / kTW;
         grid_blocks = (unsigned)p.blocks_x * (unsigned)((p.ry1 - p.ry0 + kTH - 1) / kTH);
         p.block_order = block_order;
+        int rr[4];
+        occupied_rect(t, p.cam, nullptr, cam->width, cam->height, rr);
+        p.cx0 = rr[0]; p.cy0 = rr[1]; p.cx1 = rr[2]; p.cy1 = rr[3];
         p.band_done = band_done;
         p.band_rows = band_rows;
     }
@@ -1740,6 +1808,15 @@ static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_
         memcpy(c2.c2w, inst[i].pose, sizeof(c2.c2w));
         v.cam = make_cam(c2);
         for (int k = 0; k < 12; ++k) v.inv[k] = inst[i].inv[k];
+        int rr[4];
+        if (v.mode == 0) {  // rigid: the pulled-back camera shoots the rays in tree space
+            occupied_rect(inst[i].tree, v.cam, nullptr, cam->width, cam->height, rr);
+        } else {  // general: the scene camera sees the tree through its affine
+            double A[12];
+            affine_from_inverse(inst[i].inv, A);
+            occupied_rect(inst[i].tree, p.cam, A, cam->width, cam->height, rr);
+        }
+        v.rx0 = rr[0]; v.ry0 = rr[1]; v.rx1 = rr[2]; v.ry1 = rr[3];
     }
     p.early_stop = opts.early_stop;
     p.edit_weight = opts.edit_weight;

@@ -143,6 +143,7 @@ struct CamParams {
     unsigned *band_done;
     int band_rows;
     CoverView cov;  // image / region mode: pixels that can reach the tree
+    int cx0, cy0, cx1, cy1;  // image / region mode: pixel rectangle of the tree's occupied box (inclusive)
     // optional per-pixel leaf-sample counts (render_kernel's consumed
     // segments, up to and including the early-stop one; image mode): written
     // by the production instantiation itself, so its walk is checked
@@ -233,7 +234,8 @@ __device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &
     const bool inside = ix < p.rx1 && iy < p.ry1;
     float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
     int cost = 0;
-    if (inside && !covered(p.cov, ix, iy)) {  // meets no leaf cell: the empty pixel
+    if (inside && (ix < p.cx0 || ix > p.cx1 || iy < p.cy0 || iy > p.cy1 || !covered(p.cov, ix, iy))) {
+        // meets no leaf cell: the empty pixel
         if (p.used) p.used[slot] = 0;
     } else if (inside) {
         double dx, dy, dz;
@@ -318,7 +320,8 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         pdl_wait();  // the frame slice (and node mask, coverage) is complete; earlier writers of the outputs are done
         if (inside) {
             Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
-            if (hit && (p.tile || covered(p.cov, ix, iy))) traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+            if (hit && (p.tile || (ix >= p.cx0 && ix <= p.cx1 && iy >= p.cy0 && iy <= p.cy1 && covered(p.cov, ix, iy))))
+                traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
             if (p.used) p.used[slot] = sh.used;
@@ -342,6 +345,10 @@ struct InstView {
     CamView cam;      // mode 0: pulled-back pose
     double inv[12];   // mode 1: rows of inv(affine)[:3, :4]
     int frame, mode;
+    // pixels [rx0, rx1] x [ry0, ry1] (inclusive) whose ray can reach the
+    // instance's occupied leaf cells (its tight box projected, one pixel of
+    // margin): outside, the instance's layer is exactly (0, alpha 0, far)
+    int rx0, ry0, rx1, ry1;
 };
 
 struct SceneParams {
@@ -394,9 +401,13 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
     }
     for (int i = 0; i < p.n_inst; ++i) {
         const InstView &v = p.inst[i];
-        double ox, oy, oz, dx, dy, dz, scale = 1.0;
+        double ox, oy, oz, dx = 0.0, dy = 0.0, dz = 1.0, scale = 1.0;
         bool scaled = false;
-        if (v.mode == 0) {
+        const bool reach = ix >= v.rx0 && ix <= v.rx1 && iy >= v.ry0 && iy <= v.ry1;
+        if (!reach) {  // no leaf cell on this ray: the empty layer (no setup, no walk)
+            ox = oy = oz = 0.0;
+            scaled = v.mode != 0;
+        } else if (v.mode == 0) {
             camera_ray(v.cam, ix, iy, dx, dy, dz);
             ox = v.cam.ox;
             oy = v.cam.oy;
@@ -420,7 +431,7 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
         FrameCtx F{sA[i], sB[i], v.frame, p.early_stop, p.edit_weight, sM[i][0], sM[i][1]};
         Shader<NMAX, CACHED, EDITS, false> sh(v.T, v.S, F, p.K, (float)dx, (float)dy, (float)dz);
         Ray ray;
-        if (ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
+        if (reach && ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
             traverse<Entry>(v.T.child, v.T.depth, ray, smem_raw, sh);
         // finalize_layer in float64
         const double al = sh.aacc;
