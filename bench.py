@@ -442,6 +442,7 @@ class Stepper:
         # camera kernel's persistent warps take each frame's blocks in the
         # previous frame's measured cost order; images bitwise unchanged
         self.plans = [vv.CameraPlan(dev) for _ in wl.cams]
+        self.scene_plan = vv.CameraPlan(dev)  # what render_scene() keeps per stream
         self.descs = {}
         self.launches = 0
 
@@ -468,10 +469,10 @@ class Stepper:
             cd = wl.cams[0].desc()
             if mid is not None:
                 mid.record(stream)
-            _native.check(_native.lib().vv_render_scene(descs, len(descs), ctypes.byref(oc), ctypes.byref(cd), bg,
-                                                        self.outs[0][0].data_ptr(), None, None,
-                                                        stream_ptr(self.dev)))
-            self.launches += 1
+            _native.check(_native.lib().vv_render_scene_planned(
+                descs, len(descs), ctypes.byref(oc), ctypes.byref(cd), bg, self.outs[0][0].data_ptr(), None, None,
+                self.scene_plan._handle, stream_ptr(self.dev)))
+            self.launches += 2  # scene kernel + plan order (every 4th)
             return
         # exactly what render() does: the render-internal slice pass (colour of
         # all-dark leaf chunks skipped; node masks for dark-heavy trees) ...

@@ -335,6 +335,14 @@ int vv_render_scene(const vv_instance *instances, int32_t n_instances,
 int vv_render_scene_joint(const vv_instance *inst, int32_t n_inst, const vv_render_opts *opts,
                           const vv_camera *cam, const double *background, float *image, float *alpha,
                           float *depth, void *stream);
+/* vv_render_scene scheduled by a plan (vv_camera_plan_create): persistent
+ * warps over the frame's 16x2-pixel chunks in the previous frames' cost
+ * order (a scene of <= 16 instances of one n_max; larger scenes chain
+ * launches without one).  Bitwise vv_render_scene.  Use a plan of its own
+ * (not one shared with camera renders). */
+int vv_render_scene_planned(const vv_instance *inst, int32_t n_inst, const vv_render_opts *opts,
+                            const vv_camera *cam, const double *background, float *image, float *alpha,
+                            float *depth, vv_camera_plan *plan, void *stream);
 /* Leaf-decode mode vv_render_scene picks for each instance (0: per sample
  * inside the scene kernel -- every instance 0 and no edits runs the lean
  * instantiation --, 1: a per-frame slice pass first). */

@@ -81,6 +81,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_scene",
     "vv_scene_decode_modes",
     "vv_render_scene_joint",
+    "vv_render_scene_planned",
     "vv_render_camera_multi",
     "vv_slice_build_multi",
     "vv_slice_build_frames",
@@ -283,6 +284,11 @@ _SIGNATURES = {
         ctypes.c_int,
         [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),
          _P, _P, _P, _P, _P],
+    ),
+    "vv_render_scene_planned": (
+        ctypes.c_int,
+        [ctypes.POINTER(InstanceDesc), _I32, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc),
+         _P, _P, _P, _P, _P, _P],
     ),
     "vv_scene_decode_modes": (
         ctypes.c_int, [ctypes.POINTER(InstanceDesc), _I32, _P, ctypes.POINTER(CameraDesc), _P]),

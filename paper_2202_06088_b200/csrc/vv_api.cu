@@ -664,6 +664,46 @@ bool long_queue(const vv_tree *t, const NodeMask *) {
     return t->dark_frac > 0.5f;
 }
 
+// Plan buffers for a grid of n_blocks blocks (blocks_x per row): order,
+// costs and the two chunk counters, reallocated when the grid changes.
+int plan_prepare(vv_camera_plan *plan, int n_blocks, int blocks_x, cudaStream_t st) {
+    if (plan->n_blocks == n_blocks && plan->blocks_x == blocks_x) return VV_OK;
+    cudaFree(plan->order);
+    plan->order = nullptr;
+    plan->valid = false;
+    const size_t n = (size_t)n_blocks;
+    if (cudaMalloc(&plan->order, n * 8 + 256) != cudaSuccess) {
+        cudaGetLastError();
+        plan->order = nullptr;
+        plan->n_blocks = 0;
+        return set_error(VV_E_NOMEM, "camera plan allocation failed");
+    }
+    plan->cost = reinterpret_cast<uint32_t *>(plan->order + n);
+    plan->counter = reinterpret_cast<int *>(plan->cost + n);
+    plan->n_blocks = n_blocks;
+    plan->blocks_x = blocks_x;
+    plan->renders = 0;
+    // zero once; afterwards the kernel's last warp re-zeroes the counters
+    // and k_plan_order the costs it consumes
+    VV_CUDA(cudaMemsetAsync(plan->cost, 0, n * 4 + 256, st));
+    return VV_OK;
+}
+
+// After a planned launch: the launch order is re-sorted from the costs
+// accumulated over the last kPlanResort renders (the first render sorts at
+// once) -- a view's block costs change slowly, and the sort (one CTA, ~15
+// us) is amortised.
+int plan_finish(vv_camera_plan *plan, cudaStream_t st) {
+    constexpr int kPlanResort = 4;
+    if (!plan->valid || ++plan->renders >= kPlanResort) {
+        int rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st);
+        if (rc) return rc;
+        plan->valid = true;
+        plan->renders = 0;
+    }
+    return VV_OK;
+}
+
 // Persistent warp-chunk queue for the camera kernel (k_render_camera, p.work):
 // VV_CAM_QUEUE=0 / 1 forces it off / on; by default only region renders
 // with a launch order use it.
@@ -1337,26 +1377,8 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         if (tile) return set_error(VV_E_INVALID, "camera plans render images or regions, not packed tiles");
         if (plan->device != t->device) return set_error(VV_E_INVALID, "camera plan belongs to another device");
         plan_lock = std::unique_lock<std::mutex>(plan->mu);
-        if (plan->n_blocks != (int)grid_blocks || plan->blocks_x != p.blocks_x) {  // new grid: new buffers
-            cudaFree(plan->order);
-            plan->order = nullptr;
-            plan->valid = false;
-            const size_t n = grid_blocks;
-            if (cudaMalloc(&plan->order, n * 8 + 256) != cudaSuccess) {
-                cudaGetLastError();
-                plan->order = nullptr;
-                plan->n_blocks = 0;
-                return set_error(VV_E_NOMEM, "camera plan allocation failed");
-            }
-            plan->cost = reinterpret_cast<uint32_t *>(plan->order + n);
-            plan->counter = reinterpret_cast<int *>(plan->cost + n);
-            plan->n_blocks = (int)grid_blocks;
-            plan->blocks_x = p.blocks_x;
-            plan->renders = 0;
-            // zero once; afterwards the kernel's last warp re-zeroes the
-            // counters and k_plan_order the costs it consumes
-            VV_CUDA(cudaMemsetAsync(plan->cost, 0, n * 4 + 256, st));
-        }
+        int prc = plan_prepare(plan, (int)grid_blocks, p.blocks_x, st);
+        if (prc) return prc;
         p.work = plan->counter;
         p.n_work = (int)grid_blocks * kWarpsPerTile;
         p.block_order = plan->valid ? plan->order : nullptr;
@@ -1420,17 +1442,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     p.T.child = image_child(t, nm);
     rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
     if (rc || !plan) return rc;
-    // the launch order is re-sorted from the costs accumulated over the
-    // last kPlanResort renders (the first render sorts at once): a camera's
-    // block costs change slowly, and the sort (one CTA, ~15 us) is then
-    // amortised
-    constexpr int kPlanResort = 4;
-    if (!plan->valid || ++plan->renders >= kPlanResort) {
-        if ((rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st))) return rc;
-        plan->valid = true;
-        plan->renders = 0;
-    }
-    return VV_OK;
+    return plan_finish(plan, st);
 }
 
 // ---- render straight to the host: banded device->host copies behind the render
@@ -1787,7 +1799,8 @@ int vv_scene_decode_modes(const vv_instance *inst, int32_t n_inst, const vv_rend
 // mixed n_max); decode modes consider every instance sharing a tree.
 static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_render_opts &opts,
                      const vv_camera *cam, const double *background, float *image, float *alpha, float *depth,
-                     cudaStream_t st, bool joint, double *state_in, double *state_out) {
+                     cudaStream_t st, bool joint, double *state_in, double *state_out,
+                     vv_camera_plan *plan = nullptr) {
     const vv_tree *t0 = inst[b].tree;
     int max_depth = 0;
     for (int i = b; i < e; ++i) max_depth = std::max(max_depth, inst[i].tree->depth);
@@ -1856,12 +1869,27 @@ static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_
     bool lean = true;  // every instance decoded per sample, no edits: the lean instantiation
     for (int i = b; i < e; ++i)
         if (p.inst[i - b].S.rec || inst[i].tree->has_edits) lean = false;
-    return launch_scene(t0->n_max, wide, lean, p, grid, smem, st);
+    std::unique_lock<std::mutex> plan_lock;
+    if (plan) {  // persistent warps over 16x2-pixel chunks in the previous frames' cost order
+        if (plan->device != t0->device) return set_error(VV_E_INVALID, "plan belongs to another device");
+        plan_lock = std::unique_lock<std::mutex>(plan->mu);
+        const int n_blocks = (int)(grid.x * grid.y);
+        int rc = plan_prepare(plan, n_blocks, (int)grid.x, st);
+        if (rc) return rc;
+        p.work = plan->counter;
+        p.n_work = n_blocks * 4;
+        p.blocks_x = (int)grid.x;
+        p.block_order = plan->valid ? plan->order : nullptr;
+        p.block_cost = plan->cost;
+    }
+    int rc = launch_scene(t0->n_max, wide, lean, p, grid, smem, st);
+    if (rc || !plan) return rc;
+    return plan_finish(plan, st);
 }
 
 static int render_scene_impl(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
                              const double *background, float *image, float *alpha, float *depth, void *stream,
-                             bool joint) {
+                             bool joint, vv_camera_plan *plan = nullptr) {
     NvtxRange nv(joint ? "vv:render_scene_joint" : "vv:render_scene");
     if (!inst || !cam) return set_error(VV_E_INVALID, "null argument");
     if (!image && !alpha && !depth) return set_error(VV_E_INVALID, "no output");
@@ -1896,7 +1924,7 @@ static int render_scene_impl(const vv_instance *inst, int32_t n_inst, const vv_r
     }
     if (runs.size() == 1)
         return scene_run(inst, n_inst, 0, n_inst, opts, cam, background, image, alpha, depth, st, false, nullptr,
-                         nullptr);
+                         nullptr, plan);
     // several launches: the per-pixel Algorithm-1 state (I rgb, D, A; f64)
     // carried between them in a stream-ordered buffer
     Transient state;
@@ -1927,6 +1955,13 @@ int vv_render_scene(const vv_instance *inst, int32_t n_inst, const vv_render_opt
 int vv_render_scene_joint(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
                           const double *background, float *image, float *alpha, float *depth, void *stream) {
     return render_scene_impl(inst, n_inst, o, cam, background, image, alpha, depth, stream, true);
+}
+
+int vv_render_scene_planned(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
+                            const double *background, float *image, float *alpha, float *depth,
+                            vv_camera_plan *plan, void *stream) {
+    if (!plan) return set_error(VV_E_INVALID, "null plan");
+    return render_scene_impl(inst, n_inst, o, cam, background, image, alpha, depth, stream, false, plan);
 }
 
 static int segments_impl(const vv_tree *t, const double *origins, const double *dirs, int64_t n, double tmin,

@@ -368,26 +368,26 @@ struct SceneParams {
     const double *state_in;
     double *state_out;
     int total_inst;
+    // persistent warps (a scene plan): counters [next chunk, warps done],
+    // launch order and per-block costs of the 16x8-pixel blocks
+    int *work;
+    int n_work, blocks_x;
+    const int32_t *block_order;
+    uint32_t *block_cost;
 };
 
 // CACHED 2: per-instance decode decided at run time (some instances sliced);
 // CACHED 0 with EDITS false: every instance decoded per sample and no
 // edits (the common scene case, k_render_scene_lean).
+// One pixel of the scene kernel: every instance through its pulled-back ray,
+// finalized, blended by Algorithm 1 in instance order, then unpremultiplied
+// and composited (or handed on to the next launch of a chained scene).
+// Returns the pixel's walk cost (samples + 1 per reached instance + 1).
 template <int NMAX, class Entry, int CACHED, bool EDITS>
-__device__ __forceinline__ void scene_body(const SceneParams &p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
-    __shared__ uint32_t sM[kMaxInst][2];
-    for (int i = 0; i < p.n_inst; ++i) load_rows(p.inst[i].T, p.inst[i].frame, sA[i], sB[i]);
-    __syncthreads();
-    if ((int)threadIdx.x < p.n_inst) {
-        sM[threadIdx.x][0] = nz_chunks(sA[threadIdx.x], p.inst[threadIdx.x].T.C);
-        sM[threadIdx.x][1] = nz_chunks(sB[threadIdx.x], p.inst[threadIdx.x].T.C);
-    }
-    __syncthreads();
-    int ix, iy;
-    block_pixel(blockIdx.x, blockIdx.y, ix, iy);
-    if (ix >= p.cam.width || iy >= p.cam.height) return;
+__device__ __forceinline__ int scene_pixel(const SceneParams &p, unsigned char *smem_raw, const float (*sA)[kMaxC],
+                                           const float (*sB)[kMaxC], const uint32_t (*sM)[2], int ix, int iy) {
+    if (ix >= p.cam.width || iy >= p.cam.height) return 0;
+    int cost = 1;
     double cdx, cdy, cdz;
     camera_ray(p.cam, ix, iy, cdx, cdy, cdz);
     // blended state (compose.py:386-405): I (3), D, A
@@ -433,6 +433,7 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
         Ray ray;
         if (reach && ray_setup(v.T, ox, oy, oz, dx, dy, dz, p.tmin, p.tmax, ray))
             traverse<Entry>(v.T.child, v.T.depth, ray, smem_raw, sh);
+        cost += reach ? sh.used + 1 : 0;
         // finalize_layer in float64
         const double al = sh.aacc;
         const double safe = al > 1e-300 ? al : 1e-300;
@@ -467,7 +468,7 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
     if (p.state_out) {  // a later launch continues the blend
         double *s = p.state_out + 5 * pix;
         s[0] = I0; s[1] = I1; s[2] = I2; s[3] = D; s[4] = A;
-        return;
+        return cost;
     }
     if (p.total_inst > 1) {  // unpremultiply the blend (compose.py:457-460)
         const double safe = A > 1e-300 ? A : 1e-300;
@@ -492,6 +493,47 @@ __device__ __forceinline__ void scene_body(const SceneParams &p) {
     }
     if (p.alpha) p.alpha[pix] = (float)A;
     if (p.depth) p.depth[pix] = (float)D;
+    return cost;
+}
+
+template <int NMAX, class Entry, int CACHED, bool EDITS>
+__device__ __forceinline__ void scene_body(const SceneParams &p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxInst][kMaxC], sB[kMaxInst][kMaxC];
+    __shared__ uint32_t sM[kMaxInst][2];
+    for (int i = 0; i < p.n_inst; ++i) load_rows(p.inst[i].T, p.inst[i].frame, sA[i], sB[i]);
+    __syncthreads();
+    if ((int)threadIdx.x < p.n_inst) {
+        sM[threadIdx.x][0] = nz_chunks(sA[threadIdx.x], p.inst[threadIdx.x].T.C);
+        sM[threadIdx.x][1] = nz_chunks(sB[threadIdx.x], p.inst[threadIdx.x].T.C);
+    }
+    __syncthreads();
+    if (p.work) {  // persistent warps over the 16x2-pixel warp chunks, in cost order when planned
+        const int lane = threadIdx.x & 31;
+        while (true) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.work, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx >= p.n_work) break;
+            const int tb = p.block_order ? __ldg(p.block_order + idx / 4) : idx / 4;
+            const int w = idx % 4;
+            const int ix = (tb % p.blocks_x) * 16 + (lane & 15), iy = (tb / p.blocks_x) * 8 + w * 2 + (lane >> 4);
+            const int cost = scene_pixel<NMAX, Entry, CACHED, EDITS>(p, smem_raw, sA, sB, sM, ix, iy);
+            __syncwarp();
+            if (p.block_cost) {
+                const unsigned sum = __reduce_add_sync(0xffffffffu, (unsigned)cost);
+                if (lane == 0) atomicAdd(p.block_cost + tb, sum);
+            }
+        }
+        if (lane == 0 && atomicAdd(p.work + 1, 1) == (int)(gridDim.x * (blockDim.x / 32)) - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+        }
+        return;
+    }
+    int ix, iy;
+    block_pixel(blockIdx.x, blockIdx.y, ix, iy);
+    scene_pixel<NMAX, Entry, CACHED, EDITS>(p, smem_raw, sA, sB, sM, ix, iy);
 }
 
 template <int NMAX, class Entry>

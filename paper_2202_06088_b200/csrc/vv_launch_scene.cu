@@ -8,6 +8,10 @@ static int go(const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st) {
     auto kern = LEAN ? k_render_scene_lean<NM, Entry> : k_render_scene<NM, Entry>;
     int r = prep_smem(kern, smem);
     if (r) return r;
+    if (p.work) {  // persistent warps: one resident grid pulls the warp chunks
+        kern<<<persistent_grid(kern, kBlock, smem, grid.x * grid.y), kBlock, smem, st>>>(p);
+        return check_launch("render_scene");
+    }
     kern<<<grid, kBlock, smem, st>>>(p);
     return check_launch("render_scene");
 }

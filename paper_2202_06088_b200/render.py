@@ -262,10 +262,11 @@ class CameraPlan:
 _PLANS = {}
 
 
-def _stream_plan(dev, stream_handle: int) -> CameraPlan:
-    """The camera plan render() keeps per (device, stream): renders on one
-    stream are ordered, so its plan is never used concurrently."""
-    key = (dev.index, stream_handle)
+def _stream_plan(dev, stream_handle: int, kind: str = "camera") -> CameraPlan:
+    """The plan render() (kind "camera") or render_scene() ("scene") keeps per
+    (device, stream): renders on one stream are ordered, so its plan is never
+    used concurrently."""
+    key = (dev.index, stream_handle, kind)
     p = _PLANS.get(key)
     if p is None:
         if len(_PLANS) > 16:
