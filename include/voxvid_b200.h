@@ -111,10 +111,11 @@ int vv_device_count(int *count);
  * _lib/debug/libvoxvid_b200.so, -DVV_DEBUG_CHECKS): node rows, stack slots,
  * segment-queue fill, leaf rows and slice chunks are checked in the render
  * kernels; a failed check is counted (no trap).  enabled = 1 in that build;
- * violations / first_code (VV_DBG_* codes in vv_device.cuh) since the last
- * reset.  Synchronizes the device. */
+ * violations / first_code (VV_DBG_* codes in vv_device.cuh) and the deepest
+ * traversal stack (slots in use) since the last reset.  Synchronizes the
+ * device. */
 int vv_debug_checks(int32_t device, int32_t *enabled, uint32_t *violations, uint32_t *first_code,
-                    int32_t reset);
+                    uint32_t *stack_high_water, int32_t reset);
 
 /* Basis tables of kernels.basis_tables (kernels.py:56-76); host only, for
  * parity checks of the constants.  sizes = {K, S, n_pairs}. */

@@ -213,7 +213,7 @@ _SIGNATURES = {
     "vv_abi_version": (ctypes.c_int, []),
     "vv_last_error": (ctypes.c_char_p, []),
     "vv_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
-    "vv_debug_checks": (ctypes.c_int, [_I32, _P, _P, _P, _I32]),
+    "vv_debug_checks": (ctypes.c_int, [_I32, _P, _P, _P, _P, _I32]),
     "vv_basis_tables": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, _P, _P, _P, _P]),
     "vv_tree_upload": (ctypes.c_int, [ctypes.POINTER(TreeDesc), ctypes.c_int, ctypes.POINTER(_P)]),
     "vv_tree_bind": (ctypes.c_int, [ctypes.POINTER(TreeDesc), ctypes.c_int, ctypes.POINTER(_P)]),

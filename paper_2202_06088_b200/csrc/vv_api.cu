@@ -717,14 +717,15 @@ bool warp_queue(bool ordered) {
 const int32_t *image_child(const vv_tree *t, const NodeMask *m) { return m ? m->mask : t->d_child; }
 
 // Bounds-check counter of the debug build (VV_DEBUG_CHECKS), one per device:
-// [violations, first violation code]; null in release builds.
+// [violations, first violation code, stack high-water slots]; null in
+// release builds.
 static unsigned *debug_counter(int device) {
     if (!kDebugChecks) return nullptr;
     static std::mutex mu;
     static unsigned *ctr[64] = {};
     std::lock_guard<std::mutex> lk(mu);
     unsigned *&c = ctr[device & 63];
-    if (!c && cudaMalloc(&c, 2 * sizeof(unsigned)) == cudaSuccess) cudaMemset(c, 0, 2 * sizeof(unsigned));
+    if (!c && cudaMalloc(&c, 3 * sizeof(unsigned)) == cudaSuccess) cudaMemset(c, 0, 3 * sizeof(unsigned));
     cudaGetLastError();
     return c;
 }
@@ -1011,19 +1012,22 @@ int tree_alloc_common(const vv_tree_desc *d, int device, vv_tree **out, bool hos
 // ====================================================================== C ABI
 extern "C" {
 
-int vv_debug_checks(int32_t device, int32_t *enabled, uint32_t *violations, uint32_t *first_code, int32_t reset) {
+int vv_debug_checks(int32_t device, int32_t *enabled, uint32_t *violations, uint32_t *first_code,
+                    uint32_t *stack_high_water, int32_t reset) {
     if (enabled) *enabled = kDebugChecks ? 1 : 0;
     if (violations) *violations = 0;
     if (first_code) *first_code = 0;
+    if (stack_high_water) *stack_high_water = 0;
     if (!kDebugChecks) return VV_OK;
     DeviceGuard g(device);
     unsigned *c = debug_counter(device);
     if (!c) return set_error(VV_E_CUDA, "debug counter unavailable");
-    unsigned h[2] = {0, 0};
+    unsigned h[3] = {0, 0, 0};
     VV_CUDA(cudaDeviceSynchronize());
     VV_CUDA(cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost));
     if (violations) *violations = h[0];
     if (first_code) *first_code = h[1];
+    if (stack_high_water) *stack_high_water = h[2];
     if (reset) VV_CUDA(cudaMemset(c, 0, sizeof(h)));
     return VV_OK;
 }

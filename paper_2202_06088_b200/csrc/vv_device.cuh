@@ -743,6 +743,7 @@ struct Shader {
     __device__ __forceinline__ void check_node(uint32_t ptr, uint32_t slots) const {
         if (ptr >= (uint64_t)T.n_internal) debug_violation(T.dbg, VV_DBG_NODE);
         if (slots > (uint32_t)stack_cap(T.depth)) debug_violation(T.dbg, VV_DBG_STACK);
+        if (T.dbg) atomicMax(T.dbg + 2, slots);  // stack high-water mark
     }
     __device__ __forceinline__ void check_queue(int n, int slots) const {
         if (n > slots) debug_violation(T.dbg, VV_DBG_QUEUE);
@@ -923,6 +924,7 @@ struct ShaderMulti {
     __device__ __forceinline__ void check_node(uint32_t ptr, uint32_t slots) const {
         if (ptr >= (uint64_t)T.n_internal) debug_violation(T.dbg, VV_DBG_NODE);
         if (slots > (uint32_t)stack_cap(T.depth)) debug_violation(T.dbg, VV_DBG_STACK);
+        if (T.dbg) atomicMax(T.dbg + 2, slots);  // stack high-water mark
     }
     __device__ __forceinline__ void check_queue(int n, int slots) const {
         if (n > slots) debug_violation(T.dbg, VV_DBG_QUEUE);

@@ -44,6 +44,6 @@ def _debug_checks_clean(request):
     from paper_2202_06088_b200 import _native
 
     en, n, code = ctypes.c_int32(), ctypes.c_uint32(), ctypes.c_uint32()
-    _native.check(_native.lib().vv_debug_checks(0, ctypes.byref(en), ctypes.byref(n), ctypes.byref(code), 1))
+    _native.check(_native.lib().vv_debug_checks(0, ctypes.byref(en), ctypes.byref(n), ctypes.byref(code), None, 1))
     assert en.value == 1, "VV_DEBUG_EXPECT_CLEAN set but the loaded library has no bounds checks"
     assert n.value == 0, f"{n.value} device-side bounds violations (first code {code.value})"
