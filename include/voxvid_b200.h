@@ -227,10 +227,11 @@ int vv_render_camera_region(const vv_tree *tree, int32_t frame, const vv_slice *
  * kernel has stored it -- the device->host copy overlaps the render (a copy
  * stream waits on per-band counters with cuStreamWaitValue32).  All work
  * is ordered on `stream`: the frame is on the host once it has reached the
- * end of it. */
+ * end of it.  plan (optional, vv_camera_plan_create): its chunk counters
+ * and cached coverage; the blocks run in row-major order regardless. */
 int vv_render_camera_to_host(const vv_tree *tree, int32_t frame, const vv_slice *cache,
                              const vv_render_opts *opts, const vv_camera *cam, float *device_planes,
-                             float *host_planes, void *stream);
+                             float *host_planes, vv_camera_plan *plan, void *stream);
 
 /* Camera plans: renders of a camera stream (playback, a fixed view, one
  * rank's region) through a plan run the camera kernel as persistent warps

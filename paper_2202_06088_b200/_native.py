@@ -247,7 +247,7 @@ _SIGNATURES = {
     ),
     "vv_camera_block_shape": (ctypes.c_int, [_P, _P]),
     "vv_render_camera_to_host": (
-        ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P]),
+        ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(RenderOpts), ctypes.POINTER(CameraDesc), _P, _P, _P, _P]),
     "vv_camera_plan_create": (ctypes.c_int, [_I32, ctypes.POINTER(_P)]),
     "vv_camera_plan_free": (ctypes.c_int, [_P]),
     "vv_render_camera_planned": (

@@ -1310,7 +1310,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
                               int tile, int shard, int n_shards, int peer, void *stream, int32_t *used = nullptr,
                               const int32_t *rect = nullptr, const int32_t *block_order = nullptr,
                               vv_camera_plan *plan = nullptr, unsigned *band_done = nullptr, int band_rows = 0,
-                              bool force_queue = false) {
+                              bool force_queue = false, bool natural_order = false) {
     NvtxRange nv("vv:render_camera");
     if (!t || !cam) return set_error(VV_E_INVALID, "null argument");
     int rc = check_frame(t, frame);
@@ -1385,7 +1385,8 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         if (prc) return prc;
         p.work = plan->counter;
         p.n_work = (int)grid_blocks * kWarpsPerTile;
-        p.block_order = plan->valid ? plan->order : nullptr;
+        // natural order: bands finish top to bottom (banded host copies)
+        p.block_order = plan->valid && !natural_order ? plan->order : nullptr;
         p.block_cost = plan->cost;
     } else if (!tile && (force_queue || warp_queue(block_order != nullptr))) {
         // persistent warps over the warp chunks: the chunk counter is zeroed
@@ -1511,7 +1512,8 @@ static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_ban
 }
 
 int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,
-                             const vv_camera *cam, float *device_planes, float *host_planes, void *stream) {
+                             const vv_camera *cam, float *device_planes, float *host_planes, vv_camera_plan *plan,
+                             void *stream) {
     NvtxRange nv("vv:render_camera_to_host");
     if (!t || !cam || !device_planes || !host_planes) return set_error(VV_E_INVALID, "null argument");
     if (cam->width <= 0 || cam->height <= 0) return set_error(VV_E_INVALID, "bad camera size");
@@ -1542,9 +1544,10 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
     VV_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
     cudaEventRecord(ready, st);  // counters zeroed, earlier work on the caller's stream ordered
     cudaStreamWaitEvent(cs, ready, 0);
-    // persistent warps in row-major order: bands finish top to bottom
+    // persistent warps in row-major order: bands finish top to bottom (a
+    // plan contributes its counters and cached coverage, not its cost order)
     int rc = render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream, nullptr,
-                                nullptr, nullptr, nullptr, band_done, band_rows, true);
+                                nullptr, nullptr, plan, band_done, band_rows, true, true);
     if (rc) {
         cudaStreamWaitEvent(st, ready, 0);
         cudaEventDestroy(ready);

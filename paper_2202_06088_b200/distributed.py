@@ -112,11 +112,12 @@ def block_order(costs, rect):
 
 
 def render_region(tree, cam, frame, rect, rgb, alpha, depth, opts=None, cache=None, *, peer: bool = False,
-                  device=None, order=None):
+                  device=None, order=None, plan=None):
     """Render the pixel rectangle rect = (x0, y0, x1, y1) of ``cam`` into
     full-size planes (device pointers or tensors; may be a peer's IPC
-    mapping), its blocks launched in ``order`` (block_order) if given.
-    Async on the device's current stream."""
+    mapping), its blocks launched in ``order`` (block_order) if given, or
+    scheduled by a CameraPlan (``plan``: the rank's own cost order and cached
+    coverage).  Async on the device's current stream."""
     from .device import replica, stream_ptr, torch_device
     from .render import RenderOptions, _check_cache
 
@@ -126,6 +127,11 @@ def render_region(tree, cam, frame, rect, rgb, alpha, depth, opts=None, cache=No
     ch = _check_cache(cache, int(frame), rep)
     ptr = (lambda x: x if isinstance(x, int) or x is None else x.data_ptr())
     r = (ctypes.c_int32 * 4)(*[int(v) for v in rect])
+    if plan is not None:
+        _native.check(_native.lib().vv_render_camera_planned(
+            rep.handle, int(frame), ch, ctypes.byref(opts.c_struct()), ctypes.byref(cam.desc()), r, plan._handle,
+            ptr(rgb), ptr(alpha), ptr(depth), int(bool(peer)), stream_ptr(dev)))
+        return
     _native.check(_native.lib().vv_render_camera_region(
         rep.handle, int(frame), ch, ctypes.byref(opts.c_struct()), ctypes.byref(cam.desc()), r, ptr(order), ptr(rgb),
         ptr(alpha), ptr(depth), int(bool(peer)), stream_ptr(dev)))

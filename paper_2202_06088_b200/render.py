@@ -534,6 +534,7 @@ def render(tree, cam: Camera, frame: int, opts: RenderOptions = RenderOptions(),
     host, a = _PINNED.get(5 * h * w)
     _native.check(_native.lib().vv_render_camera_to_host(rep.handle, frame, ch, ctypes.byref(opts.c_struct()),
                                                           ctypes.byref(cam.desc()), buf.data_ptr(), host.data_ptr(),
+                                                          _stream_plan(dev, stream.cuda_stream)._handle,
                                                           stream.cuda_stream))
     stream.synchronize()
     return LayerImages(a[: 3 * h * w].reshape(h, w, 3), a[3 * h * w: 4 * h * w].reshape(h, w),

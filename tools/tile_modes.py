@@ -26,7 +26,7 @@ import torch  # noqa: E402
 import paper_2202_06088_b200 as vv  # noqa: E402
 from paper_2202_06088_b200 import _native, synthetic  # noqa: E402
 from paper_2202_06088_b200.device import replica, stream_ptr  # noqa: E402
-from paper_2202_06088_b200.distributed import band_plan, block_order, pixel_costs, render_region  # noqa: E402
+from paper_2202_06088_b200.distributed import band_plan, pixel_costs, render_region  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--tree", default="shell", choices=["shell", "motion"])
@@ -74,9 +74,12 @@ def tiles(world, rank):
 
 
 def bands(edges, rank, ordered=True):
+    """ordered: the rank's own camera plan (what TileRenderer "regions" runs:
+    persistent warps in its measured cost order, cached coverage); else the
+    static row-major launch."""
     rect = (0, edges[rank], w, edges[rank + 1])
-    order = block_order(costs, rect) if ordered else None
-    return lambda f: render_region(tree, cam, f, rect, rgb, alpha, depth, order=order)
+    plan = vv.CameraPlan(dev) if ordered else None
+    return lambda f: render_region(tree, cam, f, rect, rgb, alpha, depth, plan=plan)
 
 
 out = {"tree": args.tree, "single_gpu_frame_ms": round(share_ms(lambda f: vv.render_into(tree, cam, f, rgb, alpha,
