@@ -606,6 +606,7 @@ def playback_group(tree) -> int:
 SEQUENCE_GROUP = 3
 
 _PLAYBACK = {}
+_PLAYBACK_MAX = 4  # cached playback states per device (concurrent sequences)
 
 
 def _playback_state(torch, dev, n: int):
@@ -616,10 +617,17 @@ def _playback_state(torch, dev, n: int):
     stream-ordered (cudaMallocAsync) on the render stream, and the pool only
     recycles a block on the stream that freed it -- a fresh stream per call
     re-maps ~1.9 GB of slice memory on its first frame (tens of ms).
+    Several playbacks live at once (e.g. the two eyes of a stereo sequence,
+    zipped) each get a cached state of their own (up to _PLAYBACK_MAX).
     """
     key = (dev.index if dev.index is not None else torch.cuda.current_device(), n)
-    st = _PLAYBACK.get(key)
-    if st is None or st[3][0]:
+    states = _PLAYBACK.get(key)
+    if states is None:
+        for k in [k for k in _PLAYBACK if k[0] == key[0]]:
+            del _PLAYBACK[k]  # one resolution per device at a time
+        states = _PLAYBACK[key] = []
+    st = next((s for s in states if not s[3][0]), None)
+    if st is None:
         comp, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         with torch.cuda.stream(comp):
             bufs = [[torch.empty(n, dtype=torch.float32, device=dev) for _ in range(PLAYBACK_GROUP)]
@@ -627,12 +635,9 @@ def _playback_state(torch, dev, n: int):
         for grp in bufs:
             for b in grp:
                 b.record_stream(copy)
-        fresh = (comp, copy, bufs, [False])
-        if st is not None:
-            return fresh  # another playback is live on this device: private state, not cached
-        for k in [k for k in _PLAYBACK if k[0] == key[0]]:
-            del _PLAYBACK[k]  # one resolution per device at a time
-        st = _PLAYBACK[key] = fresh
+        st = (comp, copy, bufs, [False])
+        if len(states) < _PLAYBACK_MAX:
+            states.append(st)  # else a private state, not cached
     st[0].wait_stream(st[1])  # an abandoned playback may still be copying out of the buffers
     return st
 

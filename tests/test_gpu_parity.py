@@ -776,3 +776,19 @@ def test_bbox_placement_vs_oracle(cuda, lo, side):
     p, a, t = vv.render_rays(tree, o, d, 2)
     assert np.abs(a - ref["alpha"]).max() <= 1e-12
     assert np.abs(p - ref["premult"]).max() <= TOL
+
+
+def test_render_sequences_zipped_stereo(cuda):
+    """Two playbacks live at once (the eyes of a stereo sequence, zipped):
+    each gets a cached playback state of its own; every frame bitwise render()."""
+    tree = synthetic.shell_tree(depth=7, n_max=1, frames=8, seed=3)
+    eyes = [vv.Camera.look_at(e, [0.5, 0.5, 0.5], width=96, height=80) for e in ([1.7, 1.2, 0.9], [1.6, 1.35, 0.9])]
+    frames = [0, 3, 5, 6, 1, 7, 2]
+    for _ in range(2):  # second round: cached states reused
+        got = list(zip(*[vv.render_sequence(tree, cam, frames) for cam in eyes]))
+        assert len(got) == len(frames)
+        for f, pair in zip(frames, got):
+            for cam, layer in zip(eyes, pair):
+                ref = vv.render(tree, cam, f)
+                _exact(layer.rgb, ref.rgb, f"rgb {f}")
+                _exact(layer.depth, ref.depth, f"depth {f}")
