@@ -146,6 +146,16 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
+def ncu_summary(config: int):
+    p = ROOT / "profiles" / f"r02_ncu_cfg{config}.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
 def ncu_traffic(config: int):
     """DRAM bytes per launch of the config's dominant kernel from its committed
     ncu --set full capture (profiles/r02_ncu_cfg<N>.json), else null."""
@@ -666,9 +676,15 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         te = time.perf_counter()
         got = 0
+        gaps = []
+        tp = te
         for layer in vv.render_sequence(wl.tree, cam, e2e_frames):
             got += 1
+            tn = time.perf_counter()
+            gaps.append(round((tn - tp) * 1e3, 3))
+            tp = tn
         e2e_s = time.perf_counter() - te
+        log(f"[bench] e2e per-frame delivery gaps (ms): {gaps}")
         assert got == len(e2e_frames) and layer.rgb.shape == (cam.height, cam.width, 3)
         del layer
         api = ("paper_2202_06088_b200.render_sequence(tree, cam, frames) -> numpy LayerImages (fp32) per frame on "
@@ -746,6 +762,15 @@ def run_ours(args, rank, world, local_rank):
                     "reference_formula_bytes_per_step": float(np.mean([ab[f]["reference_bytes"] for f in step_frames])),
                     "reference_formula_achieved": round(sum(ab[f]["reference_bytes"] for f in step_frames)
                                                         / (total_ms / 1e3) / 1e9, 1)}
+        # the kernel's issue roofline: its warp instructions (committed ncu
+        # capture of this config) / (148 SM x 4 schedulers x SM clock)
+        ns = ncu_summary(args.config)
+        if ns and ns.get("warp_instructions") and clk and clk.get("sm_mhz"):
+            floor_ms = ns["warp_instructions"] / (148 * 4 * clk["sm_mhz"] * 1e6) * 1e3
+            roofline["issue"] = {"warp_instructions": ns["warp_instructions"], "floor_ms": round(floor_ms, 4),
+                                 "frac": round(floor_ms / (render_ms / n), 4),
+                                 "source": f"profiles/r02_ncu_cfg{args.config}.json",
+                                 "note": "issue-limited kernel: one warp instruction per scheduler per cycle"}
         if wl.kind == "scene":
             roofline["bytes_formula"] = ("sum over instance rays 32 P + 16 nzA V + (16 nzB + 12 K) S + 12 B/px "
                                          "(per-sample decode, nonzero-basis chunks; P/V/S reference counts)")

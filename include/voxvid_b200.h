@@ -309,6 +309,13 @@ int vv_camera_decode_mode(const vv_tree *tree, const vv_camera *cam, const vv_re
 int vv_render_camera_multi(const vv_tree *tree, int32_t n_frames, const int32_t *frames,
                            const vv_slice *const *caches, const vv_render_opts *opts, const vv_camera *cam,
                            float *const *rgb, float *const *alpha, float *const *depth, void *stream);
+/* vv_render_camera_multi scheduled by a plan (vv_camera_plan_create):
+ * persistent warps in the previous walks' cost order, the plan's cached
+ * coverage; bitwise vv_render_camera_multi.  Use a plan of its own. */
+int vv_render_camera_multi_planned(const vv_tree *tree, int32_t n_frames, const int32_t *frames,
+                                   const vv_slice *const *caches, const vv_render_opts *opts, const vv_camera *cam,
+                                   float *const *rgb, float *const *alpha, float *const *depth,
+                                   vv_camera_plan *plan, void *stream);
 
 /* ---- multi-instance scene -------------------------------------------------
  * Replaces render_scene (compose.py:443-475) without lights: per pixel,

@@ -83,6 +83,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_scene_joint",
     "vv_render_scene_planned",
     "vv_render_camera_multi",
+    "vv_render_camera_multi_planned",
     "vv_slice_build_multi",
     "vv_slice_build_frames",
     "vv_camera_decode_mode",
@@ -272,6 +273,7 @@ _SIGNATURES = {
     "vv_slice_build_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
     "vv_slice_build_frames": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P]),
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vv_render_camera_multi_planned": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),
     "vv_scene_lighting": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P]),
     "vv_scene_lighting_ex": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P]),

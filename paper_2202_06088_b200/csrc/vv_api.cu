@@ -689,6 +689,39 @@ int plan_prepare(vv_camera_plan *plan, int n_blocks, int blocks_x, cudaStream_t 
     return VV_OK;
 }
 
+// The plan's coverage for (tree, camera): built once per view, reused by
+// every frame of it (plan->cov stays empty -- everything covered -- for
+// trees without chunk boxes or with VV_COVERAGE=0).
+int plan_coverage(vv_camera_plan *plan, const vv_tree *t, const vv_camera &cam, const CamView &cv, cudaStream_t st) {
+    if (!coverage_wanted(t)) {
+        plan->cov = CoverView{};
+        plan->cov_valid = false;
+        return VV_OK;
+    }
+    if (plan->cov_valid && plan->cov_tree == t->serial && memcmp(&plan->cov_cam, &cam, sizeof(cam)) == 0)
+        return VV_OK;
+    const size_t bytes = coverage_bytes(cam.width, cam.height);
+    if (plan->cov_cap < bytes) {
+        cudaFree(plan->cov_mem);
+        plan->cov_mem = nullptr;
+        plan->cov_cap = 0;
+        if (cudaMalloc(&plan->cov_mem, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            plan->cov_mem = nullptr;
+            return set_error(VV_E_NOMEM, "coverage allocation failed");
+        }
+        plan->cov_cap = bytes;
+    }
+    plan->cov_valid = false;
+    int r = build_coverage_into(t, cv, cam.width, cam.height, nullptr, st, static_cast<char *>(plan->cov_mem),
+                                plan->cov);
+    if (r) return r;
+    plan->cov_tree = t->serial;
+    plan->cov_cam = cam;
+    plan->cov_valid = true;
+    return VV_OK;
+}
+
 // After a planned launch: the launch order is re-sorted from the costs
 // accumulated over the last kPlanResort renders (the first render sorts at
 // once) -- a view's block costs change slowly, and the sort (one CTA, ~15
@@ -1405,30 +1438,9 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     // coverage (planned renders: built once per tree and camera, ~30 us,
     // then reused by every frame of that view -- per call it costs about
     // what it saves, measured on cfg2 / cfg3)
-    if (plan && coverage_wanted(t)) {
-        const bool same =
-            plan->cov_valid && plan->cov_tree == t->serial && memcmp(&plan->cov_cam, cam, sizeof(*cam)) == 0;
-        if (!same) {
-            const size_t bytes = coverage_bytes(cam->width, cam->height);
-            if (plan->cov_cap < bytes) {
-                cudaFree(plan->cov_mem);
-                plan->cov_mem = nullptr;
-                plan->cov_cap = 0;
-                if (cudaMalloc(&plan->cov_mem, bytes) != cudaSuccess) {
-                    cudaGetLastError();
-                    plan->cov_mem = nullptr;
-                    return set_error(VV_E_NOMEM, "coverage allocation failed");
-                }
-                plan->cov_cap = bytes;
-            }
-            plan->cov_valid = false;
-            int r = build_coverage_into(t, p.cam, cam->width, cam->height, nullptr, st,
-                                        static_cast<char *>(plan->cov_mem), plan->cov);
-            if (r) return r;
-            plan->cov_tree = t->serial;
-            plan->cov_cam = *cam;
-            plan->cov_valid = true;
-        }
+    if (plan) {
+        int r = plan_coverage(plan, t, *cam, p.cam, st);
+        if (r) return r;
         p.cov = plan->cov;
     }
     const double lo[3] = {t->view.lo0, t->view.lo1, t->view.lo2};
@@ -1642,9 +1654,9 @@ int vv_camera_decode_mode(const vv_tree *t, const vv_camera *cam, const vv_rende
     return VV_OK;
 }
 
-int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
-                           const vv_render_opts *o, const vv_camera *cam, float *const *rgb, float *const *alpha,
-                           float *const *depth, void *stream) {
+static int render_multi_impl(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
+                             const vv_render_opts *o, const vv_camera *cam, float *const *rgb, float *const *alpha,
+                             float *const *depth, vv_camera_plan *plan, void *stream) {
     NvtxRange nv("vv:render_camera_multi");
     if (!t || !frames || !caches || !cam || !rgb || !alpha || !depth) return set_error(VV_E_INVALID, "null argument");
     if (n_frames < 2 || n_frames > kMaxMulti)
@@ -1678,6 +1690,23 @@ int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *fr
     p.blocks_x = (cam->width + kTW - 1) / kTW;
     const unsigned grid = (unsigned)p.blocks_x * (unsigned)((cam->height + kTH - 1) / kTH);
     if (grid == 0) return VV_OK;
+    int rr[4];
+    occupied_rect(t, p.cam, nullptr, cam->width, cam->height, rr);
+    p.cx0 = rr[0]; p.cy0 = rr[1]; p.cx1 = rr[2]; p.cy1 = rr[3];
+    cudaStream_t st = (cudaStream_t)stream;
+    std::unique_lock<std::mutex> plan_lock;
+    if (plan) {  // persistent warps in the plan's cost order; its cached coverage
+        if (plan->device != t->device) return set_error(VV_E_INVALID, "plan belongs to another device");
+        plan_lock = std::unique_lock<std::mutex>(plan->mu);
+        int rc = plan_prepare(plan, (int)grid, p.blocks_x, st);
+        if (rc) return rc;
+        if ((rc = plan_coverage(plan, t, *cam, p.cam, st))) return rc;
+        p.cov = plan->cov;
+        p.work = plan->counter;
+        p.n_work = (int)grid * kWarpsPerTile;
+        p.block_order = plan->valid ? plan->order : nullptr;
+        p.block_cost = plan->cost;
+    }
     // a node mask built for a group holding every frame of this walk (slices
     // of one vv_slice_build_frames call share it) keeps every subtree lit
     // in any of them
@@ -1685,8 +1714,24 @@ int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *fr
     for (int k = 1; k < n_frames && nm; ++k)
         if (caches[k]->nmask.get() != nm) nm = nullptr;
     p.T.child = image_child(t, nm);
-    return launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid,
-                               (cudaStream_t)stream, long_queue(t, nm));
+    int rc = launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid, st,
+                                 long_queue(t, nm));
+    if (rc || !plan) return rc;
+    return plan_finish(plan, st);
+}
+
+int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
+                           const vv_render_opts *o, const vv_camera *cam, float *const *rgb, float *const *alpha,
+                           float *const *depth, void *stream) {
+    return render_multi_impl(t, n_frames, frames, caches, o, cam, rgb, alpha, depth, nullptr, stream);
+}
+
+int vv_render_camera_multi_planned(const vv_tree *t, int32_t n_frames, const int32_t *frames,
+                                   const vv_slice *const *caches, const vv_render_opts *o, const vv_camera *cam,
+                                   float *const *rgb, float *const *alpha, float *const *depth, vv_camera_plan *plan,
+                                   void *stream) {
+    if (!plan) return set_error(VV_E_INVALID, "null plan");
+    return render_multi_impl(t, n_frames, frames, caches, o, cam, rgb, alpha, depth, plan, stream);
 }
 
 int vv_render_camera_tiles(const vv_tree *t, int32_t frame, const vv_slice *cache, const vv_render_opts *opts,

@@ -906,6 +906,7 @@ struct ShaderMulti {
     float dx, dy, dz;
     double trans[KF], acc0[KF], acc1[KF], acc2[KF], aacc[KF], tacc[KF];
     unsigned alive;
+    int used = 0;  // segments consumed by the shared walk (a plan's cost)
     bool y_ready;
     float y[Basis<NMAX>::S];
 
@@ -942,6 +943,7 @@ struct ShaderMulti {
         for (int s = 0; s < n; ++s) {
             const uint32_t L = (uint32_t)seg.leaf_at(s);
             const double tin = seg.t0_at(s), tout = seg.t1_at(s);
+            ++used;
             double sg[KF];  // every live frame's sigma requested at once (independent loads)
 #pragma unroll
             for (int k = 0; k < KF; ++k) sg[k] = ((alive >> k) & 1u) ? S[k].sigma(L) : 0.0;

@@ -564,45 +564,83 @@ struct CamMultiParams {
     double early_stop, edit_weight, tmin, tmax, far_plane, alpha_floor;
     float *rgb[kMaxMulti], *alpha[kMaxMulti], *depth[kMaxMulti];
     int blocks_x;
+    int cx0, cy0, cx1, cy1;  // pixel rectangle of the tree's occupied box (inclusive)
+    CoverView cov;           // pixels that can reach the tree (a plan's cached coverage)
+    // persistent warps (a plan): counters, launch order and per-block costs
+    int *work;
+    int n_work;
+    const int32_t *block_order;
+    uint32_t *block_cost;
 };
 
 #ifndef VV_MULTI_MINB_HI
 #define VV_MULTI_MINB_HI kCamMinBlocks  // resident blocks for 3- and 4-frame walks
 #endif
+
+// One pixel of the shared-walk playback kernel; returns its walk cost.
+template <int NMAX, int KF, bool EDITS, class Entry, int SEG>
+__device__ __forceinline__ int multi_pixel(const CamMultiParams &p, unsigned char *smem_raw, int ix, int iy) {
+    if (ix >= p.cam.width || iy >= p.cam.height) return 0;
+    const bool reach = ix >= p.cx0 && ix <= p.cx1 && iy >= p.cy0 && iy <= p.cy1 && covered(p.cov, ix, iy);
+    double dx = 0.0, dy = 0.0, dz = 1.0;
+    if (reach) camera_ray(p.cam, ix, iy, dx, dy, dz);
+    ShaderMulti<NMAX, KF, EDITS, SEG> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
+                                        (float)dz);
+    Ray ray;
+    int cost = 1;
+    if (reach && ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray)) {
+        traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+        cost += sh.used;
+    }
+    const long long slot = (long long)iy * p.cam.width + ix;
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+        float r, g, b, a, d;
+        finalize(sh.acc0[k], sh.acc1[k], sh.acc2[k], sh.aacc[k], sh.tacc[k], 1.0, false, p.alpha_floor,
+                 p.far_plane, r, g, b, a, d);
+        if (p.rgb[k]) {
+            p.rgb[k][3 * slot + 0] = r;
+            p.rgb[k][3 * slot + 1] = g;
+            p.rgb[k][3 * slot + 2] = b;
+        }
+        if (p.alpha[k]) p.alpha[k][slot] = a;
+        if (p.depth[k]) p.depth[k][slot] = d;
+    }
+    return cost;
+}
+
 template <int NMAX, int KF, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
 __global__ void __launch_bounds__(kTileRays, KF >= 3 ? VV_MULTI_MINB_HI : kCamMinBlocks)
     k_render_camera_multi(const __grid_constant__ CamMultiParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int bx = blockIdx.x % p.blocks_x, by = blockIdx.x / p.blocks_x;
-    const int x0 = bx * kTW, y0 = by * kTH;
-    {
-        const int rid = (int)threadIdx.x;  // blockDim.x == kTileRays
-        int dx_, dy_;
-        local_pixel(rid, dx_, dy_);
-        const int ix = x0 + dx_, iy = y0 + dy_;
-        if (ix >= p.cam.width || iy >= p.cam.height) return;
-        double dx, dy, dz;
-        camera_ray(p.cam, ix, iy, dx, dy, dz);
-        ShaderMulti<NMAX, KF, EDITS, SEG> sh(p.T, p.S, p.frames, p.K, p.early_stop, p.edit_weight, (float)dx, (float)dy,
-                                        (float)dz);
-        Ray ray;
-        if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
-            traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
-        const long long slot = (long long)iy * p.cam.width + ix;
-#pragma unroll
-        for (int k = 0; k < KF; ++k) {
-            float r, g, b, a, d;
-            finalize(sh.acc0[k], sh.acc1[k], sh.acc2[k], sh.aacc[k], sh.tacc[k], 1.0, false, p.alpha_floor,
-                     p.far_plane, r, g, b, a, d);
-            if (p.rgb[k]) {
-                p.rgb[k][3 * slot + 0] = r;
-                p.rgb[k][3 * slot + 1] = g;
-                p.rgb[k][3 * slot + 2] = b;
+    if (p.work) {  // persistent warps over the warp chunks, in the plan's cost order
+        const int lane = threadIdx.x & 31;
+        while (true) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(p.work, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx >= p.n_work) break;
+            const int tb = p.block_order ? __ldg(p.block_order + idx / kWarpsPerTile) : idx / kWarpsPerTile;
+            int dx_, dy_;
+            local_pixel((idx % kWarpsPerTile) * 32 + lane, dx_, dy_);
+            const int cost = multi_pixel<NMAX, KF, EDITS, Entry, SEG>(p, smem_raw, (tb % p.blocks_x) * kTW + dx_,
+                                                                     (tb / p.blocks_x) * kTH + dy_);
+            __syncwarp();
+            if (p.block_cost) {
+                const unsigned sum = __reduce_add_sync(0xffffffffu, (unsigned)cost);
+                if (lane == 0) atomicAdd(p.block_cost + tb, sum);
             }
-            if (p.alpha[k]) p.alpha[k][slot] = a;
-            if (p.depth[k]) p.depth[k][slot] = d;
         }
+        if (lane == 0 && atomicAdd(p.work + 1, 1) == (int)(gridDim.x * kWarpsPerTile) - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+        }
+        return;
     }
+    const int bx = blockIdx.x % p.blocks_x, by = blockIdx.x / p.blocks_x;
+    int dx_, dy_;
+    local_pixel((int)threadIdx.x, dx_, dy_);  // blockDim.x == kTileRays
+    multi_pixel<NMAX, KF, EDITS, Entry, SEG>(p, smem_raw, bx * kTW + dx_, by * kTH + dy_);
 }
 
 // ------------------------------------------------------------------ slice

@@ -16,7 +16,8 @@ static int go(const CamMultiParams &p, unsigned grid, cudaStream_t st) {
     const size_t smem = stack_bytes(p.T.depth, Entry::kBytes == EntryW::kBytes, false, kTileRays, SEG + 3);
     int r = prep_smem(kern, smem);
     if (r) return r;
-    kern<<<grid, kTileRays, smem, st>>>(p);
+    // persistent warps (a plan): one resident grid pulls the warp chunks
+    kern<<<p.work ? persistent_grid(kern, kTileRays, smem, grid) : grid, kTileRays, smem, st>>>(p);
     return check_launch("render_camera_multi");
 }
 

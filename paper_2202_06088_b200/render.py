@@ -584,9 +584,10 @@ def render_frames_into(tree, cam: Camera, frames, outs, opts: RenderOptions = Re
         def ptrs(j):
             return (P * n)(*[o[j].data_ptr() if o[j] is not None else None for o in outs])
 
-        _native.check(_native.lib().vv_render_camera_multi(
+        s = stream_ptr(dev)
+        _native.check(_native.lib().vv_render_camera_multi_planned(
             rep.handle, n, (ctypes.c_int32 * n)(*frames), (P * n)(*[c._handle for c in caches]),
-            ctypes.byref(oc), ctypes.byref(cd), ptrs(0), ptrs(1), ptrs(2), stream_ptr(dev)))
+            ctypes.byref(oc), ctypes.byref(cd), ptrs(0), ptrs(1), ptrs(2), _stream_plan(dev, s, "multi")._handle, s))
         del caches
 
 
