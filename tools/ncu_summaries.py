@@ -28,7 +28,8 @@ METRICS = {
     "sm__maximum_warps_per_active_cycle_pct": "theoretical_occupancy_pct",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
 }
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "nsecond": 1e-3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3,
+        "nsecond": 1e-3, "ns": 1e-3}
 
 
 def summarise(rep):
