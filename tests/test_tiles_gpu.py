@@ -395,3 +395,34 @@ def test_camera_plan_coverage_reuse_and_invalidation(cuda):
                 _eq(out[1], ref.alpha, f"alpha it{it} f{f}")
                 _eq(out[2], ref.depth, f"depth it{it} f{f}")
         del tree
+
+
+def test_plans_with_eye_inside_and_grazing_views(cuda):
+    """Coverage and occupied-box skipping are conservative: an eye inside the
+    tree's cube (box corners behind it), a view from below with the tree half
+    off-screen, and a narrow field of view on a cube edge -- planned renders
+    (camera, playback) bitwise equal to unplanned ones."""
+    import torch
+
+    tree = _tree()
+    cams = [vv.Camera.look_at([0.5, 0.45, 0.5], [1.0, 0.9, 0.7], width=W, height=H, focal=0.6 * W),
+            vv.Camera.look_at([0.9, 0.2, -1.2], [0.9, 0.3, 0.5], width=W, height=H, focal=1.5 * W),
+            vv.Camera.look_at([3.0, 3.1, 2.9], [1.0, 1.0, 0.5], width=W, height=H, focal=9.0 * W)]
+    plan = vv.CameraPlan(cuda)
+    for cam in cams:
+        for f in (1, 6):
+            out = [torch.empty((H, W, 3), device=cuda), torch.empty((H, W), device=cuda),
+                   torch.empty((H, W), device=cuda)]
+            vv.render_into(tree, cam, f, *out, plan=plan)
+            ref = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="per_sample"), out="torch")
+            torch.cuda.synchronize()
+            _eq(out[0], ref.rgb, "rgb")
+            _eq(out[2], ref.depth, "depth")
+        outs = [(torch.empty((H, W, 3), device=cuda), torch.empty((H, W), device=cuda),
+                 torch.empty((H, W), device=cuda)) for _ in range(3)]
+        vv.render_frames_into(tree, cam, [0, 3, 5], outs, vv.RenderOptions(frame_slice="per_frame"))
+        torch.cuda.synchronize()
+        for f, o in zip([0, 3, 5], outs):
+            ref = vv.render(tree, cam, f, out="torch")
+            _eq(o[0], ref.rgb, f"playback rgb {f}")
+            _eq(o[1], ref.alpha, f"playback alpha {f}")

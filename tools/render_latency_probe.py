@@ -1,0 +1,32 @@
+"""Where render() -> numpy spends its time at cfg2: wall time per call, the
+device time from its first launch to the last band copy (events on the
+caller's stream, which waits for the copies), and the host time before the
+first launch."""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import paper_2202_06088_b200 as vv  # noqa: E402
+from paper_2202_06088_b200 import synthetic  # noqa: E402
+
+tree = synthetic.shell_tree()
+cam = synthetic.bench_camera()
+for f in range(5):
+    vv.render(tree, cam, f)
+torch.cuda.synchronize()
+walls, devs = [], []
+for i in range(20):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    s.record()
+    layer = vv.render(tree, cam, i % 30)
+    e.record()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    walls.append((t1 - t0) * 1e3)
+    devs.append(s.elapsed_time(e))
+print(json.dumps({"wall_ms": round(sum(walls) / len(walls), 4), "device_ms": round(sum(devs) / len(devs), 4)}))
