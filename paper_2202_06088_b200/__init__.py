@@ -18,6 +18,7 @@ from .compose import (
     paint,
     render_instance,
     render_scene,
+    render_scene_sequence,
     shadow_pass,
     termination_leaves,
 )
@@ -57,7 +58,7 @@ __all__ = [
     "ChecksumError", "Camera", "LayerImages", "RenderOptions", "FrameSlice", "CameraPlan", "render", "render_into", "render_frames_into", "render_sequence",
     "render_rays", "render_ray_visits", "finalize_layer", "composite_background", "build_frame_cache", "build_frame_caches",
     "count_segments", "collect_segments", "TimeMap", "SceneInstance", "Scene", "Light", "blend_layers",
-    "render_instance", "render_scene", "duplicate", "paint", "termination_leaves", "ShadowMap", "shadow_pass",
+    "render_instance", "render_scene", "render_scene_sequence", "duplicate", "paint", "termination_leaves", "ShadowMap", "shadow_pass",
     "falloff_pass", "TemporalBases",
     "make_bump_bases",
 ]

@@ -94,3 +94,34 @@ def test_many_lights(cuda):
     ref = a * rgb + (1 - a) * scene.background
     assert np.abs(img - ref).max() < TOL
     assert np.abs(np.asarray(blended.rgb) - rgb).max() < TOL
+
+
+@pytest.mark.parametrize("lit", [False, True])
+def test_render_scene_sequence_bitwise(cuda, lit):
+    """The compose loop (cli.py:184-200) pipelined: every yielded image is
+    bitwise render_scene(scene, cam_i, g_i), with a camera per frame (the
+    orbit) and with lights; closing the generator early is safe."""
+    rng = np.random.default_rng(6)
+    t = random_payload_tree(rng, depth=4, fill=0.4, frames=8, sigma_scale=6.0)
+    insts = [vv.SceneInstance(name="a", tree=t, affine=_tr(0.0, 0.0, 0.3), timemap=vv.TimeMap.parse("shift(2)")),
+             vv.SceneInstance(name="b", tree=t, affine=_tr(0.7, 0.3, 0.2) @ np.diag([0.9, 0.9, 0.9, 1.0]),
+                              yaw_rate=12.0)]
+    lights = [vv.Light(position=(0.9, 0.4, 3.5), blur_sigma=1.0, shadow_resolution=64, falloff_enabled=True)] if lit \
+        else []
+    scene = vv.Scene(instances=insts, lights=lights, background=np.array([0.1, 0.2, 0.3]))
+    frames = list(range(7))
+    cams = [vv.Camera.look_at([0.5 + 2.5 * np.cos(0.3 * i), 0.5 + 2.5 * np.sin(0.3 * i), 1.6], [0.5, 0.5, 0.5],
+                              width=40, height=30) for i in frames]
+    seq = list(vv.render_scene_sequence(scene, cams, frames))
+    assert len(seq) == len(frames)
+    for g, c, img in zip(frames, cams, seq):
+        assert np.array_equal(img, vv.render_scene(scene, c, g)), g
+    one = list(vv.render_scene_sequence(scene, cams[2], [5, 1]))
+    assert np.array_equal(one[0], vv.render_scene(scene, cams[2], 5))
+    assert np.array_equal(one[1], vv.render_scene(scene, cams[2], 1))
+    gen = vv.render_scene_sequence(scene, cams, frames)
+    first = next(gen)
+    gen.close()
+    assert np.array_equal(first, seq[0])
+    with pytest.raises(ValueError):
+        vv.render_scene_sequence(scene, cams[:3], frames)
