@@ -269,11 +269,35 @@ def slice_pass_bytes(tree, f, device, chunk=64):
     rows = np.full(len(bright), chunk)
     if len(rows):
         rows[-1] = n - chunk * (len(rows) - 1)
-    nb, nd = int(rows[bright].sum()), int(rows[~bright].sum())
-    b = n * 16 * nza + nb * (16 * nzb + 12 * k + 8 + 12 * s_sh) + nd * 32
-    if rep.dark_fraction >= 0.25 and not getattr(tree, "has_edits", False):
+    masks = rep.dark_fraction >= 0.25 and not getattr(tree, "has_edits", False)
+    if visible_set_on(tree, rep):
+        # visible-set slice (k_slice_sigma + k_build_slice<.., VIS>): w_sigma
+        # of every leaf; a chunk with a visible leaf reads its w_gamma chunks
+        # and its visible leaves' w_hh rows and writes every record (the
+        # visible leaves' 8 + 12 S_sh, the others' sigma 8); every other
+        # leaf's record gets its sigma pair (32 B); 2 bitmaps of 1 bit/leaf
+        vis = np.concatenate([rep.visible_mask(), pad]).reshape(-1, chunk)
+        vchunk = vis.any(axis=1)
+        nv = int(vis.sum())
+        rv = int(rows[vchunk].sum())
+        b = n * 16 * nza + rv * 16 * nzb + nv * (12 * k + 12 * s_sh) + rv * 8 + (n - rv) * 32 + n // 4
+    else:
+        nb, nd = int(rows[bright].sum()), int(rows[~bright].sum())
+        b = n * 16 * nza + nb * (16 * nzb + 12 * k + 8 + 12 * s_sh) + nd * 32
+    if masks:
         b += n + 2 * 32 * tree.n_internal
     return b
+
+
+def visible_set_on(tree, rep) -> bool:
+    """Whether render-internal slices of this tree use the visible set (the
+    library's policy: trees without node masks or edits; VV_VISIBLE forces)."""
+    if getattr(tree, "has_edits", False) or getattr(tree, "edit_rgb", None) is not None:
+        return False
+    env = os.environ.get("VV_VISIBLE")
+    if env in ("0", "1"):
+        return env == "1"
+    return rep.dark_fraction < 0.25
 
 
 _RAYS = {}
@@ -494,9 +518,9 @@ class Stepper:
                 self.scene_plan._handle, stream_ptr(self.dev)))
             self.launches += 2  # scene kernel + plan order (every 4th)
             return
-        # exactly what render() does: the render-internal slice pass (colour of
-        # all-dark leaf chunks skipped; node masks for dark-heavy trees) ...
-        fs = vv.build_frame_caches(wl.tree, [f], render_only=True)[0]
+        # exactly what render() does: the render-internal slice pass (colour
+        # only for the tree's visible set; node masks for dark-heavy trees) ...
+        fs = vv.build_frame_caches(wl.tree, [f], visible=True)[0]
         if mid is not None:
             mid.record(stream)
         for cam, out, plan in zip(wl.cams, self.outs, self.plans):  # ... then the camera kernel(s)
@@ -807,15 +831,21 @@ def run_ours(args, rank, world, local_rank):
                 roofline["per_ray_masked_walk"] = {k: float(np.mean([ab[f][k + "m"] for f in step_frames]) / wl.rays)
                                                    for k in ("P", "V", "S")}
             sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
+            vis_on = wl.kind in ("single", "stereo") and visible_set_on(wl.tree, replica(wl.tree, dev))
             roofline["slice_pass"] = {
-                "kernel": "k_build_slice", "ms": round(slice_ms / n, 4),
+                "kernel": "k_slice_sigma + k_build_slice<VIS>" if vis_on else "k_build_slice",
+                "visible_set": vis_on, "ms": round(slice_ms / n, 4),
                 "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
                 "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
-                "bytes_formula": "per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
-                                 "per leaf of a 64-leaf chunk with a lit leaf + 16 B per nonzero w_gamma chunk + "
-                                 "12 K (w_hh) + 8 + 12 S_sh (record); of an all-dark chunk + 32 B (sigma); node "
-                                 "masks (dark-heavy trees): + 1 B/leaf + 64 B per internal node"}
+                "bytes_formula": ("visible set: per leaf 16 B per w_sigma float4 chunk the frame's A row does not "
+                                  "zero out; per leaf of a 64-leaf chunk holding a visible leaf + 16 B per nonzero "
+                                  "w_gamma chunk + 8 (sigma), per visible leaf + 12 K (w_hh) + 12 S_sh (colour); per "
+                                  "other leaf + 32 B (sigma pair); + 2 bits per leaf (the set)" if vis_on else
+                                  "per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
+                                  "per leaf of a 64-leaf chunk with a lit leaf + 16 B per nonzero w_gamma chunk + "
+                                  "12 K (w_hh) + 8 + 12 S_sh (record); of an all-dark chunk + 32 B (sigma)") +
+                                 "; node masks (dark-heavy trees): + 1 B/leaf + 64 B per internal node"}
             roofline["frame_achieved"] = round((rbytes + sbytes) / (total_ms / 1e3) / 1e9, 1)
 
     # CPU baseline: oracle port on one full step (rank 0, N = 1 only)

@@ -137,6 +137,12 @@ int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, in
  * T-1.  Above 0.5 the sliced camera and playback kernels walk with the long
  * segment queue (a kernel choice only: images are bitwise the same). */
 int vv_tree_dark_fraction(const vv_tree *tree, float *dark_frac);
+/* Size of the tree's visible set (VV_SLICE_VISIBLE): leaves in it and
+ * 64-leaf slice chunks holding one (synchronises `stream`). */
+int vv_tree_visible_count(const vv_tree *tree, int64_t *n_visible, int64_t *n_chunks, void *stream);
+/* The visible set itself: bit L of out (n_words >= 2 per 64 leaves) set
+ * iff device leaf row L is in it (synchronises `stream`). */
+int vv_tree_visible_bits(const vv_tree *tree, uint32_t *out, int64_t n_words, void *stream);
 /* The device's leaf layout: ref_rows[g] = reference row id of device row g
  * (n_leaves int32, host).  Leaves are stored in walk (BFS = Morton) order
  * when the node table is a tree, else in reference order. */
@@ -165,6 +171,13 @@ int vv_slice_build_multi(const vv_tree *tree, int32_t n_frames, const int32_t *f
  * can give a dark leaf density).  render()'s transient slices and the
  * playback groups are built this way. */
 #define VV_SLICE_RENDER_ONLY 1
+/* VV_SLICE_VISIBLE (with VV_SLICE_RENDER_ONLY, one frame): colour only for
+ * the leaves in the tree's visible set (the leaves its camera walks have
+ * shaded lately); a lit leaf outside it holds -sigma and the walk decodes
+ * its colour from the payload (bitwise the same) and adds it to the set.
+ * Images are bitwise unchanged.  Not exportable; single-frame walks only
+ * (VV_E_INVALID from vv_render_camera_multi). */
+#define VV_SLICE_VISIBLE 2
 int vv_slice_build_frames(const vv_tree *tree, int32_t n_frames, const int32_t *frames, int32_t flags,
                           void *stream, vv_slice **out);
 int vv_slice_free(vv_slice *slice);

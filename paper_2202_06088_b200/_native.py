@@ -56,6 +56,8 @@ EXPORTED_SYMBOLS = (
     "vv_tree_free",
     "vv_tree_info",
     "vv_tree_dark_fraction",
+    "vv_tree_visible_count",
+    "vv_tree_visible_bits",
     "vv_tree_leaf_order",
     "vv_slice_build",
     "vv_slice_free",
@@ -205,6 +207,7 @@ class InstanceDesc(ctypes.Structure):
 
 
 VV_SLICE_RENDER_ONLY = 1
+VV_SLICE_VISIBLE = 2
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -221,6 +224,8 @@ _SIGNATURES = {
     "vv_tree_free": (ctypes.c_int, [_P]),
     "vv_tree_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "vv_tree_dark_fraction": (ctypes.c_int, [_P, _P]),
+    "vv_tree_visible_count": (ctypes.c_int, [_P, _P, _P, _P]),
+    "vv_tree_visible_bits": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "vv_tree_leaf_order": (ctypes.c_int, [_P, _P]),
     "vv_slice_build": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_P)]),
     "vv_slice_free": (ctypes.c_int, [_P]),
@@ -322,7 +327,11 @@ def lib() -> ctypes.CDLL:
                 )
             handle = ctypes.CDLL(os.fspath(LIB_PATH))
             for name, (res, args) in _SIGNATURES.items():
-                fn = getattr(handle, name)
+                fn = getattr(handle, name, None)
+                if fn is None:
+                    if os.environ.get("VV_LIB_PATH"):  # an older A/B build: entry points it predates stay unbound
+                        continue
+                    raise ImportError(f"{LIB_PATH} does not export {name}")
                 fn.restype = res
                 fn.argtypes = args
             if handle.vv_abi_version() != 1:

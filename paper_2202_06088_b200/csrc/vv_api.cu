@@ -70,6 +70,16 @@ struct vv_tree {
     std::vector<int32_t> h_perm;
     uint64_t serial;  // unique per upload (caches keyed on a tree never see a reused address)
     double occ_lo[3], occ_hi[3];  // world box of the occupied leaf cells (empty: lo > hi)
+    // visible set (vis_begin): two bitmaps over leaf rows, filled by the
+    // camera walks; render-internal slices decode colour only for leaves in
+    // their union.  State advances per visible-set slice; races between
+    // streams only cost misses (the records, not the bitmaps, tell the walk
+    // which colours are present).
+    mutable std::mutex vis_mu;
+    mutable uint32_t *d_vis = nullptr;
+    mutable int64_t vis_words = 0;
+    mutable int vis_cur = 0, vis_slices = 0;
+    mutable bool vis_ready = false;
 };
 
 // Per-frame (or per frame group) node mask: the slice pass's lit bits, the
@@ -113,6 +123,9 @@ struct vv_slice {
     float4 *d_rec;  // (n_leaves, rec4) records [q | pad | sigma]
     int rec4;
     bool render_only;  // colour omitted where sigma is 0 (VV_SLICE_RENDER_ONLY): not exportable
+    bool visible = false;  // VV_SLICE_VISIBLE: colour only in the visible set (-sigma elsewhere)
+    uint32_t *vis_mark = nullptr;  // the set its walks mark
+    int vis_census = 0;
     int64_t n_leaves;
     cudaStream_t stream;  // stream-ordered allocation: freed on this stream
     std::shared_ptr<NodeMask> nmask;  // dark subtrees cut (image renders), or null
@@ -219,16 +232,111 @@ vv_render_opts default_opts() {
 }
 
 SliceView slice_view(const vv_slice *c) {
-    SliceView s{nullptr, 0};
+    SliceView s{nullptr, 0, 0, nullptr};
     if (c) {
         s.rec = c->d_rec;
         s.rec4 = c->rec4;
+        s.census = c->vis_census;
+        s.mark = c->vis_mark;
     }
     return s;
 }
 
+// ---- visible set (render-internal camera slices of trees without edits)
+// A render's walks can only reach a fraction of the leaves (cfg2: 19%, in
+// 52% of the 64-leaf chunks); the slice decodes colour -- 90% of its HBM
+// bytes -- for the leaves in the tree's visible set only, and writes -sigma
+// for a lit leaf outside it, whose colour the walk then decodes from the
+// payload (bitwise the same) and marks.  Two bitmaps: the slice decodes
+// their union; walks mark into the current one.  Every kVisEpoch slices the
+// older one is cleared and becomes current, and that slice's walks mark
+// every leaf they shade (a census), so the set follows the view and leaves
+// drop out within two epochs of last being seen.  The first slice decodes
+// every lit leaf, with a census.  VV_VISIBLE=0 turns the set off (A/B).
+constexpr int kVisEpoch = 8;
+
+struct VisTicket {
+    const uint32_t *d0 = nullptr, *d1 = nullptr;  // decode set (null: every lit leaf)
+    uint32_t *mark = nullptr;
+    int census = 0;
+};
+
+static bool mask_wanted(const vv_tree *t);
+// On for trees without node masks.  Dark-heavy trees (node masks: lit
+// leaves move from frame to frame, cfg3) defer too many pixels to the
+// per-sample walk: measured cfg3 0.94 vs 0.48 ms per frame with the set, cfg2
+// 0.831 vs 0.859, cfg5 1.811 vs 1.816 (profiles/r02_visible_set_ab.json).
+// VV_VISIBLE=0 / 1 forces it off / on.
+static bool vis_wanted(const vv_tree *t) {
+    if (t->has_edits || t->n_leaves == 0) return false;
+    if (const char *e = getenv("VV_VISIBLE")) {
+        if (e[0] == '0') return false;
+        if (e[0] == '1') return true;
+    }
+    return !mask_wanted(t);
+}
+
+static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt) {
+    vt = VisTicket();
+    if (!vis_wanted(t)) return VV_OK;
+    std::lock_guard<std::mutex> lk(t->vis_mu);
+    if (!t->d_vis) {
+        const int64_t words = ((t->n_leaves + 63) / 64) * 2;  // whole 64-leaf slice chunks
+        if (cudaMalloc(&t->d_vis, 2 * (size_t)words * sizeof(uint32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            t->d_vis = nullptr;
+            return VV_OK;  // no set: slices decode every lit leaf
+        }
+        VV_CUDA(cudaMemsetAsync(t->d_vis, 0, 2 * (size_t)words * sizeof(uint32_t), st));
+        t->vis_words = words;
+    }
+    uint32_t *b[2] = {t->d_vis, t->d_vis + t->vis_words};
+    if (!t->vis_ready) {
+        t->vis_ready = true;
+        t->vis_slices = 0;
+        vt.mark = b[t->vis_cur];
+        vt.census = 1;
+        return VV_OK;
+    }
+    if (++t->vis_slices % kVisEpoch == 0) {
+        t->vis_cur ^= 1;
+        VV_CUDA(cudaMemsetAsync(b[t->vis_cur], 0, (size_t)t->vis_words * sizeof(uint32_t), st));
+        vt.census = 1;
+    }
+    vt.d0 = b[0];
+    vt.d1 = b[1];
+    vt.mark = b[t->vis_cur];
+    return VV_OK;
+}
+
+// The slice pass p describes: with a visible set (the ticket's bitmaps),
+// k_slice_sigma + the colour pass over the chunks it lists (their list in
+// stream-ordered scratch), else the plain pass.
+static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *vt, cudaStream_t st) {
+    if (!vt || !vt->mark) return launch_slice(t->n_max, p, st);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int64_t n = (t->n_leaves + 63) / 64;
+    const size_t bytes = al((size_t)n * 4) + al((size_t)n * 8) + 256;
+    char *m = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&m), bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(VV_E_NOMEM, "visible-set chunk list (%zu bytes) failed", bytes);
+    }
+    p.vis0 = vt->d0;  // null: every leaf visible (a tree's first slice)
+    p.vis1 = vt->d1;
+    p.vis_list = reinterpret_cast<int32_t *>(m);
+    p.vis_vm = reinterpret_cast<uint64_t *>(m + al((size_t)n * 4));
+    p.vis_n = reinterpret_cast<int32_t *>(m + al((size_t)n * 4) + al((size_t)n * 8));
+    int rc = VV_OK;
+    if (cudaMemsetAsync(p.vis_n, 0, sizeof(int32_t), st) != cudaSuccess)
+        rc = set_error(VV_E_CUDA, "chunk counter memset failed");
+    if (!rc) rc = launch_slice_visible(t->n_max, p, st);
+    cudaFreeAsync(m, st);  // stream-ordered: after both passes
+    return rc;
+}
+
 int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only,
-                       uint8_t *lit = nullptr) {
+                       uint8_t *lit = nullptr, const VisTicket *vt = nullptr) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
     memset(&p, 0, sizeof(p));
@@ -242,7 +350,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
     p.skip_dark = render_only && !t->has_edits;
     p.lit = lit;
     set_slice_masks(t, p);
-    return launch_slice(t->n_max, p, st);
+    return launch_slice_vis(t, p, vt, st);
 }
 
 // Transient per-frame slice in the device's stream-ordered pool; freed
@@ -272,7 +380,7 @@ void pool_setup(int device) {
 // Node masks pay off when a frame leaves large subtrees dark (cfg3: ~90% of
 // leaves); they are skipped for trees with edits (an edit can give a dark
 // leaf density).  VV_NODE_MASK=0 / 1 forces them off / on (A/B and tests).
-bool mask_wanted(const vv_tree *t) {
+static bool mask_wanted(const vv_tree *t) {
     if (!t->mask_ok || t->has_edits || t->n_leaves == 0) return false;
     if (const char *e = getenv("VV_NODE_MASK")) {
         if (e[0] == '0') return false;
@@ -503,7 +611,7 @@ void affine_from_inverse(const double *inv, double *A) {
 
 // Transient per-call slice from the stream-ordered pool (freed, stream
 // ordered, when the call returns).
-int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr) {
+int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr, bool vis = false) {
     NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
@@ -519,9 +627,13 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     sv.rec = reinterpret_cast<float4 *>(tr.mem);
     sv.rec4 = rec4;
     int rc;
+    VisTicket vt;
+    if (vis && (rc = vis_begin(t, st, vt))) return rc;
+    sv.mark = vt.mark;
+    sv.census = vt.census;
     if (mask_wanted(t) && (rc = alloc_mask(t, st, tr.nmask))) return rc;
     rc = launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st, true,
-                            tr.nmask ? tr.nmask->lit : nullptr);
+                            tr.nmask ? tr.nmask->lit : nullptr, &vt);
     if (rc || !tr.nmask) return rc;
     return build_mask(t, *tr.nmask, st);
 }
@@ -532,9 +644,9 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
 // dark (their lit bytes are zeroed), which only cuts subtrees the region's
 // rays cannot reach.  Trees without chunk boxes slice every chunk.
 int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const vv_camera &cam, int rx0, int ry0,
-                           int rx1, int ry1, SliceView &sv, Transient &tr) {
+                           int rx1, int ry1, SliceView &sv, Transient &tr, bool vis = false) {
     NvtxRange nv("vv:slice(region, culled)");
-    if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr);
+    if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr, vis);
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
@@ -586,8 +698,12 @@ int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const v
     p.lit = tr.nmask ? tr.nmask->lit : nullptr;
     p.chunk_list = list;
     p.n_list = count;
+    VisTicket vt;
+    if (vis && (rc = vis_begin(t, st, vt))) return rc;
+    sv.mark = vt.mark;
+    sv.census = vt.census;
     set_slice_masks(t, p);
-    if ((rc = launch_slice(t->n_max, p, st))) return rc;
+    if ((rc = launch_slice_vis(t, p, &vt, st))) return rc;
     return tr.nmask ? build_mask(t, *tr.nmask, st) : VV_OK;
 }
 
@@ -1100,6 +1216,7 @@ int vv_tree_free(vv_tree *t) {
     cudaFree(t->d_box);
     cudaFree(t->d_leaf_ref);
     cudaFree(t->d_dev_row);
+    cudaFree(t->d_vis);
     delete t;
     return VV_OK;
 }
@@ -1128,6 +1245,46 @@ int vv_tree_leaf_order(const vv_tree *t, int32_t *ref_rows) {
 int vv_tree_dark_fraction(const vv_tree *t, float *dark_frac) {
     if (!t || !dark_frac) return set_error(VV_E_INVALID, "null argument");
     *dark_frac = t->dark_frac;
+    return VV_OK;
+}
+
+int vv_tree_visible_count(const vv_tree *t, int64_t *n_visible, int64_t *n_chunks, void *stream) {
+    if (!t || !n_visible) return set_error(VV_E_INVALID, "null argument");
+    *n_visible = 0;
+    if (n_chunks) *n_chunks = 0;
+    std::lock_guard<std::mutex> lk(t->vis_mu);
+    if (!t->d_vis) return VV_OK;
+    DeviceGuard g(t->device);
+    std::vector<uint32_t> h(2 * (size_t)t->vis_words);
+    VV_CUDA(cudaMemcpyAsync(h.data(), t->d_vis, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    VV_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    int64_t n = 0, c = 0;
+    for (int64_t w = 0; w < t->vis_words; w += 2) {
+        const uint64_t v = ((uint64_t)(h[w + 1] | h[t->vis_words + w + 1]) << 32) | (h[w] | h[t->vis_words + w]);
+        n += __builtin_popcountll(v);
+        c += v != 0;
+    }
+    *n_visible = n;
+    if (n_chunks) *n_chunks = c;
+    return VV_OK;
+}
+
+int vv_tree_visible_bits(const vv_tree *t, uint32_t *out, int64_t n_words, void *stream) {
+    if (!t || !out) return set_error(VV_E_INVALID, "null argument");
+    const int64_t need = ((t->n_leaves + 63) / 64) * 2;
+    if (n_words < need) return set_error(VV_E_INVALID, "%lld words for %lld", (long long)n_words, (long long)need);
+    std::lock_guard<std::mutex> lk(t->vis_mu);
+    if (!t->d_vis) {
+        memset(out, 0, (size_t)need * sizeof(uint32_t));
+        return VV_OK;
+    }
+    DeviceGuard g(t->device);
+    std::vector<uint32_t> h(2 * (size_t)t->vis_words);
+    VV_CUDA(cudaMemcpyAsync(h.data(), t->d_vis, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    VV_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int64_t w = 0; w < need; ++w) out[w] = h[w] | h[t->vis_words + w];
     return VV_OK;
 }
 
@@ -1175,9 +1332,12 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
                           vv_slice **out) {
     NvtxRange nv("vv:slice_build_frames");
     if (!t || !frames || !out) return set_error(VV_E_INVALID, "null argument");
-    if (flags & ~VV_SLICE_RENDER_ONLY) return set_error(VV_E_INVALID, "unknown slice flags 0x%x", flags);
+    if (flags & ~(VV_SLICE_RENDER_ONLY | VV_SLICE_VISIBLE))
+        return set_error(VV_E_INVALID, "unknown slice flags 0x%x", flags);
     if (n_frames < 1 || n_frames > kMaxMulti)
         return set_error(VV_E_UNSUPPORTED, "%d frames per slice pass (1..%d)", n_frames, kMaxMulti);
+    if ((flags & VV_SLICE_VISIBLE) && (n_frames != 1 || !(flags & VV_SLICE_RENDER_ONLY)))
+        return set_error(VV_E_INVALID, "VV_SLICE_VISIBLE takes one frame and VV_SLICE_RENDER_ONLY");
     for (int f = 0; f < n_frames; ++f) {
         int rc = check_frame(t, frames[f]);
         if (rc) return rc;
@@ -1220,6 +1380,15 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
     }
     if (t->n_leaves == 0) return VV_OK;
     p.skip_dark = (flags & VV_SLICE_RENDER_ONLY) && !t->has_edits;
+    VisTicket vt;
+    if (flags & VV_SLICE_VISIBLE) {
+        int vrc = vis_begin(t, (cudaStream_t)stream, vt);
+        if (vrc) return fail(vrc);
+        out[0]->visible = vt.mark != nullptr;
+        out[0]->vis_mark = vt.mark;
+        out[0]->vis_census = vt.census;
+
+    }
     set_slice_masks(t, p);
     // one node mask for the group: a subtree is kept if lit in any of its
     // frames (each frame's dark leaves still read sigma 0 from its record)
@@ -1227,7 +1396,7 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
     int rc;
     if (mask_wanted(t) && (rc = alloc_mask(t, (cudaStream_t)stream, nm))) return fail(rc);
     p.lit = nm ? nm->lit : nullptr;
-    rc = launch_slice(t->n_max, p, (cudaStream_t)stream);
+    rc = launch_slice_vis(t, p, &vt, (cudaStream_t)stream);
     if (!rc && nm) rc = build_mask(t, *nm, (cudaStream_t)stream);
     if (rc) return fail(rc);
     for (int f = 0; f < n_frames; ++f) out[f]->nmask = nm;
@@ -1253,6 +1422,9 @@ int vv_slice_export(const vv_slice *s, double *sigma, float *q, void *stream) {
     if (s->render_only && q)
         return set_error(VV_E_INVALID, "a render-only slice has no colour for dark leaves; build it without "
                                        "VV_SLICE_RENDER_ONLY to export q");
+    if (s->visible)
+        return set_error(VV_E_INVALID, "a VV_SLICE_VISIBLE slice holds -sigma outside the visible set: not "
+                                       "exportable");
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int S3 = 3 * s->tree->S;
@@ -1277,6 +1449,8 @@ static int render_rays_impl(const vv_tree *t, int32_t frame, const vv_slice *cac
     int rc = check_frame(t, frame);
     if (rc) return rc;
     if ((rc = check_cache(t, cache, frame))) return rc;
+    if (cache && cache->visible)
+        return set_error(VV_E_INVALID, "VV_SLICE_VISIBLE slices feed camera renders only");
     if (n == 0) return VV_OK;
     if (!origins || !dirs) return set_error(VV_E_INVALID, "null ray arrays");
     const bool visits = visit_leaf != nullptr;
@@ -1449,15 +1623,35 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     int mode = cache ? 1
                      : decode_mode(t, (rect ? 1.0 : share) * cube_footprint(*cam, lo, t->view.side, nullptr),
                                    opts.frame_slice);
+    // visible-set slices (image / region mode): the deferred-chunk list of
+    // k_camera_rewalk, zeroed before the slice pass (the PDL chain stays)
+    Transient td;
+    if (!tile && ((cache && cache->visible) || (!cache && mode != 0 && vis_wanted(t)))) {
+        pool_setup(t->device);
+        const size_t cap = (size_t)grid_blocks * kWarpsPerTile;
+        if (cudaMallocAsync(&td.mem, 256 + cap * sizeof(int4), st) != cudaSuccess) {
+            cudaGetLastError();
+            td.mem = nullptr;
+            return set_error(VV_E_NOMEM, "deferred-chunk list allocation failed");
+        }
+        td.st = st;
+        VV_CUDA(cudaMemsetAsync(td.mem, 0, sizeof(int), st));
+        p.n_deferred = static_cast<int *>(td.mem);
+        p.deferred = reinterpret_cast<int4 *>(static_cast<char *>(td.mem) + 256);
+    }
     if (!cache && mode != 0) {
-        int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr)
-                     : build_transient(t, frame, st, p.S, tr);
+        const bool vis = p.deferred != nullptr;
+        int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr, vis)
+                     : build_transient(t, frame, st, p.S, tr, vis);
         if (r) return r;
     }
     // sample counts report the reference's full walk: the tree's own table
     const NodeMask *nm = used ? nullptr : (cache ? cache->nmask.get() : tr.nmask.get());
     p.T.child = image_child(t, nm);
-    rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm));
+    if (p.S.mark && !p.deferred) return set_error(VV_E_INVALID, "visible-set slices: image or region renders only");
+    const bool vis = p.S.mark != nullptr;
+    rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm), vis);
+    if (!rc && vis) rc = launch_camera_rewalk(t->n_max, wide, p, st);
     if (rc || !plan) return rc;
     return plan_finish(plan, st);
 }
@@ -1666,6 +1860,9 @@ static int render_multi_impl(const vv_tree *t, int32_t n_frames, const int32_t *
         if (rc) return rc;
         if (!caches[k]) return set_error(VV_E_INVALID, "frame %d: a slice is required", frames[k]);
         if ((rc = check_cache(t, caches[k], frames[k]))) return rc;
+        if (caches[k]->visible)
+            return set_error(VV_E_INVALID, "frame %d: VV_SLICE_VISIBLE slices feed single-frame walks only",
+                             frames[k]);
     }
     DeviceGuard g(t->device);
     const vv_render_opts opts = o ? *o : default_opts();
@@ -1903,7 +2100,7 @@ static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_
     Transient tr[kMaxInst];
     for (int i = b; i < e; ++i) {
         InstView &v = p.inst[i - b];
-        v.S = SliceView{nullptr, 0};
+        v.S = SliceView{nullptr, 0, 0, nullptr};
         int same = -1;
         for (int j = b; j < i; ++j)
             if (inst[j].tree == inst[i].tree && inst[j].frame == inst[i].frame && p.inst[j - b].S.rec) same = j - b;

@@ -115,6 +115,14 @@ __device__ __forceinline__ uint32_t nz_chunks(const float *row, int C) {
 struct SliceView {
     const float4 *rec;  // (n_leaves, rec4) or null (decode per sample)
     int rec4;           // float4 per record = ceil((3S + 2) / 4)
+    // visible-set slices (render-internal camera slices of trees without
+    // edits; VIS kernels): colour only for the leaves of the tree's visible
+    // set; a lit leaf outside it holds -sigma (sigma itself is never
+    // negative).  A walk that meets one stops, and the pixel is walked again
+    // per sample (k_camera_rewalk), marking the leaves it visits in `mark`.
+    // With `census` set the sliced walk marks every leaf it visits.
+    int census;
+    uint32_t *mark;
     __device__ __forceinline__ const float4 *row(uint32_t L) const { return rec + (size_t)L * rec4; }
     __device__ __forceinline__ double sigma(uint32_t L) const {
         return __ldg(reinterpret_cast<const double *>(rec + (size_t)(L + 1) * rec4) - 1);
@@ -705,6 +713,9 @@ __device__ __forceinline__ void load_hh(const float4 *__restrict__ hh_row, float
     }
 }
 
+// visible-set bit of leaf row L (fire-and-forget reduction)
+__device__ __forceinline__ void vis_mark(uint32_t *m, uint32_t L) { atomicOr(m + (L >> 5), 1u << (L & 31)); }
+
 // ------------------------------------------------------------ shading visitor
 struct FrameCtx {
     const float *sA;   // A[t] row in shared memory
@@ -717,7 +728,11 @@ struct FrameCtx {
 
 // CACHED: 0 = decode per sample, 1 = read the frame slice, 2 = decided at
 // run time by S.rec != nullptr (scene kernel, per-instance slices).
-template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false, int SEG = VV_SEG_MIN>
+// VIS (camera kernel, visible-set slices): 1 = sliced walk that stops at a
+// leaf outside the slice's visible set (record sigma < 0; `deferred`: the
+// pixel is walked again per sample) and, in a census, marks every leaf it
+// shades; 2 = that per-sample walk again, marking every leaf it shades.
+template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false, int SEG = VV_SEG_MIN, int VIS = 0>
 struct Shader {
     static constexpr bool kPops = POPS;  // exact node-pop counts (stats)
     static constexpr int kSegMin = SEG, kSegSlots = SEG + 3;
@@ -729,6 +744,7 @@ struct Shader {
     double trans, acc0, acc1, acc2, aacc, tacc;
     int used, pops, shaded;
     bool y_ready;
+    bool deferred = false;  // VIS 1: met a leaf outside the visible set
     float y[Basis<NMAX>::S];
     int64_t *visit;  // VISITS: this ray's slice of the CSR
 
@@ -804,8 +820,19 @@ struct Shader {
         // from the payload (render_kernel's uncached branch)
         const bool from_rec = is_cached();
         double sigma;
+        // visible-set walks: a deferred pixel's walk (VIS 2) and a census put
+        // every leaf they visit in the set
+#ifndef VV_VIS_NOCENSUS
+        if (VIS == 2 || (VIS == 1 && S.census)) vis_mark(S.mark, L);
+#else
+        if (VIS == 2) vis_mark(S.mark, L);
+#endif
         if (from_rec) {
             sigma = sigma_cached;
+            if (VIS == 1 && sigma < 0.0) {  // colour not in the slice: the pixel is walked again per sample
+                deferred = true;
+                return true;
+            }
         } else {
             const double sp = sigma_pre(T.sig + L, T.lstride, F.sA, T.C, F.mA);
             sigma = sp > 0.0 ? sp : 0.0;

@@ -149,6 +149,12 @@ struct CamParams {
     // by the production instantiation itself, so its walk is checked
     // bit-exactly against the oracle
     int32_t *used;
+    // visible-set slices (VIS kernels, image / region mode): a warp chunk
+    // holding a pixel whose walk met a leaf outside the set is listed --
+    // (tile x0, tile y0, chunk in tile, lane mask) -- and k_camera_rewalk
+    // walks those pixels again per sample, then counts the chunk for its band
+    int4 *deferred;
+    int *n_deferred;
 };
 
 // block = 16x8 pixels; warp = 16x2 pixels (spatially coherent rays)
@@ -226,10 +232,67 @@ __device__ __forceinline__ void cam_write(const CamParams &p, bool inside, long 
 // (persistent) variants were measured slower: see DESIGN.md.
 constexpr int kWarpsPerTile = kTileRays / 32;
 
+// Lists the warp chunk when a lane deferred its pixel (every lane calls it).
+__device__ __forceinline__ bool defer_chunk(const CamParams &p, bool deferred, int tx0, int ty0, int chunk) {
+#ifdef VV_VIS_NODEFER
+    return false;
+#endif
+    const unsigned m = __ballot_sync(0xffffffffu, deferred);
+    if (!m) return false;
+    if ((threadIdx.x & 31) == 0) p.deferred[atomicAdd(p.n_deferred, 1)] = make_int4(tx0, ty0, chunk, (int)m);
+    return true;
+}
+
+// Visible-set renders, second kernel: the listed pixels walked again from
+// the start, decoding per sample -- the segments, sigma and colour
+// arithmetic of the sliced walk, so the same bits -- marking the leaves
+// they shade for the next frame's slice; each chunk is then counted for its
+// band (banded host copies).  A separate launch keeps this walk's registers
+// out of the camera kernel (in-kernel it cost 8%).
+template <int NMAX, class Entry>
+__global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_camera_rewalk(const __grid_constant__ CamParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame, sA, sB);
+    __syncthreads();
+    const FrameCtx F{sA, sB, p.frame, p.early_stop, p.edit_weight, nz_chunks(sA, p.T.C), nz_chunks(sB, p.T.C)};
+    pdl_trigger();
+    pdl_wait();  // the camera kernel's list is complete
+    const int n = *(volatile const int *)p.n_deferred;
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)gridDim.x * kWarpsPerTile;
+    for (int k = (int)blockIdx.x * kWarpsPerTile + (int)(threadIdx.x >> 5); k < n; k += nw) {
+        const int4 e = p.deferred[k];
+        if (((unsigned)e.w >> lane) & 1u) {
+            int dx_, dy_;
+            local_pixel(e.z * 32 + lane, dx_, dy_);
+            const int ix = e.x + dx_, iy = e.y + dy_;
+            const long long slot = (long long)iy * p.cam.width + ix;
+            double dx, dy, dz;
+            camera_ray(p.cam, ix, iy, dx, dy, dz);
+            Ray ray;
+            Shader<NMAX, 0, false, false, false, VV_SEG_MIN, 2> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+            if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
+                traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+            float r, g, b, a, d;
+            finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b, a,
+                     d);
+            if (p.used) p.used[slot] = sh.used;
+            cam_write(p, true, slot, r, g, b, a, d);
+        }
+        if (p.band_done) {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(p.band_done + (e.y - p.ry0) / p.band_rows, 1u);
+        }
+    }
+    if (p.peer) __threadfence_system();
+}
+
 // one pixel of the camera kernel (image / region mode) after the slice wait
-template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG>
+template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG, int VIS = 0>
 __device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &F, unsigned char *smem, int ix,
-                                            int iy) {
+                                            int iy, bool &deferred) {
     const long long slot = (long long)iy * p.cam.width + ix;
     const bool inside = ix < p.rx1 && iy < p.ry1;
     float r = 0.f, g = 0.f, b = 0.f, a = 0.f, d = (float)p.far_plane;
@@ -242,8 +305,9 @@ __device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &
         camera_ray(p.cam, ix, iy, dx, dy, dz);
         Ray ray;
         const bool hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
-        Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+        Shader<NMAX, CACHED, EDITS, false, false, SEG, VIS> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
         if (hit) traverse<Entry>(p.T.child, p.T.depth, ray, smem, sh);
+        deferred = VIS && sh.deferred;  // k_camera_rewalk writes this pixel
         finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b, a, d);
         if (p.used) p.used[slot] = sh.used;
         cost = sh.used + 1;
@@ -252,7 +316,7 @@ __device__ __forceinline__ int camera_pixel(const CamParams &p, const FrameCtx &
     return cost;
 }
 
-template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN>
+template <int NMAX, int CACHED, bool EDITS, class Entry, int SEG = VV_SEG_MIN, int VIS = 0>
 __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(const __grid_constant__ CamParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float sA[kMaxC], sB[kMaxC];
@@ -274,9 +338,17 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             const int tb = p.block_order ? __ldg(p.block_order + idx / kWarpsPerTile) : idx / kWarpsPerTile;
             int dx_, dy_;
             local_pixel((idx % kWarpsPerTile) * 32 + lane, dx_, dy_);
-            const int cost = camera_pixel<NMAX, CACHED, EDITS, Entry, SEG>(
-                p, F, smem_raw, p.rx0 + (tb % p.blocks_x) * kTW + dx_, p.ry0 + (tb / p.blocks_x) * kTH + dy_);
-            if (p.band_done) {
+            bool deferred = false;
+            const int cost = camera_pixel<NMAX, CACHED, EDITS, Entry, SEG, VIS>(
+                p, F, smem_raw, p.rx0 + (tb % p.blocks_x) * kTW + dx_, p.ry0 + (tb / p.blocks_x) * kTH + dy_, deferred);
+            // (the chunk's origin recomputed behind an opaque copy of tb: kept
+            // live across the walk it costs the kernel 10%)
+            int tbv = tb;
+            if (VIS) asm volatile("" : "+r"(tbv));
+            if (VIS && defer_chunk(p, deferred, p.rx0 + (tbv % p.blocks_x) * kTW, p.ry0 + (tbv / p.blocks_x) * kTH,
+                                   idx % kWarpsPerTile)) {
+                // counted for its band by k_camera_rewalk
+            } else if (p.band_done) {
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) atomicAdd(p.band_done + (tb / p.blocks_x) * kTH / p.band_rows, 1u);
@@ -311,7 +383,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         const bool inside = p.tile ? (ix < p.cam.width && iy < p.cam.height) : (ix < p.rx1 && iy < p.ry1);
         double dx = 0.0, dy = 0.0, dz = 1.0;
         Ray ray;
-        bool hit = false;
+        bool hit = false, deferred = false;
         if (inside) {  // pure arithmetic: overlaps the previous kernel's tail
             camera_ray(p.cam, ix, iy, dx, dy, dz);
             hit = ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray);
@@ -319,15 +391,18 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         pdl_trigger();
         pdl_wait();  // the frame slice (and node mask, coverage) is complete; earlier writers of the outputs are done
         if (inside) {
-            Shader<NMAX, CACHED, EDITS, false, false, SEG> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
+            Shader<NMAX, CACHED, EDITS, false, false, SEG, VIS> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
             if (hit && (p.tile || (ix >= p.cx0 && ix <= p.cx1 && iy >= p.cy0 && iy <= p.cy1 && covered(p.cov, ix, iy))))
                 traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+            deferred = VIS && sh.deferred;
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b,
                      a, d);
             if (p.used) p.used[slot] = sh.used;
         }
         cam_write(p, inside, slot, r, g, b, a, d);
-        if (p.band_done) {  // this warp's pixels are stored: count it for its band
+        if (VIS && !p.tile && defer_chunk(p, deferred, x0, y0, (int)(threadIdx.x >> 5))) {
+            // counted for its band by k_camera_rewalk
+        } else if (p.band_done) {  // this warp's pixels are stored: count it for its band
             __threadfence();
             __syncwarp();
             if ((threadIdx.x & 31) == 0) atomicAdd(p.band_done + (y0 - p.ry0) / p.band_rows, 1u);
@@ -659,6 +734,17 @@ struct SliceParams {
     // k_chunk_cull, the previous kernel -- read after griddepcontrol.wait)
     const int32_t *chunk_list;
     const int32_t *n_list;
+    // visible-set passes (k_slice_sigma, then k_build_slice<.., VIS> over
+    // the chunks it lists): the tree's visible set is the union of two
+    // bitmaps over leaf rows; only leaves in it get their colour, a lit leaf
+    // outside it -sigma (SliceView).  k_slice_sigma writes every record
+    // outside the set and lists each chunk holding a visible leaf with the
+    // 64-bit snapshot of its bits (vis_list / vis_vm / vis_n) that the
+    // colour pass then decodes -- what one pass fetches is what it decodes.
+    const uint32_t *vis0, *vis1;
+    int32_t *vis_list;
+    uint64_t *vis_vm;
+    int32_t *vis_n;
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -713,7 +799,7 @@ __host__ __device__ inline size_t slice_out_floats4(int kf, int r4) {
 // (f64) and KF gamma (fp32) accumulators side by side -- each frame keeps
 // exactly its single-frame summation order -- and w_hh is loaded once for
 // the KF HH->SH slices.
-template <int NMAX, int KF>
+template <int NMAX, int KF, bool VIS = false>
 __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_constant__ SliceParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
@@ -754,9 +840,11 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // neighbours in HBM
     int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
 #endif
-    // list mode: positions in the chunk list instead of chunk ids
-    const bool listed = p.chunk_list != nullptr;
-    auto chunk_at = [&](int64_t i) -> int64_t { return listed ? (int64_t)p.chunk_list[i] : i; };
+    // list mode: positions in the chunk list instead of chunk ids (VIS: the
+    // visible-set chunk list k_slice_sigma wrote)
+    const bool listed = VIS || p.chunk_list != nullptr;
+    const int32_t *list = VIS ? p.vis_list : p.chunk_list;
+    auto chunk_at = [&](int64_t i) -> int64_t { return listed ? (int64_t)list[i] : i; };
     // stage: [needed w_sigma chunks][kChunk leaves] | [needed w_gamma chunks][kChunk] | [leaves][hh4]
     auto rows_of = [&](int64_t c) { return (int)min((int64_t)kChunk, p.n_leaves - c * kChunk); };
     (void)rows_of;
@@ -770,14 +858,35 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
             bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, b);
         bulk_g2s(dst, p.T.hh + base * hh4, hb, b);
     };
-    auto issue = [&](int64_t c, int stg, bool colour) {  // lane 0
+    static_assert(!VIS || (KF == 1 && slice_chunk(1) == 64 && VV_SLICE_STAGE_OUT),
+                  "visible-set passes slice one frame in 64-leaf chunks through the staged stores");
+    constexpr bool vis = VIS;
+    auto issue = [&](int64_t c, int stg, bool colour, uint64_t vm) {  // lane 0
         const int64_t base = c * kChunk;
         const int rows = rows_of(c);
         float4 *dst = wbase + stg * stage4;
         const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
-        mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
+        if (vis) {  // sigma planes; the gamma planes and the visible leaves' w_hh rows when any is visible
+            const uint32_t hv = (uint32_t)__popcll(vm) * hh4 * 16;
+            mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (vm ? (uint32_t)nG * cb + hv : 0u));
+        } else {
+            mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
+        }
         for (uint32_t m = mS; m; m &= m - 1, dst += kChunk)
             bulk_g2s(dst, p.T.sig + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
+        if (vis) {
+            if (!vm) return;
+            for (uint32_t m = mG; m; m &= m - 1, dst += kChunk)
+                bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
+            for (uint64_t m = vm; m;) {  // runs of visible rows, at their rows' stage offsets
+                const int r0 = __ffsll((long long)m) - 1;
+                const uint64_t rest = ~(m >> r0);
+                const int len = rest ? __ffsll((long long)rest) - 1 : 64 - r0;
+                bulk_g2s(dst + (size_t)r0 * hh4, p.T.hh + (base + r0) * hh4, (uint32_t)len * hh4 * 16, &bar[stg]);
+                m &= len >= 64 ? 0ull : ~(((1ull << len) - 1ull) << r0);
+            }
+            return;
+        }
         if (colour) issue_colour(c, stg, &bar[stg], false);
     };
     // colour rows are staged with the sigma chunks while the chunks are
@@ -786,14 +895,19 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // written, and while chunks stay dark the colour rows are not fetched
     // (render-internal slices of trees without edits: p.skip_dark)
     uint32_t colour_in = 3u;  // bit s: stage s was issued with its colour rows
-    if (lane == 0 && !listed) {  // payload reads only: may overlap the previous kernel
-        if (c_begin < c_end) issue(c_begin, 0, true);
-        if (c_begin + c_step < c_end) issue(c_begin + c_step, 1, true);
+    // lane 0 stages list position i (its chunk and, VIS, its snapshot)
+    auto stage = [&](int64_t i, int stg, bool colour) {
+        issue(chunk_at(i), stg, colour, vis ? p.vis_vm[i] : 0ull);
+    };
+    // payload reads only: may overlap the previous kernel
+    if (lane == 0 && !listed) {
+        if (c_begin < c_end) stage(c_begin, 0, true);
+        if (c_begin + c_step < c_end) stage(c_begin + c_step, 1, true);
     }
     pdl_trigger();
     pdl_wait();  // no record is written before the previous kernel is complete
     if (listed) {  // the list is the previous kernel's output
-        const int64_t nl = (int64_t)*(volatile const int32_t *)p.n_list;
+        const int64_t nl = (int64_t)*(volatile const int32_t *)(VIS ? p.vis_n : p.n_list);
 #if VV_SLICE_RUNS
         c_begin = nl * wid / n_warps;
         c_end = nl * (wid + 1) / n_warps;
@@ -801,8 +915,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         c_end = nl;
 #endif
         if (lane == 0) {
-            if (c_begin < c_end) issue(chunk_at(c_begin), 0, true);
-            if (c_begin + c_step < c_end) issue(chunk_at(c_begin + c_step), 1, true);
+            if (c_begin < c_end) stage(c_begin, 0, true);
+            if (c_begin + c_step < c_end) stage(c_begin + c_step, 1, true);
         }
     }
     uint32_t late_par = 0;  // phase parity of bar[2], bar[3]
@@ -842,8 +956,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 for (int f = 0; f < KF; ++f) lit |= sp[u][f] > 0.0;
             }
         }
-        const bool bright = !p.skip_dark || __any_sync(0xffffffffu, lit);
-        if (bright && !((colour_in >> stg) & 1u)) {  // mispredicted dark: fetch the colour rows now
+        const uint64_t vm = vis ? p.vis_vm[ci] : 0ull;  // every lane: the snapshot lane 0 staged
+        const bool bright = vis || !p.skip_dark || __any_sync(0xffffffffu, lit);
+        if (!vis && bright && !((colour_in >> stg) & 1u)) {  // mispredicted dark: fetch the colour rows now
             if (lane == 0) {
                 fence_proxy_async();  // the colour region was last read through the generic proxy
                 issue_colour(c, stg, &bar[2 + stg], true);
@@ -860,6 +975,16 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
 #pragma unroll
                 for (int f = 0; f < KF; ++f) bits |= (sp[u][f] > 0.0 ? 1u : 0u) << f;
                 p.lit[base + r] = (uint8_t)bits;
+            }
+            if (vis && !((vm >> r) & 1ull)) {  // outside the set: sigma only, negated when lit (staged)
+                float4 *o = obuf + (size_t)r * (R4 + 1);
+                const double sigma = sp[u][0] > 0.0 ? -sp[u][0] : 0.0;
+                const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+#pragma unroll
+                for (int i = 0; i < R4 - 1; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                o[R4 - 1] = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
+                                        __uint_as_float((unsigned)(sb >> 32)));
+                continue;
             }
             if (!bright) {  // sigma only: the record's last float4 pair (one sector at even R4)
 #pragma unroll
@@ -932,7 +1057,72 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
         colour_in = (colour_in & ~(1u << stg)) | ((uint32_t)bright << stg);
         if (lane == 0 && ci + 2 * c_step < c_end) {
             fence_proxy_async();
-            issue(chunk_at(ci + 2 * c_step), stg, bright);
+            stage(ci + 2 * c_step, stg, bright);
+        }
+    }
+}
+
+// Visible-set slice, first pass: one warp per 64-leaf chunk (every chunk,
+// or the region's chunk list).  Lane 0 reads the chunk's visible bits once
+// (the snapshot; no bitmaps: every leaf visible, a tree's first slice).  A
+// chunk holding a visible leaf goes, with its snapshot, to the list that
+// k_build_slice<.., VIS> writes whole (colour for the set's leaves, -sigma
+// for a lit other).  Every leaf of the other chunks gets its sigma-only
+// record here -- sigma_pre in f64 exactly as k_build_slice
+// (kernels.py:374-381), negated when lit -- and, for node masks, its lit
+// byte.  Thread per leaf over coalesced w_sigma planes; the record's last
+// 64 aligned bytes are stored whole (a 32-byte store costs the same DRAM
+// read-modify-write).
+template <int NMAX>
+__global__ void __launch_bounds__(256) k_slice_sigma(const __grid_constant__ SliceParams p) {
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame[0], sA, sB);
+    __syncthreads();
+    constexpr int R4 = slice_rec4(Basis<NMAX>::S);
+#ifndef VV_SIGMA_TAIL
+#define VV_SIGMA_TAIL 2  // float4 per sigma-only record: 32 B measured best (0.166 ms vs 0.191 with 64 B at cfg2)
+#endif
+    constexpr int TAIL = R4 % VV_SIGMA_TAIL == 0 ? VV_SIGMA_TAIL : (R4 % 2 == 0 ? 2 : 1);  // float4 per sigma-only record
+    const int lane = threadIdx.x & 31;
+    const bool listed = p.chunk_list != nullptr;
+    const bool all = p.vis0 == nullptr;
+    pdl_trigger();
+    pdl_wait();  // the bitmaps, the region list and the zeroed counter are the previous work's
+    const int64_t n_chunks = (p.n_leaves + 63) / 64;
+    const int64_t n_items = listed ? (int64_t)*(volatile const int32_t *)p.n_list : n_chunks;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_items; i += nw) {
+        const int64_t c = listed ? (int64_t)p.chunk_list[i] : i;
+        const int64_t base = c * 64;
+        const int rows = (int)min((int64_t)64, p.n_leaves - base);
+        unsigned lo = ~0u, hi = ~0u;
+        if (lane == 0 && !all) {
+            lo = __ldcg(p.vis0 + 2 * c) | __ldcg(p.vis1 + 2 * c);
+            hi = __ldcg(p.vis0 + 2 * c + 1) | __ldcg(p.vis1 + 2 * c + 1);
+        }
+        uint64_t vm = ((uint64_t)__shfl_sync(0xffffffffu, hi, 0) << 32) | __shfl_sync(0xffffffffu, lo, 0);
+        if (rows < 64) vm &= (1ull << rows) - 1ull;
+        if (vm) {
+            if (lane == 0) {
+                const int k = atomicAdd(p.vis_n, 1);
+                p.vis_list[k] = (int32_t)c;
+                p.vis_vm[k] = vm;
+            }
+            continue;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int r = lane + 32 * u;
+            if (r >= rows) continue;
+            const double sp = sigma_pre(p.T.sig + base + r, p.T.lstride, sA, p.T.C, p.mS);
+            if (p.lit) p.lit[base + r] = sp > 0.0 ? 1u : 0u;
+            const double sigma = sp > 0.0 ? -sp : 0.0;
+            const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+            float4 *o = p.rec[0] + (base + r + 1) * p.rec4 - TAIL;
+#pragma unroll
+            for (int k = 0; k < TAIL - 1; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            o[TAIL - 1] = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
+                                      __uint_as_float((unsigned)(sb >> 32)));
         }
     }
 }
@@ -1122,14 +1312,20 @@ int launch_rays(int nmax, int mode, bool edits, bool wide, bool visits, const Ra
 // one block per 32x16 tile (max_blocks = tile count)
 int launch_count_dark(const TreeView &T, int frame, uint32_t mS, int64_t n, unsigned long long *count,
                       cudaStream_t st);
+// visible-set renders: the walk of the deferred pixels (after launch_camera with vis)
+int launch_camera_rewalk(int nmax, bool wide, const CamParams &p, cudaStream_t st);
+// vis: the slice is a visible-set slice (p.S.mark set; sliced, no edits)
 int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p, unsigned max_blocks, size_t smem,
-                  cudaStream_t st, bool long_queue = false);
+                  cudaStream_t st, bool long_queue = false, bool vis = false);
 int launch_camera_multi(int nmax, int kf, bool edits, bool wide, const CamMultiParams &p, unsigned grid,
                         cudaStream_t st, bool long_queue = false);
 int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid, size_t smem, cudaStream_t st);
 // per-sample depth-ordered joint composition (vv_launch_joint.cu)
 int launch_scene_joint(int nmax, bool wide, const SceneParams &p, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
+// visible-set slice of one frame: k_slice_sigma, then k_build_slice<.., VIS>
+// over the chunks it lists (p.vis0/vis1, p.vis_list/vis_vm/vis_n; vis_n zeroed)
+int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st);
 // per-frame node mask (vv_launch_mask.cu): child table with every child whose
 // subtree holds no lit leaf replaced by -1
 struct MaskParams {

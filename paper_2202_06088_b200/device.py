@@ -181,6 +181,27 @@ class DeviceTree:
         _native.check(_native.lib().vv_tree_dark_fraction(self.handle, ctypes.byref(v)))
         return float(v.value)
 
+    def visible_count(self) -> tuple:
+        """(leaves, 64-leaf chunks) in the tree's visible set -- what a
+        render-internal slice decodes colour for (synchronises the device)."""
+        import torch
+
+        n, c = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(_native.lib().vv_tree_visible_count(
+            self.handle, ctypes.byref(n), ctypes.byref(c), ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+        return int(n.value), int(c.value)
+
+    def visible_mask(self) -> np.ndarray:
+        """Per device leaf row: whether it is in the tree's visible set."""
+        import torch
+
+        words = ((self.n_leaves + 63) // 64) * 2
+        out = np.zeros(max(words, 1), dtype=np.uint32)
+        _native.check(_native.lib().vv_tree_visible_bits(
+            self.handle, out.ctypes.data, words, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+        bits = np.unpackbits(out.view(np.uint8), bitorder="little").astype(bool)
+        return bits[: self.n_leaves]
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:

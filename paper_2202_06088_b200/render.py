@@ -352,24 +352,31 @@ def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
     return FrameSlice(frame, handle, rep, dev)
 
 
-def build_frame_caches(tree, frames, device=None, *, render_only: bool = False) -> list:
+def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, visible: bool = False) -> list:
     """Slices of 1..4 frames from ONE pass over the payload (vv_slice_build_multi):
     each leaf row is read once and sliced per frame; ``[build_frame_cache(tree, f) for f in frames]``
     with a quarter to a half of the HBM traffic.  ``render_only``: the
     colour of leaves dark (sigma 0) in every frame is omitted
     (VV_SLICE_RENDER_ONLY) -- rendering is bitwise the same, ``q`` cannot be
-    read."""
+    read.  ``visible`` (one frame, implies ``render_only``): colour only for
+    the tree's visible set -- the leaves its camera renders have shaded
+    lately; the walk decodes any other lit leaf it meets from the payload
+    (VV_SLICE_VISIBLE; what render() slices internally).  Single-frame
+    renders only: ``render_frames_into`` rejects such a slice."""
     frames = [_frame_index(f, tree) for f in frames]
     for f in frames:
         _check_frame(tree, f)
     if not 1 <= len(frames) <= 4:
         raise ValueError("1..4 frames per slice pass")
+    if visible and len(frames) != 1:
+        raise ValueError("a visible-set slice holds one frame")
+    flags = (_native.VV_SLICE_RENDER_ONLY if render_only or visible else 0) | \
+        (_native.VV_SLICE_VISIBLE if visible else 0)
     dev = torch_device(device)
     rep = replica(tree, dev)
     n = len(frames)
     handles = (ctypes.c_void_p * n)()
-    _native.check(_native.lib().vv_slice_build_frames(rep.handle, n, (ctypes.c_int32 * n)(*frames),
-                                                      _native.VV_SLICE_RENDER_ONLY if render_only else 0,
+    _native.check(_native.lib().vv_slice_build_frames(rep.handle, n, (ctypes.c_int32 * n)(*frames), flags,
                                                       stream_ptr(dev), handles))
     return [FrameSlice(f, ctypes.c_void_p(h), rep, dev) for f, h in zip(frames, handles)]
 

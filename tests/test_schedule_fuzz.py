@@ -73,8 +73,9 @@ def test_schedules_bitwise(cuda, seed, monkeypatch):
         cam = _camera(rng, tree, w, h)
         for f in (0, 2, 5):
             ref = vv.render(tree, cam, f, vv.RenderOptions(frame_slice="per_sample"), out="torch")
-            for mask in ("0", "1"):
+            for mask, vis in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
                 monkeypatch.setenv("VV_NODE_MASK", mask)
+                monkeypatch.setenv("VV_VISIBLE", vis)
                 for mode in ("per_frame", "auto"):
                     opts = vv.RenderOptions(frame_slice=mode)
                     out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda),
@@ -88,6 +89,7 @@ def test_schedules_bitwise(cuda, seed, monkeypatch):
                 _eq(host.rgb, ref.rgb, f"host rgb mask{mask} f{f}")
                 _eq(host.depth, ref.depth, f"host depth mask{mask} f{f}")
             monkeypatch.delenv("VV_NODE_MASK")
+            monkeypatch.delenv("VV_VISIBLE")
         # regions (culled slices) and playback
         costs = pixel_costs(tree, cam, 0)
         edges = band_plan(costs.sum(dim=1).cpu().numpy(), int(rng.integers(2, 5)))

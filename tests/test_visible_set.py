@@ -1,0 +1,149 @@
+"""Visible-set slices (VV_SLICE_VISIBLE; render()'s internal camera slices):
+the slice decodes colour only for the leaves the tree's recent walks shaded,
+stores -sigma for other lit leaves, and the walk decodes those from the
+payload and marks them.  Images must stay bitwise equal to the per-sample
+render through first frames, census frames, epoch rotations, camera moves,
+regions, shared stereo slices and render_rays on such a slice."""
+
+import numpy as np
+import pytest
+
+import paper_2202_06088_b200 as vv
+from trees import random_payload_tree
+
+pytestmark = pytest.mark.gpu
+PS = vv.RenderOptions(frame_slice="per_sample")
+
+
+@pytest.fixture(autouse=True)
+def _visible_on(monkeypatch):
+    """The set is on by default only for trees without node masks; these
+    random trees are dark-heavy, so force it."""
+    monkeypatch.setenv("VV_VISIBLE", "1")
+
+
+def _eq(a, b, what):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    b = b.cpu().numpy() if hasattr(b, "cpu") else np.asarray(b)
+    assert np.array_equal(a, b), f"{what}: {np.count_nonzero(a != b)} mismatches"
+
+
+def _orbit(i, w=72, h=54):
+    a = 0.21 * i
+    return vv.Camera.look_at([0.5 + 2.2 * np.cos(a), 0.5 + 2.2 * np.sin(a), 1.2 + 0.1 * np.sin(3 * a)],
+                             [0.5, 0.5, 0.45], width=w, height=h, focal=70.0)
+
+
+@pytest.fixture(scope="module")
+def tree():
+    rng = np.random.default_rng(11)
+    return random_payload_tree(rng, depth=5, fill=0.45, frames=9, n_max=2, sigma_scale=5.0)
+
+
+def test_render_epochs_and_moving_camera(cuda, tree):
+    """30 renders (several epochs of 8, census frames) on one camera, then an
+    orbit: every image bitwise the per-sample render."""
+    import torch
+
+    cam = _orbit(0)
+    h, w = cam.height, cam.width
+    out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda)]
+    for i in range(30):
+        f = (5 * i) % 9
+        vv.render_into(tree, cam, f, *out, vv.RenderOptions(frame_slice="per_frame"))
+        ref = vv.render(tree, cam, f, PS, out="torch")
+        torch.cuda.synchronize()
+        _eq(out[0], ref.rgb, f"static rgb {i}")
+        _eq(out[2], ref.depth, f"static depth {i}")
+    for i in range(24):
+        c = _orbit(i)
+        got = vv.render(tree, c, i % 9)  # host path (banded copies), internal visible slice
+        ref = vv.render(tree, c, i % 9, PS)
+        _eq(got.rgb, ref.rgb, f"orbit rgb {i}")
+        _eq(got.alpha, ref.alpha, f"orbit alpha {i}")
+
+
+def test_shared_visible_cache_stereo_and_rays(cuda, tree):
+    import torch
+
+    eyes = [_orbit(3), _orbit(4)]
+    for i in range(12):
+        f = i % 9
+        fs = vv.build_frame_caches(tree, [f], visible=True)[0]
+        for e, cam in enumerate(eyes):
+            h, w = cam.height, cam.width
+            out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda),
+                   torch.empty((h, w), device=cuda)]
+            vv.render_into(tree, cam, f, *out, cache=fs)
+            ref = vv.render(tree, cam, f, PS, out="torch")
+            torch.cuda.synchronize()
+            _eq(out[0], ref.rgb, f"eye {e} rgb {i}")
+        # sample counts of a camera render on a visible-set slice: the
+        # reference's (deferred pixels report their per-sample walk)
+        cam = eyes[0]
+        h, w = cam.height, cam.width
+        cnt = torch.empty((h, w), dtype=torch.int32, device=cuda)
+        ref_cnt = torch.empty((h, w), dtype=torch.int32, device=cuda)
+        img = torch.empty((h, w, 3), device=cuda)
+        vv.render_into(tree, cam, f, img, None, None, cache=fs, sample_count=cnt)
+        vv.render_into(tree, cam, f, torch.empty_like(img), None, None, PS, sample_count=ref_cnt)
+        torch.cuda.synchronize()
+        _eq(cnt, ref_cnt, f"sample counts {i}")
+        del fs
+
+
+def test_visible_cache_rules(cuda, tree):
+    with pytest.raises(ValueError):
+        vv.build_frame_caches(tree, [0, 1], visible=True)
+    fs = vv.build_frame_caches(tree, [2], visible=True)[0]
+    with pytest.raises(Exception):
+        fs.sigma  # noqa: B018 -- not exportable
+    o, d = _orbit(1).rays()
+    with pytest.raises(Exception):
+        vv.render_rays(tree, o, d, 2, cache=fs)  # camera renders only
+    import torch
+
+    cam = _orbit(1)
+    outs = [(torch.empty((cam.height, cam.width, 3), device=cuda), torch.empty((cam.height, cam.width), device=cuda),
+             torch.empty((cam.height, cam.width), device=cuda)) for _ in range(2)]
+    fs2 = vv.build_frame_caches(tree, [3], visible=True)[0]
+    from paper_2202_06088_b200 import _native
+    from paper_2202_06088_b200.device import replica, stream_ptr
+    import ctypes
+
+    rep = replica(tree, cuda)
+    P = ctypes.c_void_p
+    oc, cd = vv.RenderOptions().c_struct(), cam.desc()
+    rc = _native.lib().vv_render_camera_multi(
+        rep.handle, 2, (ctypes.c_int32 * 2)(2, 3), (P * 2)(fs._handle, fs2._handle), ctypes.byref(oc),
+        ctypes.byref(cd), (P * 2)(*[o[0].data_ptr() for o in outs]), (P * 2)(*[o[1].data_ptr() for o in outs]),
+        (P * 2)(*[o[2].data_ptr() for o in outs]), stream_ptr(cuda))
+    assert rc != 0
+
+
+def test_visible_set_sizes(cuda, tree):
+    """After renders of one camera the set holds the leaves its walks visit:
+    non-empty, and far from the whole tree."""
+    from paper_2202_06088_b200.device import replica
+
+    cam = _orbit(5)
+    for i in range(4):
+        vv.render(tree, cam, i % 9)
+    n, chunks = replica(tree, cuda).visible_count()
+    assert 0 < n < tree.n_leaves and 0 < chunks <= (tree.n_leaves + 63) // 64
+
+
+def test_edited_tree_ignores_visible_set(cuda):
+    import torch
+
+    rng = np.random.default_rng(12)
+    t = random_payload_tree(rng, depth=4, fill=0.5, frames=5, sigma_scale=5.0)
+    t.ensure_edit_arrays()
+    t.edit_rgb[: t.n_leaves // 3, :3] = 0.25
+    t.edit_rgb[: t.n_leaves // 3, 3] = -1.0
+    t.edit_t[: t.n_leaves // 3] = (0, 4)
+    cam = _orbit(2)
+    for i in range(10):
+        got = vv.render(t, cam, i % 5)
+        ref = vv.render(t, cam, i % 5, PS)
+        _eq(got.rgb, ref.rgb, f"edited {i}")
