@@ -309,30 +309,13 @@ static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt) {
     return VV_OK;
 }
 
-// The slice pass p describes: with a visible set (the ticket's bitmaps),
-// k_slice_sigma + the colour pass over the chunks it lists (their list in
-// stream-ordered scratch), else the plain pass.
+// The slice pass p describes: a visible-set slice (k_slice_visible) when
+// the ticket has a set to fill, else the plain pass.
 static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *vt, cudaStream_t st) {
     if (!vt || !vt->mark) return launch_slice(t->n_max, p, st);
-    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const int64_t n = (t->n_leaves + 63) / 64;
-    const size_t bytes = al((size_t)n * 4) + al((size_t)n * 8) + 256;
-    char *m = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&m), bytes, st) != cudaSuccess) {
-        cudaGetLastError();
-        return set_error(VV_E_NOMEM, "visible-set chunk list (%zu bytes) failed", bytes);
-    }
     p.vis0 = vt->d0;  // null: every leaf visible (a tree's first slice)
     p.vis1 = vt->d1;
-    p.vis_list = reinterpret_cast<int32_t *>(m);
-    p.vis_vm = reinterpret_cast<uint64_t *>(m + al((size_t)n * 4));
-    p.vis_n = reinterpret_cast<int32_t *>(m + al((size_t)n * 4) + al((size_t)n * 8));
-    int rc = VV_OK;
-    if (cudaMemsetAsync(p.vis_n, 0, sizeof(int32_t), st) != cudaSuccess)
-        rc = set_error(VV_E_CUDA, "chunk counter memset failed");
-    if (!rc) rc = launch_slice_visible(t->n_max, p, st);
-    cudaFreeAsync(m, st);  // stream-ordered: after both passes
-    return rc;
+    return launch_slice_visible(t->n_max, p, st);
 }
 
 int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only,

@@ -700,6 +700,81 @@ __device__ __forceinline__ double sigma_pre(const float4 *__restrict__ w, int64_
     return sp;
 }
 
+// sigma_pre / the gamma dot with the first P chunk loads issued together
+// (independent loads in flight; the sums keep the same order, so the same
+// bits as sigma_pre / gamma_s)
+template <int P>
+__device__ __forceinline__ double sigma_pre_batched(const float4 *__restrict__ w, int64_t cs, const float *sA, int C,
+                                                    uint32_t mask) {
+    float4 v[P];
+    int at[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        at[k] = -1;
+        if (mask) {
+            at[k] = __ffs(mask) - 1;
+            mask &= mask - 1;
+            v[k] = __ldg(w + at[k] * cs);
+        }
+    }
+    double sp = 0.0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        if (at[k] < 0) break;
+        const int c = 4 * at[k];
+        sp = xadd(sp, xmul((double)sA[c], (double)v[k].x));
+        if (c + 1 < C) sp = xadd(sp, xmul((double)sA[c + 1], (double)v[k].y));
+        if (c + 2 < C) sp = xadd(sp, xmul((double)sA[c + 2], (double)v[k].z));
+        if (c + 3 < C) sp = xadd(sp, xmul((double)sA[c + 3], (double)v[k].w));
+    }
+    for (uint32_t m = mask; m; m &= m - 1) {  // chunks beyond the first P
+        const int i = __ffs(m) - 1;
+        const float4 x = __ldg(w + i * cs);
+        const int c = 4 * i;
+        sp = xadd(sp, xmul((double)sA[c], (double)x.x));
+        if (c + 1 < C) sp = xadd(sp, xmul((double)sA[c + 1], (double)x.y));
+        if (c + 2 < C) sp = xadd(sp, xmul((double)sA[c + 2], (double)x.z));
+        if (c + 3 < C) sp = xadd(sp, xmul((double)sA[c + 3], (double)x.w));
+    }
+    return sp;
+}
+
+template <int P>
+__device__ __forceinline__ float gamma_s_batched(const float4 *__restrict__ g, int64_t cs, const float *sB, int C,
+                                                 uint32_t mask) {
+    float4 v[P];
+    int at[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        at[k] = -1;
+        if (mask) {
+            at[k] = __ffs(mask) - 1;
+            mask &= mask - 1;
+            v[k] = __ldg(g + at[k] * cs);
+        }
+    }
+    float gp = 0.0f;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        if (at[k] < 0) break;
+        const int c = 4 * at[k];
+        gp = __fmaf_rn(sB[c], v[k].x, gp);
+        if (c + 1 < C) gp = __fmaf_rn(sB[c + 1], v[k].y, gp);
+        if (c + 2 < C) gp = __fmaf_rn(sB[c + 2], v[k].z, gp);
+        if (c + 3 < C) gp = __fmaf_rn(sB[c + 3], v[k].w, gp);
+    }
+    for (uint32_t m = mask; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const float4 x = __ldg(g + i * cs);
+        const int c = 4 * i;
+        gp = __fmaf_rn(sB[c], x.x, gp);
+        if (c + 1 < C) gp = __fmaf_rn(sB[c + 1], x.y, gp);
+        if (c + 2 < C) gp = __fmaf_rn(sB[c + 2], x.z, gp);
+        if (c + 3 < C) gp = __fmaf_rn(sB[c + 3], x.w, gp);
+    }
+    return sigmoidf_(gp);
+}
+
 template <int NMAX, bool G = true>
 __device__ __forceinline__ void load_hh(const float4 *__restrict__ hh_row, float *wh) {
     constexpr int H4 = Basis<NMAX>::HH4;

@@ -734,17 +734,10 @@ struct SliceParams {
     // k_chunk_cull, the previous kernel -- read after griddepcontrol.wait)
     const int32_t *chunk_list;
     const int32_t *n_list;
-    // visible-set passes (k_slice_sigma, then k_build_slice<.., VIS> over
-    // the chunks it lists): the tree's visible set is the union of two
-    // bitmaps over leaf rows; only leaves in it get their colour, a lit leaf
-    // outside it -sigma (SliceView).  k_slice_sigma writes every record
-    // outside the set and lists each chunk holding a visible leaf with the
-    // 64-bit snapshot of its bits (vis_list / vis_vm / vis_n) that the
-    // colour pass then decodes -- what one pass fetches is what it decodes.
+    // visible-set slices (k_slice_visible): the tree's visible set is the
+    // union of two bitmaps over leaf rows (null: every leaf); only leaves in
+    // it get their colour, a lit leaf outside it -sigma (SliceView)
     const uint32_t *vis0, *vis1;
-    int32_t *vis_list;
-    uint64_t *vis_vm;
-    int32_t *vis_n;
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -799,7 +792,7 @@ __host__ __device__ inline size_t slice_out_floats4(int kf, int r4) {
 // (f64) and KF gamma (fp32) accumulators side by side -- each frame keeps
 // exactly its single-frame summation order -- and w_hh is loaded once for
 // the KF HH->SH slices.
-template <int NMAX, int KF, bool VIS = false>
+template <int NMAX, int KF>
 __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_constant__ SliceParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ float sA[KF][kMaxC], sB[KF][kMaxC];
@@ -840,11 +833,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // neighbours in HBM
     int64_t c_begin = wid, c_end = n_chunks, c_step = n_warps;
 #endif
-    // list mode: positions in the chunk list instead of chunk ids (VIS: the
-    // visible-set chunk list k_slice_sigma wrote)
-    const bool listed = VIS || p.chunk_list != nullptr;
-    const int32_t *list = VIS ? p.vis_list : p.chunk_list;
-    auto chunk_at = [&](int64_t i) -> int64_t { return listed ? (int64_t)list[i] : i; };
+    // list mode: positions in the chunk list instead of chunk ids
+    const bool listed = p.chunk_list != nullptr;
+    auto chunk_at = [&](int64_t i) -> int64_t { return listed ? (int64_t)p.chunk_list[i] : i; };
     // stage: [needed w_sigma chunks][kChunk leaves] | [needed w_gamma chunks][kChunk] | [leaves][hh4]
     auto rows_of = [&](int64_t c) { return (int)min((int64_t)kChunk, p.n_leaves - c * kChunk); };
     (void)rows_of;
@@ -858,35 +849,14 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
             bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, b);
         bulk_g2s(dst, p.T.hh + base * hh4, hb, b);
     };
-    static_assert(!VIS || (KF == 1 && slice_chunk(1) == 64 && VV_SLICE_STAGE_OUT),
-                  "visible-set passes slice one frame in 64-leaf chunks through the staged stores");
-    constexpr bool vis = VIS;
-    auto issue = [&](int64_t c, int stg, bool colour, uint64_t vm) {  // lane 0
+    auto issue = [&](int64_t c, int stg, bool colour) {  // lane 0
         const int64_t base = c * kChunk;
         const int rows = rows_of(c);
         float4 *dst = wbase + stg * stage4;
         const uint32_t cb = (uint32_t)rows * 16, hb = (uint32_t)rows * hh4 * 16;
-        if (vis) {  // sigma planes; the gamma planes and the visible leaves' w_hh rows when any is visible
-            const uint32_t hv = (uint32_t)__popcll(vm) * hh4 * 16;
-            mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (vm ? (uint32_t)nG * cb + hv : 0u));
-        } else {
-            mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
-        }
+        mbar_expect_tx(&bar[stg], (uint32_t)nS * cb + (colour ? (uint32_t)nG * cb + hb : 0u));
         for (uint32_t m = mS; m; m &= m - 1, dst += kChunk)
             bulk_g2s(dst, p.T.sig + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
-        if (vis) {
-            if (!vm) return;
-            for (uint32_t m = mG; m; m &= m - 1, dst += kChunk)
-                bulk_g2s(dst, p.T.gam + (__ffs(m) - 1) * ls + base, cb, &bar[stg]);
-            for (uint64_t m = vm; m;) {  // runs of visible rows, at their rows' stage offsets
-                const int r0 = __ffsll((long long)m) - 1;
-                const uint64_t rest = ~(m >> r0);
-                const int len = rest ? __ffsll((long long)rest) - 1 : 64 - r0;
-                bulk_g2s(dst + (size_t)r0 * hh4, p.T.hh + (base + r0) * hh4, (uint32_t)len * hh4 * 16, &bar[stg]);
-                m &= len >= 64 ? 0ull : ~(((1ull << len) - 1ull) << r0);
-            }
-            return;
-        }
         if (colour) issue_colour(c, stg, &bar[stg], false);
     };
     // colour rows are staged with the sigma chunks while the chunks are
@@ -895,10 +865,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     // written, and while chunks stay dark the colour rows are not fetched
     // (render-internal slices of trees without edits: p.skip_dark)
     uint32_t colour_in = 3u;  // bit s: stage s was issued with its colour rows
-    // lane 0 stages list position i (its chunk and, VIS, its snapshot)
-    auto stage = [&](int64_t i, int stg, bool colour) {
-        issue(chunk_at(i), stg, colour, vis ? p.vis_vm[i] : 0ull);
-    };
+    // lane 0 stages list position i
+    auto stage = [&](int64_t i, int stg, bool colour) { issue(chunk_at(i), stg, colour); };
     // payload reads only: may overlap the previous kernel
     if (lane == 0 && !listed) {
         if (c_begin < c_end) stage(c_begin, 0, true);
@@ -907,7 +875,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     pdl_trigger();
     pdl_wait();  // no record is written before the previous kernel is complete
     if (listed) {  // the list is the previous kernel's output
-        const int64_t nl = (int64_t)*(volatile const int32_t *)(VIS ? p.vis_n : p.n_list);
+        const int64_t nl = (int64_t)*(volatile const int32_t *)p.n_list;
 #if VV_SLICE_RUNS
         c_begin = nl * wid / n_warps;
         c_end = nl * (wid + 1) / n_warps;
@@ -956,9 +924,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
                 for (int f = 0; f < KF; ++f) lit |= sp[u][f] > 0.0;
             }
         }
-        const uint64_t vm = vis ? p.vis_vm[ci] : 0ull;  // every lane: the snapshot lane 0 staged
-        const bool bright = vis || !p.skip_dark || __any_sync(0xffffffffu, lit);
-        if (!vis && bright && !((colour_in >> stg) & 1u)) {  // mispredicted dark: fetch the colour rows now
+        const bool bright = !p.skip_dark || __any_sync(0xffffffffu, lit);
+        if (bright && !((colour_in >> stg) & 1u)) {  // mispredicted dark: fetch the colour rows now
             if (lane == 0) {
                 fence_proxy_async();  // the colour region was last read through the generic proxy
                 issue_colour(c, stg, &bar[2 + stg], true);
@@ -975,16 +942,6 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
 #pragma unroll
                 for (int f = 0; f < KF; ++f) bits |= (sp[u][f] > 0.0 ? 1u : 0u) << f;
                 p.lit[base + r] = (uint8_t)bits;
-            }
-            if (vis && !((vm >> r) & 1ull)) {  // outside the set: sigma only, negated when lit (staged)
-                float4 *o = obuf + (size_t)r * (R4 + 1);
-                const double sigma = sp[u][0] > 0.0 ? -sp[u][0] : 0.0;
-                const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
-#pragma unroll
-                for (int i = 0; i < R4 - 1; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                o[R4 - 1] = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
-                                        __uint_as_float((unsigned)(sb >> 32)));
-                continue;
             }
             if (!bright) {  // sigma only: the record's last float4 pair (one sector at even R4)
 #pragma unroll
@@ -1062,67 +1019,100 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
     }
 }
 
-// Visible-set slice, first pass: one warp per 64-leaf chunk (every chunk,
-// or the region's chunk list).  Lane 0 reads the chunk's visible bits once
-// (the snapshot; no bitmaps: every leaf visible, a tree's first slice).  A
-// chunk holding a visible leaf goes, with its snapshot, to the list that
-// k_build_slice<.., VIS> writes whole (colour for the set's leaves, -sigma
-// for a lit other).  Every leaf of the other chunks gets its sigma-only
-// record here -- sigma_pre in f64 exactly as k_build_slice
-// (kernels.py:374-381), negated when lit -- and, for node masks, its lit
-// byte.  Thread per leaf over coalesced w_sigma planes; the record's last
-// 64 aligned bytes are stored whole (a 32-byte store costs the same DRAM
-// read-modify-write).
+#ifndef VV_SIGMA_TAIL
+#define VV_SIGMA_TAIL 2  // float4 per sigma-only record: 32 B measured best (0.166 ms vs 0.191 with 64 B at cfg2)
+#endif
+// Visible-set slice in one pass (k_slice_visible): one warp per 64-leaf
+// chunk (every chunk, or the region's chunk list); lane 0 reads the chunk's
+// visible bits once (no bitmaps: every leaf visible, a tree's first slice).
+// Each lane takes leaves lane and lane + 32 straight from global memory:
+// sigma_pre (f64, kernels.py:374-381), and for a leaf in the set the colour
+// -- gamma_s -> radial -> slice_col, the operations and order of
+// k_build_slice and of the per-sample shader, so the same bits -- stored as
+// its whole record (one 128-byte line at n_max 2); any other leaf gets its
+// sigma pair, negated when lit.  No staging: the set is a fifth of the
+// leaves, scattered over a third of the chunks, and a thread per leaf keeps
+// ~15 independent loads in flight where the staged pass's two stages per
+// warp left it latency-bound (0.41 of HBM peak).
 template <int NMAX>
-__global__ void __launch_bounds__(256) k_slice_sigma(const __grid_constant__ SliceParams p) {
+__global__ void __launch_bounds__(256) k_slice_visible(const __grid_constant__ SliceParams p) {
     __shared__ float sA[kMaxC], sB[kMaxC];
     load_rows(p.T, p.frame[0], sA, sB);
     __syncthreads();
     constexpr int R4 = slice_rec4(Basis<NMAX>::S);
-#ifndef VV_SIGMA_TAIL
-#define VV_SIGMA_TAIL 2  // float4 per sigma-only record: 32 B measured best (0.166 ms vs 0.191 with 64 B at cfg2)
-#endif
-    constexpr int TAIL = R4 % VV_SIGMA_TAIL == 0 ? VV_SIGMA_TAIL : (R4 % 2 == 0 ? 2 : 1);  // float4 per sigma-only record
+    constexpr int TAIL = R4 % VV_SIGMA_TAIL == 0 ? VV_SIGMA_TAIL : (R4 % 2 == 0 ? 2 : 1);
     const int lane = threadIdx.x & 31;
     const bool listed = p.chunk_list != nullptr;
     const bool all = p.vis0 == nullptr;
     pdl_trigger();
-    pdl_wait();  // the bitmaps, the region list and the zeroed counter are the previous work's
+    pdl_wait();  // the bitmaps and the region list are the previous work's; records written after
     const int64_t n_chunks = (p.n_leaves + 63) / 64;
     const int64_t n_items = listed ? (int64_t)*(volatile const int32_t *)p.n_list : n_chunks;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_items; i += nw) {
-        const int64_t c = listed ? (int64_t)p.chunk_list[i] : i;
-        const int64_t base = c * 64;
-        const int rows = (int)min((int64_t)64, p.n_leaves - base);
+    // a warp's next 32 chunks: lane j reads the bits of the j-th (one round trip for 32 chunks)
+    for (int64_t i0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i0 < n_items; i0 += 32 * nw) {
+        const int64_t ij = i0 + (int64_t)lane * nw;
+        int64_t cj = 0;
         unsigned lo = ~0u, hi = ~0u;
-        if (lane == 0 && !all) {
-            lo = __ldcg(p.vis0 + 2 * c) | __ldcg(p.vis1 + 2 * c);
-            hi = __ldcg(p.vis0 + 2 * c + 1) | __ldcg(p.vis1 + 2 * c + 1);
-        }
-        uint64_t vm = ((uint64_t)__shfl_sync(0xffffffffu, hi, 0) << 32) | __shfl_sync(0xffffffffu, lo, 0);
-        if (rows < 64) vm &= (1ull << rows) - 1ull;
-        if (vm) {
-            if (lane == 0) {
-                const int k = atomicAdd(p.vis_n, 1);
-                p.vis_list[k] = (int32_t)c;
-                p.vis_vm[k] = vm;
+        if (ij < n_items) {
+            cj = listed ? (int64_t)p.chunk_list[ij] : ij;
+            if (!all) {
+                lo = __ldcg(p.vis0 + 2 * cj) | __ldcg(p.vis1 + 2 * cj);
+                hi = __ldcg(p.vis0 + 2 * cj + 1) | __ldcg(p.vis1 + 2 * cj + 1);
             }
-            continue;
         }
+        const int nj = (int)min((int64_t)32, (n_items - i0 + nw - 1) / nw);
+#pragma unroll 1
+        for (int j = 0; j < nj; ++j) {
+            const int64_t c = __shfl_sync(0xffffffffu, cj, j);
+            const uint64_t vm = ((uint64_t)__shfl_sync(0xffffffffu, hi, j) << 32) | __shfl_sync(0xffffffffu, lo, j);
+            const int64_t base = c * 64;
+            const int rows = (int)min((int64_t)64, p.n_leaves - base);
+            double sp[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int r = lane + 32 * u;
-            if (r >= rows) continue;
-            const double sp = sigma_pre(p.T.sig + base + r, p.T.lstride, sA, p.T.C, p.mS);
-            if (p.lit) p.lit[base + r] = sp > 0.0 ? 1u : 0u;
-            const double sigma = sp > 0.0 ? -sp : 0.0;
-            const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
-            float4 *o = p.rec[0] + (base + r + 1) * p.rec4 - TAIL;
+            for (int u = 0; u < 2; ++u) {  // both leaves' w_sigma loads in flight together
+                const int r = lane + 32 * u;
+                sp[u] = r < rows ? sigma_pre_batched<2>(p.T.sig + base + r, p.T.lstride, sA, p.T.C, p.mS) : 0.0;
+            }
+#pragma unroll 1
+            for (int u = 0; u < 2; ++u) {
+                const int r = lane + 32 * u;
+                if (r >= rows) continue;
+                const int64_t L = base + r;
+                if (p.lit) p.lit[L] = sp[u] > 0.0 ? 1u : 0u;
+                if ((vm >> r) & 1ull) {
+                    float q[4 * R4];
 #pragma unroll
-            for (int k = 0; k < TAIL - 1; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            o[TAIL - 1] = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
-                                      __uint_as_float((unsigned)(sb >> 32)));
+                    for (int k = 0; k < 4 * R4; ++k) q[k] = 0.0f;
+                    float wh[4 * Basis<NMAX>::HH4];
+                    load_hh<NMAX>(p.T.hh + L * p.T.hh4, wh);  // in flight with the gamma chunks
+                    const float s = gamma_s_batched<2>(p.T.gam + L, p.T.lstride, sB, p.T.C, p.mG);
+                    float R[Basis<NMAX>::NPAIRS];
+                    radial<NMAX>(s, p.K, R);
+#pragma unroll
+                    for (int l = 0; l <= NMAX; ++l)
+#pragma unroll
+                        for (int m = -l; m <= l; ++m) {
+                            const int jj = l * l + l + m;
+                            slice_col<NMAX>(R, wh, l, m, q[3 * jj + 0], q[3 * jj + 1], q[3 * jj + 2]);
+                        }
+                    const double sigma = sp[u] > 0.0 ? sp[u] : 0.0;
+                    const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+                    q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
+                    q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
+                    float4 *o = p.rec[0] + L * p.rec4;
+#pragma unroll
+                    for (int k = 0; k < R4; ++k) o[k] = make_float4(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
+                } else {
+                    const double sigma = sp[u] > 0.0 ? -sp[u] : 0.0;  // a lit leaf outside the set: its pixels re-walk
+                    const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+                    float4 *o = p.rec[0] + (L + 1) * p.rec4 - TAIL;
+#pragma unroll
+                    for (int k = 0; k < TAIL - 1; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    o[TAIL - 1] = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)),
+                                              __uint_as_float((unsigned)(sb >> 32)));
+                }
+            }
         }
     }
 }
@@ -1323,8 +1313,7 @@ int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid
 // per-sample depth-ordered joint composition (vv_launch_joint.cu)
 int launch_scene_joint(int nmax, bool wide, const SceneParams &p, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
-// visible-set slice of one frame: k_slice_sigma, then k_build_slice<.., VIS>
-// over the chunks it lists (p.vis0/vis1, p.vis_list/vis_vm/vis_n; vis_n zeroed)
+// visible-set slice of one frame (k_slice_visible; p.vis0/vis1, or neither: every leaf)
 int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st);
 // per-frame node mask (vv_launch_mask.cu): child table with every child whose
 // subtree holds no lit leaf replaced by -1

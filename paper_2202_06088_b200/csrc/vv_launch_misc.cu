@@ -82,7 +82,7 @@ int launch_count_dark(const TreeView &T, int frame, uint32_t mS, int64_t n, unsi
     return check_launch("count_dark");
 }
 
-template <int NM, int KF, bool VIS = false>
+template <int NM, int KF>
 static int go_slice(const SliceParams &p, cudaStream_t st) {
     constexpr int kChunk = slice_chunk(KF);
     const size_t per_warp =
@@ -93,7 +93,7 @@ static int go_slice(const SliceParams &p, cudaStream_t st) {
     if (nw < 1)
         return set_error(VV_E_UNSUPPORTED, "slice stage of %zu bytes per warp exceeds shared memory", per_warp);
     const size_t smem = (size_t)nw * per_warp;
-    auto kern = k_build_slice<NM, KF, VIS>;
+    auto kern = k_build_slice<NM, KF>;
     int r = prep_smem(kern, smem);
     if (r) return r;
     const int64_t chunks = (p.n_leaves + kChunk - 1) / kChunk;
@@ -123,8 +123,8 @@ int launch_slice(int nmax, const SliceParams &p, cudaStream_t st) {
 }
 
 int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
-    if (p.n_frames != 1 || !p.vis0 != !p.vis1 || !p.vis_list || !p.vis_vm || !p.vis_n)
-        return set_error(VV_E_INVALID, "visible-set slice: one frame and a chunk list required");
+    if (p.n_frames != 1 || !p.vis0 != !p.vis1)
+        return set_error(VV_E_INVALID, "visible-set slice: one frame and both bitmaps (or neither)");
     return with_nmax(nmax, [&](auto N) {
         constexpr int NM = decltype(N)::value;
         int dev = 0, sms = 0;
@@ -132,13 +132,8 @@ int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t chunks = (p.n_leaves + 63) / 64;
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 7) / 8, (int64_t)sms * 8));
-        launch_pdl(k_slice_sigma<NM>, dim3(grid), dim3(256), 0, st, p);
-        int r = check_launch("slice_sigma");
-        if (r) return r;
-        SliceParams q = p;
-        q.chunk_list = nullptr;  // the colour pass walks the visible-set list
-        q.n_list = nullptr;
-        return go_slice<NM, 1, true>(q, st);
+        launch_pdl(k_slice_visible<NM>, dim3(grid), dim3(256), 0, st, p);
+        return check_launch("slice_visible");
     });
 }
 
