@@ -833,7 +833,7 @@ def run_ours(args, rank, world, local_rank):
             sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
             vis_on = wl.kind in ("single", "stereo") and visible_set_on(wl.tree, replica(wl.tree, dev))
             roofline["slice_pass"] = {
-                "kernel": "k_slice_sigma + k_build_slice<VIS>" if vis_on else "k_build_slice",
+                "kernel": "k_slice_visible" if vis_on else "k_build_slice",
                 "visible_set": vis_on, "ms": round(slice_ms / n, 4),
                 "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
