@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <memory>
+#include <deque>
 #include <mutex>
 #include <vector>
 
@@ -1665,29 +1666,31 @@ static WaitValue32Fn wait_value32() {  // the driver's cuStreamWaitValue32 (stre
 // waiting for its copies, so the counters are reused safely.
 struct HostCopyState {
     int device;
-    cudaStream_t caller, copy;
+    cudaStream_t caller, copy[2];  // bands alternate between two copy streams (per-copy setup overlaps)
     unsigned *counters;
     int capacity;
 };
 
 static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_bands) {
     static std::mutex mu;
-    static std::vector<HostCopyState> states;
+    static std::deque<HostCopyState> states;  // stable addresses: callers keep the pointer
     std::lock_guard<std::mutex> lk(mu);
     HostCopyState *st = nullptr;
     for (auto &e : states)
         if (e.device == device && e.caller == caller) st = &e;
     if (!st) {
-        HostCopyState e{device, caller, nullptr, nullptr, 0};
-        if (cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking) != cudaSuccess) {
-            cudaGetLastError();
-            return nullptr;
-        }
+        HostCopyState e{device, caller, {nullptr, nullptr}, nullptr, 0};
+        for (int k = 0; k < 2; ++k)
+            if (cudaStreamCreateWithFlags(&e.copy[k], cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
         states.push_back(e);
         st = &states.back();
     }
     if (st->capacity < n_bands) {
-        cudaStreamSynchronize(st->copy);
+        cudaStreamSynchronize(st->copy[0]);
+        cudaStreamSynchronize(st->copy[1]);
         cudaFree(st->counters);
         st->counters = nullptr;
         st->capacity = 0;
@@ -1725,14 +1728,17 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
                                 st));
         return VV_OK;
     }
-    cudaStream_t cs = hs->copy;
+    // VV_HOST_COPY_STREAMS=1: every band on one copy stream (A/B)
+    const char *ncs_env = getenv("VV_HOST_COPY_STREAMS");
+    const int ncs = (ncs_env && ncs_env[0] == '1') ? 1 : 2;
     unsigned *band_done = hs->counters;
     VV_CUDA(cudaMemsetAsync(band_done, 0, (size_t)n_bands * sizeof(unsigned), st));
-    cudaEvent_t ready, copied;
+    cudaEvent_t ready, copied[2];
     VV_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    VV_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    VV_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
+    VV_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
     cudaEventRecord(ready, st);  // counters zeroed, earlier work on the caller's stream ordered
-    cudaStreamWaitEvent(cs, ready, 0);
+    for (int k = 0; k < ncs; ++k) cudaStreamWaitEvent(hs->copy[k], ready, 0);
     // persistent warps in row-major order: bands finish top to bottom (a
     // plan contributes its counters and cached coverage, not its cost order)
     int rc = render_camera_impl(t, frame, cache, opts, cam, rgb, alpha, depth, nullptr, 0, 0, 1, 0, stream, nullptr,
@@ -1740,7 +1746,8 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
     if (rc) {
         cudaStreamWaitEvent(st, ready, 0);
         cudaEventDestroy(ready);
-        cudaEventDestroy(copied);
+        cudaEventDestroy(copied[0]);
+        cudaEventDestroy(copied[1]);
         return rc;
     }
     const int blocks_x = (cam->width + kTW - 1) / kTW;
@@ -1748,6 +1755,7 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
     for (int b = 0; b < n_bands && !rc; ++b) {
         const int y0 = b * band_rows, y1 = std::min(cam->height, y0 + band_rows);
         const unsigned target = (unsigned)(((y1 - y0 + kTH - 1) / kTH) * blocks_x * kWarpsPerTile);
+        cudaStream_t cs = hs->copy[b % ncs];
         const CUresult wr = wait(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(band_done + b), target,
                                  CU_STREAM_WAIT_VALUE_GEQ);
         if (wr != CUDA_SUCCESS) {
@@ -1760,10 +1768,13 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
             cudaMemcpyAsync(host_planes + 4 * hw + px0, depth + px0, npx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
             rc = set_error(VV_E_CUDA, "band copy failed");
     }
-    cudaEventRecord(copied, cs);
-    cudaStreamWaitEvent(st, copied, 0);  // the caller's stream: frame on the host, counters free again
+    for (int k = 0; k < ncs; ++k) {  // the caller's stream: frame on the host, counters free again
+        cudaEventRecord(copied[k], hs->copy[k]);
+        cudaStreamWaitEvent(st, copied[k], 0);
+    }
     cudaEventDestroy(ready);
-    cudaEventDestroy(copied);
+    cudaEventDestroy(copied[0]);
+    cudaEventDestroy(copied[1]);
     return rc;
 }
 
