@@ -1763,9 +1763,10 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
             break;
         }
         const size_t px0 = (size_t)y0 * W, npx = (size_t)(y1 - y0) * W;
+        // rgb rows, then the alpha and depth rows as one 2-row copy (the planes are hw floats apart)
         if (cudaMemcpyAsync(host_planes + 3 * px0, rgb + 3 * px0, npx * 12, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
-            cudaMemcpyAsync(host_planes + 3 * hw + px0, alpha + px0, npx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
-            cudaMemcpyAsync(host_planes + 4 * hw + px0, depth + px0, npx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            cudaMemcpy2DAsync(host_planes + 3 * hw + px0, (size_t)hw * 4, alpha + px0, (size_t)hw * 4, npx * 4, 2,
+                              cudaMemcpyDeviceToHost, cs) != cudaSuccess)
             rc = set_error(VV_E_CUDA, "band copy failed");
     }
     for (int k = 0; k < ncs; ++k) {  // the caller's stream: frame on the host, counters free again
