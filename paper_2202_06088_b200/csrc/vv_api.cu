@@ -1669,6 +1669,7 @@ struct HostCopyState {
     cudaStream_t caller, copy[2];  // bands alternate between two copy streams (per-copy setup overlaps)
     unsigned *counters;
     int capacity;
+    cudaEvent_t ready, copied[2];  // reused by every call on this caller stream
 };
 
 static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_bands) {
@@ -1679,12 +1680,17 @@ static HostCopyState *host_copy_state(int device, cudaStream_t caller, int n_ban
     for (auto &e : states)
         if (e.device == device && e.caller == caller) st = &e;
     if (!st) {
-        HostCopyState e{device, caller, {nullptr, nullptr}, nullptr, 0};
+        HostCopyState e{device, caller, {nullptr, nullptr}, nullptr, 0, nullptr, {nullptr, nullptr}};
         for (int k = 0; k < 2; ++k)
-            if (cudaStreamCreateWithFlags(&e.copy[k], cudaStreamNonBlocking) != cudaSuccess) {
+            if (cudaStreamCreateWithFlags(&e.copy[k], cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&e.copied[k], cudaEventDisableTiming) != cudaSuccess) {
                 cudaGetLastError();
                 return nullptr;
             }
+        if (cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
         states.push_back(e);
         st = &states.back();
     }
@@ -1733,10 +1739,7 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
     const int ncs = (ncs_env && ncs_env[0] == '1') ? 1 : 2;
     unsigned *band_done = hs->counters;
     VV_CUDA(cudaMemsetAsync(band_done, 0, (size_t)n_bands * sizeof(unsigned), st));
-    cudaEvent_t ready, copied[2];
-    VV_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    VV_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
-    VV_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
+    cudaEvent_t ready = hs->ready, *copied = hs->copied;
     cudaEventRecord(ready, st);  // counters zeroed, earlier work on the caller's stream ordered
     for (int k = 0; k < ncs; ++k) cudaStreamWaitEvent(hs->copy[k], ready, 0);
     // persistent warps in row-major order: bands finish top to bottom (a
@@ -1745,9 +1748,6 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
                                 nullptr, nullptr, plan, band_done, band_rows, true, true);
     if (rc) {
         cudaStreamWaitEvent(st, ready, 0);
-        cudaEventDestroy(ready);
-        cudaEventDestroy(copied[0]);
-        cudaEventDestroy(copied[1]);
         return rc;
     }
     const int blocks_x = (cam->width + kTW - 1) / kTW;
@@ -1773,9 +1773,6 @@ int vv_render_camera_to_host(const vv_tree *t, int32_t frame, const vv_slice *ca
         cudaEventRecord(copied[k], hs->copy[k]);
         cudaStreamWaitEvent(st, copied[k], 0);
     }
-    cudaEventDestroy(ready);
-    cudaEventDestroy(copied[0]);
-    cudaEventDestroy(copied[1]);
     return rc;
 }
 
