@@ -489,6 +489,7 @@ class Stepper:
         self.scene_plan = vv.CameraPlan(dev)  # what render_scene() keeps per stream
         self.descs = {}
         self.launches = 0
+        self.renders = 0  # per camera plan: k_plan_order re-sorts every 4th render
 
     def prepare(self, frames):
         """Host-side per-frame scene resolution (timemaps, affines) ahead of the
@@ -516,7 +517,8 @@ class Stepper:
             _native.check(_native.lib().vv_render_scene_planned(
                 descs, len(descs), ctypes.byref(oc), ctypes.byref(cd), bg, self.outs[0][0].data_ptr(), None, None,
                 self.scene_plan._handle, stream_ptr(self.dev)))
-            self.launches += 2  # scene kernel + plan order (every 4th)
+            self.renders += 1
+            self.launches += 1 + (self.renders % 4 == 1)  # scene kernel (+ plan order every 4th render)
             return
         # exactly what render() does: the render-internal slice pass (colour
         # only for the tree's visible set; node masks for dark-heavy trees) ...
@@ -525,7 +527,11 @@ class Stepper:
             mid.record(stream)
         for cam, out, plan in zip(wl.cams, self.outs, self.plans):  # ... then the camera kernel(s)
             vv.render_into(wl.tree, cam, f, *out, cache=fs, plan=plan)
-        self.launches += 1 + 2 * len(wl.cams)  # slice, (camera kernel + plan order) per camera
+        # slice pass; per camera: camera kernel, deferred-pixel walk (visible
+        # set), plan order every 4th render
+        self.renders += 1
+        vis = visible_set_on(wl.tree, vv.device.replica(wl.tree, self.dev))
+        self.launches += 1 + len(wl.cams) * (1 + int(vis) + int(self.renders % 4 == 1))
         del fs
 
 
