@@ -1034,8 +1034,14 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
 // leaves, scattered over a third of the chunks, and a thread per leaf keeps
 // ~15 independent loads in flight where the staged pass's two stages per
 // warp left it latency-bound (0.41 of HBM peak).
+#ifndef VV_VIS_MINB
+#define VV_VIS_MINB 1  // min resident blocks per SM for k_slice_visible (register cap)
+#endif
+#ifndef VV_VIS_BLOCK
+#define VV_VIS_BLOCK 64  // threads per block: 0.138 vs 0.143 ms with 256 (cfg2, more resident warps at 96 registers)
+#endif
 template <int NMAX>
-__global__ void __launch_bounds__(256) k_slice_visible(const __grid_constant__ SliceParams p) {
+__global__ void __launch_bounds__(VV_VIS_BLOCK, VV_VIS_MINB) k_slice_visible(const __grid_constant__ SliceParams p) {
     __shared__ float sA[kMaxC], sB[kMaxC];
     load_rows(p.T, p.frame[0], sA, sB);
     __syncthreads();

@@ -131,8 +131,10 @@ int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t chunks = (p.n_leaves + 63) / 64;
-        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 7) / 8, (int64_t)sms * 8));
-        launch_pdl(k_slice_visible<NM>, dim3(grid), dim3(256), 0, st, p);
+        constexpr int wpb = VV_VIS_BLOCK / 32;
+        const unsigned grid =
+            (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + wpb - 1) / wpb, (int64_t)sms * 64 / wpb));
+        launch_pdl(k_slice_visible<NM>, dim3(grid), dim3(VV_VIS_BLOCK), 0, st, p);
         return check_launch("slice_visible");
     });
 }
