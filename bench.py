@@ -281,6 +281,11 @@ def slice_pass_bytes(tree, f, device, chunk=64):
         nv = int(vis.sum())
         rv = int(rows[vchunk].sum())
         b = n * 16 * nza + rv * 16 * nzb + nv * (12 * k + 12 * s_sh) + rv * 8 + (n - rv) * 32 + n // 4
+    elif masks and os.environ.get("VV_LIT_PASS", "1") != "0":
+        # dark-heavy trees: the thread-per-leaf pass (k_slice_visible, lit
+        # mode): colour of every lit leaf, the sigma pair of every dark one
+        nl = int(lit.sum())
+        b = n * 16 * nza + nl * (16 * nzb + 12 * k + 8 + 12 * s_sh) + (n - nl) * 32
     else:
         nb, nd = int(rows[bright].sum()), int(rows[~bright].sum())
         b = n * 16 * nza + nb * (16 * nzb + 12 * k + 8 + 12 * s_sh) + nd * 32
@@ -838,13 +843,19 @@ def run_ours(args, rank, world, local_rank):
                                                    for k in ("P", "V", "S")}
             sbytes = sum(ab[f]["slice_bytes"] for f in step_frames)
             vis_on = wl.kind in ("single", "stereo") and visible_set_on(wl.tree, replica(wl.tree, dev))
+            lit_pass = (not vis_on and replica(wl.tree, dev).dark_fraction >= 0.25
+                        and os.environ.get("VV_LIT_PASS", "1") != "0")
             roofline["slice_pass"] = {
-                "kernel": "k_slice_visible" if vis_on else "k_build_slice",
+                "kernel": "k_slice_visible" + (" (lit leaves)" if lit_pass else "") if vis_on or lit_pass
+                else "k_build_slice",
                 "visible_set": vis_on, "ms": round(slice_ms / n, 4),
                 "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
                 "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
-                "bytes_formula": ("visible set: per leaf 16 B per w_sigma float4 chunk the frame's A row does not "
+                "bytes_formula": ("per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
+                                  "per lit leaf + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh "
+                                  "(record); per dark leaf + 32 B (sigma pair)" if lit_pass else
+                                  "visible set: per leaf 16 B per w_sigma float4 chunk the frame's A row does not "
                                   "zero out; per leaf of a 64-leaf chunk holding a visible leaf + 16 B per nonzero "
                                   "w_gamma chunk + 8 (sigma), per visible leaf + 12 K (w_hh) + 12 S_sh (colour); per "
                                   "other leaf + 32 B (sigma pair); + 2 bits per leaf (the set)" if vis_on else

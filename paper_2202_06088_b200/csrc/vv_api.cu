@@ -313,7 +313,16 @@ static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt) {
 // The slice pass p describes: a visible-set slice (k_slice_visible) when
 // the ticket has a set to fill, else the plain pass.
 static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *vt, cudaStream_t st) {
-    if (!vt || !vt->mark) return launch_slice(t->n_max, p, st);
+    if (!vt || !vt->mark) {
+        // a single-frame render-only slice of a dark-heavy tree: the
+        // thread-per-leaf pass, colour of the lit leaves only (cfg3 0.166 vs
+        // 0.191 ms; on mostly-lit trees the staged pass wins, 0.225 vs 0.276
+        // at cfg2).  VV_LIT_PASS=0 / 1 forces it off / on.
+        const char *e = getenv("VV_LIT_PASS");
+        const bool lit_pass = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : t->dark_frac >= 0.25f;
+        if (p.n_frames == 1 && p.skip_dark && lit_pass) return launch_slice_visible(t->n_max, p, st);
+        return launch_slice(t->n_max, p, st);
+    }
     p.vis0 = vt->d0;  // null: every leaf visible (a tree's first slice)
     p.vis1 = vt->d1;
     return launch_slice_visible(t->n_max, p, st);

@@ -1050,6 +1050,9 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, VV_VIS_MINB) k_slice_visible(con
     const int lane = threadIdx.x & 31;
     const bool listed = p.chunk_list != nullptr;
     const bool all = p.vis0 == nullptr;
+    // no set and skip_dark (a render-only slice without a visible set): the
+    // colour of every lit leaf, sigma alone for the dark ones
+    const bool lit_only = all && p.skip_dark;
     pdl_trigger();
     pdl_wait();  // the bitmaps and the region list are the previous work's; records written after
     const int64_t n_chunks = (p.n_leaves + 63) / 64;
@@ -1086,7 +1089,7 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, VV_VIS_MINB) k_slice_visible(con
                 if (r >= rows) continue;
                 const int64_t L = base + r;
                 if (p.lit) p.lit[L] = sp[u] > 0.0 ? 1u : 0u;
-                if ((vm >> r) & 1ull) {
+                if (lit_only ? sp[u] > 0.0 : ((vm >> r) & 1ull)) {
                     float q[4 * R4];
 #pragma unroll
                     for (int k = 0; k < 4 * R4; ++k) q[k] = 0.0f;
