@@ -748,10 +748,11 @@ def run_ours(args, rank, world, local_rank):
             for cam in wl.cams:
                 vv.render(wl.tree, cam, f)
         single_ms = (time.perf_counter() - te) / len(e2e_frames[:3]) * 1e3
-        warm_group = [(i * world + rank) % T for i in range(3)]
-        for _ in range(2):  # both eyes' playback states and pinned buffers warm
-            collections.deque(zip(*[vv.render_sequence(wl.tree, cam, warm_group * 2) for cam in wl.cams]),
-                              maxlen=0)
+        # both eyes' playback states and pinned buffers warm: one whole zipped
+        # run (two sequences in flight hold ~17 frame buffers; a pool grown
+        # lazily inside the timed run pays 100+ ms host allocations)
+        for _ in range(2):
+            collections.deque(zip(*[vv.render_sequence(wl.tree, cam, e2e_frames) for cam in wl.cams]), maxlen=0)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
