@@ -1041,7 +1041,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_build_slice(const __grid_c
 #define VV_VIS_BLOCK 64  // threads per block: 0.138 vs 0.143 ms with 256 (cfg2, more resident warps at 96 registers)
 #endif
 template <int NMAX>
-__global__ void __launch_bounds__(VV_VIS_BLOCK, VV_VIS_MINB) k_slice_visible(const __grid_constant__ SliceParams p) {
+__global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)  // n_max 3: no register cap (spills)
+    k_slice_visible(const __grid_constant__ SliceParams p) {
     __shared__ float sA[kMaxC], sB[kMaxC];
     load_rows(p.T, p.frame[0], sA, sB);
     __syncthreads();
