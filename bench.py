@@ -849,7 +849,10 @@ def run_ours(args, rank, world, local_rank):
             roofline["slice_pass"] = {
                 "kernel": "k_slice_visible" + (" (lit leaves)" if lit_pass else "") if vis_on or lit_pass
                 else "k_build_slice",
-                "visible_set": vis_on, "ms": round(slice_ms / n, 4),
+                "visible_set": ({"leaves": replica(wl.tree, dev).visible_count()[0],
+                                 "chunks": replica(wl.tree, dev).visible_count()[1],
+                                 "n_leaves": int(wl.tree.n_leaves)} if vis_on else False),
+                "ms": round(slice_ms / n, 4),
                 "achieved": round(sbytes / (slice_ms / 1e3) / 1e9, 1),
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
                 "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
