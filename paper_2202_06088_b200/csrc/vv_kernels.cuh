@@ -142,6 +142,7 @@ struct CamParams {
     // band to the host while the rest of the frame renders
     unsigned *band_done;
     int band_rows;
+    int band_first;  // rows of band 0 (a short first band starts the copies sooner); 0: band_rows
     CoverView cov;  // image / region mode: pixels that can reach the tree
     int cx0, cy0, cx1, cy1;  // image / region mode: pixel rectangle of the tree's occupied box (inclusive)
     // optional per-pixel leaf-sample counts (render_kernel's consumed
@@ -156,6 +157,12 @@ struct CamParams {
     int4 *deferred;
     int *n_deferred;
 };
+
+// band of a row offset from the rectangle's top (banded host copies)
+__device__ __forceinline__ int band_of(const CamParams &p, int dy) {
+    const int f = p.band_first > 0 ? p.band_first : p.band_rows;
+    return dy < f ? 0 : 1 + (dy - f) / p.band_rows;
+}
 
 // block = 16x8 pixels; warp = 16x2 pixels (spatially coherent rays)
 __device__ __forceinline__ void block_pixel(int bx, int by, int &ix, int &iy) {
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_camera_rewalk(cons
         if (p.band_done) {
             __threadfence();
             __syncwarp();
-            if (lane == 0) atomicAdd(p.band_done + (e.y - p.ry0) / p.band_rows, 1u);
+            if (lane == 0) atomicAdd(p.band_done + band_of(p, e.y - p.ry0), 1u);
         }
     }
     if (p.peer) __threadfence_system();
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
             } else if (p.band_done) {
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) atomicAdd(p.band_done + (tb / p.blocks_x) * kTH / p.band_rows, 1u);
+                if (lane == 0) atomicAdd(p.band_done + band_of(p, (tb / p.blocks_x) * kTH), 1u);
             }
             __syncwarp();
             if (p.block_cost) {
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_render_camera(cons
         } else if (p.band_done) {  // this warp's pixels are stored: count it for its band
             __threadfence();
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) atomicAdd(p.band_done + (y0 - p.ry0) / p.band_rows, 1u);
+            if ((threadIdx.x & 31) == 0) atomicAdd(p.band_done + band_of(p, y0 - p.ry0), 1u);
         }
     }
     // peer stores: make them visible system-wide before the kernel retires
