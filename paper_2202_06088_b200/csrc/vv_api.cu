@@ -81,6 +81,8 @@ struct vv_tree {
     mutable int64_t vis_words = 0;
     mutable int vis_cur = 0, vis_slices = 0;
     mutable bool vis_ready = false;
+    mutable uint64_t vis_view = 0;  // the camera the set is being built for (view_hash)
+    mutable int vis_static = 0;     // slices since that camera last changed
 };
 
 // Per-frame (or per frame group) node mask: the slice pass's lit bits, the
@@ -277,10 +279,54 @@ static bool vis_wanted(const vv_tree *t) {
     return !mask_wanted(t);
 }
 
-static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt) {
+// A camera's identity for the visible set (its fields, not its padding).
+static uint64_t view_hash(const vv_camera &c) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](const void *p, size_t n) {
+        const unsigned char *b = static_cast<const unsigned char *>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    };
+    mix(&c.width, sizeof(c.width));
+    mix(&c.height, sizeof(c.height));
+    mix(&c.fx, 4 * sizeof(double));
+    mix(c.c2w, sizeof(c.c2w));
+    return h ? h : 1;
+}
+
+// view: the rendering camera's view_hash (0: unknown -- a VV_SLICE_VISIBLE
+// cache, whose caller vouches for a steady view).  The set only pays for
+// a camera that holds still: a moving view meets leaves outside it on every
+// frame and re-walks those pixels (cfg2 tree orbited 1 deg / 5 deg per frame:
+// 1.31 / 2.25 ms per frame with the set, 0.92 without;
+// profiles/r02_moving_camera_probe.log).  So a slice for a camera other than
+// the last one is a plain slice; the second slice of the same camera
+// rebuilds the set for it (every lit leaf decoded, a census); from the
+// third on the set is used.
+// Whether vis_begin may hand a slice for this view a set (no state change;
+// a race only leaves a deferred-chunk list unused).
+static bool vis_may_use(const vv_tree *t, uint64_t view) {
+    if (!vis_wanted(t)) return false;
+    std::lock_guard<std::mutex> lk(t->vis_mu);
+    return !view || view == t->vis_view;
+}
+
+// allow: the caller can run a visible-set render (else only the view is noted)
+static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt, uint64_t view = 0, bool allow = true) {
     vt = VisTicket();
     if (!vis_wanted(t)) return VV_OK;
     std::lock_guard<std::mutex> lk(t->vis_mu);
+    if (view) {
+        if (view == t->vis_view) {
+            if (t->vis_static < 2) ++t->vis_static;
+        } else {
+            t->vis_view = view;
+            t->vis_static = 0;
+        }
+        if (t->vis_static == 0 || !allow) return VV_OK;  // a new view: the plain slice
+        if (t->vis_static == 1) t->vis_ready = false;    // the view held: rebuild the set for it
+    } else if (!allow) {
+        return VV_OK;
+    }
     if (!t->d_vis) {
         const int64_t words = ((t->n_leaves + 63) / 64) * 2;  // whole 64-leaf slice chunks
         if (cudaMalloc(&t->d_vis, 2 * (size_t)words * sizeof(uint32_t)) != cudaSuccess) {
@@ -292,7 +338,8 @@ static int vis_begin(const vv_tree *t, cudaStream_t st, VisTicket &vt) {
         t->vis_words = words;
     }
     uint32_t *b[2] = {t->d_vis, t->d_vis + t->vis_words};
-    if (!t->vis_ready) {
+    if (!t->vis_ready) {  // a first slice, or a new view: every lit leaf decoded, the set started afresh
+        VV_CUDA(cudaMemsetAsync(t->d_vis, 0, 2 * (size_t)t->vis_words * sizeof(uint32_t), st));
         t->vis_ready = true;
         t->vis_slices = 0;
         vt.mark = b[t->vis_cur];
@@ -609,7 +656,8 @@ void affine_from_inverse(const double *inv, double *A) {
 
 // Transient per-call slice from the stream-ordered pool (freed, stream
 // ordered, when the call returns).
-int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr, bool vis = false) {
+int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr, bool vis = false,
+                    uint64_t view = 0) {
     NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
@@ -626,7 +674,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     sv.rec4 = rec4;
     int rc;
     VisTicket vt;
-    if (vis && (rc = vis_begin(t, st, vt))) return rc;
+    if (vis_wanted(t) && (rc = vis_begin(t, st, vt, view, vis))) return rc;
     sv.mark = vt.mark;
     sv.census = vt.census;
     if (mask_wanted(t) && (rc = alloc_mask(t, st, tr.nmask))) return rc;
@@ -644,7 +692,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
 int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const vv_camera &cam, int rx0, int ry0,
                            int rx1, int ry1, SliceView &sv, Transient &tr, bool vis = false) {
     NvtxRange nv("vv:slice(region, culled)");
-    if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr, vis);
+    if (!t->d_box || t->n_leaves == 0) return build_transient(t, frame, st, sv, tr, vis, view_hash(cam));
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
@@ -697,7 +745,7 @@ int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const v
     p.chunk_list = list;
     p.n_list = count;
     VisTicket vt;
-    if (vis && (rc = vis_begin(t, st, vt))) return rc;
+    if (vis_wanted(t) && (rc = vis_begin(t, st, vt, view_hash(cam), vis))) return rc;
     sv.mark = vt.mark;
     sv.census = vt.census;
     set_slice_masks(t, p);
@@ -1625,7 +1673,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     // visible-set slices (image / region mode): the deferred-chunk list of
     // k_camera_rewalk, zeroed before the slice pass (the PDL chain stays)
     Transient td;
-    if (!tile && ((cache && cache->visible) || (!cache && mode != 0 && vis_wanted(t)))) {
+    if (!tile && ((cache && cache->visible) || (!cache && mode != 0 && vis_may_use(t, view_hash(*cam))))) {
         pool_setup(t->device);
         const size_t cap = (size_t)grid_blocks * kWarpsPerTile;
         if (cudaMallocAsync(&td.mem, 256 + cap * sizeof(int4), st) != cudaSuccess) {
@@ -1641,7 +1689,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     if (!cache && mode != 0) {
         const bool vis = p.deferred != nullptr;
         int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr, vis)
-                     : build_transient(t, frame, st, p.S, tr, vis);
+                     : build_transient(t, frame, st, p.S, tr, vis, view_hash(*cam));
         if (r) return r;
     }
     // sample counts report the reference's full walk: the tree's own table
