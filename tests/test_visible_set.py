@@ -133,6 +133,27 @@ def test_visible_set_sizes(cuda, tree):
     assert 0 < n < tree.n_leaves and 0 < chunks <= (tree.n_leaves + 63) // 64
 
 
+def test_set_follows_the_view(cuda):
+    """A camera that moves every frame never builds a set (plain slices); the
+    second render of a held camera builds it, the third uses it."""
+    from paper_2202_06088_b200.device import replica
+
+    rng = np.random.default_rng(13)
+    t = random_payload_tree(rng, depth=4, fill=0.5, frames=6, sigma_scale=5.0)
+    rep = replica(t, cuda)
+    for i in range(6):
+        vv.render(t, _orbit(i), i % 6)
+    assert rep.visible_count()[0] == 0
+    cam = _orbit(7)
+    vv.render(t, cam, 0)
+    assert rep.visible_count()[0] == 0  # a new view: plain slice
+    vv.render(t, cam, 1)
+    n = rep.visible_count()[0]
+    assert n > 0  # held: the set rebuilt for it (census)
+    got = vv.render(t, cam, 2)
+    _eq(got.rgb, vv.render(t, cam, 2, PS).rgb, "held camera, set in use")
+
+
 def test_edited_tree_ignores_visible_set(cuda):
     import torch
 
