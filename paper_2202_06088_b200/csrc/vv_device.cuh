@@ -805,8 +805,9 @@ struct FrameCtx {
 // run time by S.rec != nullptr (scene kernel, per-instance slices).
 // VIS (camera kernel, visible-set slices): 1 = sliced walk that stops at a
 // leaf outside the slice's visible set (record sigma < 0; `deferred`: the
-// pixel is walked again per sample) and, in a census, marks every leaf it
-// shades; 2 = that per-sample walk again, marking every leaf it shades.
+// pixel is walked again per sample); 3 = the same in a census frame, also
+// marking every leaf it visits; 2 = the per-sample walk of a deferred
+// pixel, marking every leaf it visits.
 template <int NMAX, int CACHED, bool EDITS, bool VISITS, bool POPS = false, int SEG = VV_SEG_MIN, int VIS = 0>
 struct Shader {
     static constexpr bool kPops = POPS;  // exact node-pop counts (stats)
@@ -898,13 +899,13 @@ struct Shader {
         // visible-set walks: a deferred pixel's walk (VIS 2) and a census put
         // every leaf they visit in the set
 #ifndef VV_VIS_NOCENSUS
-        if (VIS == 2 || (VIS == 1 && S.census)) vis_mark(S.mark, L);
+        if (VIS >= 2) vis_mark(S.mark, L);
 #else
         if (VIS == 2) vis_mark(S.mark, L);
 #endif
         if (from_rec) {
             sigma = sigma_cached;
-            if (VIS == 1 && sigma < 0.0) {  // colour not in the slice: the pixel is walked again per sample
+            if ((VIS == 1 || VIS == 3) && sigma < 0.0) {  // colour not in the slice: the pixel is walked again per sample
                 deferred = true;
                 return true;
             }

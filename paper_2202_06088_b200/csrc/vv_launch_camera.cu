@@ -60,6 +60,9 @@ int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p,
         smem = stack_bytes(p.T.depth, wide, false, kTileRays, kSegLong + 3);
         return with_nmax(nmax, [&](auto N) {
             constexpr int NM = decltype(N)::value;
+            if (vis && p.S.census)
+                return wide ? go<NM, 1, false, EntryW, kSegLong, 3>(p, grid, smem, st)
+                            : go<NM, 1, false, EntryN, kSegLong, 3>(p, grid, smem, st);
             if (vis)
                 return wide ? go<NM, 1, false, EntryW, kSegLong, 1>(p, grid, smem, st)
                             : go<NM, 1, false, EntryN, kSegLong, 1>(p, grid, smem, st);
@@ -71,6 +74,9 @@ int launch_camera(int nmax, int mode, bool edits, bool wide, const CamParams &p,
         smem = stack_bytes(p.T.depth, wide, false, kTileRays);
         return with_nmax(nmax, [&](auto N) {
             constexpr int NM = decltype(N)::value;
+            if (p.S.census)  // a census frame: the instantiation that marks every visited leaf
+                return wide ? go<NM, 1, false, EntryW, VV_SEG_MIN, 3>(p, grid, smem, st)
+                            : go<NM, 1, false, EntryN, VV_SEG_MIN, 3>(p, grid, smem, st);
             return wide ? go<NM, 1, false, EntryW, VV_SEG_MIN, 1>(p, grid, smem, st)
                         : go<NM, 1, false, EntryN, VV_SEG_MIN, 1>(p, grid, smem, st);
         });
