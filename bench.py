@@ -271,16 +271,17 @@ def slice_pass_bytes(tree, f, device, chunk=64):
         rows[-1] = n - chunk * (len(rows) - 1)
     masks = rep.dark_fraction >= 0.25 and not getattr(tree, "has_edits", False)
     if visible_set_on(tree, rep):
-        # visible-set slice (k_slice_sigma + k_build_slice<.., VIS>): w_sigma
-        # of every leaf; a chunk with a visible leaf reads its w_gamma chunks
-        # and its visible leaves' w_hh rows and writes every record (the
-        # visible leaves' 8 + 12 S_sh, the others' sigma 8); every other
-        # leaf's record gets its sigma pair (32 B); 2 bitmaps of 1 bit/leaf
-        vis = np.concatenate([rep.visible_mask(), pad]).reshape(-1, chunk)
-        vchunk = vis.any(axis=1)
+        # visible-set slice: the set's snapshot (2 bitmaps read, 1 written,
+        # 1 bit per leaf each), the walk table (the tree's table copied,
+        # its last-level rows rewritten: 64 B per internal node + 64 B per
+        # last-level node), and for each leaf of the set its w_sigma /
+        # w_gamma chunks, w_hh (12 K) and its record (8 + 12 S_sh); no other
+        # leaf is read or written
+        vis = rep.visible_mask()
         nv = int(vis.sum())
-        rv = int(rows[vchunk].sum())
-        b = n * 16 * nza + rv * 16 * nzb + nv * (12 * k + 12 * s_sh) + rv * 8 + (n - rv) * 32 + n // 4
+        n_last = _n_last_level(tree)
+        b = (3 * n // 8 + 64 * tree.n_internal + 64 * n_last
+             + nv * (16 * nza + 16 * nzb + 12 * k + 8 + 12 * s_sh))
     elif masks and os.environ.get("VV_LIT_PASS", "1") != "0":
         # dark-heavy trees: the thread-per-leaf pass (k_slice_visible, lit
         # mode): colour of every lit leaf, the sigma pair of every dark one
@@ -292,6 +293,15 @@ def slice_pass_bytes(tree, f, device, chunk=64):
     if masks:
         b += n + 2 * 32 * tree.n_internal
     return b
+
+
+def _n_last_level(tree) -> int:
+    """Internal nodes whose children are leaf rows (the walk table rewrites them)."""
+    cur = np.array([0], dtype=np.int64)
+    for _ in range(int(tree.depth) - 1):
+        nxt = tree.node_child[cur].ravel()
+        cur = nxt[nxt >= 0].astype(np.int64)
+    return int(len(cur))
 
 
 def visible_set_on(tree, rep) -> bool:
@@ -859,10 +869,10 @@ def run_ours(args, rank, world, local_rank):
                 "bytes_formula": ("per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
                                   "per lit leaf + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh "
                                   "(record); per dark leaf + 32 B (sigma pair)" if lit_pass else
-                                  "visible set: per leaf 16 B per w_sigma float4 chunk the frame's A row does not "
-                                  "zero out; per leaf of a 64-leaf chunk holding a visible leaf + 16 B per nonzero "
-                                  "w_gamma chunk + 8 (sigma), per visible leaf + 12 K (w_hh) + 12 S_sh (colour); per "
-                                  "other leaf + 32 B (sigma pair); + 2 bits per leaf (the set)" if vis_on else
+                                  "visible set: per leaf of the set 16 B per nonzero w_sigma chunk + 16 B per "
+                                  "nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh (record); + 3 bits per leaf "
+                                  "(the set's snapshot) + 64 B per internal node and 64 B per last-level node (the "
+                                  "walk table)" if vis_on else
                                   "per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
                                   "per leaf of a 64-leaf chunk with a lit leaf + 16 B per nonzero w_gamma chunk + "
                                   "12 K (w_hh) + 8 + 12 S_sh (record); of an all-dark chunk + 32 B (sigma)") +

@@ -129,6 +129,8 @@ struct vv_slice {
     bool visible = false;  // VV_SLICE_VISIBLE: colour only in the visible set (-sigma elsewhere)
     uint32_t *vis_mark = nullptr;  // the set its walks mark
     int vis_census = 0;
+    void *d_vis_mem = nullptr;               // its walk table + set snapshot (vis_prepare)
+    const int32_t *vis_table = nullptr;
     int64_t n_leaves;
     cudaStream_t stream;  // stream-ordered allocation: freed on this stream
     std::shared_ptr<NodeMask> nmask;  // dark subtrees cut (image renders), or null
@@ -262,6 +264,7 @@ struct VisTicket {
     const uint32_t *d0 = nullptr, *d1 = nullptr;  // decode set (null: every lit leaf)
     uint32_t *mark = nullptr;
     int census = 0;
+    const int32_t *table = nullptr;  // the walk table (vis_prepare), with a set in use
 };
 
 static bool mask_wanted(const vv_tree *t);
@@ -271,7 +274,7 @@ static bool mask_wanted(const vv_tree *t);
 // 0.831 vs 0.859, cfg5 1.811 vs 1.816 (profiles/r02_visible_set_ab.json).
 // VV_VISIBLE=0 / 1 forces it off / on.
 static bool vis_wanted(const vv_tree *t) {
-    if (t->has_edits || t->n_leaves == 0) return false;
+    if (t->has_edits || t->n_leaves == 0 || !t->mask_ok) return false;  // the walk table needs the last-level list
     if (const char *e = getenv("VV_VISIBLE")) {
         if (e[0] == '0') return false;
         if (e[0] == '1') return true;
@@ -380,6 +383,45 @@ static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *v
     return launch_slice_visible(t->n_max, p, st);
 }
 
+// With a set in use: one stream-ordered block (*mem, the caller frees it)
+// holding the set's snapshot (d0 | d1) and the walk table -- the tree's
+// table with every leaf outside the snapshot replaced by the stand-in row
+// n_leaves, whose record the slice writes with sigma -1.  The slice then
+// decodes from the same snapshot (vt.d0 = vt.d1 = snapshot) and writes
+// records for the set's chunks only: a leaf outside the set is never read
+// through the walk table, and any walk that reaches its stand-in re-walks
+// the pixel on the tree's own table.
+static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **mem) {
+    *mem = nullptr;
+    if (!vt.mark || !vt.d0) return VV_OK;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_table = al((size_t)t->n_internal * 8 * sizeof(int32_t));
+    const size_t b_snap = al((size_t)t->vis_words * sizeof(uint32_t));
+    if (cudaMallocAsync(mem, b_table + b_snap, st) != cudaSuccess) {
+        cudaGetLastError();
+        *mem = nullptr;
+        return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", b_table + b_snap);
+    }
+    int32_t *table = static_cast<int32_t *>(*mem);
+    uint32_t *snap = reinterpret_cast<uint32_t *>(static_cast<char *>(*mem) + b_table);
+    int rc = launch_vis_snapshot(vt.d0, vt.d1, snap, t->vis_words, st);
+    if (rc) return rc;
+    VV_CUDA(cudaMemcpyAsync(table, t->d_child, (size_t)t->n_internal * 8 * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            st));
+    VisTableParams q;
+    q.child = t->d_child;
+    q.last = t->d_last;
+    q.n_last = t->n_last;
+    q.vis0 = snap;
+    q.vis1 = snap;
+    q.stand_in = (int32_t)t->n_leaves;
+    q.out = table;
+    if ((rc = launch_vis_table(q, st))) return rc;
+    vt.d0 = vt.d1 = snap;
+    vt.table = table;
+    return VV_OK;
+}
+
 int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only,
                        uint8_t *lit = nullptr, const VisTicket *vt = nullptr) {
     if (t->n_leaves == 0) return VV_OK;
@@ -401,13 +443,15 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
 // Transient per-frame slice in the device's stream-ordered pool; freed
 // (stream-ordered) when the render call returns.
 struct Transient {
-    void *mem = nullptr;
+    void *mem = nullptr, *vis_mem = nullptr;
     cudaStream_t st = nullptr;
     std::shared_ptr<NodeMask> nmask;
+    const int32_t *vis_table = nullptr;  // visible-set walk table (in vis_mem)
     Transient() = default;
     Transient(const Transient &) = delete;
     ~Transient() {
         if (mem) cudaFreeAsync(mem, st);
+        if (vis_mem) cudaFreeAsync(vis_mem, st);
     }
 };
 
@@ -661,7 +705,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
-    const size_t bytes = (size_t)t->n_leaves * rec4 * sizeof(float4);
+    const size_t bytes = (size_t)(t->n_leaves + 1) * rec4 * sizeof(float4);  // + the walk table's stand-in row
     cudaError_t e = cudaMallocAsync(&tr.mem, bytes, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -675,6 +719,8 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     int rc;
     VisTicket vt;
     if (vis_wanted(t) && (rc = vis_begin(t, st, vt, view, vis))) return rc;
+    if ((rc = vis_prepare(t, vt, st, &tr.vis_mem))) return rc;
+    tr.vis_table = vt.table;
     sv.mark = vt.mark;
     sv.census = vt.census;
     if (mask_wanted(t) && (rc = alloc_mask(t, st, tr.nmask))) return rc;
@@ -696,7 +742,7 @@ int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const v
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t b_rec = al((size_t)t->n_leaves * rec4 * sizeof(float4));
+    const size_t b_rec = al((size_t)(t->n_leaves + 1) * rec4 * sizeof(float4));  // + the stand-in row
     const size_t bytes = b_rec + al((size_t)t->n_box * 4) + 256;
     cudaError_t e = cudaMallocAsync(&tr.mem, bytes, st);
     if (e != cudaSuccess) {
@@ -746,6 +792,8 @@ int build_transient_region(const vv_tree *t, int frame, cudaStream_t st, const v
     p.n_list = count;
     VisTicket vt;
     if (vis_wanted(t) && (rc = vis_begin(t, st, vt, view_hash(cam), vis))) return rc;
+    if ((rc = vis_prepare(t, vt, st, &tr.vis_mem))) return rc;
+    tr.vis_table = vt.table;
     sv.mark = vt.mark;
     sv.census = vt.census;
     set_slice_masks(t, p);
@@ -1398,7 +1446,7 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
     p.n_frames = n_frames;
     p.n_leaves = t->n_leaves;
     p.rec4 = slice_rec4(t->S);
-    const int64_t nrows = std::max<int64_t>(t->n_leaves, 1);
+    const int64_t nrows = std::max<int64_t>(t->n_leaves, 1) + ((flags & VV_SLICE_VISIBLE) ? 1 : 0);  // + stand-in row
     auto fail = [&](int rc) {
         for (int f = 0; f < n_frames; ++f) {
             vv_slice_free(out[f]);
@@ -1433,6 +1481,8 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
         out[0]->visible = vt.mark != nullptr;
         out[0]->vis_mark = vt.mark;
         out[0]->vis_census = vt.census;
+        if ((vrc = vis_prepare(t, vt, (cudaStream_t)stream, &out[0]->d_vis_mem))) return fail(vrc);
+        out[0]->vis_table = vt.table;
 
     }
     set_slice_masks(t, p);
@@ -1453,6 +1503,7 @@ int vv_slice_free(vv_slice *s) {
     if (!s) return VV_OK;
     DeviceGuard g(s->device);
     if (s->d_rec) cudaFreeAsync(s->d_rec, s->stream);
+    if (s->d_vis_mem) cudaFreeAsync(s->d_vis_mem, s->stream);
     delete s;
     return VV_OK;
 }
@@ -1696,6 +1747,13 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     const NodeMask *nm = used ? nullptr : (cache ? cache->nmask.get() : tr.nmask.get());
     p.T.child = image_child(t, nm);
     if (p.S.mark && !p.deferred) return set_error(VV_E_INVALID, "visible-set slices: image or region renders only");
+    // a set in use: the walk table hides the leaves outside it (their
+    // stand-in row n_leaves defers the pixel); the re-walk keeps the tree's table
+    if (const int32_t *vt_table = cache ? cache->vis_table : tr.vis_table) {
+        p.child_full = p.T.child;
+        p.T.child = vt_table;
+        p.T.n_leaves = t->n_leaves + 1;  // the stand-in row is a valid record row
+    }
     const bool vis = p.S.mark != nullptr;
     rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm), vis);
     if (!rc && vis) rc = launch_camera_rewalk(t->n_max, wide, p, st);

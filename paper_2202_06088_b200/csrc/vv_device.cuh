@@ -896,19 +896,18 @@ struct Shader {
         // from the payload (render_kernel's uncached branch)
         const bool from_rec = is_cached();
         double sigma;
-        // visible-set walks: a deferred pixel's walk (VIS 2) and a census put
-        // every leaf they visit in the set
-#ifndef VV_VIS_NOCENSUS
-        if (VIS >= 2) vis_mark(S.mark, L);
-#else
+        // visible-set walks: a deferred pixel's walk (VIS 2) and a census
+        // (VIS 3) put every leaf they visit in the set
         if (VIS == 2) vis_mark(S.mark, L);
-#endif
         if (from_rec) {
             sigma = sigma_cached;
-            if ((VIS == 1 || VIS == 3) && sigma < 0.0) {  // colour not in the slice: the pixel is walked again per sample
+            // outside the slice's set (a negative sigma, or the walk table's
+            // stand-in row): the pixel is walked again per sample
+            if ((VIS == 1 || VIS == 3) && sigma < 0.0) {
                 deferred = true;
                 return true;
             }
+            if (VIS == 3) vis_mark(S.mark, L);
         } else {
             const double sp = sigma_pre(T.sig + L, T.lstride, F.sA, T.C, F.mA);
             sigma = sp > 0.0 ? sp : 0.0;

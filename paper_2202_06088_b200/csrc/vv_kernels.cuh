@@ -156,6 +156,9 @@ struct CamParams {
     // walks those pixels again per sample, then counts the chunk for its band
     int4 *deferred;
     int *n_deferred;
+    // the tree's own child table, for the deferred pixels' walk when T.child
+    // is a visible-set walk table (leaves outside the set -> a stand-in row)
+    const int32_t *child_full;
 };
 
 // band of a row offset from the rectangle's top (banded host copies)
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(kTileRays, kCamMinBlocks) k_camera_rewalk(cons
             Ray ray;
             Shader<NMAX, 0, false, false, false, VV_SEG_MIN, 2> sh(p.T, p.S, F, p.K, (float)dx, (float)dy, (float)dz);
             if (ray_setup(p.T, p.cam.ox, p.cam.oy, p.cam.oz, dx, dy, dz, p.tmin, p.tmax, ray))
-                traverse<Entry>(p.T.child, p.T.depth, ray, smem_raw, sh);
+                traverse<Entry>(p.child_full ? p.child_full : p.T.child, p.T.depth, ray, smem_raw, sh);
             float r, g, b, a, d;
             finalize(sh.acc0, sh.acc1, sh.acc2, sh.aacc, sh.tacc, 1.0, false, p.alpha_floor, p.far_plane, r, g, b, a,
                      d);
@@ -1079,17 +1082,24 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)  //
             }
         }
         const int nj = (int)min((int64_t)32, (n_items - i0 + nw - 1) / nw);
+        if (!all && i0 == 0 && lane == 0) {  // the walk table's stand-in row: sigma -1 (deferral)
+            const unsigned long long sb = (unsigned long long)__double_as_longlong(-1.0);
+            float4 *o = p.rec[0] + (p.n_leaves + 1) * p.rec4 - 1;
+            *o = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)), __uint_as_float((unsigned)(sb >> 32)));
+        }
 #pragma unroll 1
         for (int j = 0; j < nj; ++j) {
             const int64_t c = __shfl_sync(0xffffffffu, cj, j);
             const uint64_t vm = ((uint64_t)__shfl_sync(0xffffffffu, hi, j) << 32) | __shfl_sync(0xffffffffu, lo, j);
             const int64_t base = c * 64;
             const int rows = (int)min((int64_t)64, p.n_leaves - base);
+            if (!all && !vm) continue;  // no leaf of the set: the walk table hides the chunk's leaves
             double sp[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {  // both leaves' w_sigma loads in flight together
                 const int r = lane + 32 * u;
-                sp[u] = r < rows ? sigma_pre_batched<2>(p.T.sig + base + r, p.T.lstride, sA, p.T.C, p.mS) : 0.0;
+                sp[u] = r < rows && (all || ((vm >> r) & 1ull))
+                            ? sigma_pre_batched<2>(p.T.sig + base + r, p.T.lstride, sA, p.T.C, p.mS) : 0.0;
             }
 #pragma unroll 1
             for (int u = 0; u < 2; ++u) {
@@ -1120,8 +1130,8 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)  //
                     float4 *o = p.rec[0] + L * p.rec4;
 #pragma unroll
                     for (int k = 0; k < R4; ++k) o[k] = make_float4(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
-                } else {
-                    const double sigma = sp[u] > 0.0 ? -sp[u] : 0.0;  // a lit leaf outside the set: its pixels re-walk
+                } else if (all) {  // (outside the set: no record -- the walk table hides the leaf)
+                    const double sigma = sp[u] > 0.0 ? -sp[u] : 0.0;
                     const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
                     float4 *o = p.rec[0] + (L + 1) * p.rec4 - TAIL;
 #pragma unroll
@@ -1345,6 +1355,22 @@ struct MaskParams {
     int32_t *mask;              // (n_internal, 8) out
 };
 int launch_node_mask(const MaskParams &p, cudaStream_t st);
+// visible-set walk table: the tree's table with every leaf outside the set
+// (a snapshot of vis0 | vis1) replaced by the stand-in row, whose slice
+// record holds sigma -1 (the walk defers the pixel).  `out` must already
+// hold a copy of the table (its upper rows are not rewritten).
+struct VisTableParams {
+    const int32_t *child;
+    const int32_t *last;  // last-level internal nodes
+    int64_t n_last;
+    const uint32_t *vis0, *vis1;
+    int32_t stand_in;
+    int32_t *out;
+};
+int launch_vis_table(const VisTableParams &p, cudaStream_t st);
+// out[i] = a[i] | b[i]: the slice's snapshot of the visible set (the table
+// and the slice pass both read it, so they agree whatever walks mark meanwhile)
+int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st);
 // leaf rows per box of the chunk culling (= the single-frame slice chunk)
 constexpr int kRegionChunk = kSliceChunk;
 // chunks whose leaf-cell box can project into a pixel rectangle

@@ -46,6 +46,43 @@ __global__ void __launch_bounds__(256) k_mask_last(const __grid_constant__ MaskP
     }
 }
 
+__global__ void __launch_bounds__(256) k_vis_table(const __grid_constant__ VisTableParams p) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n_last; i += stride) {
+        const int32_t n = __ldg(p.last + i);
+        const int4 *row = reinterpret_cast<const int4 *>(p.child) + 2 * (int64_t)n;
+        int4 a = __ldg(row), b = __ldg(row + 1);
+        int c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (c[k] < 0) continue;
+            const uint32_t w = __ldcg(p.vis0 + (c[k] >> 5)) | __ldcg(p.vis1 + (c[k] >> 5));
+            if (!((w >> (c[k] & 31)) & 1u)) c[k] = p.stand_in;
+        }
+        int4 *out = reinterpret_cast<int4 *>(p.out) + 2 * (int64_t)n;
+        out[0] = make_int4(c[0], c[1], c[2], c[3]);
+        out[1] = make_int4(c[4], c[5], c[6], c[7]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_vis_or(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = __ldcg(a + i) | __ldcg(b + i);
+}
+
+int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st) {
+    if (!n) return VV_OK;
+    k_vis_or<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(a, b, out, n);
+    return check_launch("vis_snapshot");
+}
+
+int launch_vis_table(const VisTableParams &p, cudaStream_t st) {
+    if (!p.n_last) return VV_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((p.n_last + 255) / 256, 148 * 8);
+    k_vis_table<<<grid, 256, 0, st>>>(p);
+    return check_launch("vis_table");
+}
+
 __global__ void __launch_bounds__(256) k_mask_upper(const __grid_constant__ MaskParams p) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n_upper; i += stride) {
