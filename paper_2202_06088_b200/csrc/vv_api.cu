@@ -265,6 +265,7 @@ struct VisTicket {
     uint32_t *mark = nullptr;
     int census = 0;
     const int32_t *table = nullptr;  // the walk table (vis_prepare), with a set in use
+    const int32_t *list = nullptr, *n_list = nullptr;  // the set's leaf rows (the slice's work list)
 };
 
 static bool mask_wanted(const vv_tree *t);
@@ -380,6 +381,8 @@ static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *v
     }
     p.vis0 = vt->d0;  // null: every leaf visible (a tree's first slice)
     p.vis1 = vt->d1;
+    p.leaf_list = vt->list;  // with a walk table: a thread per leaf of the set
+    p.n_leaf_list = vt->n_list;
     return launch_slice_visible(t->n_max, p, st);
 }
 
@@ -397,13 +400,17 @@ static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t b_table = al((size_t)t->n_internal * 8 * sizeof(int32_t));
     const size_t b_snap = al((size_t)t->vis_words * sizeof(uint32_t));
-    if (cudaMallocAsync(mem, b_table + b_snap, st) != cudaSuccess) {
+    const size_t b_list = al((size_t)t->n_leaves * sizeof(int32_t));
+    if (cudaMallocAsync(mem, b_table + b_snap + b_list + 256, st) != cudaSuccess) {
         cudaGetLastError();
         *mem = nullptr;
-        return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", b_table + b_snap);
+        return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", b_table + b_snap + b_list);
     }
     int32_t *table = static_cast<int32_t *>(*mem);
     uint32_t *snap = reinterpret_cast<uint32_t *>(static_cast<char *>(*mem) + b_table);
+    int32_t *list = reinterpret_cast<int32_t *>(static_cast<char *>(*mem) + b_table + b_snap);
+    int32_t *n_list = reinterpret_cast<int32_t *>(static_cast<char *>(*mem) + b_table + b_snap + b_list);
+    VV_CUDA(cudaMemsetAsync(n_list, 0, sizeof(int32_t), st));
     int rc = launch_vis_snapshot(vt.d0, vt.d1, snap, t->vis_words, st);
     if (rc) return rc;
     VV_CUDA(cudaMemcpyAsync(table, t->d_child, (size_t)t->n_internal * 8 * sizeof(int32_t), cudaMemcpyDeviceToDevice,
@@ -416,9 +423,13 @@ static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **
     q.vis1 = snap;
     q.stand_in = (int32_t)t->n_leaves;
     q.out = table;
+    q.list = list;
+    q.n_list = n_list;
     if ((rc = launch_vis_table(q, st))) return rc;
     vt.d0 = vt.d1 = snap;
     vt.table = table;
+    vt.list = list;
+    vt.n_list = n_list;
     return VV_OK;
 }
 

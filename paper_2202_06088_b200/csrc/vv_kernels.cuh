@@ -748,6 +748,9 @@ struct SliceParams {
     // union of two bitmaps over leaf rows (null: every leaf); only leaves in
     // it get their colour, a lit leaf outside it -sigma (SliceView)
     const uint32_t *vis0, *vis1;
+    // with a walk table (k_slice_leaves): the set's leaf rows, listed by k_vis_table
+    const int32_t *leaf_list;
+    const int32_t *n_leaf_list;
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -1144,6 +1147,57 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)  //
     }
 }
 
+// Visible-set slice with a walk table: a thread per leaf of the set (the
+// list k_vis_table wrote), its whole record decoded exactly as in
+// k_slice_visible; plus the walk table's stand-in row (sigma -1).  Every
+// lane works, where a chunk-per-warp pass left the lanes of the set's
+// sparse chunks idle.
+template <int NMAX>
+__global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)
+    k_slice_leaves(const __grid_constant__ SliceParams p) {
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame[0], sA, sB);
+    __syncthreads();
+    constexpr int R4 = slice_rec4(Basis<NMAX>::S);
+    pdl_trigger();
+    pdl_wait();  // the list is the previous kernel's
+    const int64_t n = (int64_t)*(volatile const int32_t *)p.n_leaf_list;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t0 == 0) {
+        const unsigned long long sb = (unsigned long long)__double_as_longlong(-1.0);
+        float4 *o = p.rec[0] + (p.n_leaves + 1) * p.rec4 - 1;
+        *o = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)), __uint_as_float((unsigned)(sb >> 32)));
+    }
+#pragma unroll 1
+    for (int64_t i = t0; i < n; i += stride) {
+        const int64_t L = __ldg(p.leaf_list + i);
+        float wh[4 * Basis<NMAX>::HH4];
+        load_hh<NMAX>(p.T.hh + L * p.T.hh4, wh);  // in flight with the sigma and gamma chunks
+        const double sp = sigma_pre_batched<2>(p.T.sig + L, p.T.lstride, sA, p.T.C, p.mS);
+        const float s = gamma_s_batched<2>(p.T.gam + L, p.T.lstride, sB, p.T.C, p.mG);
+        float q[4 * R4];
+#pragma unroll
+        for (int k = 0; k < 4 * R4; ++k) q[k] = 0.0f;
+        float R[Basis<NMAX>::NPAIRS];
+        radial<NMAX>(s, p.K, R);
+#pragma unroll
+        for (int l = 0; l <= NMAX; ++l)
+#pragma unroll
+            for (int m = -l; m <= l; ++m) {
+                const int jj = l * l + l + m;
+                slice_col<NMAX>(R, wh, l, m, q[3 * jj + 0], q[3 * jj + 1], q[3 * jj + 2]);
+            }
+        const double sigma = sp > 0.0 ? sp : 0.0;
+        const unsigned long long sb = (unsigned long long)__double_as_longlong(sigma);
+        q[4 * R4 - 2] = __uint_as_float((unsigned)(sb & 0xffffffffu));
+        q[4 * R4 - 1] = __uint_as_float((unsigned)(sb >> 32));
+        float4 *o = p.rec[0] + L * p.rec4;
+#pragma unroll
+        for (int k = 0; k < R4; ++k) o[k] = make_float4(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
+    }
+}
+
 // ------------------------------------------------------------------ traversal only
 struct SegParams {
     TreeView T;
@@ -1340,7 +1394,8 @@ int launch_scene(int nmax, bool wide, bool lean, const SceneParams &p, dim3 grid
 // per-sample depth-ordered joint composition (vv_launch_joint.cu)
 int launch_scene_joint(int nmax, bool wide, const SceneParams &p, cudaStream_t st);
 int launch_slice(int nmax, const SliceParams &p, cudaStream_t st);
-// visible-set slice of one frame (k_slice_visible; p.vis0/vis1, or neither: every leaf)
+// visible-set slice of one frame (k_slice_visible; p.vis0/vis1, or neither:
+// every leaf; k_slice_leaves when p.leaf_list is set)
 int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st);
 // per-frame node mask (vv_launch_mask.cu): child table with every child whose
 // subtree holds no lit leaf replaced by -1
@@ -1366,6 +1421,8 @@ struct VisTableParams {
     const uint32_t *vis0, *vis1;
     int32_t stand_in;
     int32_t *out;
+    int32_t *list;     // out: the set's leaf rows (the slice pass's work list), in last-level node order
+    int32_t *n_list;   // zeroed before the launch
 };
 int launch_vis_table(const VisTableParams &p, cudaStream_t st);
 // out[i] = a[i] | b[i]: the slice's snapshot of the visible set (the table

@@ -47,17 +47,48 @@ __global__ void __launch_bounds__(256) k_mask_last(const __grid_constant__ MaskP
 }
 
 __global__ void __launch_bounds__(256) k_vis_table(const __grid_constant__ VisTableParams p) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n_last; i += stride) {
-        const int32_t n = __ldg(p.last + i);
-        const int4 *row = reinterpret_cast<const int4 *>(p.child) + 2 * (int64_t)n;
-        int4 a = __ldg(row), b = __ldg(row + 1);
-        int c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32: warps stay whole
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < p.n_last; b0 += stride) {
+        const int64_t i = b0 + lane;
+        int c[8];
+        unsigned keep = 0;
+        int32_t n = -1;
+        if (i < p.n_last) {
+            n = __ldg(p.last + i);
+            const int4 *row = reinterpret_cast<const int4 *>(p.child) + 2 * (int64_t)n;
+            const int4 a = __ldg(row), b = __ldg(row + 1);
+            c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (c[k] < 0) continue;
+                // the snapshot (written by the previous kernel, read-only here: L1-cached)
+                const uint32_t w = p.vis0 == p.vis1 ? __ldg(p.vis0 + (c[k] >> 5))
+                                                    : __ldg(p.vis0 + (c[k] >> 5)) | __ldg(p.vis1 + (c[k] >> 5));
+                if ((w >> (c[k] & 31)) & 1u) keep |= 1u << k;
+            }
+        }
+        // the kept leaves go to the work list: one atomic per warp
+        const int cnt = __popc(keep);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int wbase = 0;
+        if (lane == 31 && incl) wbase = atomicAdd(p.n_list, incl);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        if (n < 0) continue;
+        int off = wbase + incl - cnt;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (c[k] < 0) continue;
-            const uint32_t w = __ldcg(p.vis0 + (c[k] >> 5)) | __ldcg(p.vis1 + (c[k] >> 5));
-            if (!((w >> (c[k] & 31)) & 1u)) c[k] = p.stand_in;
+            if ((keep >> k) & 1u) {
+                p.list[off++] = c[k];
+            } else {
+                c[k] = p.stand_in;
+            }
         }
         int4 *out = reinterpret_cast<int4 *>(p.out) + 2 * (int64_t)n;
         out[0] = make_int4(c[0], c[1], c[2], c[3]);

@@ -131,6 +131,10 @@ int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t chunks = (p.n_leaves + 63) / 64;
+        if (p.leaf_list) {  // a thread per leaf of the set
+            launch_pdl(k_slice_leaves<NM>, dim3((unsigned)(sms * 16)), dim3(VV_VIS_BLOCK), 0, st, p);
+            return check_launch("slice_leaves");
+        }
         constexpr int wpb = VV_VIS_BLOCK / 32;
         const unsigned grid =
             (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + wpb - 1) / wpb, (int64_t)sms * 64 / wpb));
