@@ -751,6 +751,10 @@ struct SliceParams {
     // with a walk table (k_slice_leaves): the set's leaf rows, listed by k_vis_table
     const int32_t *leaf_list;
     const int32_t *n_leaf_list;
+    // a region render: bit c set iff 64-leaf chunk c is in the region's
+    // chunk list (k_slice_leaves skips the set's other leaves: the region's
+    // rays cannot reach them)
+    const uint32_t *chunk_bits;
 };
 
 // build_slice_kernel (kernels.py:397-407).  Persistent warps take chunks of
@@ -1172,6 +1176,7 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)
 #pragma unroll 1
     for (int64_t i = t0; i < n; i += stride) {
         const int64_t L = __ldg(p.leaf_list + i);
+        if (p.chunk_bits && !((__ldg(p.chunk_bits + (L >> 11)) >> ((L >> 6) & 31)) & 1u)) continue;
         float wh[4 * Basis<NMAX>::HH4];
         load_hh<NMAX>(p.T.hh + L * p.T.hh4, wh);  // in flight with the sigma and gamma chunks
         const double sp = sigma_pre_batched<2>(p.T.sig + L, p.T.lstride, sA, p.T.C, p.mS);
@@ -1428,6 +1433,8 @@ int launch_vis_table(const VisTableParams &p, cudaStream_t st);
 // out[i] = a[i] | b[i]: the slice's snapshot of the visible set (the table
 // and the slice pass both read it, so they agree whatever walks mark meanwhile)
 int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st);
+// bits[list[i] / 32] |= 1 << (list[i] % 32) for i < *n (bits zeroed first)
+int launch_chunk_bits(const int32_t *list, const int32_t *n, uint32_t *bits, int64_t max_n, cudaStream_t st);
 // leaf rows per box of the chunk culling (= the single-frame slice chunk)
 constexpr int kRegionChunk = kSliceChunk;
 // chunks whose leaf-cell box can project into a pixel rectangle

@@ -107,6 +107,21 @@ int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int
     return check_launch("vis_snapshot");
 }
 
+__global__ void __launch_bounds__(256) k_chunk_bits(const int32_t *list, const int32_t *n, uint32_t *bits) {
+    const int64_t m = *n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const int32_t c = list[i];
+        atomicOr(bits + (c >> 5), 1u << (c & 31));
+    }
+}
+
+int launch_chunk_bits(const int32_t *list, const int32_t *n, uint32_t *bits, int64_t max_n, cudaStream_t st) {
+    if (max_n <= 0) return VV_OK;
+    k_chunk_bits<<<(unsigned)std::min<int64_t>((max_n + 255) / 256, 148 * 4), 256, 0, st>>>(list, n, bits);
+    return check_launch("chunk_bits");
+}
+
 int launch_vis_table(const VisTableParams &p, cudaStream_t st) {
     if (!p.n_last) return VV_OK;
     const unsigned grid = (unsigned)std::min<int64_t>((p.n_last + 255) / 256, 148 * 8);
