@@ -247,7 +247,7 @@ def walk_counts(tree, o, d, f, device, masked=False):
             (("P", "node_pops"), ("V", "sample_count"), ("S", "shaded"))}
 
 
-def slice_pass_bytes(tree, f, device, chunk=64):
+def slice_pass_bytes(tree, f, device, chunk=64, table_per_frame=False):
     """Bytes the render-internal slice pass of frame f needs (render() runs it):
     per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero
     out; a 64-leaf chunk with a lit leaf also reads its w_gamma chunks (16 B
@@ -271,17 +271,17 @@ def slice_pass_bytes(tree, f, device, chunk=64):
         rows[-1] = n - chunk * (len(rows) - 1)
     masks = rep.dark_fraction >= 0.25 and not getattr(tree, "has_edits", False)
     if visible_set_on(tree, rep):
-        # visible-set slice: the set's snapshot (2 bitmaps read, 1 written,
-        # 1 bit per leaf each), the walk table (the tree's table copied,
-        # its last-level rows rewritten: 64 B per internal node + 64 B per
-        # last-level node), and for each leaf of the set its w_sigma /
-        # w_gamma chunks, w_hh (12 K) and its record (8 + 12 S_sh); no other
-        # leaf is read or written
+        # visible-set slice with the camera plan's walk table: the set's two
+        # bitmaps and the kept snapshot read (1 bit per leaf each; the walk
+        # table is rebuilt only when the snapshot changes, which a held view
+        # does not), the work list (4 B per leaf of the set), and for each
+        # leaf of the set its w_sigma / w_gamma chunks, w_hh (12 K) and its
+        # record (8 + 12 S_sh); no other leaf is read or written
         vis = rep.visible_mask()
         nv = int(vis.sum())
-        n_last = _n_last_level(tree)
-        b = (3 * n // 8 + 64 * tree.n_internal + 64 * n_last
-             + nv * (16 * nza + 16 * nzb + 12 * k + 8 + 12 * s_sh))
+        b = 3 * n // 8 + nv * (4 + 16 * nza + 16 * nzb + 12 * k + 8 + 12 * s_sh)
+        if table_per_frame:
+            b += 64 * tree.n_internal + 64 * _n_last_level(tree)
     elif masks and os.environ.get("VV_LIT_PASS", "1") != "0":
         # dark-heavy trees: the thread-per-leaf pass (k_slice_visible, lit
         # mode): colour of every lit leaf, the sigma pair of every dark one
@@ -535,18 +535,31 @@ class Stepper:
             self.renders += 1
             self.launches += 1 + (self.renders % 4 == 1)  # scene kernel (+ plan order every 4th render)
             return
-        # exactly what render() does: the render-internal slice pass (colour
-        # only for the tree's visible set; node masks for dark-heavy trees) ...
-        fs = vv.build_frame_caches(wl.tree, [f], visible=True)[0]
+        vis = visible_set_on(wl.tree, vv.device.replica(wl.tree, self.dev))
+        self.renders += 1
+        if len(wl.cams) == 1:
+            # exactly what render() does: render_into with the stream's plan,
+            # its render-internal slice (the plan's visible-set walk table,
+            # node masks for dark-heavy trees) and camera kernel; the library
+            # records `mid` between the two (vv_profile_split_event)
+            if mid is not None:
+                from paper_2202_06088_b200 import _native
+
+                mid.record(stream)  # (torch creates the event on its first record)
+                _native.check(_native.lib().vv_profile_split_event(ctypes.c_void_p(mid.cuda_event)))
+            vv.render_into(wl.tree, wl.cams[0], f, *self.outs[0], plan=self.plans[0])
+            # slice pass (+ snapshot diff and walk-table pass with the set),
+            # camera kernel, deferred-pixel walk (set), plan order every 4th render
+            self.launches += 1 + 2 * int(vis) + 1 + int(vis) + int(self.renders % 4 == 1)
+            return
+        # stereo: both eyes render from one shared slice (VV_SLICE_VISIBLE),
+        # its walk table kept in the first eye's plan
+        fs = vv.build_frame_caches(wl.tree, [f], visible=True, plan=self.plans[0])[0]
         if mid is not None:
             mid.record(stream)
-        for cam, out, plan in zip(wl.cams, self.outs, self.plans):  # ... then the camera kernel(s)
+        for cam, out, plan in zip(wl.cams, self.outs, self.plans):
             vv.render_into(wl.tree, cam, f, *out, cache=fs, plan=plan)
-        # slice pass; per camera: camera kernel, deferred-pixel walk (visible
-        # set), plan order every 4th render
-        self.renders += 1
-        vis = visible_set_on(wl.tree, vv.device.replica(wl.tree, self.dev))
-        self.launches += 1 + len(wl.cams) * (1 + int(vis) + int(self.renders % 4 == 1))
+        self.launches += 1 + 2 * int(vis) + len(wl.cams) * (1 + int(vis) + int(self.renders % 4 == 1))
         del fs
 
 
@@ -869,10 +882,10 @@ def run_ours(args, rank, world, local_rank):
                 "bytes_formula": ("per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
                                   "per lit leaf + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh "
                                   "(record); per dark leaf + 32 B (sigma pair)" if lit_pass else
-                                  "visible set: per leaf of the set 16 B per nonzero w_sigma chunk + 16 B per "
-                                  "nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh (record); + 3 bits per leaf "
-                                  "(the set's snapshot) + 64 B per internal node and 64 B per last-level node (the "
-                                  "walk table)" if vis_on else
+                                  "visible set: per leaf of the set 4 B (work list) + 16 B per nonzero w_sigma "
+                                  "chunk + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh (record); + 3 "
+                                  "bits per leaf (the set and its kept snapshot; the walk table is rebuilt only when "
+                                  "the set changes)" if vis_on else
                                   "per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
                                   "per leaf of a 64-leaf chunk with a lit leaf + 16 B per nonzero w_gamma chunk + "
                                   "12 K (w_hh) + 8 + 12 S_sh (record); of an all-dark chunk + 32 B (sigma)") +

@@ -57,6 +57,7 @@ EXPORTED_SYMBOLS = (
     "vv_tree_info",
     "vv_tree_dark_fraction",
     "vv_tree_visible_count",
+    "vv_profile_split_event",
     "vv_tree_visible_bits",
     "vv_tree_leaf_order",
     "vv_slice_build",
@@ -88,6 +89,7 @@ EXPORTED_SYMBOLS = (
     "vv_render_camera_multi_planned",
     "vv_slice_build_multi",
     "vv_slice_build_frames",
+    "vv_slice_build_visible",
     "vv_camera_decode_mode",
     "vv_shadow_blur",
     "vv_scene_lighting",
@@ -225,6 +227,7 @@ _SIGNATURES = {
     "vv_tree_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "vv_tree_dark_fraction": (ctypes.c_int, [_P, _P]),
     "vv_tree_visible_count": (ctypes.c_int, [_P, _P, _P, _P]),
+    "vv_profile_split_event": (ctypes.c_int, [_P]),
     "vv_tree_visible_bits": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "vv_tree_leaf_order": (ctypes.c_int, [_P, _P]),
     "vv_slice_build": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_P)]),
@@ -277,6 +280,7 @@ _SIGNATURES = {
     "vv_camera_decode_mode": (ctypes.c_int, [_P, _P, _P, _P]),
     "vv_slice_build_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
     "vv_slice_build_frames": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P]),
+    "vv_slice_build_visible": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P]),
     "vv_render_camera_multi": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_render_camera_multi_planned": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vv_shadow_blur": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P]),

@@ -158,6 +158,13 @@ struct vv_camera_plan {
     vv_camera cov_cam;
     bool cov_valid = false;
     CoverView cov{};
+    // visible-set walk table of the last tree rendered through the plan
+    // (vis_prepare): kept across frames and rebuilt on the device only when
+    // the set's snapshot changes (a held view's set settles after a frame)
+    void *vis_mem = nullptr;
+    size_t vis_cap = 0;
+    uint64_t vis_tree = 0;
+    bool vis_fresh = false;  // buffers (re)made: the next snapshot counts as changed
     std::mutex mu;
 };
 
@@ -167,6 +174,10 @@ struct vv_camera_plan {
         if (e_ != cudaSuccess)                                                                 \
             return set_error(VV_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));      \
     } while (0)
+
+// Benchmark split point (vv_profile_split_event): recorded by the calling
+// thread's next camera render between its slice pass and its camera kernel.
+static thread_local cudaEvent_t split_event = nullptr;
 
 namespace {
 
@@ -394,27 +405,65 @@ static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *v
 // records for the set's chunks only: a leaf outside the set is never read
 // through the walk table, and any walk that reaches its stand-in re-walks
 // the pixel on the tree's own table.
-static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **mem) {
+// With a camera plan (the caller holds its lock) the table, snapshot and
+// list live in the plan and are rebuilt only when the snapshot changes
+// (k_vis_or flags it; k_vis_table then returns at once): a held view's set
+// settles after its census, so steady frames skip the table pass.
+static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **mem, vv_camera_plan *plan = nullptr) {
     *mem = nullptr;
     if (!vt.mark || !vt.d0) return VV_OK;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t b_table = al((size_t)t->n_internal * 8 * sizeof(int32_t));
     const size_t b_snap = al((size_t)t->vis_words * sizeof(uint32_t));
     const size_t b_list = al((size_t)t->n_leaves * sizeof(int32_t));
-    if (cudaMallocAsync(mem, b_table + b_snap + b_list + 256, st) != cudaSuccess) {
-        cudaGetLastError();
-        *mem = nullptr;
-        return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", b_table + b_snap + b_list);
+    const size_t total = b_table + b_snap + b_list + 256;
+    char *base = nullptr;
+    bool fresh = true;
+    if (plan) {
+        if (!plan->vis_mem || plan->vis_cap < total || plan->vis_tree != t->serial) {
+            if (plan->vis_mem) {
+                cudaStreamSynchronize(st);  // an earlier frame on this stream may still read it
+                cudaFree(plan->vis_mem);
+                plan->vis_mem = nullptr;
+                plan->vis_cap = 0;
+            }
+            if (cudaMalloc(&plan->vis_mem, total) != cudaSuccess) {
+                cudaGetLastError();
+                plan->vis_mem = nullptr;
+                return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", total);
+            }
+            plan->vis_cap = total;
+            plan->vis_tree = t->serial;
+            plan->vis_fresh = true;
+        }
+        base = static_cast<char *>(plan->vis_mem);
+        fresh = plan->vis_fresh;
+        plan->vis_fresh = false;
+    } else {
+        if (cudaMallocAsync(mem, total, st) != cudaSuccess) {
+            cudaGetLastError();
+            *mem = nullptr;
+            return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", total);
+        }
+        base = static_cast<char *>(*mem);
     }
-    int32_t *table = static_cast<int32_t *>(*mem);
-    uint32_t *snap = reinterpret_cast<uint32_t *>(static_cast<char *>(*mem) + b_table);
-    int32_t *list = reinterpret_cast<int32_t *>(static_cast<char *>(*mem) + b_table + b_snap);
-    int32_t *n_list = reinterpret_cast<int32_t *>(static_cast<char *>(*mem) + b_table + b_snap + b_list);
-    VV_CUDA(cudaMemsetAsync(n_list, 0, sizeof(int32_t), st));
-    int rc = launch_vis_snapshot(vt.d0, vt.d1, snap, t->vis_words, st);
+    int32_t *table = reinterpret_cast<int32_t *>(base);
+    uint32_t *snap = reinterpret_cast<uint32_t *>(base + b_table);
+    int32_t *list = reinterpret_cast<int32_t *>(base + b_table + b_snap);
+    int32_t *n_list = reinterpret_cast<int32_t *>(base + b_table + b_snap + b_list);
+    int32_t *flags = n_list + 1;  // [changed, blocks done]
+    if (fresh)  // the upper rows, once; every snapshot word then counts as changed
+        VV_CUDA(cudaMemcpyAsync(table, t->d_child, (size_t)t->n_internal * 8 * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, st));
+    int rc;
+    if (plan) {
+        VV_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
+        rc = launch_vis_snapshot_diff(vt.d0, vt.d1, snap, t->vis_words, fresh, flags, n_list, st);
+    } else {
+        VV_CUDA(cudaMemsetAsync(n_list, 0, sizeof(int32_t), st));
+        rc = launch_vis_snapshot(vt.d0, vt.d1, snap, t->vis_words, st);
+    }
     if (rc) return rc;
-    VV_CUDA(cudaMemcpyAsync(table, t->d_child, (size_t)t->n_internal * 8 * sizeof(int32_t), cudaMemcpyDeviceToDevice,
-                            st));
     VisTableParams q;
     q.child = t->d_child;
     q.last = t->d_last;
@@ -425,6 +474,7 @@ static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **
     q.out = table;
     q.list = list;
     q.n_list = n_list;
+    q.changed = plan ? flags : nullptr;
     if ((rc = launch_vis_table(q, st))) return rc;
     vt.d0 = vt.d1 = snap;
     vt.table = table;
@@ -712,7 +762,7 @@ void affine_from_inverse(const double *inv, double *A) {
 // Transient per-call slice from the stream-ordered pool (freed, stream
 // ordered, when the call returns).
 int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr, bool vis = false,
-                    uint64_t view = 0) {
+                    uint64_t view = 0, vv_camera_plan *plan = nullptr) {
     NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
@@ -730,7 +780,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     int rc;
     VisTicket vt;
     if (vis_wanted(t) && (rc = vis_begin(t, st, vt, view, vis))) return rc;
-    if ((rc = vis_prepare(t, vt, st, &tr.vis_mem))) return rc;
+    if ((rc = vis_prepare(t, vt, st, &tr.vis_mem, plan))) return rc;
     tr.vis_table = vt.table;
     sv.mark = vt.mark;
     sv.census = vt.census;
@@ -1360,6 +1410,11 @@ int vv_tree_dark_fraction(const vv_tree *t, float *dark_frac) {
     return VV_OK;
 }
 
+int vv_profile_split_event(void *event) {
+    split_event = static_cast<cudaEvent_t>(event);
+    return VV_OK;
+}
+
 int vv_tree_visible_count(const vv_tree *t, int64_t *n_visible, int64_t *n_chunks, void *stream) {
     if (!t || !n_visible) return set_error(VV_E_INVALID, "null argument");
     *n_visible = 0;
@@ -1440,8 +1495,23 @@ int vv_slice_build_multi(const vv_tree *t, int32_t n_frames, const int32_t *fram
     return vv_slice_build_frames(t, n_frames, frames, 0, stream, out);
 }
 
+static int slice_build_frames_impl(const vv_tree *t, int32_t n_frames, const int32_t *frames, int32_t flags,
+                                   vv_camera_plan *plan, void *stream, vv_slice **out);
+
 int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *frames, int32_t flags, void *stream,
                           vv_slice **out) {
+    return slice_build_frames_impl(t, n_frames, frames, flags, nullptr, stream, out);
+}
+
+int vv_slice_build_visible(const vv_tree *t, int32_t frame, vv_camera_plan *plan, void *stream, vv_slice **out) {
+    if (!plan) return set_error(VV_E_INVALID, "null camera plan");
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (plan->device != t->device) return set_error(VV_E_INVALID, "camera plan belongs to another device");
+    return slice_build_frames_impl(t, 1, &frame, VV_SLICE_RENDER_ONLY | VV_SLICE_VISIBLE, plan, stream, out);
+}
+
+static int slice_build_frames_impl(const vv_tree *t, int32_t n_frames, const int32_t *frames, int32_t flags,
+                                   vv_camera_plan *plan, void *stream, vv_slice **out) {
     NvtxRange nv("vv:slice_build_frames");
     if (!t || !frames || !out) return set_error(VV_E_INVALID, "null argument");
     if (flags & ~(VV_SLICE_RENDER_ONLY | VV_SLICE_VISIBLE))
@@ -1499,7 +1569,7 @@ int vv_slice_build_frames(const vv_tree *t, int32_t n_frames, const int32_t *fra
         out[0]->visible = vt.mark != nullptr;
         out[0]->vis_mark = vt.mark;
         out[0]->vis_census = vt.census;
-        if ((vrc = vis_prepare(t, vt, (cudaStream_t)stream, &out[0]->d_vis_mem))) return fail(vrc);
+        if ((vrc = vis_prepare(t, vt, (cudaStream_t)stream, &out[0]->d_vis_mem, plan))) return fail(vrc);
         out[0]->vis_table = vt.table;
 
     }
@@ -1763,7 +1833,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     if (!cache && mode != 0) {
         const bool vis = p.deferred != nullptr;
         int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr, vis)
-                     : build_transient(t, frame, st, p.S, tr, vis, view_hash(*cam));
+                     : build_transient(t, frame, st, p.S, tr, vis, view_hash(*cam), plan);
         if (r) return r;
     }
     // sample counts report the reference's full walk: the tree's own table
@@ -1778,6 +1848,10 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
         p.T.n_leaves = t->n_leaves + 1;  // the stand-in row is a valid record row
     }
     const bool vis = p.S.mark != nullptr;
+    if (split_event) {
+        cudaEventRecord(split_event, st);
+        split_event = nullptr;
+    }
     rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm), vis);
     if (!rc && vis) rc = launch_camera_rewalk(t->n_max, wide, p, st);
     if (rc || !plan) return rc;
@@ -1940,6 +2014,7 @@ int vv_camera_plan_free(vv_camera_plan *plan) {
     cudaDeviceSynchronize();  // a render may still read the order
     cudaFree(plan->order);
     cudaFree(plan->cov_mem);
+    cudaFree(plan->vis_mem);
     delete plan;
     return VV_OK;
 }

@@ -1427,12 +1427,17 @@ struct VisTableParams {
     int32_t stand_in;
     int32_t *out;
     int32_t *list;     // out: the set's leaf rows (the slice pass's work list), in last-level node order
-    int32_t *n_list;   // zeroed before the launch
+    int32_t *n_list;   // zeroed before the launch (when the snapshot changed)
+    const int32_t *changed;  // nonzero: the snapshot changed (else the table and list stand)
 };
 int launch_vis_table(const VisTableParams &p, cudaStream_t st);
 // out[i] = a[i] | b[i]: the slice's snapshot of the visible set (the table
 // and the slice pass both read it, so they agree whatever walks mark meanwhile)
 int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st);
+// the same into a kept snapshot: flags[0] = 1 if any word changed (or
+// force); the last block then zeroes *n_list for the table pass to refill
+int launch_vis_snapshot_diff(const uint32_t *a, const uint32_t *b, uint32_t *snap, int64_t n, bool force,
+                             int32_t *flags, int32_t *n_list, cudaStream_t st);
 // bits[list[i] / 32] |= 1 << (list[i] % 32) for i < *n (bits zeroed first)
 int launch_chunk_bits(const int32_t *list, const int32_t *n, uint32_t *bits, int64_t max_n, cudaStream_t st);
 // leaf rows per box of the chunk culling (= the single-frame slice chunk)

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) k_mask_last(const __grid_constant__ MaskP
 }
 
 __global__ void __launch_bounds__(256) k_vis_table(const __grid_constant__ VisTableParams p) {
+    if (p.changed && !*(volatile const int32_t *)p.changed) return;  // the kept table and list stand
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32: warps stay whole
     const int lane = threadIdx.x & 31;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < p.n_last; b0 += stride) {
@@ -99,6 +100,32 @@ __global__ void __launch_bounds__(256) k_vis_table(const __grid_constant__ VisTa
 __global__ void __launch_bounds__(256) k_vis_or(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = __ldcg(a + i) | __ldcg(b + i);
+}
+
+__global__ void __launch_bounds__(256) k_vis_or_diff(const uint32_t *a, const uint32_t *b, uint32_t *snap, int64_t n,
+                                                     int force, int32_t *flags, int32_t *n_list) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool diff = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t v = __ldcg(a + i) | __ldcg(b + i);
+        if (force || v != snap[i]) {
+            snap[i] = v;
+            diff = true;
+        }
+    }
+    if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flags, 1);
+    // the last block out: a changed set refills the list from zero
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(flags + 1, 1) == (int)gridDim.x - 1 && *(volatile int32_t *)flags) *n_list = 0;
+    }
+}
+
+int launch_vis_snapshot_diff(const uint32_t *a, const uint32_t *b, uint32_t *snap, int64_t n, bool force,
+                             int32_t *flags, int32_t *n_list, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4));
+    k_vis_or_diff<<<grid, 256, 0, st>>>(a, b, snap, n, force ? 1 : 0, flags, n_list);
+    return check_launch("vis_snapshot_diff");
 }
 
 int launch_vis_snapshot(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st) {

@@ -352,7 +352,8 @@ def build_frame_cache(tree, frame: int, device=None) -> FrameSlice:
     return FrameSlice(frame, handle, rep, dev)
 
 
-def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, visible: bool = False) -> list:
+def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, visible: bool = False,
+                       plan=None) -> list:
     """Slices of 1..4 frames from ONE pass over the payload (vv_slice_build_multi):
     each leaf row is read once and sliced per frame; ``[build_frame_cache(tree, f) for f in frames]``
     with a quarter to a half of the HBM traffic.  ``render_only``: the
@@ -362,7 +363,10 @@ def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, 
     the tree's visible set -- the leaves its camera renders have shaded
     lately; the walk decodes any other lit leaf it meets from the payload
     (VV_SLICE_VISIBLE; what render() slices internally).  Single-frame
-    renders only: ``render_frames_into`` rejects such a slice."""
+    renders only: ``render_frames_into`` rejects such a slice.  ``plan``
+    (with ``visible``): a CameraPlan keeping the slice's walk table across
+    frames (rebuilt only when the set changes); render each such slice
+    before building the plan's next one."""
     frames = [_frame_index(f, tree) for f in frames]
     for f in frames:
         _check_frame(tree, f)
@@ -376,6 +380,10 @@ def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, 
     rep = replica(tree, dev)
     n = len(frames)
     handles = (ctypes.c_void_p * n)()
+    if visible and plan is not None:
+        _native.check(_native.lib().vv_slice_build_visible(rep.handle, frames[0], plan._handle, stream_ptr(dev),
+                                                           handles))
+        return [FrameSlice(frames[0], ctypes.c_void_p(handles[0]), rep, dev)]
     _native.check(_native.lib().vv_slice_build_frames(rep.handle, n, (ctypes.c_int32 * n)(*frames), flags,
                                                       stream_ptr(dev), handles))
     return [FrameSlice(f, ctypes.c_void_p(h), rep, dev) for f, h in zip(frames, handles)]

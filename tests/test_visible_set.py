@@ -67,9 +67,10 @@ def test_shared_visible_cache_stereo_and_rays(cuda, tree):
     import torch
 
     eyes = [_orbit(3), _orbit(4)]
+    plan = vv.CameraPlan(cuda)  # every other frame: the walk table kept in a plan
     for i in range(12):
         f = i % 9
-        fs = vv.build_frame_caches(tree, [f], visible=True)[0]
+        fs = vv.build_frame_caches(tree, [f], visible=True, plan=plan if i % 2 else None)[0]
         for e, cam in enumerate(eyes):
             h, w = cam.height, cam.width
             out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda),
