@@ -421,13 +421,13 @@ static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **
     bool fresh = true;
     if (plan) {
         if (!plan->vis_mem || plan->vis_cap < total || plan->vis_tree != t->serial) {
+            // stream-ordered: frames already queued on this stream keep reading the old table
             if (plan->vis_mem) {
-                cudaStreamSynchronize(st);  // an earlier frame on this stream may still read it
-                cudaFree(plan->vis_mem);
+                cudaFreeAsync(plan->vis_mem, st);
                 plan->vis_mem = nullptr;
                 plan->vis_cap = 0;
             }
-            if (cudaMalloc(&plan->vis_mem, total) != cudaSuccess) {
+            if (cudaMallocAsync(&plan->vis_mem, total, st) != cudaSuccess) {
                 cudaGetLastError();
                 plan->vis_mem = nullptr;
                 return set_error(VV_E_NOMEM, "visible-set walk table (%zu bytes) failed", total);

@@ -155,6 +155,25 @@ def test_set_follows_the_view(cuda):
     _eq(got.rgb, vv.render(t, cam, 2, PS).rgb, "held camera, set in use")
 
 
+def test_plan_walk_table_alternating_trees(cuda):
+    """One camera plan, two trees rendered alternately: the plan's kept walk
+    table follows the tree (rebuilt on every switch), images stay exact."""
+    import torch
+
+    rng = np.random.default_rng(14)
+    trees = [random_payload_tree(rng, depth=4, fill=0.5, frames=6, sigma_scale=5.0) for _ in range(2)]
+    cam = _orbit(9)
+    plan = vv.CameraPlan(cuda)
+    h, w = cam.height, cam.width
+    out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda)]
+    for i in range(12):
+        t = trees[(i // 3) % 2]
+        vv.render_into(t, cam, i % 6, *out, plan=plan)
+        ref = vv.render(t, cam, i % 6, PS, out="torch")
+        torch.cuda.synchronize()
+        _eq(out[0], ref.rgb, f"alternating trees rgb {i}")
+
+
 def test_edited_tree_ignores_visible_set(cuda):
     import torch
 
