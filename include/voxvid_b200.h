@@ -175,12 +175,13 @@ int vv_slice_build_multi(const vv_tree *tree, int32_t n_frames, const int32_t *f
  * can give a dark leaf density).  render()'s transient slices and the
  * playback groups are built this way. */
 #define VV_SLICE_RENDER_ONLY 1
-/* VV_SLICE_VISIBLE (with VV_SLICE_RENDER_ONLY, one frame): colour only for
+/* VV_SLICE_VISIBLE (with VV_SLICE_RENDER_ONLY, one frame): records only for
  * the leaves in the tree's visible set (the leaves its camera walks have
- * shaded lately); a lit leaf outside it holds -sigma and the walk decodes
- * its colour from the payload (bitwise the same) and adds it to the set.
- * Images are bitwise unchanged.  Not exportable; single-frame walks only
- * (VV_E_INVALID from vv_render_camera_multi). */
+ * visited lately) and a walk table in which every other leaf points at a
+ * stand-in row; a camera walk that meets one re-walks that pixel per sample
+ * (bitwise the same) and adds what it visits to the set.  Images are
+ * bitwise unchanged.  Not exportable; camera renders only (VV_E_INVALID
+ * from vv_render_rays and vv_render_camera_multi). */
 #define VV_SLICE_VISIBLE 2
 int vv_slice_build_frames(const vv_tree *tree, int32_t n_frames, const int32_t *frames, int32_t flags,
                           void *stream, vv_slice **out);

@@ -259,16 +259,19 @@ SliceView slice_view(const vv_slice *c) {
 }
 
 // ---- visible set (render-internal camera slices of trees without edits)
-// A render's walks can only reach a fraction of the leaves (cfg2: 19%, in
-// 52% of the 64-leaf chunks); the slice decodes colour -- 90% of its HBM
-// bytes -- for the leaves in the tree's visible set only, and writes -sigma
-// for a lit leaf outside it, whose colour the walk then decodes from the
-// payload (bitwise the same) and marks.  Two bitmaps: the slice decodes
-// their union; walks mark into the current one.  Every kVisEpoch slices the
-// older one is cleared and becomes current, and that slice's walks mark
-// every leaf they shade (a census), so the set follows the view and leaves
-// drop out within two epochs of last being seen.  The first slice decodes
-// every lit leaf, with a census.  VV_VISIBLE=0 turns the set off (A/B).
+// A render's walks only reach a fraction of the leaves (cfg2: 19%, in 31% of
+// the 64-leaf chunks), yet a slice decodes every lit leaf.  With a set in
+// use, the slice decodes only the leaves in the tree's visible set and the
+// camera kernel walks a walk table (vis_prepare) in which every other leaf
+// points at a stand-in row whose record holds sigma -1: a walk that meets one
+// defers its pixel to k_camera_rewalk, which walks it per sample on the
+// tree's own table (bitwise the same) and marks what it visits.  Two
+// bitmaps: the slice decodes a snapshot of their union; walks mark into the
+// current one.  Every kVisEpoch slices the older one is cleared and becomes
+// current, and that slice's walks mark every leaf they visit (a census), so
+// the set follows the view and leaves drop out within two epochs of last
+// being seen.  The set is built per camera (vis_begin's view rule).
+// VV_VISIBLE=0 turns the set off (A/B).
 constexpr int kVisEpoch = 16;  // cfg2: 2,651 vs 2,637 Mrays/s with 8, 2,648 with 32 (VV_VIS_EPOCH overrides)
 
 struct VisTicket {

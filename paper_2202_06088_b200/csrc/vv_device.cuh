@@ -115,12 +115,12 @@ __device__ __forceinline__ uint32_t nz_chunks(const float *row, int C) {
 struct SliceView {
     const float4 *rec;  // (n_leaves, rec4) or null (decode per sample)
     int rec4;           // float4 per record = ceil((3S + 2) / 4)
-    // visible-set slices (render-internal camera slices of trees without
-    // edits; VIS kernels): colour only for the leaves of the tree's visible
-    // set; a lit leaf outside it holds -sigma (sigma itself is never
-    // negative).  A walk that meets one stops, and the pixel is walked again
-    // per sample (k_camera_rewalk), marking the leaves it visits in `mark`.
-    // With `census` set the sliced walk marks every leaf it visits.
+    // visible-set slices (VIS kernels): records only for the tree's visible
+    // set, walked through a table whose other leaves point at a stand-in
+    // record with sigma -1 (vv_api.cu, vis_prepare).  A walk that meets a
+    // negative sigma stops and the pixel is walked again per sample
+    // (k_camera_rewalk), marking the leaves it visits in `mark`; a census
+    // walk (VIS 3) marks every leaf it visits.
     int census;
     uint32_t *mark;
     __device__ __forceinline__ const float4 *row(uint32_t L) const { return rec + (size_t)L * rec4; }
