@@ -283,10 +283,13 @@ def slice_pass_bytes(tree, f, device, chunk=64, table_per_frame=False):
         if table_per_frame:
             b += 64 * tree.n_internal + 64 * _n_last_level(tree)
     elif masks and os.environ.get("VV_LIT_PASS", "1") != "0":
-        # dark-heavy trees: the thread-per-leaf pass (k_slice_visible, lit
-        # mode): colour of every lit leaf, the sigma pair of every dark one
+        # dark-heavy trees, two phases: k_slice_lit (every leaf's sigma and
+        # lit byte, the lit leaves listed: 4 B each), then k_slice_leaves
+        # over the list (each lit leaf's w_gamma chunks, w_hh and record);
+        # the dark leaves' records are not written (the node mask cuts them
+        # from every image walk)
         nl = int(lit.sum())
-        b = n * 16 * nza + nl * (16 * nzb + 12 * k + 8 + 12 * s_sh) + (n - nl) * 32
+        b = n * 16 * nza + 4 * nl + nl * (16 * nzb + 12 * k + 8 + 12 * s_sh)
     else:
         nb, nd = int(rows[bright].sum()), int(rows[~bright].sum())
         b = n * 16 * nza + nb * (16 * nzb + 12 * k + 8 + 12 * s_sh) + nd * 32
@@ -870,8 +873,8 @@ def run_ours(args, rank, world, local_rank):
             lit_pass = (not vis_on and replica(wl.tree, dev).dark_fraction >= 0.25
                         and os.environ.get("VV_LIT_PASS", "1") != "0")
             roofline["slice_pass"] = {
-                "kernel": "k_slice_visible" + (" (lit leaves)" if lit_pass else "") if vis_on or lit_pass
-                else "k_build_slice",
+                "kernel": ("k_slice_leaves (visible set)" if vis_on else
+                           "k_slice_lit + k_slice_leaves (lit leaves)" if lit_pass else "k_build_slice"),
                 "visible_set": ({"leaves": replica(wl.tree, dev).visible_count()[0],
                                  "chunks": replica(wl.tree, dev).visible_count()[1],
                                  "n_leaves": int(wl.tree.n_leaves)} if vis_on else False),
@@ -880,8 +883,9 @@ def run_ours(args, rank, world, local_rank):
                 "frac": round(sbytes / (slice_ms / 1e3) / 1e9 / peak, 4),
                 "bytes_per_launch": float(np.mean([ab[f]["slice_bytes"] for f in step_frames])),
                 "bytes_formula": ("per leaf 16 B per w_sigma float4 chunk the frame's A row does not zero out; "
-                                  "per lit leaf + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh "
-                                  "(record); per dark leaf + 32 B (sigma pair)" if lit_pass else
+                                  "per lit leaf + 4 B (list) + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + "
+                                  "12 S_sh (record); dark leaves' records unwritten (cut by the node mask)"
+                                  if lit_pass else
                                   "visible set: per leaf of the set 4 B (work list) + 16 B per nonzero w_sigma "
                                   "chunk + 16 B per nonzero w_gamma chunk + 12 K (w_hh) + 8 + 12 S_sh (record); + 3 "
                                   "bits per leaf (the set and its kept snapshot; the walk table is rebuilt only when "

@@ -390,8 +390,22 @@ static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *v
         // at cfg2).  VV_LIT_PASS=0 / 1 forces it off / on.
         const char *e = getenv("VV_LIT_PASS");
         const bool lit_pass = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : t->dark_frac >= 0.25f;
-        if (p.n_frames == 1 && p.skip_dark && lit_pass) return launch_slice_visible(t->n_max, p, st);
-        return launch_slice(t->n_max, p, st);
+        if (!(p.n_frames == 1 && p.skip_dark && lit_pass)) return launch_slice(t->n_max, p, st);
+        if (p.chunk_list) return launch_slice_visible(t->n_max, p, st);  // a region: its chunks, one pass
+        // the whole tree: sigma for every leaf and the lit list, then the lit leaves' records
+        void *m = nullptr;
+        if (cudaMallocAsync(&m, (size_t)t->n_leaves * sizeof(int32_t) + 256, st) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(VV_E_NOMEM, "lit-leaf list allocation failed");
+        }
+        p.lit_list = static_cast<int32_t *>(m);
+        p.lit_n = reinterpret_cast<int32_t *>(static_cast<char *>(m) + (((size_t)t->n_leaves * 4 + 255) & ~(size_t)255));
+        int rc = VV_OK;
+        if (cudaMemsetAsync(p.lit_n, 0, sizeof(int32_t), st) != cudaSuccess)
+            rc = set_error(VV_E_CUDA, "lit-list counter memset failed");
+        if (!rc) rc = launch_slice_visible(t->n_max, p, st);
+        cudaFreeAsync(m, st);
+        return rc;
     }
     p.vis0 = vt->d0;  // null: every leaf visible (a tree's first slice)
     p.vis1 = vt->d1;
@@ -487,7 +501,7 @@ static int vis_prepare(const vv_tree *t, VisTicket &vt, cudaStream_t st, void **
 }
 
 int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaStream_t st, bool render_only,
-                       uint8_t *lit = nullptr, const VisTicket *vt = nullptr) {
+                       uint8_t *lit = nullptr, const VisTicket *vt = nullptr, bool dark_unread = false) {
     if (t->n_leaves == 0) return VV_OK;
     SliceParams p;
     memset(&p, 0, sizeof(p));
@@ -500,6 +514,7 @@ int launch_build_slice(const vv_tree *t, int frame, float4 *rec, int rec4, cudaS
     p.rec4 = rec4;
     p.skip_dark = render_only && !t->has_edits;
     p.lit = lit;
+    p.dark_unread = dark_unread && lit != nullptr;  // the node mask (built from lit) cuts the dark leaves
     set_slice_masks(t, p);
     return launch_slice_vis(t, p, vt, st);
 }
@@ -764,8 +779,10 @@ void affine_from_inverse(const double *inv, double *A) {
 
 // Transient per-call slice from the stream-ordered pool (freed, stream
 // ordered, when the call returns).
+// dark_unread: every walk of this slice uses its node mask (image renders,
+// no sample counts), so the dark leaves' records need not be written
 int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv, Transient &tr, bool vis = false,
-                    uint64_t view = 0, vv_camera_plan *plan = nullptr) {
+                    uint64_t view = 0, vv_camera_plan *plan = nullptr, bool dark_unread = false) {
     NvtxRange nv("vv:slice(transient)");
     pool_setup(t->device);
     const int rec4 = slice_rec4(t->S);
@@ -789,7 +806,7 @@ int build_transient(const vv_tree *t, int frame, cudaStream_t st, SliceView &sv,
     sv.census = vt.census;
     if (mask_wanted(t) && (rc = alloc_mask(t, st, tr.nmask))) return rc;
     rc = launch_build_slice(t, frame, reinterpret_cast<float4 *>(tr.mem), rec4, st, true,
-                            tr.nmask ? tr.nmask->lit : nullptr, &vt);
+                            tr.nmask ? tr.nmask->lit : nullptr, &vt, dark_unread);
     if (rc || !tr.nmask) return rc;
     return build_mask(t, *tr.nmask, st);
 }
@@ -1836,7 +1853,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     if (!cache && mode != 0) {
         const bool vis = p.deferred != nullptr;
         int r = rect ? build_transient_region(t, frame, st, *cam, p.rx0, p.ry0, p.rx1, p.ry1, p.S, tr, vis)
-                     : build_transient(t, frame, st, p.S, tr, vis, view_hash(*cam), plan);
+                     : build_transient(t, frame, st, p.S, tr, vis, view_hash(*cam), plan, used == nullptr);
         if (r) return r;
     }
     // sample counts report the reference's full walk: the tree's own table

@@ -751,6 +751,13 @@ struct SliceParams {
     // with a walk table (k_slice_leaves): the set's leaf rows, listed by k_vis_table
     const int32_t *leaf_list;
     const int32_t *n_leaf_list;
+    // two-phase lit pass (dark-heavy trees, whole tree): k_slice_lit lists the
+    // lit leaves here (lit_n zeroed) for k_slice_leaves; dark_unread: the
+    // walks use this slice's node mask, which cuts every dark leaf, so the
+    // dark leaves' records are not written
+    int32_t *lit_list;
+    int32_t *lit_n;
+    int dark_unread;
     // a region render: bit c set iff 64-leaf chunk c is in the region's
     // chunk list (k_slice_leaves skips the set's other leaves: the region's
     // rays cannot reach them)
@@ -1151,6 +1158,42 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)  //
     }
 }
 
+// Lit pass, phase 1 (dark-heavy trees): a thread per leaf computes sigma
+// (f64, as k_build_slice), writes the node mask's lit byte, lists a lit leaf
+// for phase 2 (k_slice_leaves over the list: its whole record) and gives a
+// dark leaf its sigma pair (0) unless the walks cannot read it.  Light and
+// bandwidth-bound; the colour work, a tenth of the leaves at cfg3, then runs
+// with every lane busy.
+template <int NMAX>  // (unused: one instantiation per n_max like the other slice kernels)
+__global__ void __launch_bounds__(256) k_slice_lit(const __grid_constant__ SliceParams p) {
+    __shared__ float sA[kMaxC], sB[kMaxC];
+    load_rows(p.T, p.frame[0], sA, sB);
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // records / lit bytes / the list counter: earlier work's
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < p.n_leaves; b0 += stride) {
+        const int64_t L = b0 + lane;
+        double sp = 0.0;
+        if (L < p.n_leaves) sp = sigma_pre_batched<2>(p.T.sig + L, p.T.lstride, sA, p.T.C, p.mS);
+        const bool lit = L < p.n_leaves && sp > 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, lit);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(p.lit_n, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (L >= p.n_leaves) continue;
+        if (p.lit) p.lit[L] = lit ? 1u : 0u;
+        if (lit) {
+            p.lit_list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)L;
+        } else if (!p.dark_unread) {  // sigma 0 (two float4: the record's last sector)
+            float4 *o = p.rec[0] + (L + 1) * p.rec4 - 2;
+            o[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
 // Visible-set slice with a walk table: a thread per leaf of the set (the
 // list k_vis_table wrote), its whole record decoded exactly as in
 // k_slice_visible; plus the walk table's stand-in row (sigma -1).  Every
@@ -1168,7 +1211,7 @@ __global__ void __launch_bounds__(VV_VIS_BLOCK, NMAX >= 3 ? 4 : VV_VIS_MINB)
     const int64_t n = (int64_t)*(volatile const int32_t *)p.n_leaf_list;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t0 == 0) {
+    if (t0 == 0 && !p.lit_list) {  // the walk table's stand-in row (not in the lit pass)
         const unsigned long long sb = (unsigned long long)__double_as_longlong(-1.0);
         float4 *o = p.rec[0] + (p.n_leaves + 1) * p.rec4 - 1;
         *o = make_float4(0.f, 0.f, __uint_as_float((unsigned)(sb & 0xffffffffu)), __uint_as_float((unsigned)(sb >> 32)));

@@ -131,6 +131,17 @@ int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t chunks = (p.n_leaves + 63) / 64;
+        if (p.lit_list) {  // two-phase lit pass: sigma for every leaf, then the lit leaves' records
+            const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.n_leaves + 255) / 256, sms * 16));
+            launch_pdl(k_slice_lit<NM>, dim3(g1), dim3(256), 0, st, p);
+            int r = check_launch("slice_lit");
+            if (r) return r;
+            SliceParams q = p;
+            q.leaf_list = p.lit_list;
+            q.n_leaf_list = p.lit_n;
+            launch_pdl(k_slice_leaves<NM>, dim3((unsigned)(sms * 16)), dim3(VV_VIS_BLOCK), 0, st, q);
+            return check_launch("slice_leaves(lit)");
+        }
         if (p.leaf_list) {  // a thread per leaf of the set
             launch_pdl(k_slice_leaves<NM>, dim3((unsigned)(sms * 16)), dim3(VV_VIS_BLOCK), 0, st, p);
             return check_launch("slice_leaves");
