@@ -193,11 +193,12 @@ class FrameSlice:
     (n_leaves, 3S) float32 are exported lazily as CUDA tensors.
     """
 
-    def __init__(self, frame: int, handle, rep, device):
+    def __init__(self, frame: int, handle, rep, device, plan=None):
         self.frame = int(frame)
         self._handle = handle
         self._rep = rep
         self._device = device
+        self._plan = plan  # a plan-backed visible slice reads the plan's walk table: keep the plan alive
         self._sigma = None
         self._q = None
 
@@ -383,7 +384,7 @@ def build_frame_caches(tree, frames, device=None, *, render_only: bool = False, 
     if visible and plan is not None:
         _native.check(_native.lib().vv_slice_build_visible(rep.handle, frames[0], plan._handle, stream_ptr(dev),
                                                            handles))
-        return [FrameSlice(frames[0], ctypes.c_void_p(handles[0]), rep, dev)]
+        return [FrameSlice(frames[0], ctypes.c_void_p(handles[0]), rep, dev, plan)]
     _native.check(_native.lib().vv_slice_build_frames(rep.handle, n, (ctypes.c_int32 * n)(*frames), flags,
                                                       stream_ptr(dev), handles))
     return [FrameSlice(f, ctypes.c_void_p(h), rep, dev) for f, h in zip(frames, handles)]
