@@ -391,8 +391,7 @@ static int launch_slice_vis(const vv_tree *t, SliceParams &p, const VisTicket *v
         const char *e = getenv("VV_LIT_PASS");
         const bool lit_pass = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : t->dark_frac >= 0.25f;
         if (!(p.n_frames == 1 && p.skip_dark && lit_pass)) return launch_slice(t->n_max, p, st);
-        if (p.chunk_list) return launch_slice_visible(t->n_max, p, st);  // a region: its chunks, one pass
-        // the whole tree: sigma for every leaf and the lit list, then the lit leaves' records
+        // sigma for every leaf (of a region: of its chunks) and the lit list, then the lit leaves' records
         void *m = nullptr;
         if (cudaMallocAsync(&m, (size_t)t->n_leaves * sizeof(int32_t) + 256, st) != cudaSuccess) {
             cudaGetLastError();

@@ -1170,19 +1170,25 @@ __global__ void __launch_bounds__(256) k_slice_lit(const __grid_constant__ Slice
     load_rows(p.T, p.frame[0], sA, sB);
     __syncthreads();
     pdl_trigger();
-    pdl_wait();  // records / lit bytes / the list counter: earlier work's
+    pdl_wait();  // records / lit bytes / the list counter / a region's chunk list: earlier work's
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < p.n_leaves; b0 += stride) {
-        const int64_t L = b0 + lane;
+    // a region: the leaves of its listed 64-leaf chunks
+    const bool listed = p.chunk_list != nullptr;
+    const int64_t n_items = listed ? 64 * (int64_t)*(volatile const int32_t *)p.n_list : p.n_leaves;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < n_items; b0 += stride) {
+        const int64_t it = b0 + lane;
+        int64_t L = it;
+        if (listed && it < n_items) L = 64 * (int64_t)__ldg(p.chunk_list + (it >> 6)) + (it & 63);
+        const bool in = it < n_items && L < p.n_leaves;
         double sp = 0.0;
-        if (L < p.n_leaves) sp = sigma_pre_batched<2>(p.T.sig + L, p.T.lstride, sA, p.T.C, p.mS);
-        const bool lit = L < p.n_leaves && sp > 0.0;
+        if (in) sp = sigma_pre_batched<2>(p.T.sig + L, p.T.lstride, sA, p.T.C, p.mS);
+        const bool lit = in && sp > 0.0;
         const unsigned m = __ballot_sync(0xffffffffu, lit);
         int base = 0;
         if (lane == 0 && m) base = atomicAdd(p.lit_n, __popc(m));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (L >= p.n_leaves) continue;
+        if (!in) continue;
         if (p.lit) p.lit[L] = lit ? 1u : 0u;
         if (lit) {
             p.lit_list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)L;

@@ -133,6 +133,7 @@ int launch_slice_visible(int nmax, const SliceParams &p, cudaStream_t st) {
         const int64_t chunks = (p.n_leaves + 63) / 64;
         if (p.lit_list) {  // two-phase lit pass: sigma for every leaf, then the lit leaves' records
             const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.n_leaves + 255) / 256, sms * 16));
+            // (a region's n_list lives on the device: the grid covers the whole tree's leaves)
             launch_pdl(k_slice_lit<NM>, dim3(g1), dim3(256), 0, st, p);
             int r = check_launch("slice_lit");
             if (r) return r;
