@@ -137,11 +137,13 @@ int vv_tree_info(const vv_tree *tree, int64_t *n_leaves, int64_t *n_internal, in
  * T-1.  Above 0.5 the sliced camera and playback kernels walk with the long
  * segment queue (a kernel choice only: images are bitwise the same). */
 int vv_tree_dark_fraction(const vv_tree *tree, float *dark_frac);
-/* Benchmarking: the calling thread's next camera render records `event`
+/* (No reference counterpart: instrumentation.)  Benchmarking: the calling
+ * thread's next camera render records `event`
  * (a cudaEvent_t) on its stream between its slice pass and its camera
  * kernel, so the two can be timed apart on the render()/render_into path. */
 int vv_profile_split_event(void *event);
-/* Size of the tree's visible set (VV_SLICE_VISIBLE): leaves in it and
+/* (No reference counterpart: the visible set is this renderer's.)  Size of
+ * the tree's visible set (VV_SLICE_VISIBLE): leaves in it and
  * 64-leaf slice chunks holding one (synchronises `stream`). */
 int vv_tree_visible_count(const vv_tree *tree, int64_t *n_visible, int64_t *n_chunks, void *stream);
 /* The visible set itself: bit L of out (n_words >= 2 per 64 leaves) set
@@ -185,7 +187,8 @@ int vv_slice_build_multi(const vv_tree *tree, int32_t n_frames, const int32_t *f
 #define VV_SLICE_VISIBLE 2
 int vv_slice_build_frames(const vv_tree *tree, int32_t n_frames, const int32_t *frames, int32_t flags,
                           void *stream, vv_slice **out);
-/* A VV_SLICE_VISIBLE slice of one frame whose walk table lives in `plan`
+/* build_frame_cache (render.py:170-179) for camera renders only: a
+ * VV_SLICE_VISIBLE slice of one frame whose walk table lives in `plan`
  * (kept across frames, rebuilt only when the set changes; the slice must
  * be used before the plan builds its next one).  Several cameras of one
  * frame (stereo) may share it. */
