@@ -188,3 +188,27 @@ def test_edited_tree_ignores_visible_set(cuda):
         got = vv.render(t, cam, i % 5)
         ref = vv.render(t, cam, i % 5, PS)
         _eq(got.rgb, ref.rgb, f"edited {i}")
+
+
+def test_split_event_records_between_slice_and_kernel(cuda, tree):
+    """vv_profile_split_event: the next camera render records the event after
+    its slice pass -- the benchmark's split of slice and camera kernel."""
+    import ctypes
+
+    import torch
+
+    from paper_2202_06088_b200 import _native
+
+    cam = _orbit(6)
+    h, w = cam.height, cam.width
+    out = [torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda)]
+    plan = vv.CameraPlan(cuda)
+    s, m, e = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    stream = torch.cuda.current_stream(cuda)
+    s.record(stream)
+    m.record(stream)  # create the event; the library re-records it at the split
+    _native.check(_native.lib().vv_profile_split_event(ctypes.c_void_p(m.cuda_event)))
+    vv.render_into(tree, cam, 0, *out, plan=plan)
+    e.record(stream)
+    torch.cuda.synchronize()
+    assert 0.0 < s.elapsed_time(m) and 0.0 < m.elapsed_time(e)
