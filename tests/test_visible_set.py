@@ -212,3 +212,34 @@ def test_split_event_records_between_slice_and_kernel(cuda, tree):
     e.record(stream)
     torch.cuda.synchronize()
     assert 0.0 < s.elapsed_time(m) and 0.0 < m.elapsed_time(e)
+
+
+def test_two_streams_share_a_tree(cuda, tree):
+    """Two streams render the same tree and the same held camera concurrently
+    (different frames), each with its own plan: both use the tree's shared
+    visible set, marking its bitmaps and rotating its epochs concurrently,
+    while each keeps its own walk table -- every image bitwise the
+    per-sample one.  (Different cameras would alternate the tree's view and
+    get plain slices.)"""
+    import torch
+
+    cams = [_orbit(10), _orbit(10)]
+    streams = [torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)]
+    plans = [vv.CameraPlan(cuda), vv.CameraPlan(cuda)]
+    h, w = cams[0].height, cams[0].width
+    outs = [[(torch.empty((h, w, 3), device=cuda), torch.empty((h, w), device=cuda), torch.empty((h, w), device=cuda))
+             for _ in range(40)] for _ in range(2)]
+    for i in range(40):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                vv.render_into(tree, cams[k], (i + 3 * k) % 9, *outs[k][i], plan=plans[k])
+    torch.cuda.synchronize()
+    from paper_2202_06088_b200.device import replica
+
+    assert replica(tree, cuda).visible_count()[0] > 0  # the set was in use
+    for i in range(40):
+        for k in range(2):
+            ref = vv.render(tree, cams[k], (i + 3 * k) % 9, PS, out="torch")
+            torch.cuda.synchronize()
+            _eq(outs[k][i][0], ref.rgb, f"stream {k} frame {i} rgb")
+            _eq(outs[k][i][2], ref.depth, f"stream {k} frame {i} depth")
