@@ -29,7 +29,8 @@ def _env():
 def test_parity_suites_under_bounds_checks(cuda):
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", "-m", "gpu",
                         "tests/test_gpu_parity.py", "tests/test_node_mask.py", "tests/test_tiles_gpu.py",
-                        "tests/test_joint.py", "tests/test_paint.py", "-k", "not full_size and not cfg3"],
+                        "tests/test_joint.py", "tests/test_paint.py", "tests/test_visible_set.py",
+                        "tests/test_schedule_fuzz.py", "-k", "not full_size and not cfg3"],
                        cwd=ROOT, env=_env(), capture_output=True, text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
