@@ -507,7 +507,7 @@ class Stepper:
         self.scene_plan = vv.CameraPlan(dev)  # what render_scene() keeps per stream
         self.descs = {}
         self.launches = 0
-        self.renders = 0  # per camera plan: k_plan_order re-sorts every 4th render
+        self.renders = 0  # per camera plan: k_plan_order re-sorts every 16th render
 
     def prepare(self, frames):
         """Host-side per-frame scene resolution (timemaps, affines) ahead of the
@@ -536,7 +536,7 @@ class Stepper:
                 descs, len(descs), ctypes.byref(oc), ctypes.byref(cd), bg, self.outs[0][0].data_ptr(), None, None,
                 self.scene_plan._handle, stream_ptr(self.dev)))
             self.renders += 1
-            self.launches += 1 + (self.renders % 4 == 1)  # scene kernel (+ plan order every 4th render)
+            self.launches += 1 + (self.renders % 16 == 1)  # scene kernel (+ plan order every 16th render)
             return
         vis = visible_set_on(wl.tree, vv.device.replica(wl.tree, self.dev))
         self.renders += 1
@@ -553,7 +553,8 @@ class Stepper:
             vv.render_into(wl.tree, wl.cams[0], f, *self.outs[0], plan=self.plans[0])
             # slice pass (+ snapshot diff and walk-table pass with the set),
             # camera kernel, deferred-pixel walk (set), plan order every 4th render
-            self.launches += 1 + 2 * int(vis) + 1 + int(vis) + int(self.renders % 4 == 1)
+            every = 4 if vv.device.replica(wl.tree, self.dev).dark_fraction >= 0.25 else 16  # plan re-sort interval
+            self.launches += 1 + 2 * int(vis) + 1 + int(vis) + int(self.renders % every == 1)
             return
         # stereo: both eyes render from one shared slice (VV_SLICE_VISIBLE),
         # its walk table kept in the first eye's plan
@@ -562,7 +563,7 @@ class Stepper:
             mid.record(stream)
         for cam, out, plan in zip(wl.cams, self.outs, self.plans):
             vv.render_into(wl.tree, cam, f, *out, cache=fs, plan=plan)
-        self.launches += 1 + 2 * int(vis) + len(wl.cams) * (1 + int(vis) + int(self.renders % 4 == 1))
+        self.launches += 1 + 2 * int(vis) + len(wl.cams) * (1 + int(vis) + int(self.renders % 16 == 1))
         del fs
 
 

@@ -1021,10 +1021,18 @@ int plan_coverage(vv_camera_plan *plan, const vv_tree *t, const vv_camera &cam, 
 
 // After a planned launch: the launch order is re-sorted from the costs
 // accumulated over the last kPlanResort renders (the first render sorts at
-// once) -- a view's block costs change slowly, and the sort (one CTA, ~15
+// once) -- a view's block costs change slowly and the sort (one CTA, ~15
 // us) is amortised.
-int plan_finish(vv_camera_plan *plan, cudaStream_t st) {
-    constexpr int kPlanResort = 4;
+// moving: the content's costs move from frame to frame (dark-heavy trees:
+// cfg3's kernel 0.283 ms re-sorting every 4th render, 0.301 every 16th);
+// otherwise costs summed over more frames order the blocks better (cfg2
+// 0.6277 vs 0.6325 ms).  VV_PLAN_RESORT overrides (A/B).
+int plan_finish(vv_camera_plan *plan, cudaStream_t st, bool moving = false) {
+    static const int env_resort = [] {
+        const char *e = getenv("VV_PLAN_RESORT");
+        return e ? atoi(e) : 0;
+    }();
+    const int kPlanResort = env_resort > 0 ? env_resort : (moving ? 4 : 16);
     if (!plan->valid || ++plan->renders >= kPlanResort) {
         int rc = launch_plan_order(plan->cost, plan->n_blocks, plan->order, plan->counter, st);
         if (rc) return rc;
@@ -1874,7 +1882,7 @@ static int render_camera_impl(const vv_tree *t, int32_t frame, const vv_slice *c
     rc = launch_camera(t->n_max, mode, t->has_edits, wide, p, grid_blocks, smem, st, long_queue(t, nm), vis);
     if (!rc && vis) rc = launch_camera_rewalk(t->n_max, wide, p, st);
     if (rc || !plan) return rc;
-    return plan_finish(plan, st);
+    return plan_finish(plan, st, mask_wanted(t));
 }
 
 // ---- render straight to the host: banded device->host copies behind the render
@@ -2150,7 +2158,7 @@ static int render_multi_impl(const vv_tree *t, int32_t n_frames, const int32_t *
     int rc = launch_camera_multi(t->n_max, n_frames, t->has_edits, t->depth > kNarrowDepth, p, grid, st,
                                  long_queue(t, nm));
     if (rc || !plan) return rc;
-    return plan_finish(plan, st);
+    return plan_finish(plan, st, mask_wanted(t));
 }
 
 int vv_render_camera_multi(const vv_tree *t, int32_t n_frames, const int32_t *frames, const vv_slice *const *caches,
@@ -2369,7 +2377,7 @@ static int scene_run(const vv_instance *inst, int n_all, int b, int e, const vv_
     }
     int rc = launch_scene(t0->n_max, wide, lean, p, grid, smem, st);
     if (rc || !plan) return rc;
-    return plan_finish(plan, st);
+    return plan_finish(plan, st);  // (cfg4: 12,818 vs 12,767 Mrays/s re-sorting every 16th vs 4th render)
 }
 
 static int render_scene_impl(const vv_instance *inst, int32_t n_inst, const vv_render_opts *o, const vv_camera *cam,
